@@ -1,0 +1,269 @@
+"""Party programs shared by the golden dumper and the parity tests.
+
+Every program is written once against the reference-shaped public API and
+built for a given package (`ring3pc` for the read-only reference when the
+golden vectors are generated in the build container, or
+`paper_2411_09287_b200` for the B200 implementation under test).  The
+structure of each program follows a named program of the reference's own
+suite, cited per function; nothing here depends on the package's kernels.
+"""
+
+from __future__ import annotations
+
+import importlib
+from types import SimpleNamespace
+
+import numpy as np
+
+
+def build(pkg_name: str) -> SimpleNamespace:
+    gates = importlib.import_module(f"{pkg_name}.gates")
+    verify = importlib.import_module(f"{pkg_name}.verify")
+    sharing = importlib.import_module(f"{pkg_name}.sharing")
+    transport = importlib.import_module(f"{pkg_name}.transport")
+    nonlinear = importlib.import_module(f"{pkg_name}.nonlinear")
+    Ring, MVal = sharing.Ring, sharing.MVal
+    Phase = transport.Phase
+    shc_random, shc_input, rec = sharing.shc_random, sharing.shc_input, sharing.rec
+    shc_input_mask, shc_input_online = sharing.shc_input_mask, sharing.shc_input_online
+
+    def mulv(party, lanes, d, R, ell=64, dots_n=0, auto=False):
+        """tests/test_verify.py:17-42 (and test_acceptance.py:124-136)."""
+        ring = Ring(ell)
+        party.enter_phase(Phase.PRE)
+        x = shc_random(party, lanes, ring)
+        y = shc_random(party, lanes, ring)
+        g = gates.mul_prepare(party, x.mask, y.mask, lanes)
+        dg = None
+        if dots_n:
+            xs = shc_random(party, dots_n * 2, ring)
+            ys = shc_random(party, dots_n * 2, ring)
+            resh = lambda v: MVal(v.mask._map(lambda a: a.reshape(dots_n, 2)),
+                                  None if v.m is None else v.m.reshape(dots_n, 2))
+            dg = (gates.dot_prepare(party, resh(xs).mask, resh(ys).mask, 2),
+                  resh(xs), resh(ys))
+        verify.prepare_verification(party, d=d, r_max=max(R, 1) if not auto else 24)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        z = gates.mul_finish(party, g, x, y)
+        if dg is not None:
+            gates.dot_finish(party, dg[0], dg[1], dg[2])
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        if auto:
+            out = verify.verify_session(party, d=d, R="auto")
+        else:
+            out = {"mul": verify.batch_verify_muls(party, ell, d=d, R=R)}
+            if dots_n:
+                out["dot"] = verify.batch_verify_dots(party, ell, d=d, R=R)
+        return {"x": x, "y": y, "z": z, "verdict": out}
+
+    def mul_inputs(party, xv, yv, ell=64):
+        """tests/test_gates.py:11-22: owner inputs then one online mul."""
+        ring = Ring(ell)
+        lanes = len(xv)
+        party.enter_phase(Phase.PRE)
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input(party, 0, np.asarray(xv, dtype=np.uint64)
+                      if party.role == 0 else None, lanes, ring, "x")
+        y = shc_input(party, 1, np.asarray(yv, dtype=np.uint64)
+                      if party.role == 1 else None, lanes, ring, "y")
+        z = gates.mul(party, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return {"z": z, "open": rec(party, z, "z")}
+
+    def bool_mulv(party, lanes, d, R):
+        """tests/test_verify.py:122-135 (boolean log, GF(2^d))."""
+        ring = Ring(1)
+        party.enter_phase(Phase.PRE)
+        x = shc_random(party, lanes, ring)
+        y = shc_random(party, lanes, ring)
+        g = gates.mul_prepare(party, x.mask, y.mask, lanes)
+        verify.prepare_verification(party, d=d, r_max=max(R, 1))
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        z = gates.mul_finish(party, g, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        return {"x": x, "y": y, "z": z,
+                "verdict": {"mul": verify.batch_verify_muls(party, 1, d=d, R=R)}}
+
+    def trunc(party, xv, t):
+        """tests/test_gates.py:167-182 / test_acceptance.py:256-272."""
+        ring = Ring(64)
+        lanes = len(xv)
+        party.enter_phase(Phase.PRE)
+        mat = gates.trunc_prepare(party, lanes, t, ring)
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input(party, 0, np.asarray(xv, dtype=np.uint64)
+                      if party.role == 0 else None, lanes, ring, "x")
+        one = MVal.public(ring, party.role, np.ones(lanes, dtype=np.uint64))
+        g = gates.mul_prepare(party, x.mask, one.mask, lanes, out_mask=mat.rx_mask)
+        z = gates.trunc_online(party, gates.mul_finish(party, g, x, one), mat)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        zv = rec(party, z, "z")
+        out = {"z": z, "open": zv}
+        if party.role == 0:
+            out["rx_clear"] = mat.rx_clear
+            out["rz_clear"] = mat.rz_clear
+        return out
+
+    def dotv(party, n, lanes, d, R):
+        """Batched inner products + Pi_bsv (test_verify.py:17-42 dot branch)."""
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        xs = shc_random(party, n * lanes, ring)
+        ys = shc_random(party, n * lanes, ring)
+        resh = lambda v: MVal(v.mask._map(lambda a: a.reshape(n, lanes)),
+                              None if v.m is None else v.m.reshape(n, lanes))
+        xs, ys = resh(xs), resh(ys)
+        g = gates.dot_prepare(party, xs.mask, ys.mask, lanes)
+        verify.prepare_verification(party, d=d, r_max=max(R, 1))
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        z = gates.dot_finish(party, g, xs, ys)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        v = verify.batch_verify_dots(party, 64, d=d, R=R)
+        return {"z": z, "verdict": {"dot": v}}
+
+    def relu(party, xv, d=16, R="auto"):
+        """owner-P0 input, relu_prepare, relu_online,
+        verify_session (nonlinear.py:295-319; verify.py:321-338)."""
+        ring = Ring(64)
+        lanes = len(xv)
+        party.enter_phase(Phase.PRE)
+        xmask = shc_input_mask(party, 0, lanes, ring)
+        mat = nonlinear.relu_prepare(party, xmask, lanes, ring)
+        verify.prepare_verification(party, d=d)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input_online(party, 0, np.asarray(xv, dtype=np.uint64)
+                             if party.role == 0 else None, xmask, lanes, ring, "x")
+        out = nonlinear.relu_online(party, x, mat)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        verdict = verify.verify_session(party, d=d, R=R)
+        return {"relu": out, "verdict": verdict, "open": rec(party, out, "relu")}
+
+    def a2b_roundtrip(party, xs, ell):
+        """tests/test_acceptance.py:294-316."""
+        ring = Ring(ell)
+        lanes = len(xs)
+        party.enter_phase(Phase.PRE)
+        eda = nonlinear.edabits_prepare(party, lanes, ring)
+        dabs = [nonlinear.dabit_prepare(party, lanes, ring) for _ in range(ell)]
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input(party, 0, np.array(xs, dtype=np.uint64)
+                      if party.role == 0 else None, lanes, ring, "x")
+        bits = nonlinear.a2b(party, x, eda)
+        acc = None
+        for i in range(ell):
+            ai = nonlinear.b2a(party, bits.take(i), dabs[i], ring)
+            ai = ai.scale_pub(np.uint64((1 << i) & ring.mask))
+            acc = ai if acc is None else acc + ai
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return {"open": rec(party, acc, "x2"), "ea": rec(party, eda.arith, "ea")}
+
+    def matmul(party, Xv, Wv, t=16):
+        """Share matmul + truncation as ppml.infer runs an FC layer
+        (ppml.py:304-309, 320-328, 373-381, 412-427): X (M,K) owned by P2,
+        W (K,N) owned by P1, gathered (K, M*N) operands, one Pi_dot with the
+        truncation input mask as its output mask, then trunc_online."""
+        ring = Ring(64)
+        M, K = Xv.shape
+        N = Wv.shape[1]
+        lanes = M * N
+        party.enter_phase(Phase.PRE)
+        xmask = shc_input_mask(party, 2, M * K, ring)
+        wmask = shc_input_mask(party, 1, K * N, ring)
+        tr = gates.trunc_prepare(party, lanes, t, ring)
+        xi = (np.arange(M)[None, :, None] * K + np.arange(K)[:, None, None]
+              + np.zeros((1, 1, N), dtype=np.int64)).reshape(K, lanes)
+        wi = (np.arange(K)[:, None, None] * N + np.arange(N)[None, None, :]
+              + np.zeros((1, M, 1), dtype=np.int64)).reshape(K, lanes)
+        gx = lambda a: a[xi]
+        gw = lambda a: a[wi]
+        g = gates.dot_prepare(party, xmask._map(gx), wmask._map(gw), lanes,
+                              out_mask=tr.rx_mask)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        X = shc_input_online(party, 2, Xv.reshape(-1) if party.role == 2 else None,
+                             xmask, M * K, ring, "X")
+        W = shc_input_online(party, 1, Wv.reshape(-1) if party.role == 1 else None,
+                             wmask, K * N, ring, "W")
+        gxv = lambda v: MVal(v.mask._map(gx), None if v.m is None else gx(v.m))
+        gwv = lambda v: MVal(v.mask._map(gw), None if v.m is None else gw(v.m))
+        prod = gates.dot_finish(party, g, gxv(X), gwv(W))
+        party.round_barrier()
+        z = gates.trunc_online(party, prod, tr)
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return {"z": z, "open": rec(party, z, "z")}
+
+    return SimpleNamespace(mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
+                           trunc=trunc, dotv=dotv, relu=relu,
+                           a2b_roundtrip=a2b_roundtrip, matmul=matmul)
+
+
+# ---------------------------------------------------------------------------
+# Golden case table: (name, program, args, kwargs, session kwargs)
+# ---------------------------------------------------------------------------
+
+def _trunc_inputs(n, seed):
+    rng = np.random.default_rng(seed)
+    xs = rng.integers(-(2 ** 40) + 1, 2 ** 40, n)
+    return np.array([int(v) % 2 ** 64 for v in xs], dtype=np.uint64)
+
+
+def _relu_inputs(n, seed):
+    rng = np.random.default_rng(seed)
+    vals = np.trunc(rng.normal(0, 4, n) * 2 ** 16).astype(np.int64)
+    return vals.astype(np.uint64)
+
+
+def _mat_inputs(M, K, N, seed):
+    rng = np.random.default_rng(seed)
+    X = np.trunc(rng.normal(0, 1, (M, K)) * 2 ** 16).astype(np.int64).astype(np.uint64)
+    W = np.trunc(rng.normal(0, 1 / 8, (K, N)) * 2 ** 16).astype(np.int64).astype(np.uint64)
+    return X, W
+
+
+CASES = [
+    ("mulv_64_d16_R2", "mulv", (64, 16, 2), {}, {"seed": 3}),
+    ("mulv_1024_d16_R2", "mulv", (1024, 16, 2), {}, {"seed": 11}),
+    ("mulv_1024_d64_R7", "mulv", (1024, 64, 7), {}, {"seed": 11}),
+    ("mulv_100_d64_R3", "mulv", (100, 64, 3), {}, {"seed": 5}),
+    ("mulv_1_d16_R0", "mulv", (1, 16, 0), {}, {"seed": 6}),
+    ("mulv_37_d2_R1_ell4", "mulv", (37, 2, 1), {"ell": 4}, {"seed": 1, "ell": 4}),
+    ("mulv_33_d64_R3_dots5", "mulv", (33, 64, 3), {"dots_n": 5}, {"seed": 0}),
+    ("mulv_3000_d64_auto", "mulv", (3000, 64, 0), {"auto": True}, {"seed": 21}),
+    ("mulv_513_d8_R4", "mulv", (513, 8, 4), {}, {"seed": 8}),
+    ("mulv_200_d32_R2", "mulv", (200, 32, 2), {}, {"seed": 9}),
+    ("mul_inputs_small", "mul_inputs", ([3, 2 ** 63, 12345], [4, 2, 2 ** 64 - 1]), {}, {"seed": 0}),
+    ("bool_mulv_40_d16_R2", "bool_mulv", (40, 16, 2), {}, {"seed": 0, "ell": 1}),
+    ("trunc_small", "trunc", ([98304, 0, (-98304) % 2 ** 64, 12345 << 16], 16), {}, {"seed": 3}),
+    ("trunc_1000", "trunc", (_trunc_inputs(1000, 6), 16), {}, {"seed": 66}),
+    ("dotv_8x16_d16_R2", "dotv", (8, 16, 16, 2), {}, {"seed": 4}),
+    ("relu_64", "relu", (_relu_inputs(64, 1),), {}, {"seed": 1}),
+    ("a2b_roundtrip_ell8", "a2b_roundtrip", (list(range(16)), 8), {}, {"seed": 0, "ell": 8}),
+    ("matmul_8x8x8", "matmul", _mat_inputs(8, 8, 8, 3), {}, {"seed": 3}),
+    ("matmul_12x16x10", "matmul", _mat_inputs(12, 16, 10, 4), {}, {"seed": 4}),
+]
+
+# Tamper cases: (name, program, args, injections[(site, who, delta, gate, lane)])
+TAMPER_CASES = [
+    ("tamper_gamma", "mulv", (16, 16, 2), ("gamma", 0, 5, 0, 3), {"seed": 1000}),
+    ("tamper_z", "mulv", (16, 16, 2), ("z", 1, 7, 0, 9), {"seed": 1001}),
+    ("tamper_mz", "mulv", (16, 16, 2), ("mz", 1, 1, 0, 2), {"seed": 1002}),
+    ("tamper_z_msb", "mulv", (64, 16, 2), ("z", 2, 1 << 63, 0, 5), {"seed": 1003}),
+    ("tamper_mz_rec_abort", "mul_inputs", ([3], [4]), ("mz", 1, 1, 0, None), {"seed": 0}),
+    ("tamper_vfy_gamma", "mulv", (64, 16, 3), ("vfy.dot.gamma", 0, 11, 2, 0), {"seed": 1004}),
+]
