@@ -1,0 +1,191 @@
+/*
+ * r3b200.h -- C ABI of the B200 (sm_100a) kernels behind the ring3pc API.
+ *
+ * The reference (`ring3pc`, pure Python/numpy) has no FFI; its plugin seam is
+ * the array-kernel layer `grvec` + `prg.Prg` plus the inline numpy in
+ * gates/verify/nonlinear.  Each entry point below replaces one
+ * of those numpy hot loops; the comment names the reference file:line it
+ * stands in for.  Conventions:
+ *
+ *   - every array argument is a DEVICE pointer to uint64 words holding ring
+ *     elements (Z_2^ell, ell <= 64; booleans as 0/1 words; GR(2^ell, d)
+ *     elements as d consecutive words, constant coefficient first,
+ *     grvec.py:1-7);
+ *   - outputs are caller-allocated; no function allocates device memory;
+ *   - `mask` = 2^ell - 1 is applied to every stored result (grvec.vmask);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream);
+ *   - return value 0 = success, otherwise an R3_ERR_* code with a message in
+ *     r3_last_error() (thread-local).  Kernels are stateless and the only
+ *     globals are const tables, so the library is reentrant across the
+ *     three party threads (SURVEY.md 8b "Threading").
+ */
+#ifndef R3B200_H
+#define R3B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define R3_OK 0
+#define R3_ERR_ARG 1
+#define R3_ERR_CUDA 2
+
+#define R3_ABI_VERSION 1
+
+/* Elementwise op codes for r3_ew. */
+enum r3_ew_op {
+  R3_EW_ADD = 0,  /* a + b                                                */
+  R3_EW_SUB = 1,  /* a - b                                                */
+  R3_EW_MUL = 2,  /* a * b                                                */
+  R3_EW_AND = 3,  /* a & b                                                */
+  R3_EW_XOR = 4,  /* a ^ b                                                */
+  R3_EW_OR = 5,   /* a | b                                                */
+  R3_EW_RSUB = 6, /* b - a                                                */
+  R3_EW_COPY = 7  /* a (masked); b unused                                 */
+};
+
+/* Linear-combination operand: row i = sum_{q<nterms} coef[q] * p[q][i],
+ * p[q] row-strided (rowstride in words; d coefficients contiguous), rows at
+ * or beyond nvalid[q] read as zero. */
+typedef struct r3_lin_operand {
+  const uint64_t* p[4];
+  int64_t rowstride[4];
+  int64_t nvalid[4];
+  uint64_t coef[4];
+  int32_t nterms;
+} r3_lin_operand;
+
+int r3_abi_version(void);
+const char* r3_last_error(void);
+
+/* ---- PRF: AES-128-CTR streams (prg.py:39-65) ----------------------------
+ * Host helper: FIPS-197 key expansion, 44 big-endian round-key words. */
+void r3_aes128_expand(const uint8_t key[16], uint32_t rk[44]);
+/* Keystream u64 number j (j = first_u64 .. first_u64+n-1) of AES-128-CTR with
+ * a zero IV and 128-bit big-endian block counter: little-endian bytes
+ * [8(j&1), 8(j&1)+8) of AES_K(BE128(j>>1)).  Replaces Prg.draw_u64 /
+ * draw_base (mode 0: & mask) / draw_bits (mode 1: & 1), prg.py:50-62. */
+int r3_prf_ctr(const uint32_t rk[44], uint64_t first_u64, int64_t n,
+               uint64_t mask, int mode, uint64_t* out, void* stream);
+
+/* ---- elementwise (grvec.py:18-40; sharing.py:95-230 linear ops) ----------
+ * out[idx] = op(a[idx . a_strides], b[idx . b_strides]) over an ndim<=4 index
+ * space `shape` (out contiguous).  Stride 0 broadcasts.  b == NULL uses the
+ * scalar `imm` for b. */
+int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out,
+          const uint64_t* a, const int64_t* a_strides,
+          const uint64_t* b, const int64_t* b_strides,
+          uint64_t imm, uint64_t mask, void* stream);
+/* Sign-extending right shift on width-bit patterns (grvec.arith_rshift,
+ * grvec.py:43-51); t in [0, width). */
+int r3_ars(const uint64_t* a, int64_t n, int t, int width, uint64_t* out,
+           void* stream);
+/* out[j, l] = (a[l] >> j) & 1 for j < nbits (nonlinear.a2b public bits,
+ * nonlinear.py:273). */
+int r3_bit_planes(const uint64_t* a, int64_t lanes, int nbits, uint64_t* out,
+                  void* stream);
+/* *count += #{i : a[i] != b[i]} (b == NULL: #{a[i] != 0}).  Replaces the
+ * SHA-256 digest comparison of Party.check_digest (runtime.py:115-124) and
+ * the zero test of check_inner_product (verify.py:263).  count is a device
+ * uint64 the caller zeroes. */
+int r3_count_nonequal(const uint64_t* a, const uint64_t* b, int64_t n,
+                      uint64_t* count, void* stream);
+/* out[j] (+)= sum_i a[i*rowstride + j], i < n, j < inner (np.add.reduce over
+ * axis 0: verify._sum_lanes verify.py:149-151, gates._sum_axis0). */
+int r3_sum_axis0(const uint64_t* a, int64_t n, int64_t inner, int64_t rowstride,
+                 uint64_t* out, uint64_t mask, int accumulate, void* stream);
+/* out[l] = sum_i a[i,l] * b[i,l]   (P0's cross term, gates._pair_sum
+ * gates.py:41-49, base ring).  Element (i,l) at p + i*rs + l*ls. */
+int r3_dot_fold(int64_t n, int64_t lanes,
+                const uint64_t* a, int64_t a_rs, int64_t a_ls,
+                const uint64_t* b, int64_t b_rs, int64_t b_ls,
+                uint64_t* out, uint64_t mask, void* stream);
+/* Online Pi_dot leg of P1 (role 1) or P2 (role 2), base ring
+ * (gates.dot_finish gates.py:92-106):
+ *   P1: leg = g - sum_i mx*sy - sum_i my*sx
+ *   P2: leg = sum_i mx*(my - sy) - sum_i my*sx + g
+ * sx/sy are the party's mask halves. */
+int r3_mul_leg(int role, int64_t n, int64_t lanes,
+               const uint64_t* mx, int64_t mx_rs, int64_t mx_ls,
+               const uint64_t* my, int64_t my_rs, int64_t my_ls,
+               const uint64_t* sx, int64_t sx_rs, int64_t sx_ls,
+               const uint64_t* sy, int64_t sy_rs, int64_t sy_ls,
+               const uint64_t* g, uint64_t* out, uint64_t mask, void* stream);
+
+/* ---- GR(2^ell, d) arithmetic (grvec.py:67-167; rings.py:180-241) -------
+ * `lowterms` = bit mask of the exponents j < d with f_j = 1 (rings.py:180-188,
+ * GrModulus.low_terms). */
+/* out[i] = a[i] * b[i] in GR, rows broadcast when a_rs / b_rs == 0
+ * (grvec.gr_mul grvec.py:78-93). */
+int r3_gr_mul(const uint64_t* a, int64_t a_rs, const uint64_t* b, int64_t b_rs,
+              uint64_t* out, int64_t rows, int d, uint64_t lowterms,
+              uint64_t mask, void* stream);
+/* out[i] = s[i*s_stride] * g[i] (base scalar times GR element; the
+ * reference's embedded-scalar gr_mul, identical values at d MACs/row). */
+int r3_gr_scale_rows(const uint64_t* s, int64_t s_stride,
+                     const uint64_t* g, int64_t g_rs, uint64_t* out,
+                     int64_t rows, int d, uint64_t mask, void* stream);
+/* M (d x d): row j = x^j * c mod f, so that (a * c) = a_row . M. */
+int r3_gr_mulmat(const uint64_t* c, int d, uint64_t lowterms, uint64_t* M,
+                 void* stream);
+/* out[i] = A[i] . M (+ C[i])   -- multiplication of many GR elements by one
+ * element whose matrix is M; A and C are lin-operands (line evaluation
+ * verify.py:239-240 as f0 + (f1 - f0)*zeta, gr_powers block doubling
+ * grvec.py:130-141, scale_gr by a public element). */
+int r3_gr_matmul(r3_lin_operand A, const uint64_t* M, int has_c,
+                 r3_lin_operand C, uint64_t* out, int64_t rows, int d,
+                 uint64_t mask, void* stream);
+/* acc[0..2d-2] += unreduced polynomial sum_i F[i] (x) G[i] (the inner
+ * products of reduce_dimension / check_inner_product, verify.py:154-161,
+ * gates.dot_finish.fold over GR). acc must be zeroed by the caller before the
+ * first term. */
+int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, int d,
+                 uint64_t* acc, void* stream);
+/* out[0..d-1] (+)= acc reduced mod f and masked. */
+int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms,
+                      uint64_t* out, uint64_t mask, int accumulate,
+                      void* stream);
+
+/* ---- fused verification stages (verify.py:168-241) ----------------------
+ * Compressed triples are never materialised (SURVEY.md finding 5): x'_i =
+ * pw[i/n] * x_i (x a base share, pw the challenge powers r^k), y'_i = y_i
+ * lifted.  Element i of a base component lives at c + (i % n)*ks + (i / n)*ls
+ * (n = 1 for multiplication logs; n = dot length for Pi_bsv lane-major
+ * consolidation, verify.py:195-201).
+ *
+ * r3_vfy_powsum: out[c] = sum_l comps[c][l] * pw[l] for c < ncomp
+ * (z compression, verify.py:178 and 204). */
+int r3_vfy_powsum(int ncomp, const uint64_t* const* comps, int64_t stride,
+                  int64_t lanes, const uint64_t* pw, int d, uint64_t* out,
+                  uint64_t mask, void* stream);
+/* Level-1 h(1)/h(2) folds of one party (verify.py:220-231) on compressed
+ * operands.  Terms t < nterms: coef[t] * fold(x-comp xi[t], y-comp yi[t]);
+ * out_h1/out_h2 (d words each) receive the sums. */
+int r3_vfy_l1_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                   const uint64_t* const* yc, int64_t N, int64_t n,
+                   int64_t ks, int64_t ls, const uint64_t* pw, int d,
+                   uint64_t* out_h1, uint64_t* out_h2, uint64_t mask,
+                   void* stream);
+/* Level-1 line evaluation of x components (verify.py:239):
+ * out[c][j] = X_c[2j] * A[(2j)/tq] + X_c[2j+1] * B[(2j+1)/tq] with public
+ * tables A = pw(1-ze), B = pw ze (tq = 2 with A/B over even/odd powers for
+ * multiplication logs; tq = n with A/B over all powers for dot logs);
+ * X_c[N] reads as 0 when N is odd. */
+int r3_vfy_l1_line_x(int ncomp, const uint64_t* const* xc, int64_t N,
+                     int64_t n, int64_t ks, int64_t ls, const uint64_t* A,
+                     const uint64_t* B, int64_t tq, int d,
+                     uint64_t* const* out, uint64_t mask, void* stream);
+/* Level-1 line evaluation of y components (verify.py:240):
+ * out[c][j] = Y_c[2j] * a + Y_c[2j+1] * b with public a = 1-ze, b = ze. */
+int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N,
+                     int64_t n, int64_t ks, int64_t ls, const uint64_t* a,
+                     const uint64_t* b, int d, uint64_t* const* out,
+                     uint64_t mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* R3B200_H */

@@ -1,0 +1,158 @@
+"""ctypes binding of the in-tree CUDA library (include/r3b200.h).
+
+The product path has no CPU fallback: importing a compute helper without the
+built library, or calling one without a CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libr3b200.so")
+
+_lock = threading.Lock()
+_lib = None
+
+u64p = C.c_void_p
+i64 = C.c_int64
+u64 = C.c_uint64
+
+
+class LinOperand(C.Structure):
+    _fields_ = [("p", C.c_void_p * 4), ("rowstride", C.c_int64 * 4),
+                ("nvalid", C.c_int64 * 4), ("coef", C.c_uint64 * 4),
+                ("nterms", C.c_int32)]
+
+
+# name -> argtypes (all return c_int status unless listed in _VOID)
+_SIGS = {
+    "r3_abi_version": [],
+    "r3_last_error": [],
+    "r3_aes128_expand": [C.c_char_p, C.POINTER(C.c_uint32)],
+    "r3_prf_ctr": [C.POINTER(C.c_uint32), u64, i64, u64, C.c_int, u64p, C.c_void_p],
+    "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
+              C.POINTER(i64), u64, u64, C.c_void_p],
+    "r3_ars": [u64p, i64, C.c_int, C.c_int, u64p, C.c_void_p],
+    "r3_bit_planes": [u64p, i64, C.c_int, u64p, C.c_void_p],
+    "r3_count_nonequal": [u64p, u64p, i64, u64p, C.c_void_p],
+    "r3_sum_axis0": [u64p, i64, i64, i64, u64p, u64, C.c_int, C.c_void_p],
+    "r3_dot_fold": [i64, i64, u64p, i64, i64, u64p, i64, i64, u64p, u64, C.c_void_p],
+    "r3_mul_leg": [C.c_int, i64, i64, u64p, i64, i64, u64p, i64, i64, u64p, i64, i64,
+                   u64p, i64, i64, u64p, u64p, u64, C.c_void_p],
+    "r3_gr_mul": [u64p, i64, u64p, i64, u64p, i64, C.c_int, u64, u64, C.c_void_p],
+    "r3_gr_scale_rows": [u64p, i64, u64p, i64, u64p, i64, C.c_int, u64, C.c_void_p],
+    "r3_gr_mulmat": [u64p, C.c_int, u64, u64p, C.c_void_p],
+    "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
+                     C.c_void_p],
+    "r3_gr_dotsum": [LinOperand, LinOperand, i64, C.c_int, u64p, C.c_void_p],
+    "r3_gr_reduce_poly": [u64p, C.c_int, u64, u64p, u64, C.c_int, C.c_void_p],
+    "r3_vfy_powsum": [C.c_int, C.POINTER(C.c_void_p), i64, i64, u64p, C.c_int, u64p, u64,
+                      C.c_void_p],
+    "r3_vfy_l1_fold": [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p),
+                       C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, C.c_int, u64p,
+                       u64p, u64, C.c_void_p],
+    "r3_vfy_l1_line_x": [C.c_int, C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, u64p, i64,
+                         C.c_int, C.POINTER(C.c_void_p), u64, C.c_void_p],
+    "r3_vfy_l1_line_y": [C.c_int, C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, u64p,
+                         C.c_int, C.POINTER(C.c_void_p), u64, C.c_void_p],
+}
+_RESTYPE = {"r3_last_error": C.c_char_p, "r3_aes128_expand": None}
+
+
+class KernelError(RuntimeError):
+    """A CUDA library call failed (bad arguments or a CUDA error)."""
+
+
+def load():
+    """Load and type the shared library (idempotent); raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is not built; run `python -m paper_2411_09287_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(LIB_PATH)
+            for name, args in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPE.get(name, C.c_int)
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        msg = load().r3_last_error().decode(errors="replace")
+        raise KernelError(f"{name} failed ({rc}): {msg}")
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# tensor helpers (int64 storage, uint64 semantics)
+# ---------------------------------------------------------------------------
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("ring3pc-b200 requires a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def as_i64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >> 63 else v
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def empty(shape, dev=None) -> torch.Tensor:
+    return torch.empty(shape, dtype=torch.int64, device=dev or device())
+
+
+def zeros(shape, dev=None) -> torch.Tensor:
+    return torch.zeros(shape, dtype=torch.int64, device=dev or device())
+
+
+def to_device(x) -> torch.Tensor:
+    """Host (numpy uint64 / python ints / CPU tensor) -> device int64 tensor.
+    Device tensors pass through unchanged."""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            return x
+        return x.to(torch.int64).to(device(), non_blocking=False)
+    arr = np.asarray(x)
+    if arr.dtype != np.uint64:
+        if arr.dtype.kind in "iu":
+            arr = arr.astype(np.int64).view(np.uint64) if arr.dtype.kind == "i" else arr.astype(np.uint64)
+        elif arr.dtype == object:
+            arr = np.array([int(v) & ((1 << 64) - 1) for v in arr.reshape(-1)],
+                           dtype=np.uint64).reshape(arr.shape)
+        else:
+            arr = arr.astype(np.uint64)
+    arr = np.ascontiguousarray(arr)
+    return torch.from_numpy(arr.view(np.int64)).to(device())
+
+
+def to_host(t) -> np.ndarray:
+    """Device tensor -> numpy uint64 (copies)."""
+    if isinstance(t, np.ndarray):
+        return t.astype(np.uint64)
+    return t.detach().cpu().contiguous().numpy().view(np.uint64).copy()

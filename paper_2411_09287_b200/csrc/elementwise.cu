@@ -1,0 +1,322 @@
+// Elementwise share kernels: linear ops, masking, shifts, equality counts,
+// axis-0 reductions and the base-ring Pi_dot legs.
+//
+// Reference counterparts: grvec.vmask/vneg/vscale/arith_rshift
+// (grvec.py:18-51), the AShare/MVal linear maps (sharing.py:95-230), the
+// fold/leg algebra of gates.dot_finish (gates.py:92-113) and P0's cross term
+// gates._pair_sum (gates.py:41-49).  Contiguous same-shape operands take a
+// 128-bit vectorised path; anything else goes through a strided <=4-d index
+// walk (stride 0 broadcasts, mirroring numpy broadcasting in the reference).
+#include "r3_common.cuh"
+
+namespace r3 {
+
+__device__ __forceinline__ u64 ew_apply(int op, u64 a, u64 b) {
+  switch (op) {
+    case R3_EW_ADD: return a + b;
+    case R3_EW_SUB: return a - b;
+    case R3_EW_MUL: return a * b;
+    case R3_EW_AND: return a & b;
+    case R3_EW_XOR: return a ^ b;
+    case R3_EW_OR: return a | b;
+    case R3_EW_RSUB: return b - a;
+    default: return a;
+  }
+}
+
+struct Shape4 {
+  int64_t s[4];
+  int64_t as[4];
+  int64_t bs[4];
+};
+
+template <int OP>
+__global__ void ew_vec_kernel(int64_t n, u64* __restrict__ out, const u64* __restrict__ a,
+                              const u64* __restrict__ b, u64 imm, u64 mask) {
+  const int64_t n2 = n >> 1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+    ulonglong2 va = reinterpret_cast<const ulonglong2*>(a)[i];
+    ulonglong2 vb = b ? reinterpret_cast<const ulonglong2*>(b)[i] : make_ulonglong2(imm, imm);
+    ulonglong2 r;
+    r.x = ew_apply(OP, va.x, vb.x) & mask;
+    r.y = ew_apply(OP, va.y, vb.y) & mask;
+    reinterpret_cast<ulonglong2*>(out)[i] = r;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    u64 bv = b ? b[n - 1] : imm;
+    out[n - 1] = ew_apply(OP, a[n - 1], bv) & mask;
+  }
+}
+
+__global__ void ew_strided_kernel(int op, int64_t n, Shape4 sh, u64* __restrict__ out,
+                                  const u64* __restrict__ a, const u64* __restrict__ b, u64 imm,
+                                  u64 mask) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    int64_t rem = i, oa = 0, ob = 0;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      int64_t idx = rem % sh.s[k];
+      rem /= sh.s[k];
+      oa += idx * sh.as[k];
+      ob += idx * sh.bs[k];
+    }
+    u64 bv = b ? b[ob] : imm;
+    out[i] = ew_apply(op, a[oa], bv) & mask;
+  }
+}
+
+__global__ void ars_kernel(const u64* __restrict__ a, int64_t n, int t, int width, u64* __restrict__ out) {
+  const u64 mask = width == 64 ? ~0ull : ((1ull << width) - 1);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    u64 v = a[i];
+    if (t == 0) {
+      out[i] = v;
+      continue;
+    }
+    u64 sign = (v >> (width - 1)) & 1ull;
+    u64 fill = ((0ull - sign) << (width - t)) & mask;
+    out[i] = (v >> t) | fill;
+  }
+}
+
+__global__ void bit_planes_kernel(const u64* __restrict__ a, int64_t lanes, int nbits, u64* __restrict__ out) {
+  const int64_t total = lanes * nbits;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    int64_t j = i / lanes, l = i - j * lanes;
+    out[i] = (a[l] >> j) & 1ull;
+  }
+}
+
+__global__ void count_ne_kernel(const u64* __restrict__ a, const u64* __restrict__ b, int64_t n,
+                                u64* __restrict__ count) {
+  u64 local = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    u64 bv = b ? b[i] : 0ull;
+    local += (a[i] != bv);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+// out[j] (+)= sum_i a[i*rs + j]: each block owns a (rows chunk) x (column
+// tile) and reduces in registers; blocks meet in exact u64 atomics (addition
+// mod 2^64 is order-free, so the result is deterministic).
+__global__ void sum_axis0_kernel(const u64* __restrict__ a, int64_t n, int64_t inner, int64_t rs,
+                                 u64* __restrict__ out, int64_t rows_per_block) {
+  const int64_t col = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (col >= inner) return;
+  const int64_t r0 = blockIdx.y * rows_per_block;
+  const int64_t r1 = min(n, r0 + rows_per_block);
+  u64 acc = 0;
+  for (int64_t r = r0; r < r1; ++r) acc += a[r * rs + col];
+  atomicAdd(out + col, acc);
+}
+
+__global__ void mask_kernel(u64* out, int64_t n, u64 mask) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) out[i] &= mask;
+}
+
+__global__ void dot_fold_kernel(int64_t n, int64_t lanes, const u64* __restrict__ a, int64_t a_rs,
+                                int64_t a_ls, const u64* __restrict__ b, int64_t b_rs, int64_t b_ls,
+                                u64* __restrict__ out, u64 mask) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < lanes; l += stride) {
+    u64 acc = 0;
+    for (int64_t i = 0; i < n; ++i) acc += a[i * a_rs + l * a_ls] * b[i * b_rs + l * b_ls];
+    out[l] = acc & mask;
+  }
+}
+
+template <int ROLE>
+__global__ void mul_leg_kernel(int64_t n, int64_t lanes, const u64* __restrict__ mx, int64_t mx_rs,
+                               int64_t mx_ls, const u64* __restrict__ my, int64_t my_rs, int64_t my_ls,
+                               const u64* __restrict__ sx, int64_t sx_rs, int64_t sx_ls,
+                               const u64* __restrict__ sy, int64_t sy_rs, int64_t sy_ls,
+                               const u64* __restrict__ g, u64* __restrict__ out, u64 mask) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < lanes; l += stride) {
+    u64 acc = g[l];
+    for (int64_t i = 0; i < n; ++i) {
+      u64 vmx = mx[i * mx_rs + l * mx_ls], vmy = my[i * my_rs + l * my_ls];
+      u64 vsx = sx[i * sx_rs + l * sx_ls], vsy = sy[i * sy_rs + l * sy_ls];
+      if (ROLE == 1) {
+        acc -= vmx * vsy + vmy * vsx;
+      } else {
+        acc += vmx * (vmy - vsy) - vmy * vsx;
+      }
+    }
+    out[l] = acc & mask;
+  }
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+static bool contiguous_full(int ndim, const int64_t* shape, const int64_t* st) {
+  int64_t expect = 1;
+  for (int k = ndim - 1; k >= 0; --k) {
+    if (shape[k] != 1 && st[k] != expect) return false;
+    expect *= shape[k];
+  }
+  return true;
+}
+
+extern "C" int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out, const uint64_t* a,
+                     const int64_t* a_strides, const uint64_t* b, const int64_t* b_strides,
+                     uint64_t imm, uint64_t mask, void* stream) {
+  if (ndim < 0 || ndim > 4 || op < 0 || op > R3_EW_COPY || !out || !a) {
+    set_error("r3_ew: bad arguments (op=%d ndim=%d)", op, ndim);
+    return R3_ERR_ARG;
+  }
+  int64_t n = 1;
+  for (int k = 0; k < ndim; ++k) n *= shape[k];
+  if (n == 0) return R3_OK;
+  cudaStream_t s = as_stream(stream);
+  const bool ca = contiguous_full(ndim, shape, a_strides);
+  const bool cb = (b == nullptr) || contiguous_full(ndim, shape, b_strides);
+  const bool aligned = ((uintptr_t(out) | uintptr_t(a) | uintptr_t(b)) & 15) == 0;
+  if (op == R3_EW_COPY) b = nullptr;
+  if (ca && cb && aligned) {
+    unsigned grid = grid_for((n + 1) / 2, 256, 8);
+#define R3_EW_CASE(OPC) \
+  case OPC: ew_vec_kernel<OPC><<<grid, 256, 0, s>>>(n, (u64*)out, (const u64*)a, (const u64*)b, imm, mask); break;
+    switch (op) {
+      R3_EW_CASE(R3_EW_ADD)
+      R3_EW_CASE(R3_EW_SUB)
+      R3_EW_CASE(R3_EW_MUL)
+      R3_EW_CASE(R3_EW_AND)
+      R3_EW_CASE(R3_EW_XOR)
+      R3_EW_CASE(R3_EW_OR)
+      R3_EW_CASE(R3_EW_RSUB)
+      R3_EW_CASE(R3_EW_COPY)
+    }
+#undef R3_EW_CASE
+    return check_launch("r3_ew(vec)");
+  }
+  Shape4 sh;
+  for (int k = 0; k < 4; ++k) {
+    int src = k - (4 - ndim);
+    sh.s[k] = src >= 0 ? shape[src] : 1;
+    sh.as[k] = src >= 0 ? a_strides[src] : 0;
+    sh.bs[k] = (src >= 0 && b) ? b_strides[src] : 0;
+  }
+  ew_strided_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(op, n, sh, (u64*)out, (const u64*)a,
+                                                       (const u64*)b, imm, mask);
+  return check_launch("r3_ew(strided)");
+}
+
+extern "C" int r3_ars(const uint64_t* a, int64_t n, int t, int width, uint64_t* out, void* stream) {
+  if (width < 1 || width > 64 || t < 0 || t >= width || n < 0) {
+    set_error("r3_ars: shift %d out of range for width %d", t, width);
+    return R3_ERR_ARG;
+  }
+  if (n == 0) return R3_OK;
+  ars_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>((const u64*)a, n, t, width, (u64*)out);
+  return check_launch("r3_ars");
+}
+
+extern "C" int r3_bit_planes(const uint64_t* a, int64_t lanes, int nbits, uint64_t* out, void* stream) {
+  if (nbits < 1 || nbits > 64 || lanes < 0) {
+    set_error("r3_bit_planes: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (lanes == 0) return R3_OK;
+  bit_planes_kernel<<<grid_for(lanes * nbits, 256), 256, 0, as_stream(stream)>>>((const u64*)a, lanes, nbits,
+                                                                                   (u64*)out);
+  return check_launch("r3_bit_planes");
+}
+
+extern "C" int r3_count_nonequal(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* count,
+                                 void* stream) {
+  if (n < 0 || !count) {
+    set_error("r3_count_nonequal: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (n == 0) return R3_OK;
+  count_ne_kernel<<<grid_for(n, 256, 4), 256, 0, as_stream(stream)>>>((const u64*)a, (const u64*)b, n,
+                                                                       (u64*)count);
+  return check_launch("r3_count_nonequal");
+}
+
+extern "C" int r3_sum_axis0(const uint64_t* a, int64_t n, int64_t inner, int64_t rowstride, uint64_t* out,
+                            uint64_t mask, int accumulate, void* stream) {
+  if (n < 0 || inner < 0) {
+    set_error("r3_sum_axis0: bad arguments");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (inner == 0) return R3_OK;
+  if (!accumulate) {
+    cudaError_t e = cudaMemsetAsync(out, 0, size_t(inner) * 8, s);
+    if (e != cudaSuccess) {
+      set_error("r3_sum_axis0: memset: %s", cudaGetErrorString(e));
+      return R3_ERR_CUDA;
+    }
+  }
+  if (n > 0) {
+    const int threads = inner >= 256 ? 256 : (inner >= 64 ? 64 : 32);
+    const int64_t colblocks = (inner + threads - 1) / threads;
+    // aim for ~8 resident blocks per SM in total
+    int64_t ychunks = (int64_t(kNumSMs) * 8 + colblocks - 1) / colblocks;
+    int64_t rows_per_block = (n + ychunks - 1) / ychunks;
+    if (rows_per_block < 16) rows_per_block = 16;
+    ychunks = (n + rows_per_block - 1) / rows_per_block;
+    if (ychunks > 65535) {
+      ychunks = 65535;
+      rows_per_block = (n + ychunks - 1) / ychunks;
+    }
+    dim3 grid{unsigned(colblocks), unsigned(ychunks), 1u};
+    sum_axis0_kernel<<<grid, threads, 0, s>>>((const u64*)a, n, inner, rowstride, (u64*)out, rows_per_block);
+    int rc = check_launch("r3_sum_axis0");
+    if (rc) return rc;
+  }
+  if (mask != ~0ull) {
+    mask_kernel<<<grid_for(inner, 256), 256, 0, s>>>((u64*)out, inner, mask);
+    return check_launch("r3_sum_axis0(mask)");
+  }
+  return R3_OK;
+}
+
+extern "C" int r3_dot_fold(int64_t n, int64_t lanes, const uint64_t* a, int64_t a_rs, int64_t a_ls,
+                           const uint64_t* b, int64_t b_rs, int64_t b_ls, uint64_t* out, uint64_t mask,
+                           void* stream) {
+  if (n < 0 || lanes < 0) {
+    set_error("r3_dot_fold: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (lanes == 0) return R3_OK;
+  dot_fold_kernel<<<grid_for(lanes, 256), 256, 0, as_stream(stream)>>>(n, lanes, (const u64*)a, a_rs, a_ls,
+                                                                       (const u64*)b, b_rs, b_ls, (u64*)out,
+                                                                       mask);
+  return check_launch("r3_dot_fold");
+}
+
+extern "C" int r3_mul_leg(int role, int64_t n, int64_t lanes, const uint64_t* mx, int64_t mx_rs, int64_t mx_ls,
+                          const uint64_t* my, int64_t my_rs, int64_t my_ls, const uint64_t* sx, int64_t sx_rs,
+                          int64_t sx_ls, const uint64_t* sy, int64_t sy_rs, int64_t sy_ls, const uint64_t* g,
+                          uint64_t* out, uint64_t mask, void* stream) {
+  if ((role != 1 && role != 2) || n < 0 || lanes < 0) {
+    set_error("r3_mul_leg: bad arguments (role=%d)", role);
+    return R3_ERR_ARG;
+  }
+  if (lanes == 0) return R3_OK;
+  unsigned grid = grid_for(lanes, 256);
+  cudaStream_t s = as_stream(stream);
+  if (role == 1)
+    mul_leg_kernel<1><<<grid, 256, 0, s>>>(n, lanes, (const u64*)mx, mx_rs, mx_ls, (const u64*)my, my_rs, my_ls,
+                                            (const u64*)sx, sx_rs, sx_ls, (const u64*)sy, sy_rs, sy_ls,
+                                            (const u64*)g, (u64*)out, mask);
+  else
+    mul_leg_kernel<2><<<grid, 256, 0, s>>>(n, lanes, (const u64*)mx, mx_rs, mx_ls, (const u64*)my, my_rs, my_ls,
+                                            (const u64*)sx, sx_rs, sx_ls, (const u64*)sy, sy_rs, sy_ls,
+                                            (const u64*)g, (u64*)out, mask);
+  return check_launch("r3_mul_leg");
+}

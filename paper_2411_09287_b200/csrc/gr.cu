@@ -1,0 +1,663 @@
+// Galois-ring GR(2^ell, d) kernels and the fused verification stages.
+//
+// Reference counterparts: grvec.gr_mul / gr_dot / gr_powers / gr_line_eval
+// (grvec.py:78-167), the fixed sparse moduli f = x^d + g(x) of rings.py:180-188
+// and the compress / reduce stages of verify.py:126-241.
+//
+// Reduction mod f without the reference's dense (d-1, d) reduction matrix:
+// with x^d = -g (deg g <= 7 for every supported d), a product
+// p = low + x^d * high reduces as  low - t_low + g * t_high  where
+// t = g * high = t_low + x^d t_high (two sparse passes, exact mod 2^64).
+//
+// The bulk work maps onto two GEMM shapes on CUDA cores (64-bit MACs as
+// IMAD.WIDE + 2 IMAD):
+//   * many elements times ONE element c:  rows . M_c   (r3_gr_matmul)
+//   * sum of many products:  sum_i F_i (x) G_i, i.e. F^T G folded along
+//     anti-diagonals                                        (r3_gr_dotsum)
+#include "r3_common.cuh"
+
+namespace r3 {
+
+// ---------------------------------------------------------------------------
+// polynomial reduction helper (one warp; p has 2D-1 coefficients in smem)
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ void reduce_poly_warp(const u64* p, u64* t, u64 lowterms, u64* out, u64 mask, int lane,
+                                 const u64* addend) {
+  // t[k] = sum_{j in L} high[k - j],  high[m] = p[D + m], m <= D-2
+  constexpr int TLEN = 2 * D + 8;
+  for (int k = lane; k < TLEN; k += 32) {
+    u64 v = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if ((lowterms >> j) & 1ull) {
+        int m = k - j;
+        if (m >= 0 && m <= D - 2) v += p[D + m];
+      }
+    }
+    t[k] = v;
+  }
+  __syncwarp();
+  for (int k = lane; k < D; k += 32) {
+    u64 v = p[k] - t[k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if ((lowterms >> j) & 1ull) {
+        int m = k - j;  // index into t_high = t[D + m]
+        if (m >= 0 && D + m < TLEN) v += t[D + m];
+      }
+    }
+    if (addend) v += addend[k];
+    out[k] = v & mask;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// generic row-wise GR product (warp per row)
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void gr_mul_kernel(const u64* __restrict__ a, int64_t a_rs, const u64* __restrict__ b, int64_t b_rs,
+                              u64* __restrict__ out, int64_t rows, u64 lowterms, u64 mask) {
+  constexpr int WARPS = 4;
+  __shared__ u64 sa[WARPS][D], sb[WARPS][D], sp[WARPS][2 * D], st[WARPS][2 * D + 8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t row = blockIdx.x * int64_t(WARPS) + w; row < rows; row += int64_t(gridDim.x) * WARPS) {
+    for (int k = lane; k < D; k += 32) {
+      sa[w][k] = a[row * a_rs + k];
+      sb[w][k] = b[row * b_rs + k];
+    }
+    __syncwarp();
+    for (int idx = lane; idx < 2 * D - 1; idx += 32) {
+      int lo = idx - (D - 1) > 0 ? idx - (D - 1) : 0;
+      int hi = idx < D - 1 ? idx : D - 1;
+      u64 acc = 0;
+      for (int i = lo; i <= hi; ++i) acc += sa[w][i] * sb[w][idx - i];
+      sp[w][idx] = acc;
+    }
+    __syncwarp();
+    reduce_poly_warp<D>(sp[w], st[w], lowterms, out + row * D, mask, lane, nullptr);
+  }
+}
+
+__global__ void gr_scale_rows_kernel(const u64* __restrict__ s, int64_t s_stride, const u64* __restrict__ g,
+                                     int64_t g_rs, u64* __restrict__ out, int64_t rows, int d, u64 mask) {
+  const int64_t total = rows * d;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    int64_t r = i / d;
+    int k = int(i - r * d);
+    out[i] = (s[r * s_stride] * g[r * g_rs + k]) & mask;
+  }
+}
+
+// M row j = x^j * c mod f  (one block, D threads, D sequential shifts)
+__global__ void gr_mulmat_kernel(const u64* __restrict__ c, int d, u64 lowterms, u64* __restrict__ M) {
+  __shared__ u64 row[64];
+  const int k = threadIdx.x;
+  if (k < d) row[k] = c[k];
+  __syncthreads();
+  for (int j = 0; j < d; ++j) {
+    u64 cur = k < d ? row[k] : 0;
+    if (k < d) M[j * d + k] = cur;
+    u64 top = row[d - 1];
+    u64 prev = (k >= 1 && k < d) ? row[k - 1] : 0;
+    __syncthreads();
+    if (k < d) {
+      u64 nv = prev;
+      if ((lowterms >> k) & 1ull) nv -= top;
+      row[k] = nv;
+    }
+    __syncthreads();
+  }
+}
+
+// out[i] = A_i . M (+ C_i): 256 threads, 4x4 register tiles, whole M in smem.
+template <int D>
+__global__ void __launch_bounds__(256)
+gr_matmul_kernel(LinOperand A, const u64* __restrict__ M, int has_c, LinOperand C, u64* __restrict__ out,
+                 int64_t rows, u64 mask) {
+  constexpr int CG = D / 4;          // column groups of 4
+  constexpr int RG = 256 / CG;       // row groups of 4
+  constexpr int BM = RG * 4;
+  extern __shared__ __align__(16) u64 smem[];
+  u64* sM = smem;                    // D*D
+  u64* sA = smem + D * D;            // BM*D
+  for (int i = threadIdx.x; i < D * D; i += 256) sM[i] = M[i];
+  const int tx = threadIdx.x % CG, ty = threadIdx.x / CG;
+  for (int64_t r0 = blockIdx.x * int64_t(BM); r0 < rows; r0 += int64_t(gridDim.x) * BM) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < BM * D; i += 256) {
+      int r = i / D, k = i % D;
+      int64_t row = r0 + r;
+      sA[i] = row < rows ? lin_load(A, row, k) : 0ull;
+    }
+    __syncthreads();
+    u64 acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0;
+#pragma unroll 4
+    for (int k = 0; k < D; ++k) {
+      u64 av[4], mv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sA[(ty * 4 + a) * D + k];
+      ulonglong2 m01 = *reinterpret_cast<const ulonglong2*>(&sM[k * D + tx * 4]);
+      ulonglong2 m23 = *reinterpret_cast<const ulonglong2*>(&sM[k * D + tx * 4 + 2]);
+      mv[0] = m01.x; mv[1] = m01.y; mv[2] = m23.x; mv[3] = m23.y;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * mv[b];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      int64_t row = r0 + ty * 4 + a;
+      if (row >= rows) continue;
+      u64 v[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        v[b] = acc[a][b];
+        if (has_c) v[b] += lin_load(C, row, tx * 4 + b);
+        v[b] &= mask;
+      }
+      u64* o = out + row * D + tx * 4;
+      reinterpret_cast<ulonglong2*>(o)[0] = make_ulonglong2(v[0], v[1]);
+      reinterpret_cast<ulonglong2*>(o)[1] = make_ulonglong2(v[2], v[3]);
+    }
+  }
+}
+
+// acc[0..2D-2] += sum_i F_i (x) G_i.  Each thread owns a 4x4 tile of the
+// D x D outer-product sum; 256/(D/4)^2 thread groups split the rows.
+template <int D>
+__global__ void __launch_bounds__(256)
+gr_dotsum_kernel(LinOperand F, LinOperand G, int64_t rows, int64_t rows_per_block, u64* __restrict__ acc) {
+  constexpr int CG = D / 4;
+  constexpr int TILES = CG * CG;
+  constexpr int GROUPS = 256 / TILES;
+  constexpr int BK = 32;
+  __shared__ __align__(16) u64 sF[BK * D], sG[BK * D];
+  __shared__ u64 sP[2 * D];
+  const int grp = threadIdx.x / TILES;
+  const int tile = threadIdx.x % TILES;
+  const int ta = tile / CG, tb = tile % CG;
+  for (int i = threadIdx.x; i < 2 * D; i += 256) sP[i] = 0;
+  u64 s[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) s[a][b] = 0;
+  const int64_t r_begin = blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += BK) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < BK * D; i += 256) {
+      int r = i / D, k = i % D;
+      int64_t row = r0 + r;
+      bool ok = row < r_end;
+      sF[i] = ok ? lin_load(F, row, k) : 0ull;
+      sG[i] = ok ? lin_load(G, row, k) : 0ull;
+    }
+    __syncthreads();
+    for (int r = grp; r < BK; r += GROUPS) {
+      ulonglong2 f01 = *reinterpret_cast<const ulonglong2*>(&sF[r * D + ta * 4]);
+      ulonglong2 f23 = *reinterpret_cast<const ulonglong2*>(&sF[r * D + ta * 4 + 2]);
+      ulonglong2 g01 = *reinterpret_cast<const ulonglong2*>(&sG[r * D + tb * 4]);
+      ulonglong2 g23 = *reinterpret_cast<const ulonglong2*>(&sG[r * D + tb * 4 + 2]);
+      u64 fv[4] = {f01.x, f01.y, f23.x, f23.y};
+      u64 gv[4] = {g01.x, g01.y, g23.x, g23.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] += fv[a] * gv[b];
+    }
+  }
+  __syncthreads();
+  // fold the tile along anti-diagonals: coefficient (ta*4+a) + (tb*4+b)
+  u64 diag[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) diag[q] = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) diag[a + b] += s[a][b];
+  const int base = ta * 4 + tb * 4;
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+    if (base + q < 2 * D - 1 && diag[q]) atomicAdd(&sP[base + q], diag[q]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * D - 1; i += 256)
+    if (sP[i]) atomicAdd(acc + i, sP[i]);
+}
+
+// small-degree fallback (D in {1,2,4}): thread per row, full product in regs
+template <int D>
+__global__ void gr_dotsum_small_kernel(LinOperand F, LinOperand G, int64_t rows, u64* __restrict__ acc) {
+  u64 p[2 * D - 1];
+#pragma unroll
+  for (int q = 0; q < 2 * D - 1; ++q) p[q] = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; row < rows; row += stride) {
+    u64 f[D], g[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      f[k] = lin_load(F, row, k);
+      g[k] = lin_load(G, row, k);
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) p[a + b] += f[a] * g[b];
+  }
+#pragma unroll
+  for (int q = 0; q < 2 * D - 1; ++q) {
+    u64 v = p[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(acc + q, v);
+  }
+}
+
+template <int D>
+__global__ void reduce_poly_kernel(const u64* __restrict__ acc, u64 lowterms, u64* __restrict__ out, u64 mask,
+                                   int accumulate) {
+  __shared__ u64 sp[2 * D], st[2 * D + 8], sadd[D];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < 2 * D; i += 32) sp[i] = i < 2 * D - 1 ? acc[i] : 0;
+  for (int i = lane; i < D; i += 32) sadd[i] = accumulate ? out[i] : 0;
+  __syncwarp();
+  reduce_poly_warp<D>(sp, st, lowterms, out, mask, lane, sadd);
+}
+
+// ---------------------------------------------------------------------------
+// fused verification stages over compressed operands
+// ---------------------------------------------------------------------------
+struct CompPtrs {
+  const u64* p[8];
+};
+struct OutPtrs {
+  u64* p[8];
+};
+
+__device__ __forceinline__ int64_t comp_off(int64_t i, int64_t n, int64_t ks, int64_t ls) {
+  int64_t l = i / n;
+  return (i - l * n) * ks + l * ls;
+}
+
+// out[c][k] += sum_l comps[c][l*stride] * pw[l][k]
+template <int D>
+__global__ void __launch_bounds__(256)
+powsum_kernel(int ncomp, CompPtrs comps, int64_t stride, int64_t lanes, const u64* __restrict__ pw,
+              u64* __restrict__ out) {
+  constexpr int RP = 256 / D;  // rows in parallel
+  __shared__ u64 red[8][256];
+  const int k = threadIdx.x % D, rp = threadIdx.x / D;
+  u64 acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0;
+  for (int64_t l = blockIdx.x * int64_t(RP) + rp; l < lanes; l += int64_t(gridDim.x) * RP) {
+    u64 w = __ldg(pw + l * D + k);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < ncomp) acc[c] += __ldg(comps.p[c] + l * stride) * w;
+  }
+  for (int c = 0; c < ncomp; ++c) red[c][threadIdx.x] = acc[c];
+  __syncthreads();
+  if (rp == 0) {
+    for (int c = 0; c < ncomp; ++c) {
+      u64 v = 0;
+      for (int q = 0; q < RP; ++q) v += red[c][q * D + k];
+      atomicAdd(out + c * D + k, v);
+    }
+  }
+}
+
+// h(1)/h(2) folds at level 1 (see r3b200.h).  Terms: coef[t] * fold(x_t, y_t).
+template <int D>
+__global__ void __launch_bounds__(256)
+l1_fold_kernel(int nterms, const int64_t* __restrict__ coef_dev, CompPtrs xc, CompPtrs yc, int64_t N,
+               int64_t n, int64_t ks, int64_t ls, const u64* __restrict__ pw, u64* __restrict__ out_h1,
+               u64* __restrict__ out_h2, int64_t coef0, int64_t coef1, int64_t coef2, int64_t coef3) {
+  constexpr int RP = 256 / D;
+  __shared__ u64 red1[256], red2[256];
+  const int k = threadIdx.x % D, rp = threadIdx.x / D;
+  const int64_t coefs[4] = {coef0, coef1, coef2, coef3};
+  const int64_t npairs = (N + 1) / 2;
+  u64 h1 = 0, h2 = 0;
+  for (int64_t j = blockIdx.x * int64_t(RP) + rp; j < npairs; j += int64_t(gridDim.x) * RP) {
+    const int64_t i0 = 2 * j, i1 = 2 * j + 1;
+    const bool has1 = i1 < N;
+    const int64_t o0 = comp_off(i0, n, ks, ls);
+    const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
+    u64 c1 = 0, c2o = 0, c2e = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (t < nterms) {
+        const u64 cf = u64(coefs[t]);
+        const u64 x0 = __ldg(xc.p[t] + o0), y0 = __ldg(yc.p[t] + o0);
+        const u64 x1 = has1 ? __ldg(xc.p[t] + o1) : 0ull, y1 = has1 ? __ldg(yc.p[t] + o1) : 0ull;
+        const u64 g2 = 2 * y1 - y0;
+        c1 += cf * (x1 * y1);
+        c2o += cf * (2 * x1 * g2);
+        c2e -= cf * (x0 * g2);
+      }
+    }
+    const u64 w0 = __ldg(pw + (i0 / n) * D + k);
+    const u64 w1 = has1 ? __ldg(pw + (i1 / n) * D + k) : 0ull;
+    h1 += c1 * w1;
+    h2 += c2o * w1 + c2e * w0;
+  }
+  red1[threadIdx.x] = h1;
+  red2[threadIdx.x] = h2;
+  __syncthreads();
+  if (rp == 0) {
+    u64 v1 = 0, v2 = 0;
+    for (int q = 0; q < RP; ++q) {
+      v1 += red1[q * D + k];
+      v2 += red2[q * D + k];
+    }
+    atomicAdd(out_h1 + k, v1);
+    atomicAdd(out_h2 + k, v2);
+  }
+}
+
+template <int D>
+__global__ void l1_line_x_kernel(int ncomp, CompPtrs xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                                 const u64* __restrict__ A, const u64* __restrict__ B, int64_t tq, OutPtrs out,
+                                 u64 mask) {
+  const int64_t npairs = (N + 1) / 2;
+  const int64_t total = npairs * D;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += stride) {
+    const int64_t j = e / D;
+    const int k = int(e - j * D);
+    const int64_t i0 = 2 * j, i1 = 2 * j + 1;
+    const bool has1 = i1 < N;
+    const u64 a = __ldg(A + (i0 / tq) * D + k);
+    const u64 b = has1 ? __ldg(B + (i1 / tq) * D + k) : 0ull;
+    const int64_t o0 = comp_off(i0, n, ks, ls);
+    const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
+    for (int c = 0; c < ncomp; ++c) {
+      u64 x0 = __ldg(xc.p[c] + o0);
+      u64 x1 = has1 ? __ldg(xc.p[c] + o1) : 0ull;
+      out.p[c][e] = (x0 * a + x1 * b) & mask;
+    }
+  }
+}
+
+template <int D>
+__global__ void l1_line_y_kernel(int ncomp, CompPtrs yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                                 const u64* __restrict__ a, const u64* __restrict__ b, OutPtrs out, u64 mask) {
+  const int64_t npairs = (N + 1) / 2;
+  const int64_t total = npairs * D;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += stride) {
+    const int64_t j = e / D;
+    const int k = int(e - j * D);
+    const int64_t i0 = 2 * j, i1 = 2 * j + 1;
+    const bool has1 = i1 < N;
+    const u64 av = a[k], bv = b[k];
+    const int64_t o0 = comp_off(i0, n, ks, ls);
+    const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
+    for (int c = 0; c < ncomp; ++c) {
+      u64 y0 = __ldg(yc.p[c] + o0);
+      u64 y1 = has1 ? __ldg(yc.p[c] + o1) : 0ull;
+      out.p[c][e] = (y0 * av + y1 * bv) & mask;
+    }
+  }
+}
+
+__global__ void mask_rows_kernel(u64* out, int64_t n, u64 mask) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] &= mask;
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+static bool valid_d(int d) { return d == 1 || d == 2 || d == 4 || d == 8 || d == 16 || d == 32 || d == 64; }
+
+#define R3_DISPATCH_D(d, KERNEL_CALL)           \
+  switch (d) {                                  \
+    case 1: { constexpr int D = 1; KERNEL_CALL; } break;   \
+    case 2: { constexpr int D = 2; KERNEL_CALL; } break;   \
+    case 4: { constexpr int D = 4; KERNEL_CALL; } break;   \
+    case 8: { constexpr int D = 8; KERNEL_CALL; } break;   \
+    case 16: { constexpr int D = 16; KERNEL_CALL; } break; \
+    case 32: { constexpr int D = 32; KERNEL_CALL; } break; \
+    case 64: { constexpr int D = 64; KERNEL_CALL; } break; \
+  }
+
+static LinOperand to_lin(const r3_lin_operand& o) {
+  LinOperand l;
+  for (int q = 0; q < 4; ++q) {
+    l.p[q] = reinterpret_cast<const u64*>(o.p[q]);
+    l.rowstride[q] = o.rowstride[q];
+    l.nvalid[q] = o.nvalid[q];
+    l.coef[q] = o.coef[q];
+  }
+  l.nterms = o.nterms;
+  return l;
+}
+
+extern "C" int r3_gr_mul(const uint64_t* a, int64_t a_rs, const uint64_t* b, int64_t b_rs, uint64_t* out,
+                         int64_t rows, int d, uint64_t lowterms, uint64_t mask, void* stream) {
+  if (!valid_d(d) || rows < 0) {
+    set_error("r3_gr_mul: unsupported degree %d", d);
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  unsigned grid = grid_for(rows, 4, 16);
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (gr_mul_kernel<D><<<grid, 128, 0, s>>>((const u64*)a, a_rs, (const u64*)b, b_rs, (u64*)out,
+                                                          rows, lowterms, mask)));
+  return check_launch("r3_gr_mul");
+}
+
+extern "C" int r3_gr_scale_rows(const uint64_t* s, int64_t s_stride, const uint64_t* g, int64_t g_rs,
+                                uint64_t* out, int64_t rows, int d, uint64_t mask, void* stream) {
+  if (d < 1 || d > 64 || rows < 0) {
+    set_error("r3_gr_scale_rows: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  gr_scale_rows_kernel<<<grid_for(rows * d, 256), 256, 0, as_stream(stream)>>>(
+      (const u64*)s, s_stride, (const u64*)g, g_rs, (u64*)out, rows, d, mask);
+  return check_launch("r3_gr_scale_rows");
+}
+
+extern "C" int r3_gr_mulmat(const uint64_t* c, int d, uint64_t lowterms, uint64_t* M, void* stream) {
+  if (!valid_d(d)) {
+    set_error("r3_gr_mulmat: unsupported degree %d", d);
+    return R3_ERR_ARG;
+  }
+  gr_mulmat_kernel<<<1, 64, 0, as_stream(stream)>>>((const u64*)c, d, lowterms, (u64*)M);
+  return check_launch("r3_gr_mulmat");
+}
+
+extern "C" int r3_gr_matmul(r3_lin_operand A, const uint64_t* M, int has_c, r3_lin_operand C, uint64_t* out,
+                            int64_t rows, int d, uint64_t mask, void* stream) {
+  if (!(d == 8 || d == 16 || d == 32 || d == 64) || rows < 0 || A.nterms < 1 || A.nterms > 4) {
+    set_error("r3_gr_matmul: unsupported degree %d / operand", d);
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  cudaStream_t s = as_stream(stream);
+  LinOperand la = to_lin(A), lc = to_lin(C);
+  switch (d) {
+#define R3_MM(DD)                                                                              \
+  case DD: {                                                                                   \
+    constexpr int CG = DD / 4, RG = 256 / CG, BM = RG * 4;                                     \
+    size_t smem = size_t(DD * DD + BM * DD) * 8;                                               \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(gr_matmul_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           int(smem));                                                         \
+      attr = true;                                                                             \
+    }                                                                                          \
+    unsigned grid = grid_for((rows + BM - 1) / BM, 1, 3);                                      \
+    gr_matmul_kernel<DD><<<grid, 256, smem, s>>>(la, (const u64*)M, has_c, lc, (u64*)out, rows, \
+                                                 mask);                                        \
+  } break;
+    R3_MM(8)
+    R3_MM(16)
+    R3_MM(32)
+    R3_MM(64)
+#undef R3_MM
+  }
+  return check_launch("r3_gr_matmul");
+}
+
+extern "C" int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, int d, uint64_t* acc,
+                            void* stream) {
+  if (!valid_d(d) || rows < 0 || F.nterms < 1 || G.nterms < 1) {
+    set_error("r3_gr_dotsum: bad arguments (d=%d)", d);
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  cudaStream_t s = as_stream(stream);
+  LinOperand lf = to_lin(F), lg = to_lin(G);
+  if (d <= 4) {
+    unsigned grid = grid_for(rows, 256, 4);
+    if (d == 1) gr_dotsum_small_kernel<1><<<grid, 256, 0, s>>>(lf, lg, rows, (u64*)acc);
+    if (d == 2) gr_dotsum_small_kernel<2><<<grid, 256, 0, s>>>(lf, lg, rows, (u64*)acc);
+    if (d == 4) gr_dotsum_small_kernel<4><<<grid, 256, 0, s>>>(lf, lg, rows, (u64*)acc);
+    return check_launch("r3_gr_dotsum(small)");
+  }
+  int64_t blocks = int64_t(kNumSMs) * 4;
+  int64_t per = (rows + blocks - 1) / blocks;
+  if (per < 64) per = 64;
+  per = (per + 31) / 32 * 32;
+  blocks = (rows + per - 1) / per;
+  switch (d) {
+    case 8: gr_dotsum_kernel<8><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
+    case 16: gr_dotsum_kernel<16><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
+    case 32: gr_dotsum_kernel<32><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
+    case 64: gr_dotsum_kernel<64><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
+  }
+  return check_launch("r3_gr_dotsum");
+}
+
+extern "C" int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms, uint64_t* out, uint64_t mask,
+                                 int accumulate, void* stream) {
+  if (!valid_d(d)) {
+    set_error("r3_gr_reduce_poly: unsupported degree %d", d);
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (reduce_poly_kernel<D><<<1, 32, 0, s>>>((const u64*)acc, lowterms, (u64*)out, mask,
+                                                           accumulate)));
+  return check_launch("r3_gr_reduce_poly");
+}
+
+static int finish_mask(u64* out, int64_t n, uint64_t mask, cudaStream_t s) {
+  if (mask == ~0ull) return R3_OK;
+  mask_rows_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n, mask);
+  return check_launch("mask");
+}
+
+extern "C" int r3_vfy_powsum(int ncomp, const uint64_t* const* comps, int64_t stride, int64_t lanes,
+                             const uint64_t* pw, int d, uint64_t* out, uint64_t mask, void* stream) {
+  if (ncomp < 1 || ncomp > 8 || !valid_d(d) || lanes < 0) {
+    set_error("r3_vfy_powsum: bad arguments");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(out, 0, size_t(ncomp) * d * 8, s);
+  if (e != cudaSuccess) {
+    set_error("r3_vfy_powsum: memset: %s", cudaGetErrorString(e));
+    return R3_ERR_CUDA;
+  }
+  if (lanes == 0) return R3_OK;
+  CompPtrs cp{};
+  for (int c = 0; c < ncomp; ++c) cp.p[c] = reinterpret_cast<const u64*>(comps[c]);
+  R3_DISPATCH_D(d, ({
+                  constexpr int RP = 256 / D;
+                  unsigned grid = grid_for((lanes + RP - 1) / RP, 1, 4);
+                  powsum_kernel<D><<<grid, 256, 0, s>>>(ncomp, cp, stride, lanes, (const u64*)pw, (u64*)out);
+                }));
+  int rc = check_launch("r3_vfy_powsum");
+  if (rc) return rc;
+  return finish_mask((u64*)out, int64_t(ncomp) * d, mask, s);
+}
+
+extern "C" int r3_vfy_l1_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                              const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                              const uint64_t* pw, int d, uint64_t* out_h1, uint64_t* out_h2, uint64_t mask,
+                              void* stream) {
+  if (nterms < 1 || nterms > 4 || !valid_d(d) || N < 0 || n < 1) {
+    set_error("r3_vfy_l1_fold: bad arguments");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(out_h1, 0, size_t(d) * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(out_h2, 0, size_t(d) * 8, s) != cudaSuccess) {
+    set_error("r3_vfy_l1_fold: memset failed");
+    return R3_ERR_CUDA;
+  }
+  if (N == 0) return R3_OK;
+  CompPtrs xp{}, yp{};
+  int64_t cf[4] = {0, 0, 0, 0};
+  for (int t = 0; t < nterms; ++t) {
+    xp.p[t] = reinterpret_cast<const u64*>(xc[t]);
+    yp.p[t] = reinterpret_cast<const u64*>(yc[t]);
+    cf[t] = coef[t];
+  }
+  const int64_t npairs = (N + 1) / 2;
+  R3_DISPATCH_D(d, ({
+                  constexpr int RP = 256 / D;
+                  unsigned grid = grid_for((npairs + RP - 1) / RP, 1, 4);
+                  l1_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, nullptr, xp, yp, N, n, ks, ls, (const u64*)pw,
+                                                         (u64*)out_h1, (u64*)out_h2, cf[0], cf[1], cf[2], cf[3]);
+                }));
+  int rc = check_launch("r3_vfy_l1_fold");
+  if (rc) return rc;
+  rc = finish_mask((u64*)out_h1, d, mask, s);
+  if (rc) return rc;
+  return finish_mask((u64*)out_h2, d, mask, s);
+}
+
+extern "C" int r3_vfy_l1_line_x(int ncomp, const uint64_t* const* xc, int64_t N, int64_t n, int64_t ks,
+                                int64_t ls, const uint64_t* A, const uint64_t* B, int64_t tq, int d,
+                                uint64_t* const* out, uint64_t mask, void* stream) {
+  if (ncomp < 1 || ncomp > 8 || !valid_d(d) || N < 0 || n < 1 || tq < 1) {
+    set_error("r3_vfy_l1_line_x: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  CompPtrs xp{};
+  OutPtrs op{};
+  for (int c = 0; c < ncomp; ++c) {
+    xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  const int64_t total = (N + 1) / 2 * d;
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (l1_line_x_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
+                       ncomp, xp, N, n, ks, ls, (const u64*)A, (const u64*)B, tq, op, mask)));
+  return check_launch("r3_vfy_l1_line_x");
+}
+
+extern "C" int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
+                                int64_t ls, const uint64_t* a, const uint64_t* b, int d, uint64_t* const* out,
+                                uint64_t mask, void* stream) {
+  if (ncomp < 1 || ncomp > 8 || !valid_d(d) || N < 0 || n < 1) {
+    set_error("r3_vfy_l1_line_y: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  CompPtrs yp{};
+  OutPtrs op{};
+  for (int c = 0; c < ncomp; ++c) {
+    yp.p[c] = reinterpret_cast<const u64*>(yc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  const int64_t total = (N + 1) / 2 * d;
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (l1_line_y_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
+                       ncomp, yp, N, n, ks, ls, (const u64*)a, (const u64*)b, op, mask)));
+  return check_launch("r3_vfy_l1_line_y");
+}

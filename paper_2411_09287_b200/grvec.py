@@ -1,0 +1,387 @@
+"""uint64 / GR(2^ell, d) array kernels on B200 device tensors.
+
+Drop-in for the reference `ring3pc.grvec` (grvec.py:1-167).  Arrays are
+`torch.int64` CUDA tensors carrying uint64 bit patterns: base-ring vectors
+(n,) and extension vectors (n, d) with the constant coefficient in column 0
+(the reference layout).  Every function launches the hand-written sm_100a
+kernels of libr3b200.so (include/r3b200.h); torch is only the allocator,
+view/reshape machinery and stream carrier.  `host()` converts to numpy
+uint64 for comparison with the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import LinOperand, as_i64, call, empty, ptr, stream, to_device, zeros
+from .rings import GrModulus, ring_mask
+
+U64 = np.uint64
+
+ADD, SUB, MUL, AND, XOR, OR, RSUB, COPY = range(8)
+
+# rows at which "many elements times one element" switches from the generic
+# per-row kernel to the matrix form rows . M_c (tensor-shaped GEMM)
+_MATMUL_MIN_ROWS = 64
+
+
+def umask(width: int) -> np.uint64:
+    return U64(ring_mask(width))
+
+
+def u64(value: int) -> np.uint64:
+    return U64(value & ring_mask(64))
+
+
+def host(t) -> np.ndarray:
+    return _lib.to_host(t)
+
+
+def dev(x) -> torch.Tensor:
+    return to_device(x)
+
+
+def base_from_ints(values, width: int) -> torch.Tensor:
+    m = ring_mask(width)
+    return to_device(np.array([int(v) & m for v in values], dtype=np.uint64))
+
+
+def as_gr_rows(rows) -> torch.Tensor:
+    return to_device(np.array([[int(c) & ((1 << 64) - 1) for c in r] for r in rows],
+                              dtype=np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# elementwise
+# ---------------------------------------------------------------------------
+
+def _is_scalar(x) -> bool:
+    return not isinstance(x, torch.Tensor) and np.ndim(x) == 0
+
+
+def _scalar(x) -> int:
+    return int(x) & ((1 << 64) - 1)
+
+
+def ew(op: int, a, b, mask: int) -> torch.Tensor:
+    """out = op(a, b) & mask with numpy-style broadcasting (<= 4 dims)."""
+    if _is_scalar(a) and not _is_scalar(b):
+        inv = {ADD: ADD, MUL: MUL, AND: AND, XOR: XOR, OR: OR, SUB: RSUB}
+        return ew(inv[op], b, a, mask)
+    if not isinstance(a, torch.Tensor):
+        a = to_device(a)
+    if b is not None and not _is_scalar(b) and not isinstance(b, torch.Tensor):
+        b = to_device(b)
+    if b is None or _is_scalar(b):
+        imm = 0 if b is None else _scalar(b)
+        shape = tuple(a.shape)
+        av = a
+        bv = None
+    else:
+        shape = tuple(torch.broadcast_shapes(a.shape, b.shape))
+        av = a.expand(shape)
+        bv = b.expand(shape)
+        imm = 0
+    if len(shape) > 4:
+        raise ValueError(f"elementwise kernels take <= 4 dims, got {shape}")
+    out = empty(shape)
+    nd = len(shape)
+    shp = (C.c_int64 * 4)(*shape, *([0] * (4 - nd)))
+    ast = (C.c_int64 * 4)(*av.stride(), *([0] * (4 - nd)))
+    bst = (C.c_int64 * 4)(*(bv.stride() if bv is not None else [0] * nd), *([0] * (4 - nd)))
+    call("r3_ew", op if bv is not None or b is not None else COPY, nd, shp, ptr(out), ptr(av),
+         ast, ptr(bv), bst, imm, mask & ((1 << 64) - 1), stream())
+    return out
+
+
+def add(a, b, width: int = 64):
+    return ew(ADD, a, b, ring_mask(width))
+
+
+def sub(a, b, width: int = 64):
+    return ew(SUB, a, b, ring_mask(width))
+
+
+def mul(a, b, width: int = 64):
+    return ew(MUL, a, b, ring_mask(width))
+
+
+def vmask(a, width: int):
+    if width == 64:
+        return a
+    return ew(AND, a, ring_mask(width), ring_mask(64))
+
+
+def vneg(a, width: int):
+    return ew(RSUB, a, 0, ring_mask(width))
+
+
+def vscale(a, c: int, width: int):
+    return ew(MUL, a, _scalar(c), ring_mask(width))
+
+
+def arith_rshift(a, t: int, width: int):
+    """Arithmetic right shift of width-bit two's-complement patterns."""
+    if t == 0:
+        return ew(COPY, a, None, ring_mask(64))
+    if not 0 < t < width:
+        raise ValueError(f"shift {t} out of range for width {width}")
+    src = a.contiguous()
+    out = empty(src.shape)
+    call("r3_ars", ptr(src), src.numel(), t, width, ptr(out), stream())
+    return out
+
+
+def to_signed(a, width: int):
+    """Signed interpretation as host int64 (the reference returns int64)."""
+    h = host(a).astype(np.int64) if width == 64 else host(a)
+    if width == 64:
+        return h
+    half = 1 << (width - 1)
+    v = h.astype(np.int64)
+    return np.where(h >= half, v - (1 << width), v)
+
+
+def bit_planes(a, nbits: int) -> torch.Tensor:
+    """(nbits, lanes) of (a >> j) & 1 (nonlinear.py:273)."""
+    src = a.contiguous()
+    out = empty((nbits, src.shape[0]))
+    call("r3_bit_planes", ptr(src), src.shape[0], nbits, ptr(out), stream())
+    return out
+
+
+def count_nonequal(a, b=None) -> torch.Tensor:
+    """Device scalar #{a != b} (b None: #{a != 0})."""
+    a = a.contiguous()
+    cnt = zeros((1,))
+    if b is not None:
+        b = b.contiguous()
+        if b.shape != a.shape:
+            cnt.fill_(1)
+            return cnt
+    call("r3_count_nonequal", ptr(a), ptr(b), a.numel(), ptr(cnt), stream())
+    return cnt
+
+
+def sum_axis0(a: torch.Tensor, width: int, keepdims: bool = False) -> torch.Tensor:
+    """np.add.reduce(a, axis=0) masked to width bits."""
+    if a.dim() == 0:
+        raise ValueError("sum over a scalar")
+    n = a.shape[0]
+    rest = tuple(a.shape[1:])
+    inner = int(np.prod(rest)) if rest else 1
+    src = a.reshape(n, inner)
+    if inner > 1 and src.stride(1) != 1:
+        src = src.contiguous()
+    rs = src.stride(0) if n > 1 else inner
+    out = empty((inner,))
+    call("r3_sum_axis0", ptr(src), n, inner, rs, ptr(out), ring_mask(width), 0, stream())
+    shape = ((1,) if keepdims else ()) + rest
+    return out.reshape(shape)
+
+
+# ---------------------------------------------------------------------------
+# GR(2^ell, d)
+# ---------------------------------------------------------------------------
+
+def gr_embed(base, mod: GrModulus) -> torch.Tensor:
+    """(n,) base values -> (n, d), constant coefficient set."""
+    base = base if isinstance(base, torch.Tensor) else to_device(base)
+    out = zeros(tuple(base.shape) + (mod.degree,))
+    out[..., 0] = base
+    return out
+
+
+def gr_const(value: int, mod: GrModulus, width: int) -> torch.Tensor:
+    out = zeros((1, mod.degree))
+    out[0, 0] = as_i64(value & ring_mask(width))
+    return out
+
+
+def lin(*terms, nvalid=None) -> LinOperand:
+    """LinOperand from (coef, tensor2d) pairs; each tensor (rows, d) with
+    unit coefficient stride (row stride may be anything, 0 = broadcast)."""
+    op = LinOperand()
+    op.nterms = len(terms)
+    for q, (coef, t) in enumerate(terms):
+        if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+            raise ValueError("lin operand wants (rows, d) with contiguous coefficients")
+        op.p[q] = ptr(t)
+        op.rowstride[q] = t.stride(0) if t.shape[0] > 1 else 0
+        op.nvalid[q] = (1 << 62) if (nvalid is None or nvalid[q] is None) else nvalid[q]
+        op.coef[q] = _scalar(coef)
+    for q in range(len(terms), 4):
+        op.p[q] = None
+        op.rowstride[q] = 0
+        op.nvalid[q] = 0
+        op.coef[q] = 0
+    return op
+
+
+def _rows2d(t: torch.Tensor, d: int) -> torch.Tensor:
+    if t.dim() != 2 or t.shape[-1] != d:
+        raise ValueError("coefficient count does not match modulus degree")
+    if d > 1 and t.stride(1) != 1:
+        t = t.contiguous()
+    return t
+
+
+def gr_mulmat(c: torch.Tensor, mod: GrModulus) -> torch.Tensor:
+    """(d, d) matrix M with (a * c) = a . M."""
+    d = mod.degree
+    c = c.reshape(-1, d)[0].contiguous()
+    M = empty((d, d))
+    call("r3_gr_mulmat", ptr(c), d, mod.lowterms_mask, ptr(M), stream())
+    return M
+
+
+def gr_matmul(A: LinOperand, M: torch.Tensor, rows: int, d: int, width: int,
+              C_add: LinOperand | None = None, out: torch.Tensor | None = None):
+    if out is None:
+        out = empty((rows, d))
+    call("r3_gr_matmul", A, ptr(M), 1 if C_add is not None else 0,
+         C_add if C_add is not None else LinOperand(), ptr(out), rows, d, ring_mask(width),
+         stream())
+    return out
+
+
+def gr_mul(a, b, width: int, mod: GrModulus) -> torch.Tensor:
+    """Product in GR(2^width, d) mod f, rows broadcast on axis 0."""
+    d = mod.degree
+    a = a if isinstance(a, torch.Tensor) else to_device(a)
+    b = b if isinstance(b, torch.Tensor) else to_device(b)
+    if a.shape[-1] != d or b.shape[-1] != d:
+        raise ValueError("coefficient count does not match modulus degree")
+    if d == 1:
+        return ew(MUL, a, b, ring_mask(width))
+    a, b = _rows2d(a, d), _rows2d(b, d)
+    n = max(a.shape[0], b.shape[0])
+    if a.shape[0] not in (1, n) or b.shape[0] not in (1, n):
+        raise ValueError(f"cannot broadcast {tuple(a.shape)} with {tuple(b.shape)}")
+    a_one = a.shape[0] == 1 or a.stride(0) == 0
+    b_one = b.shape[0] == 1 or b.stride(0) == 0
+    if d >= 8 and n >= _MATMUL_MIN_ROWS and a_one != b_one:
+        one, many = (a, b) if a_one else (b, a)
+        M = gr_mulmat(one[:1], mod)
+        return gr_matmul(lin((1, many)), M, n, d, width)
+    out = empty((n, d))
+    a_rs = 0 if a_one else a.stride(0)
+    b_rs = 0 if b_one else b.stride(0)
+    call("r3_gr_mul", ptr(a), a_rs, ptr(b), b_rs, ptr(out), n, d, mod.lowterms_mask,
+         ring_mask(width), stream())
+    return out
+
+
+def gr_scale_rows(s: torch.Tensor, g: torch.Tensor, width: int) -> torch.Tensor:
+    """out[i] = s[i] * g[i] for base scalars s (n,) and GR rows g (n|1, d)."""
+    d = g.shape[-1]
+    g = _rows2d(g, d)
+    n = max(s.shape[0], g.shape[0])
+    out = empty((n, d))
+    s_st = 0 if s.shape[0] == 1 else s.stride(0)
+    g_rs = 0 if g.shape[0] == 1 else g.stride(0)
+    call("r3_gr_scale_rows", ptr(s), s_st, ptr(g), g_rs, ptr(out), n, d, ring_mask(width),
+         stream())
+    return out
+
+
+def _mul_gf2_packed(a, b, mod):  # pragma: no cover - parity alias
+    return gr_mul(a, b, 1, mod)
+
+
+def gr_scale_base(a, c, width: int):
+    """Coefficient-wise product with base scalars c of shape (n,) or ()."""
+    if _is_scalar(c):
+        return ew(MUL, a, _scalar(c), ring_mask(width))
+    c = c if isinstance(c, torch.Tensor) else to_device(c)
+    return ew(MUL, a, c[..., None], ring_mask(width))
+
+
+def dotsum_acc(d: int) -> torch.Tensor:
+    return zeros((2 * d - 1,))
+
+
+def dotsum_add(acc: torch.Tensor, F: LinOperand, G: LinOperand, rows: int, d: int) -> None:
+    call("r3_gr_dotsum", F, G, rows, d, ptr(acc), stream())
+
+
+def reduce_poly(acc: torch.Tensor, mod: GrModulus, width: int, out: torch.Tensor | None = None,
+                accumulate: bool = False) -> torch.Tensor:
+    d = mod.degree
+    if out is None:
+        out = empty((1, d))
+    call("r3_gr_reduce_poly", ptr(acc), d, mod.lowterms_mask, ptr(out), ring_mask(width),
+         1 if accumulate else 0, stream())
+    return out
+
+
+def gr_dot(a, b, width: int, mod: GrModulus) -> torch.Tensor:
+    """Sum of pairwise products, shape (1, d)."""
+    d = mod.degree
+    a, b = _rows2d(a, d), _rows2d(b, d)
+    n = max(a.shape[0], b.shape[0])
+    acc = dotsum_acc(d)
+    dotsum_add(acc, lin((1, a)), lin((1, b)), n, d)
+    return reduce_poly(acc, mod, width)
+
+
+def gr_powers(r, n: int, width: int, mod: GrModulus) -> torch.Tensor:
+    """(n, d) array r^0 .. r^(n-1) by block doubling (grvec.py:130-141):
+    each doubling round is one rows . M_step matrix product."""
+    d = mod.degree
+    r = r.reshape(1, d)
+    out = zeros((n, d))
+    if n == 0:
+        return out
+    out[0, 0] = 1
+    filled = 1
+    while filled < n:
+        take = min(filled, n - filled)
+        step = gr_mul(out[filled - 1:filled], r, width, mod)
+        if d >= 8:
+            M = gr_mulmat(step, mod)
+            gr_matmul(lin((1, out[:take])), M, take, d, width, out=out[filled:filled + take])
+        else:
+            out[filled:filled + take] = gr_mul(out[:take], step, width, mod)
+        filled += take
+    return out
+
+
+def gr_line_eval(p0, p1, z, width: int, mod: GrModulus):
+    """z*p1 - (z-1)*p0, rows of p0/p1; z shaped (1, d)."""
+    one = gr_const(1, mod, width)
+    zm1 = sub(z, one, width)
+    return sub(gr_mul(z, p1, width, mod), gr_mul(zm1, p0, width, mod), width)
+
+
+def _check_even(z_even) -> None:
+    if int(count_nonequal(ew(AND, z_even, 1, ring_mask(64))).item()):
+        raise ValueError("even evaluation point required")
+
+
+def gr_quad_coeffs(z_even, width: int, mod: GrModulus, check: bool = True):
+    """Lagrange weights (l0, l1, l2) at an even point, each (1, d)."""
+    if check:
+        _check_even(z_even)
+    u = _shr1(z_even)
+    one = gr_const(1, mod, width)
+    two = gr_const(2, mod, width)
+    l0 = gr_mul(sub(z_even, one, width), sub(u, one, width), width, mod)
+    l1 = gr_mul(z_even, sub(two, z_even, width), width, mod)
+    l2 = gr_mul(u, sub(z_even, one, width), width, mod)
+    return l0, l1, l2
+
+
+def _shr1(a):
+    # logical shift right by one: (a >> 1) == arith_rshift(a,1,64) & (2^63-1)
+    return ew(AND, arith_rshift(a, 1, 64), (1 << 63) - 1, ring_mask(64))
+
+
+def gr_quad_eval(h0, h1, h2, z_even, width: int, mod: GrModulus):
+    l0, l1, l2 = gr_quad_coeffs(z_even, width, mod)
+    out = add(gr_mul(l0, h0, width, mod), gr_mul(l1, h1, width, mod), width)
+    return add(out, gr_mul(l2, h2, width, mod), width)
