@@ -1,0 +1,408 @@
+"""Benchmark: verified 3PC multiplications per second on B200.
+
+Workload (BASELINE.json configs[1]): the reference's `mulv` program
+(tests/test_acceptance.py:124-136) -- x, y = shc_random over Z_2^64, one
+batched Pi_mul, prepare_verification, online mul_finish, then the GR(2^64, d)
+batch verification Pi_mulv -- run end to end through the drop-in API
+(`Session(seed).run(program)`), all three parties simulated on each GPU.
+A "step" is one complete verified session over N multiplications.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--log2n L] [--d D]
+                    [--R R|auto] [--impl b200|reference]
+
+One process per GPU (torchrun for N > 1).  Ranks run independent sessions
+over N multiplications each (weak scaling; the verification of a batch is a
+single inner-product check, shards never need a collective on this path).
+Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified 3PC mults/sec and secure ReLU comparisons/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "verified mults/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--log2n", type=int, default=22)
+    ap.add_argument("--d", type=int, default=64)
+    ap.add_argument("--R", default="auto")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--engine", default="coop", choices=["coop", "threads"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-kernel", default="r3_gr_dotsum")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm on host cores
+# ---------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    lanes, d, seed = args
+    from oracle import mpc
+    from oracle.verify_model import pick_r
+    R = pick_r(lanes, 64, d)
+    t0 = time.perf_counter()
+    res = mpc.mulv(seed=seed, lanes=lanes, d=d, R=R)
+    dt = time.perf_counter() - t0
+    assert res.verdict
+    return lanes, dt
+
+
+def cpu_baseline(d: int, budget_s: float) -> dict:
+    """Time the oracle port (numpy restatement of the reference's mulv path,
+    single-threaded numpy per process) on all host cores: one independent
+    session per process, throughput = total mults / wall time."""
+    import concurrent.futures as cf
+    cores = os.cpu_count() or 1
+    # size one session so each worker spends roughly budget/2 seconds
+    probe_lanes = 1 << 10
+    _, t_probe = _cpu_worker((probe_lanes, d, 1))
+    per_mult = t_probe / probe_lanes
+    lanes = 1 << max(10, min(16, int(math.log2(max(1, budget_s / 2 / per_mult)))))
+    t0 = time.perf_counter()
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        outs = list(ex.map(_cpu_worker, [(lanes, d, 100 + i) for i in range(cores)]))
+    wall = time.perf_counter() - t0
+    total = sum(o[0] for o in outs)
+    return {"value": total / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{cores} independent oracle-port mulv sessions x {lanes} mults, d={d}, "
+                      f"R=pick_r(lan), ell=64 (numpy restatement of ring3pc; wall {wall:.1f}s)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# programs
+# ---------------------------------------------------------------------------
+
+def make_programs(N: int, d: int, R: int):
+    from paper_2411_09287_b200 import gates, verify
+    from paper_2411_09287_b200.sharing import (Ring, rec, shc_input_mask, shc_input_online,
+                                               shc_random)
+    from paper_2411_09287_b200.transport import Phase
+
+    def mulv(party):
+        """tests/test_acceptance.py:124-136."""
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        x = shc_random(party, N, ring)
+        y = shc_random(party, N, ring)
+        g = gates.mul_prepare(party, x.mask, y.mask, N)
+        verify.prepare_verification(party, d=d, r_max=max(R, 1))
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        gates.mul_finish(party, g, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        return verify.batch_verify_muls(party, 64, d=d, R=R)
+
+    def e2e(party, xh, yh):
+        """Owner inputs from pinned host memory (P0: x, P1: y), verified
+        product opened and copied back to the host."""
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        xm = shc_input_mask(party, 0, N, ring)
+        ym = shc_input_mask(party, 1, N, ring)
+        g = gates.mul_prepare(party, xm, ym, N)
+        verify.prepare_verification(party, d=d, r_max=max(R, 1))
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input_online(party, 0, xh if party.role == 0 else None, xm, N, ring, "x")
+        y = shc_input_online(party, 1, yh if party.role == 1 else None, ym, N, ring, "y")
+        z = gates.mul_finish(party, g, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        if not verify.batch_verify_muls(party, 64, d=d, R=R):
+            party.abort("verification failed")
+        out = rec(party, z, "z")
+        return out.cpu() if party.role == 0 else None
+
+    return mulv, e2e
+
+
+class KernelTimer:
+    """CUDA events around every launch of one library entry point, on the
+    launching (current) stream."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.events = []
+        self.work = 0
+        self.launches = 0
+
+    def hook(self, name, args, run):
+        import torch
+        if name != self.name:
+            return run()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = run()
+        b.record()
+        self.events.append((a, b))
+        self.launches += 1
+        self.work += work_of(name, args)
+        return rc
+
+    def seconds(self) -> float:
+        return sum(a.elapsed_time(b) for a, b in self.events) / 1e3
+
+
+def work_of(name, args) -> int:
+    """Algorithmic u64 multiply-accumulates of one call (rows x d^2 for the
+    GR contractions)."""
+    if name == "r3_gr_dotsum":
+        rows, d = args[2], args[3]
+        return int(rows) * int(d) * int(d)
+    if name == "r3_gr_matmul":
+        rows, d = args[5], args[6]
+        return int(rows) * int(d) * int(d)
+    return 0
+
+
+def imad_peak_macs(torch, lib) -> float:
+    """Measured u64-MAC ceiling of the integer pipe (r3_imad_peak)."""
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    it = 4096
+    lib.call("r3_imad_peak", 256, sink.data_ptr(), lib.stream())
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        lib.call("r3_imad_peak", it, sink.data_ptr(), lib.stream())
+        b.record()
+        torch.cuda.synchronize()
+        secs = a.elapsed_time(b) / 1e3
+        best = max(best, 148 * 8 * 256 * 8 * it / secs)
+    return best
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import numpy as np
+
+    from paper_2411_09287_b200 import _lib, verify
+    from paper_2411_09287_b200.runtime import Session
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.load()
+
+    N = 1 << args.log2n
+    d = args.d
+    R = verify.pick_r(N, 64, d, "lan") if args.R == "auto" else int(args.R)
+    mulv, e2e = make_programs(N, d, R)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(i):
+        sess = Session(seed=1000 * rank + i, engine=args.engine)
+        res = sess.run(mulv)
+        return res
+
+    for i in range(args.warmup):
+        res = step(i)
+        assert all(res), "honest verification rejected"
+
+    timer = KernelTimer(args.profile_kernel)
+    launches0 = _lib.load().r3_launch_count()
+    _lib.CALL_HOOK = timer.hook
+    barrier()
+    with Clocks(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            res = step(args.warmup + i)
+        t1.record()
+        barrier()
+        wall = time.perf_counter() - wall0
+    _lib.CALL_HOOK = None
+    launches = _lib.load().r3_launch_count() - launches0
+    assert all(res)
+    secs = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt.item())
+    ms_per_step = secs / args.steps * 1e3
+    value = N * world * args.steps / secs
+
+    # roofline of the dominant kernel, timed live in the region above
+    kt = timer.seconds()
+    peak = imad_peak_macs(torch, _lib)
+    achieved = timer.work / kt if kt else 0.0
+
+    # end-to-end: host inputs in pinned memory, opened product back to host
+    rng = np.random.default_rng(rank)
+    xh = torch.from_numpy(rng.integers(0, 2**63, N, dtype=np.int64)).pin_memory()
+    yh = torch.from_numpy(rng.integers(0, 2**63, N, dtype=np.int64)).pin_memory()
+    Session(seed=7).run(e2e, xh, yh)
+    barrier()
+    e0 = time.perf_counter()
+    for i in range(args.e2e_steps):
+        out = Session(seed=70 + i).run(e2e, xh, yh)[0]
+    barrier()
+    e2e_s = time.perf_counter() - e0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    want = (xh.numpy().view(np.uint64) * yh.numpy().view(np.uint64))
+    assert np.array_equal(out.numpy().view(np.uint64), want), "e2e product mismatch"
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: PRF-generated (AES-128-CTR) random shares, seed per rank/step",
+        "config": {"workload": "mulv: batched 3PC Pi_mul + GR(2^64,d) batch verification "
+                               "(tests/test_acceptance.py:124-136), 3 parties per GPU",
+                   "N_per_gpu": N, "ell": 64, "d": d, "R": R, "engine": args.engine,
+                   "l2": f"inputs larger than L2 ({N * 8 * 12 / 2**20:.0f} MiB of shares per step)",
+                   "parallelism": f"weak dp{world}: independent sessions per rank"},
+        "roofline": {"bound": "int-alu", "kernel": args.profile_kernel,
+                     "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tu64MAC/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "launches": timer.launches, "kernel_s_per_step": kt / args.steps,
+                     "kernel_share_of_step": kt / secs if secs else None,
+                     "peak_source": "measured in-run by r3_imad_peak (MEASURED_PEAKS.json has no "
+                                    "integer peak); algorithmic work = rows*d^2 u64 MACs per launch"},
+        "e2e": {"value": N * args.e2e_steps / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": N * 8},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "wall_s_timed": wall,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the
+    host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    d = args.d
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(d, args.cpu_seconds / 4)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(d, args.cpu_seconds))
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "impl": "reference",
+            "data": "synthetic: PRF-generated random shares",
+            "config": {"workload": "mulv (CPU oracle port of the reference algorithm)", "d": d,
+                       "ell": 64},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

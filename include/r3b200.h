@@ -59,6 +59,12 @@ typedef struct r3_lin_operand {
 
 int r3_abi_version(void);
 const char* r3_last_error(void);
+/* Number of kernels this library has launched in the process (bench
+ * accounting of gpu_launches). */
+uint64_t r3_launch_count(void);
+/* Integer-ALU ceiling probe: 148*8 blocks x 256 threads x 8 chains x iters
+ * dependent-free u64 multiply-adds (the u64 MAC of the GR kernels). */
+int r3_imad_peak(int iters, uint64_t* sink, void* stream);
 
 /* ---- PRF: AES-128-CTR streams (prg.py:39-65) ----------------------------
  * Host helper: FIPS-197 key expansion, 44 big-endian round-key words. */

@@ -34,6 +34,8 @@ class LinOperand(C.Structure):
 _SIGS = {
     "r3_abi_version": [],
     "r3_last_error": [],
+    "r3_launch_count": [],
+    "r3_imad_peak": [C.c_int, u64p, C.c_void_p],
     "r3_aes128_expand": [C.c_char_p, C.POINTER(C.c_uint32)],
     "r3_prf_ctr": [C.POINTER(C.c_uint32), u64, i64, u64, C.c_int, u64p, C.c_void_p],
     "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
@@ -62,7 +64,7 @@ _SIGS = {
     "r3_vfy_l1_line_y": [C.c_int, C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, u64p,
                          C.c_int, C.POINTER(C.c_void_p), u64, C.c_void_p],
 }
-_RESTYPE = {"r3_last_error": C.c_char_p, "r3_aes128_expand": None}
+_RESTYPE = {"r3_last_error": C.c_char_p, "r3_aes128_expand": None, "r3_launch_count": C.c_uint64}
 
 
 class KernelError(RuntimeError):
@@ -93,8 +95,17 @@ def exported_symbols() -> list[str]:
     return list(_SIGS)
 
 
+# optional instrumentation: callable(name, args, run) -> rc (bench.py times
+# one entry point with CUDA events around its launches)
+CALL_HOOK = None
+
+
 def call(name: str, *args) -> None:
-    rc = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    if CALL_HOOK is None:
+        rc = fn(*args)
+    else:
+        rc = CALL_HOOK(name, args, lambda: fn(*args))
     if rc != 0:
         msg = load().r3_last_error().decode(errors="replace")
         raise KernelError(f"{name} failed ({rc}): {msg}")

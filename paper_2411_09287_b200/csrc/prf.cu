@@ -10,6 +10,7 @@
 // both 64-bit halves; the kernel is seekable (any first_u64), so party
 // streams, shards and mid-block continuations cost nothing extra.
 #include <cstdarg>
+#include <atomic>
 #include <cstring>
 
 #include "r3_common.cuh"
@@ -113,6 +114,34 @@ prf_ctr_kernel(RoundKeys rk, u64 first, int64_t n, u64 mask, int mode, u64* __re
 using namespace r3;
 
 static thread_local char g_err[512];
+static std::atomic<unsigned long long> g_launches{0};
+
+void r3::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" uint64_t r3_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// Integer-ALU ceiling for the GR kernels: each thread runs 8 independent
+// chains of 64-bit multiply-accumulates (the IMAD.WIDE + 2 IMAD sequence of
+// every u64 MAC in gr.cu); `iters` MACs per chain.
+__global__ void imad_peak_kernel(u64 seed, int iters, u64* __restrict__ sink) {
+  u64 a[8], b = seed ^ (threadIdx.x * 0x9e3779b97f4a7c15ull), c = seed + blockIdx.x;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = c + q;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = a[q] * b + c;
+    b += 0x1234567ull;
+  }
+  u64 s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s ^= a[q];
+  if (s == 0x5151515151ull) sink[0] = s;
+}
+
+extern "C" int r3_imad_peak(int iters, uint64_t* sink, void* stream) {
+  imad_peak_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(0x243f6a8885a308d3ull, iters, (u64*)sink);
+  return check_launch("r3_imad_peak");
+}
 
 void r3::set_error(const char* fmt, ...) {
   va_list ap;

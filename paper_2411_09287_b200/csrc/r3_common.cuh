@@ -22,7 +22,12 @@ constexpr int kNumSMs = 148;
 // Thread-local last-error text for r3_last_error().
 void set_error(const char* fmt, ...);
 
+// Number of kernels this library has launched (every launch site goes
+// through check_launch exactly once); read by r3_launch_count().
+void count_launch();
+
 inline int check_launch(const char* what) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));

@@ -154,14 +154,15 @@ def bit_planes(a, nbits: int) -> torch.Tensor:
     return out
 
 
-def count_nonequal(a, b=None) -> torch.Tensor:
-    """Device scalar #{a != b} (b None: #{a != 0})."""
+def count_nonequal(a, b=None, into: torch.Tensor | None = None) -> torch.Tensor:
+    """Device scalar #{a != b} (b None: #{a != 0}); accumulates into `into`
+    when given (deferred consistency checks)."""
     a = a.contiguous()
-    cnt = zeros((1,))
+    cnt = zeros((1,)) if into is None else into
     if b is not None:
         b = b.contiguous()
         if b.shape != a.shape:
-            cnt.fill_(1)
+            cnt.add_(1)
             return cnt
     call("r3_count_nonequal", ptr(a), ptr(b), a.numel(), ptr(cnt), stream())
     return cnt

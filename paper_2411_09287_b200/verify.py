@@ -173,15 +173,26 @@ def _public(party, key, build):
         return cache[key]
 
 
+def _opened_key(party, value: torch.Tensor):
+    """Cache identity of a just-opened public value.  With eager checks (an
+    adversary is configured) parties may disagree on an opening until the
+    digest check aborts, so the key is the opened bytes themselves; in
+    honest sessions every party opens the same value under the same rec tag,
+    so the tag identifies it without a device->host read."""
+    if party.sess.eager_checks:
+        return to_host(value).tobytes()
+    return ("rec", party._ids.get("rec", 0))
+
+
 def _powers(party, r: torch.Tensor, n: int, gr: Ring) -> torch.Tensor:
-    key = ("pow", gr.ell, gr.d, to_host(r).tobytes(), n)
+    key = ("pow", gr.ell, gr.d, _opened_key(party, r), n)
     return _public(party, key, lambda: grvec.gr_powers(r, n, gr.ell, gr.mod))
 
 
 def _line_tables(party, r, pw: torch.Tensor, dot_n: int, ze: torch.Tensor, gr: Ring):
     """Public level-1 tables A = pw (1 - ze), B = pw ze.  For multiplication
     logs (dot_n == 1) only even powers feed A and odd powers feed B."""
-    key = ("ab", gr.ell, gr.d, to_host(r).tobytes(), pw.shape[0], dot_n, to_host(ze).tobytes())
+    key = ("ab", gr.ell, gr.d, id(pw), pw.shape[0], dot_n, _opened_key(party, ze))
 
     def build():
         one = grvec.gr_const(1, gr.mod, gr.ell)
@@ -313,7 +324,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     h2 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h2f)
     h0 = z - h1
     ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod)
+    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
     z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
     tq = 2 if comp.n == 1 else comp.n
@@ -384,9 +395,91 @@ def consolidate_dot_triples(party, batches, gr: Ring, chal: Challenges):
     return xs, ys, z_acc
 
 
+class _Halves:
+    """Even/odd rows of one dense (N, d) component as lazy linear operands.
+    A zero lane appended to odd N (verify.py:220-222) is expressed by row
+    validity, never materialised; f2 = 2 f1 - f0 and f1 - f0 are combined
+    inside the kernels' operand loads."""
+
+    def __init__(self, t: torch.Tensor):
+        n = t.shape[0]
+        self.ev, self.od = t[0::2], t[1::2]
+        self.n0, self.n1 = (n + 1) // 2, n // 2
+
+    def f0(self, c=1):
+        return [(c, self.ev, self.n0)]
+
+    def f1(self, c=1):
+        return [(c, self.od, self.n1)]
+
+    def f2(self, c=1):
+        return [(2 * c, self.od, self.n1), (-c, self.ev, self.n0)]
+
+    def d10(self):
+        return [(1, self.od, self.n1), (-1, self.ev, self.n0)]
+
+
+def _lin(terms):
+    return grvec.lin(*[(c, t) for c, t, _ in terms], nvalid=[nv for _, _, nv in terms])
+
+
+def _dotsum_terms(pairs, rows: int, gr: Ring) -> torch.Tensor:
+    """sum over (F-terms, G-terms) of sum_i F_i (x) G_i, reduced: (1, d)."""
+    acc = grvec.dotsum_acc(gr.d)
+    for F, G in pairs:
+        grvec.dotsum_add(acc, _lin(F), _lin(G), rows, gr.d)
+    return grvec.reduce_poly(acc, gr.mod, gr.ell)
+
+
+def _level_folds(role: int, X: dict, Y: dict, which: str, rows: int, gr: Ring) -> torch.Tensor:
+    """The party's local fold of h(1) (which="f1") or h(2) (which="f2"):
+    P0 sum F.total G.total; P1 -(F.m G.s1) - (G.m F.s1);
+    P2 F.m (G.m - G.s2) - F.s2 G.m  (gates.dot_finish legs, gates.py:100-106)."""
+    F = lambda c, k: getattr(X[c], which)(k)
+    G = lambda c, k: getattr(Y[c], which)(k)
+    if role == 0:
+        pairs = [(F("total", 1), G("total", 1))]
+    elif role == 1:
+        pairs = [(F("m", -1), G("s1", 1)), (G("m", -1), F("s1", 1))]
+    else:
+        pairs = [(F("m", 1), G("m", 1) + G("s2", -1)), (F("s2", -1), G("m", 1))]
+    return _dotsum_terms(pairs, rows, gr)
+
+
+def _line_eval(H: _Halves, M: torch.Tensor, gr: Ring) -> torch.Tensor:
+    """f0 + (f1 - f0) * zeta as one rows . M_zeta product (verify.py:239)."""
+    return grvec.gr_matmul(_lin(H.d10()), M, H.n0, gr.d, gr.ell, C_add=_lin(H.f0()))
+
+
 def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     """Halve the triple (verify.py:215-241): pad odd lengths with a zero lane,
     h(1), h(2) by inner products, h(0) = z - h(1), evaluate at 2*zeta."""
+    role = party.role
+    names = [k for k in ("s1", "s2", "total") if getattr(xs.mask, k) is not None]
+    X = {k: _Halves(getattr(xs.mask, k)) for k in names}
+    Y = {k: _Halves(getattr(ys.mask, k)) for k in names}
+    if xs.m is not None:
+        X["m"], Y["m"] = _Halves(xs.m), _Halves(ys.m)
+    rows = next(iter(X.values())).n0
+    small = gr.d < 8
+    if small:  # degrees 1..4: generic kernels, materialised halves
+        return _reduce_dimension_small(party, xs, ys, z, gr, zeta)
+    h1 = _gr_dot_folded(party, gr, rows, _level_folds(role, X, Y, "f1", rows, gr))
+    h2 = _gr_dot_folded(party, gr, rows, _level_folds(role, X, Y, "f2", rows, gr))
+    h0 = z - h1
+    ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
+    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
+    z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
+    M = grvec.gr_mulmat(ze, gr.mod)
+    out = lambda V, k: _line_eval(V[k], M, gr)
+    mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
+                                  p0_halves=v.mask.p0_halves),
+                           out(V, "m") if "m" in V else None)
+    return mk(X, xs), mk(Y, ys), z_out
+
+
+def _reduce_dimension_small(party, xs, ys, z, gr, zeta):
+    """Reference-shaped reduction for tiny degrees (d < 8)."""
     if xs.lanes % 2 == 1:
         pad = _zero_lanes(party, gr, 1)
         xs, ys = xs.concat(pad), ys.concat(pad)
@@ -398,7 +491,7 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     h2 = _gr_dot(party, f2, g2, gr)
     h0 = z - h1
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod)
+    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
     z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
     xs_out = f0 + (f1 - f0).scale_gr(ze)
     ys_out = g0 + (g1 - g0).scale_gr(ze)
