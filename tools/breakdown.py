@@ -1,0 +1,69 @@
+"""Per-entry-point GPU time breakdown of one mulv step (CUDA events around
+every library call, on the launching stream).  Diagnostic only.
+
+    python tools/breakdown.py --log2n 22 --d 64
+"""
+
+import argparse
+import collections
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2411_09287_b200 import _lib, verify  # noqa: E402
+from paper_2411_09287_b200.runtime import Session  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--log2n", type=int, default=22)
+    ap.add_argument("--d", type=int, default=64)
+    ap.add_argument("--engine", default="coop")
+    a = ap.parse_args()
+    N = 1 << a.log2n
+    R = verify.pick_r(N, 64, a.d)
+    mulv, _ = bench.make_programs(N, a.d, R)
+    for i in range(2):
+        Session(seed=i, engine=a.engine).run(mulv)
+    torch.cuda.synchronize()
+    ev = []
+
+    def hook(name, args, run):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        rc = run()
+        e.record()
+        ev.append((name, s, e))
+        return rc
+
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    t0.record()
+    _lib.CALL_HOOK = hook
+    Session(seed=99, engine=a.engine).run(mulv)
+    _lib.CALL_HOOK = None
+    t1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    step = t0.elapsed_time(t1)
+    tot = collections.Counter()
+    cnt = collections.Counter()
+    for name, s, e in ev:
+        tot[name] += s.elapsed_time(e)
+        cnt[name] += 1
+    busy = sum(tot.values())
+    print(f"N=2^{a.log2n} d={a.d} R={R}: step {step:.1f} ms (wall {wall*1e3:.1f} ms), "
+          f"library GPU time {busy:.1f} ms in {len(ev)} calls")
+    for k, v in tot.most_common():
+        print(f"  {k:24s} {v:9.2f} ms {100 * v / step:5.1f}%  calls={cnt[k]}")
+
+
+if __name__ == "__main__":
+    main()
