@@ -143,6 +143,14 @@ int r3_gr_mulmat(const uint64_t* c, int d, uint64_t lowterms, uint64_t* M,
 int r3_gr_matmul(r3_lin_operand A, const uint64_t* M, int has_c,
                  r3_lin_operand C, uint64_t* out, int64_t rows, int d,
                  uint64_t mask, void* stream);
+/* Pipelined tensor-core contraction for d = 64:
+ *   out[r] = P0[r] . M0 + P1[r] . M1      (P1 == NULL: out[r] = P0[r] . M0)
+ * P0/P1 rows at p + r*rs (16-byte aligned), rows >= nv read as zero.  The
+ * line evaluation f0 + (f1 - f0) zeta is f0 . M_{1-zeta} + f1 . M_zeta. */
+int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0,
+                     const uint64_t* p1, int64_t rs1, int64_t nv1,
+                     const uint64_t* M0, const uint64_t* M1, uint64_t* out,
+                     int64_t rows, uint64_t mask, void* stream);
 /* acc[0..2d-2] += unreduced polynomial sum_i F[i] (x) G[i] (the inner
  * products of reduce_dimension / check_inner_product, verify.py:154-161,
  * gates.dot_finish.fold over GR). acc must be zeroed by the caller before the

@@ -52,6 +52,7 @@ _SIGS = {
     "r3_gr_mulmat": [u64p, C.c_int, u64, u64p, C.c_void_p],
     "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
                      C.c_void_p],
+    "r3_gr_matmul2_tc": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
     "r3_gr_dotsum": [LinOperand, LinOperand, i64, C.c_int, u64p, C.c_void_p],
     "r3_gr_reduce_poly": [u64p, C.c_int, u64, u64p, u64, C.c_int, C.c_void_p],
     "r3_vfy_powsum": [C.c_int, C.POINTER(C.c_void_p), i64, i64, u64p, C.c_int, u64p, u64,
@@ -112,17 +113,24 @@ def call(name: str, *args) -> None:
 
 
 def stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """Raw handle of the calling thread's current CUDA stream."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 # ---------------------------------------------------------------------------
 # tensor helpers (int64 storage, uint64 semantics)
 # ---------------------------------------------------------------------------
 
+_cuda_ok = None
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
+    global _cuda_ok
+    if _cuda_ok is None:
+        _cuda_ok = torch.cuda.is_available()
+    if not _cuda_ok:
         raise RuntimeError("ring3pc-b200 requires a CUDA device (no CPU fallback)")
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cuda", torch._C._cuda_getDevice())
 
 
 def as_i64(v: int) -> int:

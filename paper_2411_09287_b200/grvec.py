@@ -81,6 +81,8 @@ def ew(op: int, a, b, mask: int) -> torch.Tensor:
         shape = tuple(a.shape)
         av = a
         bv = None
+    elif a.shape == b.shape:
+        shape, av, bv, imm = tuple(a.shape), a, b, 0
     else:
         shape = tuple(torch.broadcast_shapes(a.shape, b.shape))
         av = a.expand(shape)
@@ -268,7 +270,7 @@ def gr_mul(a, b, width: int, mod: GrModulus) -> torch.Tensor:
     if d >= 8 and n >= _MATMUL_MIN_ROWS and a_one != b_one:
         one, many = (a, b) if a_one else (b, a)
         M = gr_mulmat(one[:1], mod)
-        return gr_matmul(lin((1, many)), M, n, d, width)
+        return rows_times(many, M, n, width)
     out = empty((n, d))
     a_rs = 0 if a_one else a.stride(0)
     b_rs = 0 if b_one else b.stride(0)
@@ -345,7 +347,7 @@ def gr_powers(r, n: int, width: int, mod: GrModulus) -> torch.Tensor:
         step = gr_mul(out[filled - 1:filled], r, width, mod)
         if d >= 8:
             M = gr_mulmat(step, mod)
-            gr_matmul(lin((1, out[:take])), M, take, d, width, out=out[filled:filled + take])
+            rows_times(out[:take], M, take, width, out=out[filled:filled + take])
         else:
             out[filled:filled + take] = gr_mul(out[:take], step, width, mod)
         filled += take
@@ -386,3 +388,44 @@ def gr_quad_eval(h0, h1, h2, z_even, width: int, mod: GrModulus):
     l0, l1, l2 = gr_quad_coeffs(z_even, width, mod)
     out = add(gr_mul(l0, h0, width, mod), gr_mul(l1, h1, width, mod), width)
     return add(out, gr_mul(l2, h2, width, mod), width)
+
+
+# ---------------------------------------------------------------------------
+# many elements times one element: tensor-core dispatch
+# ---------------------------------------------------------------------------
+
+def _tc_ok(t: torch.Tensor) -> bool:
+    return (t.shape[0] <= 1 or t.stride(0) % 2 == 0) and t.data_ptr() % 16 == 0 and t.stride(-1) == 1
+
+
+def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
+               P1: torch.Tensor | None = None, M1: torch.Tensor | None = None,
+               nvalid=(None, None), out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[r] = P0[r] . M0 (+ P1[r] . M1): rows of GR elements times fixed
+    elements given by their multiplication matrices.  d = 64 runs on the
+    tensor cores (r3_gr_matmul2_tc, int8 byte limbs); other degrees on the
+    CUDA-core matrix kernel.  Rows at or beyond nvalid[q] of P_q are zero."""
+    d = M0.shape[0]
+    n0 = rows if nvalid[0] is None else nvalid[0]
+    n1 = rows if nvalid[1] is None else nvalid[1]
+    if out is None:
+        out = empty((rows, d))
+    if rows == 0:
+        return out
+    if d == 64 and _tc_ok(P0) and (P1 is None or _tc_ok(P1)):
+        rs0 = P0.stride(0) if P0.shape[0] > 1 else 64
+        if P1 is not None and P1.shape[0] > 0:
+            rs1 = P1.stride(0) if P1.shape[0] > 1 else 64
+            call("r3_gr_matmul2_tc", ptr(P0), rs0, n0, ptr(P1), rs1, n1, ptr(M0), ptr(M1),
+                 ptr(out), rows, ring_mask(width), stream())
+        else:
+            call("r3_gr_matmul2_tc", ptr(P0), rs0, n0, None, 0, 0, ptr(M0), None,
+                 ptr(out), rows, ring_mask(width), stream())
+        return out
+    if P1 is None or P1.shape[0] == 0:
+        return gr_matmul(lin((1, P0), nvalid=[n0]), M0, rows, d, width, out=out)
+    # CUDA-core form: P0.M0 + P1.M1 with M0 = M(1 - z), M1 = M(z) is
+    # P0 + (P1 - P0).M1 when M0 + M1 = I (line evaluation); general case:
+    tmp = gr_matmul(lin((1, P1), nvalid=[n1]), M1, rows, d, width)
+    return gr_matmul(lin((1, P0), nvalid=[n0]), M0, rows, d, width,
+                     C_add=lin((1, tmp)), out=out)

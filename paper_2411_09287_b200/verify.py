@@ -201,9 +201,8 @@ def _line_tables(party, r, pw: torch.Tensor, dot_n: int, ze: torch.Tensor, gr: R
         M_b = grvec.gr_mulmat(ze, gr.mod) if gr.d >= 8 else None
         ev, od = (pw[0::2], pw[1::2]) if dot_n == 1 else (pw, pw)
         if gr.d >= 8:
-            A = grvec.gr_matmul(grvec.lin((1, ev)), M_a, ev.shape[0], gr.d, gr.ell)
-            B = grvec.gr_matmul(grvec.lin((1, od)), M_b, od.shape[0], gr.d, gr.ell) \
-                if od.shape[0] else empty((0, gr.d))
+            A = grvec.rows_times(ev, M_a, ev.shape[0], gr.ell)
+            B = grvec.rows_times(od, M_b, od.shape[0], gr.ell) if od.shape[0] else empty((0, gr.d))
         else:
             A = grvec.gr_mul(ev.contiguous(), one_m, gr.ell, gr.mod)
             B = grvec.gr_mul(od.contiguous(), ze, gr.ell, gr.mod) if od.shape[0] else empty((0, gr.d))
@@ -446,9 +445,15 @@ def _level_folds(role: int, X: dict, Y: dict, which: str, rows: int, gr: Ring) -
     return _dotsum_terms(pairs, rows, gr)
 
 
-def _line_eval(H: _Halves, M: torch.Tensor, gr: Ring) -> torch.Tensor:
-    """f0 + (f1 - f0) * zeta as one rows . M_zeta product (verify.py:239)."""
-    return grvec.gr_matmul(_lin(H.d10()), M, H.n0, gr.d, gr.ell, C_add=_lin(H.f0()))
+def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:
+    """f0 + (f1 - f0) * zeta (verify.py:239) = f0 . M(1 - zeta) + f1 . M(zeta):
+    one K-concatenated contraction on the tensor cores for d = 64; the CUDA
+    core form rows . M(zeta) + f0 otherwise."""
+    M_one_m, M_z = Ms
+    if gr.d == 64:
+        return grvec.rows_times(H.ev, M_one_m, H.n0, gr.ell, P1=H.od, M1=M_z,
+                                nvalid=(H.n0, H.n1))
+    return grvec.gr_matmul(_lin(H.d10()), M_z, H.n0, gr.d, gr.ell, C_add=_lin(H.f0()))
 
 
 def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
@@ -470,8 +475,9 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
     l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
     z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
-    M = grvec.gr_mulmat(ze, gr.mod)
-    out = lambda V, k: _line_eval(V[k], M, gr)
+    one_m = grvec.sub(grvec.gr_const(1, gr.mod, gr.ell), ze, gr.ell)
+    Ms = (grvec.gr_mulmat(one_m, gr.mod) if gr.d == 64 else None, grvec.gr_mulmat(ze, gr.mod))
+    out = lambda V, k: _line_eval(V[k], Ms, gr)
     mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
                                   p0_halves=v.mask.p0_halves),
                            out(V, "m") if "m" in V else None)
