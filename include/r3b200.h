@@ -182,6 +182,14 @@ int r3_vfy_l1_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                    int64_t ks, int64_t ls, const uint64_t* pw, int d,
                    uint64_t* out_h1, uint64_t* out_h2, uint64_t mask,
                    void* stream);
+/* One party's h(1) and h(2) leg folds of a dense reduction level in one pass
+ * (verify.py:223-230 with gates.py:100-106): rows of dense (N, d) component
+ * arrays, pairs (2j, 2j+1), zero pad for odd N.  role 0: xa/ya = x/y total;
+ * role 1: xa/ya = m, xb/yb = s1; role 2: m and s2.  acc1/acc2 (2d-1 words
+ * each, zeroed by the caller) receive the unreduced polynomial sums. */
+int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* xb,
+                      const uint64_t* ya, const uint64_t* yb, int64_t N, int d,
+                      uint64_t* acc1, uint64_t* acc2, void* stream);
 /* Level-1 line evaluation of x components (verify.py:239):
  * out[c][j] = X_c[2j] * A[(2j)/tq] + X_c[2j+1] * B[(2j+1)/tq] with public
  * tables A = pw(1-ze), B = pw ze (tq = 2 with A/B over even/odd powers for

@@ -170,16 +170,22 @@ gr_matmul_kernel(LinOperand A, const u64* __restrict__ M, int has_c, LinOperand 
 }
 
 // acc[0..2D-2] += sum_i F_i (x) G_i.  Each thread owns a 4x4 tile of the
-// D x D outer-product sum; 256/(D/4)^2 thread groups split the rows.
+// D x D outer-product sum; 256/(D/4)^2 thread groups split the rows.  Rows
+// stream through a double-buffered smem stage: the next BK rows (lazy linear
+// combinations of up to 4 views each) are loaded into registers while the
+// current stage is multiplied.
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 gr_dotsum_kernel(LinOperand F, LinOperand G, int64_t rows, int64_t rows_per_block, u64* __restrict__ acc) {
   constexpr int CG = D / 4;
   constexpr int TILES = CG * CG;
   constexpr int GROUPS = 256 / TILES;
   constexpr int BK = 32;
-  __shared__ __align__(16) u64 sF[BK * D], sG[BK * D];
-  __shared__ u64 sP[2 * D];
+  constexpr int PER = BK * D / 256;     // elements of F (and of G) per thread per stage
+  extern __shared__ __align__(16) u64 dsm[];
+  u64* sF = dsm;                        // [2][BK*D]
+  u64* sG = dsm + 2 * BK * D;           // [2][BK*D]
+  u64* sP = dsm + 4 * BK * D;           // [2D]
   const int grp = threadIdx.x / TILES;
   const int tile = threadIdx.x % TILES;
   const int ta = tile / CG, tb = tile % CG;
@@ -191,21 +197,34 @@ gr_dotsum_kernel(LinOperand F, LinOperand G, int64_t rows, int64_t rows_per_bloc
     for (int b = 0; b < 4; ++b) s[a][b] = 0;
   const int64_t r_begin = blockIdx.x * rows_per_block;
   const int64_t r_end = min(rows, r_begin + rows_per_block);
+  u64 pf[PER], pg[PER];
+  auto fetch = [&](int64_t r0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = threadIdx.x + 256 * q;
+      const int64_t row = r0 + i / D;
+      const bool ok = row < r_end;
+      pf[q] = ok ? lin_load(F, row, i % D) : 0ull;
+      pg[q] = ok ? lin_load(G, row, i % D) : 0ull;
+    }
+  };
+  int buf = 0;
+  if (r_begin < r_end) fetch(r_begin);
   for (int64_t r0 = r_begin; r0 < r_end; r0 += BK) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < BK * D; i += 256) {
-      int r = i / D, k = i % D;
-      int64_t row = r0 + r;
-      bool ok = row < r_end;
-      sF[i] = ok ? lin_load(F, row, k) : 0ull;
-      sG[i] = ok ? lin_load(G, row, k) : 0ull;
+    u64* cF = sF + buf * BK * D;
+    u64* cG = sG + buf * BK * D;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      cF[threadIdx.x + 256 * q] = pf[q];
+      cG[threadIdx.x + 256 * q] = pg[q];
     }
     __syncthreads();
+    if (r0 + BK < r_end) fetch(r0 + BK);
     for (int r = grp; r < BK; r += GROUPS) {
-      ulonglong2 f01 = *reinterpret_cast<const ulonglong2*>(&sF[r * D + ta * 4]);
-      ulonglong2 f23 = *reinterpret_cast<const ulonglong2*>(&sF[r * D + ta * 4 + 2]);
-      ulonglong2 g01 = *reinterpret_cast<const ulonglong2*>(&sG[r * D + tb * 4]);
-      ulonglong2 g23 = *reinterpret_cast<const ulonglong2*>(&sG[r * D + tb * 4 + 2]);
+      ulonglong2 f01 = *reinterpret_cast<const ulonglong2*>(&cF[r * D + ta * 4]);
+      ulonglong2 f23 = *reinterpret_cast<const ulonglong2*>(&cF[r * D + ta * 4 + 2]);
+      ulonglong2 g01 = *reinterpret_cast<const ulonglong2*>(&cG[r * D + tb * 4]);
+      ulonglong2 g23 = *reinterpret_cast<const ulonglong2*>(&cG[r * D + tb * 4 + 2]);
       u64 fv[4] = {f01.x, f01.y, f23.x, f23.y};
       u64 gv[4] = {g01.x, g01.y, g23.x, g23.y};
 #pragma unroll
@@ -213,6 +232,7 @@ gr_dotsum_kernel(LinOperand F, LinOperand G, int64_t rows, int64_t rows_per_bloc
 #pragma unroll
         for (int b = 0; b < 4; ++b) s[a][b] += fv[a] * gv[b];
     }
+    buf ^= 1;
   }
   __syncthreads();
   // fold the tile along anti-diagonals: coefficient (ta*4+a) + (tb*4+b)
@@ -230,6 +250,157 @@ gr_dotsum_kernel(LinOperand F, LinOperand G, int64_t rows, int64_t rows_per_bloc
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * D - 1; i += 256)
     if (sP[i]) atomicAdd(acc + i, sP[i]);
+}
+
+// ---------------------------------------------------------------------------
+// One party's h(1)/h(2) folds of a dense reduction level in ONE pass
+// (verify.py:223-230 + gates.py:100-106).  With F from the x side and G from
+// the y side, the party's leg products are
+//     h = FA (x) (c3 GA + c1 GB) + c2 FB (x) GA
+// (P0: FA = x.total, GA = y.total, c3 = 1; P1: c1 = c2 = -1 over m / s1;
+//  P2: c3 = 1, c1 = c2 = -1 over m / s2), with F = f1 (odd rows) for h(1)
+// and F = 2 f1 - f0 for h(2) (same for G).  The four component arrays stream
+// through a 3-stage cp.async pipeline (odd and even row of each pair, zero
+// fill past the end = the reference's zero pad); threads [0,256) own 4x4
+// tiles of h(1), threads [256,512) of h(2).
+// ---------------------------------------------------------------------------
+struct LevelArrays {
+  const u64* xa;
+  const u64* xb;
+  const u64* ya;
+  const u64* yb;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int D, int ROLE>
+__global__ void __launch_bounds__(512, 1)
+level_fold_kernel(LevelArrays A, int64_t N, int64_t pairs_per_block, u64* __restrict__ out1, u64* __restrict__ out2) {
+  constexpr int NARR = ROLE == 0 ? 2 : 4;  // xa, ya (+ xb, yb)
+  constexpr int BK = 8;                    // pairs per stage
+  constexpr int STAGES = 3;
+  constexpr int ROWW = 2 * D;              // odd + even row, in words
+  constexpr int STAGE_WORDS = NARR * BK * ROWW;
+  constexpr int CG = D / 4, TILES = CG * CG, GROUPS = 256 / TILES;
+  extern __shared__ __align__(16) u64 sm[];
+  u64* stage_base = sm;                              // [STAGES][NARR][BK][2][D]
+  u64* sP = sm + STAGES * STAGE_WORDS;               // [2][2D]
+  const int tid = threadIdx.x;
+  const int which = tid >> 8;                        // 0: h(1), 1: h(2)
+  const int t8 = tid & 255;
+  const int grp = t8 / TILES, tile = t8 % TILES;
+  const int ta = tile / CG, tb = tile % CG;
+  for (int i = tid; i < 4 * D; i += 512) sP[i] = 0;
+  const int64_t npairs = (N + 1) / 2;
+  const int64_t p_begin = blockIdx.x * pairs_per_block;
+  const int64_t p_end = min(npairs, p_begin + pairs_per_block);
+  const int64_t nst = (p_end - p_begin + BK - 1) / BK;
+  const u64* arr[4] = {A.xa, A.ya, A.xb, A.yb};
+
+  auto issue = [&](int64_t st) {
+    if (st < nst) {
+      u64* dst = stage_base + (st % STAGES) * STAGE_WORDS;
+      constexpr int CHUNKS = STAGE_WORDS / 2;        // 16-byte chunks
+      for (int c = tid; c < CHUNKS; c += 512) {
+        const int w = c * 2;
+        const int a = w / (BK * ROWW);
+        const int rem = w % (BK * ROWW);
+        const int pr = rem / ROWW, half = (rem % ROWW) / D, k = rem % D;  // half 0: odd, 1: even
+        const int64_t pj = p_begin + st * BK + pr;
+        const int64_t row = 2 * pj + (half == 0 ? 1 : 0);
+        const bool ok = pj < p_end && row < N;
+        cp_async16(dst + w, ok ? arr[a] + row * D + k : arr[a], ok);
+      }
+    }
+    cp_async_commit();
+  };
+
+  u64 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0;
+
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) issue(s0);
+  for (int64_t st = 0; st < nst; ++st) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue(st + STAGES - 1);
+    const u64* cur = stage_base + (st % STAGES) * STAGE_WORDS;
+    for (int pr = grp; pr < BK; pr += GROUPS) {
+      // F/G vectors (4 coefficients each) for this thread's tile
+      u64 fa[4], fb[4], ga[4], gb[4];
+      auto ld4 = [&](int a, int half, int off, u64 (&v)[4]) {
+        const u64* src = cur + (a * BK + pr) * ROWW + half * D + off;
+        ulonglong2 v01 = *reinterpret_cast<const ulonglong2*>(src);
+        ulonglong2 v23 = *reinterpret_cast<const ulonglong2*>(src + 2);
+        v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
+      };
+      ld4(0, 0, ta * 4, fa);
+      ld4(1, 0, tb * 4, ga);
+      if (ROLE != 0) {
+        ld4(2, 0, ta * 4, fb);
+        ld4(3, 0, tb * 4, gb);
+      }
+      if (which == 1) {  // f2 = 2 f1 - f0
+        u64 e[4];
+        ld4(0, 1, ta * 4, e);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fa[q] = 2 * fa[q] - e[q];
+        ld4(1, 1, tb * 4, e);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ga[q] = 2 * ga[q] - e[q];
+        if (ROLE != 0) {
+          ld4(2, 1, ta * 4, e);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) fb[q] = 2 * fb[q] - e[q];
+          ld4(3, 1, tb * 4, e);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) gb[q] = 2 * gb[q] - e[q];
+        }
+      }
+      if (ROLE == 0) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] += fa[a] * ga[b];
+      } else {
+        u64 gp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gp[q] = (ROLE == 2 ? ga[q] : 0ull) - gb[q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] += fa[a] * gp[b] - fb[a] * ga[b];
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  u64 diag[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) diag[q] = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) diag[a + b] += acc[a][b];
+  const int base = ta * 4 + tb * 4;
+  u64* myP = sP + which * 2 * D;
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+    if (base + q < 2 * D - 1 && diag[q]) atomicAdd(&myP[base + q], diag[q]);
+  __syncthreads();
+  for (int i = tid; i < 2 * D - 1; i += 512) {
+    if (sP[i]) atomicAdd(out1 + i, sP[i]);
+    if (sP[2 * D + i]) atomicAdd(out2 + i, sP[2 * D + i]);
+  }
 }
 
 // small-degree fallback (D in {1,2,4}): thread per row, full product in regs
@@ -527,16 +698,28 @@ extern "C" int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, in
     if (d == 4) gr_dotsum_small_kernel<4><<<grid, 256, 0, s>>>(lf, lg, rows, (u64*)acc);
     return check_launch("r3_gr_dotsum(small)");
   }
-  int64_t blocks = int64_t(kNumSMs) * 4;
+  int64_t blocks = int64_t(kNumSMs) * 2;
   int64_t per = (rows + blocks - 1) / blocks;
   if (per < 64) per = 64;
   per = (per + 31) / 32 * 32;
   blocks = (rows + per - 1) / per;
   switch (d) {
-    case 8: gr_dotsum_kernel<8><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
-    case 16: gr_dotsum_kernel<16><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
-    case 32: gr_dotsum_kernel<32><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
-    case 64: gr_dotsum_kernel<64><<<unsigned(blocks), 256, 0, s>>>(lf, lg, rows, per, (u64*)acc); break;
+#define R3_DS(DD)                                                                                 \
+  case DD: {                                                                                      \
+    const size_t smem = size_t(4 * 32 * DD + 2 * DD) * 8;                                         \
+    static bool attr = false;                                                                     \
+    if (!attr) {                                                                                  \
+      cudaFuncSetAttribute(gr_dotsum_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                           int(smem));                                                            \
+      attr = true;                                                                                \
+    }                                                                                             \
+    gr_dotsum_kernel<DD><<<unsigned(blocks), 256, smem, s>>>(lf, lg, rows, per, (u64*)acc);      \
+  } break;
+    R3_DS(8)
+    R3_DS(16)
+    R3_DS(32)
+    R3_DS(64)
+#undef R3_DS
   }
   return check_launch("r3_gr_dotsum");
 }
@@ -660,4 +843,43 @@ extern "C" int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N,
   R3_DISPATCH_D(d, (l1_line_y_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
                        ncomp, yp, N, n, ks, ls, (const u64*)a, (const u64*)b, op, mask)));
   return check_launch("r3_vfy_l1_line_y");
+}
+
+extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* xb, const uint64_t* ya,
+                                 const uint64_t* yb, int64_t N, int d, uint64_t* acc1, uint64_t* acc2,
+                                 void* stream) {
+  if (role < 0 || role > 2 || !(d == 16 || d == 32 || d == 64) || N < 0 || !xa || !ya ||
+      (role != 0 && (!xb || !yb))) {
+    set_error("r3_vfy_level_fold: bad arguments (role=%d d=%d)", role, d);
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  cudaStream_t s = as_stream(stream);
+  LevelArrays la{(const u64*)xa, (const u64*)xb, (const u64*)ya, (const u64*)yb};
+  const int64_t npairs = (N + 1) / 2;
+  int64_t blocks = kNumSMs;
+  int64_t per = (npairs + blocks - 1) / blocks;
+  if (per < 32) per = 32;
+  per = (per + 7) / 8 * 8;
+  blocks = (npairs + per - 1) / per;
+#define R3_LF(DD, RR)                                                                                   \
+  {                                                                                                     \
+    constexpr int NARR = RR == 0 ? 2 : 4;                                                               \
+    const size_t smem = size_t(3 * NARR * 8 * 2 * DD + 4 * DD) * 8;                                     \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      cudaFuncSetAttribute(level_fold_kernel<DD, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           int(smem));                                                                  \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    level_fold_kernel<DD, RR><<<unsigned(blocks), 512, smem, s>>>(la, N, per, (u64*)acc1, (u64*)acc2); \
+  }
+#define R3_LF_D(DD)                 \
+  if (role == 0) R3_LF(DD, 0)       \
+  else if (role == 1) R3_LF(DD, 1)  \
+  else R3_LF(DD, 2)
+  if (d == 16) { R3_LF_D(16) } else if (d == 32) { R3_LF_D(32) } else { R3_LF_D(64) }
+#undef R3_LF_D
+#undef R3_LF
+  return check_launch("r3_vfy_level_fold");
 }

@@ -445,6 +445,30 @@ def _level_folds(role: int, X: dict, Y: dict, which: str, rows: int, gr: Ring) -
     return _dotsum_terms(pairs, rows, gr)
 
 
+def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring):
+    """Both folds of one party in one pass (r3_vfy_level_fold) when the
+    component arrays are dense (N, d) rows; None -> use the dot-sum path."""
+    if gr.d not in (16, 32, 64):
+        return None
+    if role == 0:
+        names = ("total", None)
+    else:
+        names = ("m", "s1" if role == 1 else "s2")
+    arrs = []
+    for side in (xt, yt):
+        for nm in names:
+            t = None if nm is None else side.get(nm)
+            if nm is not None and (t is None or not t.is_contiguous()):
+                return None
+            arrs.append(t)
+    xa, xb, ya, yb = arrs
+    N = xa.shape[0]
+    acc = grvec.zeros((2, 2 * gr.d - 1))
+    call("r3_vfy_level_fold", role, ptr(xa), ptr(xb), ptr(ya), ptr(yb), N, gr.d,
+         ptr(acc[0]), ptr(acc[1]), stream())
+    return (grvec.reduce_poly(acc[0], gr.mod, gr.ell), grvec.reduce_poly(acc[1], gr.mod, gr.ell))
+
+
 def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:
     """f0 + (f1 - f0) * zeta (verify.py:239) = f0 . M(1 - zeta) + f1 . M(zeta):
     one K-concatenated contraction on the tensor cores for d = 64; the CUDA
@@ -469,8 +493,18 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     small = gr.d < 8
     if small:  # degrees 1..4: generic kernels, materialised halves
         return _reduce_dimension_small(party, xs, ys, z, gr, zeta)
-    h1 = _gr_dot_folded(party, gr, rows, _level_folds(role, X, Y, "f1", rows, gr))
-    h2 = _gr_dot_folded(party, gr, rows, _level_folds(role, X, Y, "f2", rows, gr))
+    xt = {k: getattr(xs.mask, k) for k in names}
+    yt = {k: getattr(ys.mask, k) for k in names}
+    if xs.m is not None:
+        xt["m"], yt["m"] = xs.m, ys.m
+    fused = _level_folds_fused(role, xt, yt, gr)
+    if fused is not None:
+        fold1, fold2 = fused
+    else:
+        fold1 = _level_folds(role, X, Y, "f1", rows, gr)
+        fold2 = _level_folds(role, X, Y, "f2", rows, gr)
+    h1 = _gr_dot_folded(party, gr, rows, fold1)
+    h2 = _gr_dot_folded(party, gr, rows, fold2)
     h0 = z - h1
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
     l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)

@@ -92,3 +92,40 @@ def test_gr_matmul2_tc_line_eval(cuda, rows):
     _lib.call("r3_gr_matmul2_tc", Xd.data_ptr(), 64, rows, None, 0, 0, Mb.data_ptr(), None, out1.data_ptr(),
               rows, (1 << 64) - 1, _lib.stream())
     np.testing.assert_array_equal(host(out1), ogr.mul(X, z, 64, 64))
+
+
+@pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 40001), (16, 1000), (32, 77)])
+def test_level_fold_matches_oracle(cuda, d, N):
+    """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
+    (verify.py:220-230 + gates.py:100-106) restated with oracle/gr.py."""
+    from oracle import gr as ogr
+    from paper_2411_09287_b200 import grvec, host, _lib
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    mod = modulus_for_degree(d)
+    rng = np.random.default_rng(N + d)
+    arrs = [_rand(rng, (N, d)) for _ in range(4)]
+    xa, xb, ya, yb = arrs
+    pad = lambda a: np.concatenate([a, np.zeros((1, d), np.uint64)]) if N % 2 else a
+    with np.errstate(over="ignore"):
+        o = lambda a: pad(a)[1::2]
+        e = lambda a: pad(a)[0::2]
+        two = lambda a: 2 * o(a) - e(a)
+        dot = lambda f, g: ogr.dot(f, g, 64, d)
+        for role in (0, 1, 2):
+            if role == 0:
+                w1, w2 = dot(o(xa), o(ya)), dot(two(xa), two(ya))
+            elif role == 1:
+                w1 = 0 - dot(o(xa), o(yb)) - dot(o(xb), o(ya))
+                w2 = 0 - dot(two(xa), two(yb)) - dot(two(xb), two(ya))
+            else:
+                w1 = dot(o(xa), o(ya) - o(yb)) - dot(o(xb), o(ya))
+                w2 = dot(two(xa), two(ya) - two(yb)) - dot(two(xb), two(ya))
+            D = [grvec.dev(a) for a in arrs]
+            acc = grvec.zeros((2, 2 * d - 1))
+            _lib.call("r3_vfy_level_fold", role, D[0].data_ptr(), D[1].data_ptr() if role else None,
+                      D[2].data_ptr(), D[3].data_ptr() if role else None, N, d,
+                      acc[0].data_ptr(), acc[1].data_ptr(), _lib.stream())
+            g1 = host(grvec.reduce_poly(acc[0], mod, 64))
+            g2 = host(grvec.reduce_poly(acc[1], mod, 64))
+            np.testing.assert_array_equal(g1, w1 & np.uint64(2**64 - 1), err_msg=f"h1 role {role}")
+            np.testing.assert_array_equal(g2, w2, err_msg=f"h2 role {role}")
