@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-kernel", default="r3_gr_dotsum")
+    ap.add_argument("--profile-kernel", default="r3_vfy_level_fold")
+    ap.add_argument("--relu-log2n", type=int, default=16)
     return ap.parse_args()
 
 
@@ -194,6 +195,63 @@ def make_programs(N: int, d: int, R: int):
     return mulv, e2e
 
 
+def make_relu_program(N: int, d: int = 16):
+    """x owned by P0, relu_prepare in PRE, relu_online,
+    verify_session(d, R="auto") in POST (nonlinear.py:295-319)."""
+    from paper_2411_09287_b200 import nonlinear, verify
+    from paper_2411_09287_b200.sharing import Ring, rec, shc_input_mask, shc_input_online
+    from paper_2411_09287_b200.transport import Phase
+
+    def relu(party, xh, check):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        xm = shc_input_mask(party, 0, N, ring)
+        mat = nonlinear.relu_prepare(party, xm, N, ring)
+        if check:
+            verify.prepare_verification(party, d=d)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input_online(party, 0, xh if party.role == 0 else None, xm, N, ring, "x")
+        out = nonlinear.relu_online(party, x, mat)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        if check:
+            v = verify.verify_session(party, d=d, R="auto")
+            if not all(v.values()):
+                party.abort("verification failed")
+        else:
+            party.freeze_logs()
+        return rec(party, out, "relu")
+
+    return relu
+
+
+def relu_rates(N: int, d: int, steps: int) -> dict:
+    """Secure ReLU/s (execution and verified) on C1-shaped inputs."""
+    import numpy as np
+    import torch
+    from paper_2411_09287_b200.runtime import Session
+    rng = np.random.default_rng(1)
+    xv = np.trunc(rng.normal(0, 4, N) * 2 ** 16).astype(np.int64)
+    xh = torch.from_numpy(xv).pin_memory()
+    want = np.where(xv >= 0, xv, 0)
+    prog = make_relu_program(N, d)
+    out = {"N": N, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s"}
+    for check in (False, True):
+        Session(seed=1).run(prog, xh, check)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(steps):
+            res = Session(seed=10 + i).run(prog, xh, check)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / steps
+        got = res[0].cpu().numpy()
+        assert np.array_equal(got, want), "relu output mismatch"
+        out["verified" if check else "exec"] = N / dt
+        out[("verified" if check else "exec") + "_ms"] = dt * 1e3
+    return out
+
+
 class KernelTimer:
     """CUDA events around every launch of one library entry point, on the
     launching (current) stream."""
@@ -225,6 +283,11 @@ class KernelTimer:
 def work_of(name, args) -> int:
     """Algorithmic u64 multiply-accumulates of one call (rows x d^2 for the
     GR contractions)."""
+    if name == "r3_vfy_level_fold":
+        # per pair: h(1) and h(2), one outer product each for P0, two for P1/P2
+        role, N, d = args[0], args[5], args[6]
+        pairs = (int(N) + 1) // 2
+        return pairs * (2 if role == 0 else 4) * int(d) * int(d)
     if name == "r3_gr_dotsum":
         rows, d = args[2], args[3]
         return int(rows) * int(d) * int(d)
@@ -363,6 +426,8 @@ def run_b200(args):
         "clocks": clk.summary(),
         "wall_s_timed": wall,
     }
+    if args.relu_log2n:
+        line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
     print(json.dumps(line), flush=True)
