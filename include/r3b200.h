@@ -76,6 +76,13 @@ void r3_aes128_expand(const uint8_t key[16], uint32_t rk[44]);
 int r3_prf_ctr(const uint32_t rk[44], uint64_t first_u64, int64_t n,
                uint64_t mask, int mode, uint64_t* out, void* stream);
 
+/* Bit-packed draw_bits of an (nbits, lanes) bit matrix drawn row-major from
+ * the stream at first_u64 (gates.py:255-257 / nonlinear.py:90-92):
+ * out[l] = sum_j (keystream[first + j*lanes + l] & 1) << j.  The stream
+ * advances by nbits*lanes words exactly as the reference's draw_bits. */
+int r3_prf_bits_packed(const uint32_t rk[44], uint64_t first_u64, int nbits,
+                       int64_t lanes, uint64_t* out, void* stream);
+
 /* ---- elementwise (grvec.py:18-40; sharing.py:95-230 linear ops) ----------
  * out[idx] = op(a[idx . a_strides], b[idx . b_strides]) over an ndim<=4 index
  * space `shape` (out contiguous).  Stride 0 broadcasts.  b == NULL uses the
@@ -161,6 +168,26 @@ int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, int d,
 int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms,
                       uint64_t* out, uint64_t mask, int accumulate,
                       void* stream);
+
+/* ---- share-domain matmul on the tensor cores (ppml.py:412-427 algebra) ----
+ * Operand preparation: value = c0*P0 + c1*P1 (P1 may be NULL) split into 8
+ * byte-limb planes laid out as UMMA-ready tiles.
+ *   A: rows x K row-major  -> [rows/128][K/32][8][128x32]   (32 KB per tile)
+ *   B: K x cols row-major  -> [cols/64][K/32][8][64x32]      (16 KB per tile)
+ * rows % 128 == 0, cols % 64 == 0, K % 32 == 0. */
+int r3_limb_tiles_a(const uint64_t* p0, uint64_t c0, const uint64_t* p1,
+                    uint64_t c1, int64_t rows, int64_t K, uint8_t* dst,
+                    void* stream);
+int r3_limb_tiles_b(const uint64_t* p0, uint64_t c0, const uint64_t* p1,
+                    uint64_t c1, int64_t K, int64_t cols, uint8_t* dst,
+                    void* stream);
+/* out = addend (+ or, sub != 0, -) sum_p A_p . B_p  mod 2^64 (masked), M x N
+ * row-major; up to 3 K-concatenated (A, B) tile pairs, total K <= 16384
+ * (exact 32-bit diagonal accumulation).  addend may be NULL. */
+int r3_u64_gemm_tc(int npairs, const uint8_t* const* a_tiles,
+                   const uint8_t* const* b_tiles, const int64_t* K, int64_t M,
+                   int64_t N, const uint64_t* addend, int sub, uint64_t* out,
+                   uint64_t mask, void* stream);
 
 /* ---- fused verification stages (verify.py:168-241) ----------------------
  * Compressed triples are never materialised (SURVEY.md finding 5): x'_i =

@@ -38,6 +38,7 @@ _SIGS = {
     "r3_imad_peak": [C.c_int, u64p, C.c_void_p],
     "r3_aes128_expand": [C.c_char_p, C.POINTER(C.c_uint32)],
     "r3_prf_ctr": [C.POINTER(C.c_uint32), u64, i64, u64, C.c_int, u64p, C.c_void_p],
+    "r3_prf_bits_packed": [C.POINTER(C.c_uint32), u64, C.c_int, i64, u64p, C.c_void_p],
     "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
               C.POINTER(i64), u64, u64, C.c_void_p],
     "r3_ars": [u64p, i64, C.c_int, C.c_int, u64p, C.c_void_p],
@@ -53,6 +54,10 @@ _SIGS = {
     "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
                      C.c_void_p],
     "r3_gr_matmul2_tc": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
+    "r3_limb_tiles_a": [u64p, u64, u64p, u64, i64, i64, u64p, C.c_void_p],
+    "r3_limb_tiles_b": [u64p, u64, u64p, u64, i64, i64, u64p, C.c_void_p],
+    "r3_u64_gemm_tc": [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(i64), i64,
+                       i64, u64p, C.c_int, u64p, u64, C.c_void_p],
     "r3_gr_dotsum": [LinOperand, LinOperand, i64, C.c_int, u64p, C.c_void_p],
     "r3_gr_reduce_poly": [u64p, C.c_int, u64, u64p, u64, C.c_int, C.c_void_p],
     "r3_vfy_powsum": [C.c_int, C.POINTER(C.c_void_p), i64, i64, u64p, C.c_int, u64p, u64,

@@ -1,0 +1,314 @@
+// Share-domain matmul over Z_2^64 on the tensor cores (BASELINE config C3).
+//
+// The reference evaluates a linear layer as one gathered Pi_dot (ppml.py:
+// 412-427 + gates.py:52-117): with X (M x K), W (K x N) and lanes m*N + n,
+//   P0:  Gamma = R_X R_W + r_z
+//   P1:  leg   = Gamma_1 - M_X R_W1 - R_X1 M_W
+//   P2:  leg   = M_X (M_W - R_W2) - R_X2 M_W + Gamma_2
+// i.e. every party's work is one or two u64 GEMMs (K-concatenated here).  Each
+// u64 GEMM runs as byte-limb int8 GEMMs (tc.cu header comment): operands are
+// first split into 8 limb planes laid out as ready-to-copy UMMA tiles
+// (r3_limb_tiles_a / _b), then r3_u64_gemm_tc streams tiles with bulk async
+// copies (cp.async.bulk + mbarrier complete_tx) through a 4-stage ring,
+// issues the 36 surviving limb MMAs per 32-wide K step from one thread into
+// 8 TMEM diagonal accumulators, and an epilogue recombines the diagonals in
+// u64 and applies out = addend +/- sum.
+//
+// Exactness: the K-concatenated depth is <= 16384, so every diagonal sum
+// (s+1) K 255^2 < 2^32 is held exactly by the 32-bit accumulator.
+#include "tc_common.cuh"
+
+namespace r3 {
+
+constexpr int MM_BM = 128, MM_BN = 64, MM_BK = 32;        // tile: rows x cols x K bytes
+constexpr int MM_A_PLANE = MM_BM * MM_BK;                  // 4 KB
+constexpr int MM_B_PLANE = MM_BN * MM_BK;                  // 2 KB
+constexpr int MM_A_TILE = 8 * MM_A_PLANE;                  // 32 KB
+constexpr int MM_B_TILE = 8 * MM_B_PLANE;                  // 16 KB
+constexpr int MM_STAGES = 4;
+constexpr int MM_THREADS = 6 * 32;                         // producer, MMA, 4 epilogue
+constexpr int MM_SMEM = MM_STAGES * (MM_A_TILE + MM_B_TILE) + 256;
+
+// 16 u64 -> 8 planes of 16 bytes (limb i of each value)
+__device__ __forceinline__ void split16(const u64 (&v)[16], uint4 (&out)[8]) {
+  uint32_t w[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    w[2 * q] = uint32_t(v[q]);
+    w[2 * q + 1] = uint32_t(v[q] >> 32);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int hiw = i >> 2, bi = i & 3;
+    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
+    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
+    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
+    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
+  }
+}
+
+// A operand (rows x K, row-major u64, value = c0*P0 + c1*P1) -> tiles
+// [mb][kb][plane][128 x 32 core layout]
+__global__ void limb_tiles_a_kernel(const u64* __restrict__ p0, u64 c0, const u64* __restrict__ p1, u64 c1,
+                                    int64_t rows, int64_t K, uint8_t* __restrict__ dst) {
+  const int64_t kchunks = K / 16;
+  const int64_t total = rows * kchunks;
+  const int64_t KB = K / MM_BK;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = t % rows, kc = t / rows;       // consecutive threads: consecutive rows
+    u64 v[16];
+    const u64* s0 = p0 + row * K + kc * 16;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = c0 * __ldg(s0 + q);
+    if (p1) {
+      const u64* s1 = p1 + row * K + kc * 16;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += c1 * __ldg(s1 + q);
+    }
+    uint4 pk[8];
+    split16(v, pk);
+    const int64_t mb = row / MM_BM, kb = (kc * 16) / MM_BK;
+    uint8_t* tile = dst + (mb * KB + kb) * MM_A_TILE;
+    const uint32_t off = core_off(int(row % MM_BM), int((kc * 16) % MM_BK), MM_BM / 8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(tile + i * MM_A_PLANE + off) = pk[i];
+  }
+}
+
+// B operand (K x cols, row-major u64, value = c0*P0 + c1*P1) -> K-major tiles
+// [nb][kb][plane][64 x 32 core layout], B_j[n][k] = limb j of B[k][n]
+__global__ void limb_tiles_b_kernel(const u64* __restrict__ p0, u64 c0, const u64* __restrict__ p1, u64 c1,
+                                    int64_t K, int64_t cols, uint8_t* __restrict__ dst) {
+  const int64_t kchunks = K / 16;
+  const int64_t total = cols * kchunks;
+  const int64_t KB = K / MM_BK;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = t % cols, kc = t / cols;         // consecutive threads: consecutive columns
+    u64 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t k = kc * 16 + q;
+      u64 x = c0 * __ldg(p0 + k * cols + n);
+      if (p1) x += c1 * __ldg(p1 + k * cols + n);
+      v[q] = x;
+    }
+    uint4 pk[8];
+    split16(v, pk);
+    const int64_t nb = n / MM_BN, kb = (kc * 16) / MM_BK;
+    uint8_t* tile = dst + (nb * KB + kb) * MM_B_TILE;
+    const uint32_t off = core_off(int(n % MM_BN), int((kc * 16) % MM_BK), MM_BN / 8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(tile + i * MM_B_PLANE + off) = pk[i];
+  }
+}
+
+struct GemmPairs {
+  const uint8_t* a[3];
+  const uint8_t* b[3];
+  int64_t kb[3];   // K / 32 of each pair
+  int n;
+};
+
+__global__ void __launch_bounds__(MM_THREADS, 1)
+u64_gemm_tc_kernel(GemmPairs P, int64_t M, int64_t N, const u64* __restrict__ addend, int sub,
+                   u64* __restrict__ out, u64 mask) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + MM_STAGES * MM_A_TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MM_STAGES * (MM_A_TILE + MM_B_TILE));
+  uint64_t* full = bars;                       // [STAGES]
+  uint64_t* empty = bars + MM_STAGES;          // [STAGES]
+  uint64_t* tfull = bars + 2 * MM_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4 * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t mtiles = M / MM_BM, ntiles = N / MM_BN, tiles = mtiles * ntiles;
+
+  if (warp == 0) {
+    // ---------------- producer: bulk copies of pre-split tiles
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph[MM_STAGES] = {0, 0, 0, 0};
+      int64_t it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t mb = t % mtiles, nb = t / mtiles;   // neighbouring CTAs share B tiles
+        for (int p = 0; p < P.n; ++p) {
+          for (int64_t kb = 0; kb < P.kb[p]; ++kb, ++it) {
+            if (it >= MM_STAGES) {
+              mbar_wait(&empty[stage], ph[stage]);
+              ph[stage] ^= 1;
+            }
+            mbar_expect_tx(&full[stage], MM_A_TILE + MM_B_TILE);
+            bulk_copy_g2s(sA + stage * MM_A_TILE, P.a[p] + (mb * P.kb[p] + kb) * MM_A_TILE, MM_A_TILE,
+                          &full[stage]);
+            bulk_copy_g2s(sB + stage * MM_B_TILE, P.b[p] + (nb * P.kb[p] + kb) * MM_B_TILE, MM_B_TILE,
+                          &full[stage]);
+            stage = (stage + 1) % MM_STAGES;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    constexpr uint32_t IDESC = idesc_u8(MM_BM, MM_BN);
+    int stage = 0;
+    uint32_t ph[MM_STAGES] = {0, 0, 0, 0};
+    uint32_t tph = 0;
+    bool first = true;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      if (!first) {
+        mbar_wait(tempty, tph);
+        tph ^= 1;
+      }
+      first = false;
+      tc_fence_after();
+      bool fresh = true;
+      for (int p = 0; p < P.n; ++p) {
+        for (int64_t kb = 0; kb < P.kb[p]; ++kb) {
+          mbar_wait(&full[stage], ph[stage]);
+          ph[stage] ^= 1;
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sA + stage * MM_A_TILE);
+            const uint32_t b0 = smem_u32(sB + stage * MM_B_TILE);
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+#pragma unroll
+              for (int i = 0; i <= s; ++i) {
+                const uint64_t ad = umma_desc(a0 + i * MM_A_PLANE, (MM_BM / 8) * 128, 128);
+                const uint64_t bd = umma_desc(b0 + (s - i) * MM_B_PLANE, (MM_BN / 8) * 128, 128);
+                mma_u8(tmem + uint32_t(s * MM_BN), ad, bd, IDESC, (fresh && i == 0) ? 0u : 1u);
+              }
+            }
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          fresh = false;
+          stage = (stage + 1) % MM_STAGES;
+        }
+      }
+      if (lane == 0) mma_commit(tfull);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 -> TMEM lane quadrants 2,3,0,1
+    const int quad = warp & 3;
+    uint32_t tph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int64_t mb = t % mtiles, nb = t / mtiles;
+      mbar_wait(tfull, tph);
+      tph ^= 1;
+      tc_fence_after();
+      const int64_t row = mb * MM_BM + quad * 32 + lane;
+      const uint32_t lane_base = tmem + (uint32_t(quad * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < MM_BN; c0 += 8) {
+        uint32_t v[8][8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * MM_BN + c0), v[s]);
+        tmem_wait_ld();
+        u64* o = out + row * N + nb * MM_BN + c0;
+        const u64* ad = addend ? addend + row * N + nb * MM_BN + c0 : nullptr;
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          u64 x[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            u64 a = 0;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) a += u64(v[s][q + h]) << (8 * s);
+            const u64 base = ad ? ad[q + h] : 0ull;
+            x[h] = (sub ? base - a : base + a) & mask;
+          }
+          *reinterpret_cast<ulonglong2*>(o + q) = make_ulonglong2(x[0], x[1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+extern "C" int r3_limb_tiles_a(const uint64_t* p0, uint64_t c0, const uint64_t* p1, uint64_t c1, int64_t rows,
+                               int64_t K, uint8_t* dst, void* stream) {
+  if (!p0 || !dst || rows % MM_BM || K % MM_BK || rows <= 0) {
+    set_error("r3_limb_tiles_a: rows %% 128 and K %% 32 must be 0");
+    return R3_ERR_ARG;
+  }
+  limb_tiles_a_kernel<<<grid_for(rows * (K / 16), 256), 256, 0, as_stream(stream)>>>(
+      (const u64*)p0, c0, (const u64*)p1, c1, rows, K, dst);
+  return check_launch("r3_limb_tiles_a");
+}
+
+extern "C" int r3_limb_tiles_b(const uint64_t* p0, uint64_t c0, const uint64_t* p1, uint64_t c1, int64_t K,
+                               int64_t cols, uint8_t* dst, void* stream) {
+  if (!p0 || !dst || cols % MM_BN || K % MM_BK || cols <= 0) {
+    set_error("r3_limb_tiles_b: cols %% 64 and K %% 32 must be 0");
+    return R3_ERR_ARG;
+  }
+  limb_tiles_b_kernel<<<grid_for(cols * (K / 16), 256), 256, 0, as_stream(stream)>>>(
+      (const u64*)p0, c0, (const u64*)p1, c1, K, cols, dst);
+  return check_launch("r3_limb_tiles_b");
+}
+
+extern "C" int r3_u64_gemm_tc(int npairs, const uint8_t* const* a_tiles, const uint8_t* const* b_tiles,
+                              const int64_t* K, int64_t M, int64_t N, const uint64_t* addend, int sub,
+                              uint64_t* out, uint64_t mask, void* stream) {
+  if (npairs < 1 || npairs > 3 || M % MM_BM || N % MM_BN || M <= 0 || N <= 0) {
+    set_error("r3_u64_gemm_tc: need 1..3 pairs, M %% 128 == 0, N %% 64 == 0");
+    return R3_ERR_ARG;
+  }
+  GemmPairs gp{};
+  int64_t ktot = 0;
+  for (int p = 0; p < npairs; ++p) {
+    if (K[p] % MM_BK || K[p] <= 0) {
+      set_error("r3_u64_gemm_tc: K %% 32 must be 0");
+      return R3_ERR_ARG;
+    }
+    gp.a[p] = a_tiles[p];
+    gp.b[p] = b_tiles[p];
+    gp.kb[p] = K[p] / MM_BK;
+    ktot += K[p];
+  }
+  gp.n = npairs;
+  if (ktot > 16384) {
+    set_error("r3_u64_gemm_tc: concatenated K %lld exceeds the exact-accumulation bound 16384",
+              (long long)ktot);
+    return R3_ERR_ARG;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(u64_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MM_SMEM);
+    attr = true;
+  }
+  const int64_t tiles = (M / MM_BM) * (N / MM_BN);
+  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  u64_gemm_tc_kernel<<<grid, MM_THREADS, MM_SMEM, as_stream(stream)>>>(gp, M, N, (const u64*)addend, sub,
+                                                                        (u64*)out, mask);
+  return check_launch("r3_u64_gemm_tc");
+}

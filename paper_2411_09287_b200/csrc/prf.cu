@@ -55,44 +55,58 @@ __device__ __forceinline__ u32 bswap32(u32 x) { return __byte_perm(x, 0, 0x0123)
 
 constexpr int kPrfThreads = 256;
 
-__global__ void __launch_bounds__(kPrfThreads)
-prf_ctr_kernel(RoundKeys rk, u64 first, int64_t n, u64 mask, int mode, u64* __restrict__ out) {
-  // T[x*32 + lane] = Te0[x]: lane-private bank, conflict-free lookups.
-  __shared__ u32 T[256 * 32];
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) T[i] = te0_of(d_sbox[i >> 5]);
-  __syncthreads();
-  const u32 lane = threadIdx.x & 31;
-  const u32* Tl = T + lane;
+// AES-128 of the counter block BE128(ctr) with the per-lane replicated
+// T-table Tl (= T + lane); returns the two little-endian keystream words.
+__device__ __forceinline__ void aes_ctr_words(const RoundKeys& rk, const u32* Tl, u64 ctr, u64& lo, u64& hi) {
 #define TE0(x) Tl[(x) << 5]
 #define TE1(x) __funnelshift_r(TE0(x), TE0(x), 8)
 #define TE2(x) __funnelshift_r(TE0(x), TE0(x), 16)
 #define TE3(x) __funnelshift_r(TE0(x), TE0(x), 24)
 #define SB(x) ((TE0(x) >> 8) & 0xffu)
+  u32 s0 = rk.w[0];
+  u32 s1 = rk.w[1];
+  u32 s2 = u32(ctr >> 32) ^ rk.w[2];
+  u32 s3 = u32(ctr) ^ rk.w[3];
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    u32 t0 = TE0(s0 >> 24) ^ TE1((s1 >> 16) & 0xff) ^ TE2((s2 >> 8) & 0xff) ^ TE3(s3 & 0xff) ^ rk.w[4 * r + 0];
+    u32 t1 = TE0(s1 >> 24) ^ TE1((s2 >> 16) & 0xff) ^ TE2((s3 >> 8) & 0xff) ^ TE3(s0 & 0xff) ^ rk.w[4 * r + 1];
+    u32 t2 = TE0(s2 >> 24) ^ TE1((s3 >> 16) & 0xff) ^ TE2((s0 >> 8) & 0xff) ^ TE3(s1 & 0xff) ^ rk.w[4 * r + 2];
+    u32 t3 = TE0(s3 >> 24) ^ TE1((s0 >> 16) & 0xff) ^ TE2((s1 >> 8) & 0xff) ^ TE3(s2 & 0xff) ^ rk.w[4 * r + 3];
+    s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+  }
+  u32 o0 = (SB(s0 >> 24) << 24) ^ (SB((s1 >> 16) & 0xff) << 16) ^ (SB((s2 >> 8) & 0xff) << 8) ^ SB(s3 & 0xff) ^ rk.w[40];
+  u32 o1 = (SB(s1 >> 24) << 24) ^ (SB((s2 >> 16) & 0xff) << 16) ^ (SB((s3 >> 8) & 0xff) << 8) ^ SB(s0 & 0xff) ^ rk.w[41];
+  u32 o2 = (SB(s2 >> 24) << 24) ^ (SB((s3 >> 16) & 0xff) << 16) ^ (SB((s0 >> 8) & 0xff) << 8) ^ SB(s1 & 0xff) ^ rk.w[42];
+  u32 o3 = (SB(s3 >> 24) << 24) ^ (SB((s0 >> 16) & 0xff) << 16) ^ (SB((s1 >> 8) & 0xff) << 8) ^ SB(s2 & 0xff) ^ rk.w[43];
+#undef TE0
+#undef TE1
+#undef TE2
+#undef TE3
+#undef SB
+  // keystream bytes are o0..o3 big-endian; u64 halves are little-endian reads
+  lo = u64(bswap32(o0)) | (u64(bswap32(o1)) << 32);
+  hi = u64(bswap32(o2)) | (u64(bswap32(o3)) << 32);
+}
 
+__device__ __forceinline__ void load_ttable(u32* T) {
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) T[i] = te0_of(d_sbox[i >> 5]);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPrfThreads)
+prf_ctr_kernel(RoundKeys rk, u64 first, int64_t n, u64 mask, int mode, u64* __restrict__ out) {
+  // T[x*32 + lane] = Te0[x]: lane-private bank, conflict-free lookups.
+  __shared__ u32 T[256 * 32];
+  load_ttable(T);
+  const u32* Tl = T + (threadIdx.x & 31);
   const u64 b0 = first >> 1;
   const u64 b_end = (first + u64(n) + 1) >> 1;
   const u64 nb = b_end - b0;
   for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < nb; t += u64(gridDim.x) * blockDim.x) {
     const u64 ctr = b0 + t;
-    u32 s0 = rk.w[0];
-    u32 s1 = rk.w[1];
-    u32 s2 = u32(ctr >> 32) ^ rk.w[2];
-    u32 s3 = u32(ctr) ^ rk.w[3];
-#pragma unroll
-    for (int r = 1; r < 10; ++r) {
-      u32 t0 = TE0(s0 >> 24) ^ TE1((s1 >> 16) & 0xff) ^ TE2((s2 >> 8) & 0xff) ^ TE3(s3 & 0xff) ^ rk.w[4 * r + 0];
-      u32 t1 = TE0(s1 >> 24) ^ TE1((s2 >> 16) & 0xff) ^ TE2((s3 >> 8) & 0xff) ^ TE3(s0 & 0xff) ^ rk.w[4 * r + 1];
-      u32 t2 = TE0(s2 >> 24) ^ TE1((s3 >> 16) & 0xff) ^ TE2((s0 >> 8) & 0xff) ^ TE3(s1 & 0xff) ^ rk.w[4 * r + 2];
-      u32 t3 = TE0(s3 >> 24) ^ TE1((s0 >> 16) & 0xff) ^ TE2((s1 >> 8) & 0xff) ^ TE3(s2 & 0xff) ^ rk.w[4 * r + 3];
-      s0 = t0; s1 = t1; s2 = t2; s3 = t3;
-    }
-    u32 o0 = (SB(s0 >> 24) << 24) ^ (SB((s1 >> 16) & 0xff) << 16) ^ (SB((s2 >> 8) & 0xff) << 8) ^ SB(s3 & 0xff) ^ rk.w[40];
-    u32 o1 = (SB(s1 >> 24) << 24) ^ (SB((s2 >> 16) & 0xff) << 16) ^ (SB((s3 >> 8) & 0xff) << 8) ^ SB(s0 & 0xff) ^ rk.w[41];
-    u32 o2 = (SB(s2 >> 24) << 24) ^ (SB((s3 >> 16) & 0xff) << 16) ^ (SB((s0 >> 8) & 0xff) << 8) ^ SB(s1 & 0xff) ^ rk.w[42];
-    u32 o3 = (SB(s3 >> 24) << 24) ^ (SB((s0 >> 16) & 0xff) << 16) ^ (SB((s1 >> 8) & 0xff) << 8) ^ SB(s2 & 0xff) ^ rk.w[43];
-    // keystream bytes are o0..o3 big-endian; u64 halves are little-endian reads
-    u64 lo = u64(bswap32(o0)) | (u64(bswap32(o1)) << 32);
-    u64 hi = u64(bswap32(o2)) | (u64(bswap32(o3)) << 32);
+    u64 lo, hi;
+    aes_ctr_words(rk, Tl, ctr, lo, hi);
     if (mode == 1) { lo &= 1ull; hi &= 1ull; } else { lo &= mask; hi &= mask; }
     const int64_t i0 = int64_t(2 * ctr - first);
     if (i0 >= 0 && i0 + 1 < n && (((uintptr_t)(out + i0)) & 15) == 0) {
@@ -102,11 +116,41 @@ prf_ctr_kernel(RoundKeys rk, u64 first, int64_t n, u64 mask, int mode, u64* __re
       if (i0 + 1 >= 0 && i0 + 1 < n) out[i0 + 1] = hi;
     }
   }
-#undef TE0
-#undef TE1
-#undef TE2
-#undef TE3
-#undef SB
+}
+
+// Bit-packed draw_bits of an (nbits, lanes) matrix (gates.py:255-257,
+// nonlinear.py:90-92): out[l] = sum_j (word(first + j*lanes + l) & 1) << j.
+// When first and lanes are even one AES block serves lanes (2p, 2p+1).
+__global__ void __launch_bounds__(kPrfThreads)
+prf_bits_packed_kernel(RoundKeys rk, u64 first, int nbits, int64_t lanes, u64* __restrict__ out) {
+  __shared__ u32 T[256 * 32];
+  load_ttable(T);
+  const u32* Tl = T + (threadIdx.x & 31);
+  const bool paired = ((first | u64(lanes)) & 1) == 0;
+  const int64_t units = paired ? lanes / 2 : lanes;
+  for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < units; u += int64_t(gridDim.x) * blockDim.x) {
+    if (paired) {
+      const int64_t l0 = 2 * u;
+      u64 a0 = 0, a1 = 0;
+      for (int j = 0; j < nbits; ++j) {
+        const u64 w = first + u64(j) * u64(lanes) + u64(l0);
+        u64 lo, hi;
+        aes_ctr_words(rk, Tl, w >> 1, lo, hi);
+        a0 |= (lo & 1ull) << j;
+        a1 |= (hi & 1ull) << j;
+      }
+      *reinterpret_cast<ulonglong2*>(out + l0) = make_ulonglong2(a0, a1);
+    } else {
+      u64 a = 0;
+      for (int j = 0; j < nbits; ++j) {
+        const u64 w = first + u64(j) * u64(lanes) + u64(u);
+        u64 lo, hi;
+        aes_ctr_words(rk, Tl, w >> 1, lo, hi);
+        a |= (((w & 1) ? hi : lo) & 1ull) << j;
+      }
+      out[u] = a;
+    }
+  }
 }
 
 }  // namespace r3
@@ -185,4 +229,20 @@ extern "C" int r3_prf_ctr(const uint32_t rk[44], uint64_t first_u64, int64_t n, 
   prf_ctr_kernel<<<grid, kPrfThreads, 0, as_stream(stream)>>>(k, first_u64, n, mask, mode,
                                                               reinterpret_cast<u64*>(out));
   return check_launch("r3_prf_ctr");
+}
+
+extern "C" int r3_prf_bits_packed(const uint32_t rk[44], uint64_t first_u64, int nbits, int64_t lanes,
+                                  uint64_t* out, void* stream) {
+  if (!rk || !out || nbits < 1 || nbits > 64 || lanes < 0) {
+    set_error("r3_prf_bits_packed: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (lanes == 0) return R3_OK;
+  RoundKeys k;
+  memcpy(k.w, rk, sizeof(k.w));
+  const bool paired = ((first_u64 | uint64_t(lanes)) & 1) == 0;
+  const int64_t units = paired ? lanes / 2 : lanes;
+  prf_bits_packed_kernel<<<grid_for(units, kPrfThreads, 7), kPrfThreads, 0, as_stream(stream)>>>(
+      k, first_u64, nbits, lanes, reinterpret_cast<u64*>(out));
+  return check_launch("r3_prf_bits_packed");
 }

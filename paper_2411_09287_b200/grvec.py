@@ -429,3 +429,38 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
     tmp = gr_matmul(lin((1, P1), nvalid=[n1]), M1, rows, d, width)
     return gr_matmul(lin((1, P0), nvalid=[n0]), M0, rows, d, width,
                      C_add=lin((1, tmp)), out=out)
+
+
+# ---------------------------------------------------------------------------
+# u64 GEMM on the tensor cores (share-domain matmul)
+# ---------------------------------------------------------------------------
+
+def limb_tiles_a(P0: torch.Tensor, c0: int = 1, P1: torch.Tensor | None = None, c1: int = 0):
+    """rows x K operand (c0 P0 + c1 P1) -> UMMA-ready byte-limb tiles."""
+    rows, K = P0.shape
+    dst = torch.empty(rows * K * 8, dtype=torch.uint8, device=P0.device)
+    call("r3_limb_tiles_a", ptr(P0.contiguous()), _scalar(c0),
+         ptr(P1.contiguous()) if P1 is not None else None, _scalar(c1), rows, K, ptr(dst), stream())
+    return dst
+
+
+def limb_tiles_b(P0: torch.Tensor, c0: int = 1, P1: torch.Tensor | None = None, c1: int = 0):
+    """K x cols operand (c0 P0 + c1 P1) -> K-major byte-limb tiles."""
+    K, cols = P0.shape
+    dst = torch.empty(K * cols * 8, dtype=torch.uint8, device=P0.device)
+    call("r3_limb_tiles_b", ptr(P0.contiguous()), _scalar(c0),
+         ptr(P1.contiguous()) if P1 is not None else None, _scalar(c1), K, cols, ptr(dst), stream())
+    return dst
+
+
+def u64_gemm(pairs, M: int, N: int, width: int = 64, addend: torch.Tensor | None = None,
+             sub: bool = False) -> torch.Tensor:
+    """addend +/- sum_p A_p . B_p over Z_2^width; pairs = [(a_tiles, b_tiles, K)]."""
+    out = empty((M, N))
+    a = (C.c_void_p * len(pairs))(*[ptr(p[0]) for p in pairs])
+    b = (C.c_void_p * len(pairs))(*[ptr(p[1]) for p in pairs])
+    k = (C.c_int64 * len(pairs))(*[p[2] for p in pairs])
+    call("r3_u64_gemm_tc", len(pairs), a, b, k, M, N,
+         ptr(addend.contiguous()) if addend is not None else None, 1 if sub else 0,
+         ptr(out), ring_mask(width), stream())
+    return out

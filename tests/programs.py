@@ -112,6 +112,26 @@ def build(pkg_name: str) -> SimpleNamespace:
             out["rz_clear"] = mat.rz_clear
         return out
 
+    def trunc_verify(party, xv, t, d):
+        """Truncation whose two logged bit inner products (gates.py:237-238)
+        are then batch-verified (verify.py:294-303) with the multiplication."""
+        ring = Ring(64)
+        lanes = len(xv)
+        party.enter_phase(Phase.PRE)
+        mat = gates.trunc_prepare(party, lanes, t, ring)
+        verify.prepare_verification(party, d=d)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input(party, 0, np.asarray(xv, dtype=np.uint64)
+                      if party.role == 0 else None, lanes, ring, "x")
+        one = MVal.public(ring, party.role, np.ones(lanes, dtype=np.uint64))
+        g = gates.mul_prepare(party, x.mask, one.mask, lanes, out_mask=mat.rx_mask)
+        z = gates.trunc_online(party, gates.mul_finish(party, g, x, one), mat)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        v = verify.verify_session(party, d=d, R="auto")
+        return {"z": z, "verdict": v, "open": rec(party, z, "z")}
+
     def dotv(party, n, lanes, d, R):
         """Batched inner products + Pi_bsv (test_verify.py:17-42 dot branch)."""
         ring = Ring(64)
@@ -208,8 +228,33 @@ def build(pkg_name: str) -> SimpleNamespace:
         party.freeze_logs()
         return {"z": z, "open": rec(party, z, "z")}
 
-    return SimpleNamespace(mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
-                           trunc=trunc, dotv=dotv, relu=relu,
+    def matmul_gemm(party, Xv, Wv, t=16):
+        """The matmul program through the GEMM-form gate API
+        (paper_2411_09287_b200 only: gates.matmul_prepare / matmul_finish);
+        must reproduce the gathered-dot golden run exactly."""
+        ring = Ring(64)
+        M, K = Xv.shape
+        N = Wv.shape[1]
+        party.enter_phase(Phase.PRE)
+        xmask = shc_input_mask(party, 2, M * K, ring)
+        wmask = shc_input_mask(party, 1, K * N, ring)
+        tr = gates.trunc_prepare(party, M * N, t, ring)
+        g = gates.matmul_prepare(party, xmask, wmask, M, K, N, out_mask=tr.rx_mask)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        X = shc_input_online(party, 2, Xv.reshape(-1) if party.role == 2 else None,
+                             xmask, M * K, ring, "X")
+        W = shc_input_online(party, 1, Wv.reshape(-1) if party.role == 1 else None,
+                             wmask, K * N, ring, "W")
+        prod = gates.matmul_finish(party, g, X, W)
+        party.round_barrier()
+        z = gates.trunc_online(party, prod, tr)
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return {"z": z, "open": rec(party, z, "z")}
+
+    return SimpleNamespace(matmul_gemm=matmul_gemm, mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
+                           trunc=trunc, trunc_verify=trunc_verify, dotv=dotv, relu=relu,
                            a2b_roundtrip=a2b_roundtrip, matmul=matmul)
 
 
@@ -251,6 +296,7 @@ CASES = [
     ("bool_mulv_40_d16_R2", "bool_mulv", (40, 16, 2), {}, {"seed": 0, "ell": 1}),
     ("trunc_small", "trunc", ([98304, 0, (-98304) % 2 ** 64, 12345 << 16], 16), {}, {"seed": 3}),
     ("trunc_1000", "trunc", (_trunc_inputs(1000, 6), 16), {}, {"seed": 66}),
+    ("trunc_verify_200_d16", "trunc_verify", (_trunc_inputs(200, 12), 16, 16), {}, {"seed": 12}),
     ("dotv_8x16_d16_R2", "dotv", (8, 16, 16, 2), {}, {"seed": 4}),
     ("relu_64", "relu", (_relu_inputs(64, 1),), {}, {"seed": 1}),
     ("a2b_roundtrip_ell8", "a2b_roundtrip", (list(range(16)), 8), {}, {"seed": 0, "ell": 8}),

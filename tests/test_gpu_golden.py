@@ -41,7 +41,7 @@ def _flatten(role, res, out, prefix, MVal, host):
     out["arrays"][f"p{role}.{prefix}"] = host(res)
 
 
-def run_case(name, engine="coop"):
+def run_case(name, engine="coop", prog_override=None):
     import programs
     from paper_2411_09287_b200 import host
     from paper_2411_09287_b200.runtime import Session
@@ -59,7 +59,7 @@ def run_case(name, engine="coop"):
         kwargs = {}
     # inputs come from the golden file where they were arrays
     args = tuple(arrays[f"arg{i}"] if f"arg{i}" in arrays else a for i, a in enumerate(args))
-    prog = getattr(programs.build(PKG), prog_name)
+    prog = getattr(programs.build(PKG), prog_override or prog_name)
     adv = None
     if inj is not None:
         site, who, delta, gate, lane = inj
@@ -123,3 +123,17 @@ def test_golden_threads_engine(cuda):
     assert status == "ok"
     assert out["scalars"] == meta["scalars"]
     np.testing.assert_array_equal(out["arrays"]["p1.z.m"], arrays["p1.z.m"])
+
+
+@pytest.mark.parametrize("name", ["matmul_8x8x8", "matmul_12x16x10"])
+def test_matmul_gemm_form_matches_gathered_golden(cuda, name):
+    """gates.matmul_prepare/finish (tensor-core GEMMs) reproduce the
+    reference's gathered Pi_dot linear layer bit for bit."""
+    meta, arrays, sess, log, out, status = run_case(name, prog_override="matmul_gemm")
+    assert status == meta["status"]
+    counters = sorted([[f, t, p.value, c, n] for (f, t, p, c), n in sess.transcript.counters.items()])
+    assert counters == meta["counters"]
+    assert _per_sender(log) == _per_sender([tuple(x) for x in meta["payloads"]])
+    want = {k: v for k, v in arrays.items() if not k.startswith("arg")}
+    for k, v in want.items():
+        np.testing.assert_array_equal(out["arrays"][k].reshape(v.shape), v, err_msg=k)

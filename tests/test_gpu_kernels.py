@@ -129,3 +129,27 @@ def test_level_fold_matches_oracle(cuda, d, N):
             g2 = host(grvec.reduce_poly(acc[1], mod, 64))
             np.testing.assert_array_equal(g1, w1 & np.uint64(2**64 - 1), err_msg=f"h1 role {role}")
             np.testing.assert_array_equal(g2, w2, err_msg=f"h2 role {role}")
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 32, 64), (256, 96, 128), (384, 4096, 192)])
+def test_u64_gemm_tc_exact(cuda, M, K, N):
+    """Byte-limb tcgen05 GEMM is exact mod 2^64 (incl. K-concatenation,
+    linear-combination operands and addend +/-)."""
+    from paper_2411_09287_b200 import grvec, host
+    rng = np.random.default_rng(M + K + N)
+    X = _rand(rng, (M, K))
+    Y = _rand(rng, (M, K))
+    W = _rand(rng, (K, N))
+    V = _rand(rng, (K, N))
+    Z = _rand(rng, (M, N))
+    Xd, Yd, Wd, Vd, Zd = (grvec.dev(a) for a in (X, Y, W, V, Z))
+    with np.errstate(over="ignore"):
+        want = X @ W
+        got = host(grvec.u64_gemm([(grvec.limb_tiles_a(Xd), grvec.limb_tiles_b(Wd), K)], M, N))
+        np.testing.assert_array_equal(got, want)
+        # Z - [X | Y - X] . [W ; V + 3W]
+        want2 = Z - (X @ W + (Y - X) @ (V + np.uint64(3) * W))
+        pairs = [(grvec.limb_tiles_a(Xd), grvec.limb_tiles_b(Wd), K),
+                 (grvec.limb_tiles_a(Yd, 1, Xd, -1), grvec.limb_tiles_b(Vd, 1, Wd, 3), K)]
+        got2 = host(grvec.u64_gemm(pairs, M, N, addend=Zd, sub=True))
+        np.testing.assert_array_equal(got2, want2)
