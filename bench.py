@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-kernel", default="r3_vfy_level_fold")
     ap.add_argument("--relu-log2n", type=int, default=16)
+    ap.add_argument("--matmul-n", type=int, default=4096)
     return ap.parse_args()
 
 
@@ -252,6 +253,68 @@ def relu_rates(N: int, d: int, steps: int) -> dict:
     return out
 
 
+def matmul_c3(n: int, steps: int) -> dict:
+    """BASELINE config C3: share-domain matmul n x n x n over Z_2^64 with
+    truncation t = 16 (ppml linear-layer algebra, X owned by P2, W by P1,
+    fixed-point encode(normal), default_rng(3)), through
+    gates.matmul_prepare/finish + trunc_prepare/trunc_online."""
+    import numpy as np
+    import torch
+    from paper_2411_09287_b200 import gates
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import Ring, rec, shc_input_mask, shc_input_online
+    from paper_2411_09287_b200.transport import Phase
+
+    rng = np.random.default_rng(3)
+    Xf = rng.normal(0, 1, (n, n))
+    Wf = rng.normal(0, 1 / 64, (n, n))
+    enc = lambda a: torch.from_numpy(np.trunc(a * 2 ** 16).astype(np.int64)).pin_memory()
+    Xh, Wh = enc(Xf), enc(Wf)
+    t_ev = {}
+
+    def prog(party, open_out):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        xm = shc_input_mask(party, 2, n * n, ring)
+        wm = shc_input_mask(party, 1, n * n, ring)
+        tr = gates.trunc_prepare(party, n * n, 16, ring)
+        g = gates.matmul_prepare(party, xm, wm, n, n, n, out_mask=tr.rx_mask)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        X = shc_input_online(party, 2, Xh.reshape(-1) if party.role == 2 else None, xm, n * n, ring, "X")
+        W = shc_input_online(party, 1, Wh.reshape(-1) if party.role == 1 else None, wm, n * n, ring, "W")
+        z = gates.trunc_online(party, gates.matmul_finish(party, g, X, W, log=False), tr)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return rec(party, z, "z").cpu() if open_out else None
+
+    out = Session(seed=3).run(prog, True)[0]
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        Session(seed=30 + i).run(prog, False)
+    b.record()
+    torch.cuda.synchronize()
+    sec = a.elapsed_time(b) / 1e3 / steps
+    # probabilistic truncation: |open - X W / 2^16| <= 1 ulp on sampled entries
+    rs = np.random.default_rng(5)
+    idx = rs.integers(0, n, (64, 2))
+    Xi, Wi = Xh.numpy(), Wh.numpy()
+    got = out.numpy().reshape(n, n)
+    exact = np.array([sum(int(Xi[r, k]) * int(Wi[k, c]) for k in range(n)) for r, c in idx], dtype=object)
+    want = np.array([int(v) >> 16 for v in exact], dtype=object)
+    err = max(abs(int(got[r, c]) - int(w)) for (r, c), w in zip(idx, want))
+    assert err <= 1, f"matmul+trunc off by {err}"
+    u64_macs = 5 * n ** 3     # P0 1, P1 2, P2 2 u64 GEMM MACs
+    return {"n": n, "ms_per_matmul": sec * 1e3, "matmuls_per_s": 1 / sec,
+            "u64_macs_per_s": u64_macs / sec, "int8_tops_equiv": 2 * 36 * u64_macs / sec / 1e12,
+            "check": "64 sampled outputs within 1 ulp of trunc(XW)",
+            "scope": "PRE (masks, trunc_prepare 2^24 lanes, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online)"}
+
+
 class KernelTimer:
     """CUDA events around every launch of one library entry point, on the
     launching (current) stream."""
@@ -426,6 +489,8 @@ def run_b200(args):
         "clocks": clk.summary(),
         "wall_s_timed": wall,
     }
+    if args.matmul_n:
+        line["matmul"] = matmul_c3(args.matmul_n, 3)
     if args.relu_log2n:
         line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
     if not args.no_cpu_baseline:
