@@ -233,6 +233,26 @@ int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N,
                      const uint64_t* b, int d, uint64_t* const* out,
                      uint64_t mask, void* stream);
 
+/* Second reduction straight from the base log (vfy2.cu): for blocks of four
+ * elements 4j+a, acc[(a*4+b)] = sum_j s^{ab}_j pw[(4j+a)/n] with the party's
+ * scalar leg products s^{ab}_j = sum_t coef_t x_t[4j+a] y_t[4j+b]; 16 x d
+ * words, zeroed here.  The caller applies the 16 public line weights. */
+int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                   const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
+                   int64_t ls, const uint64_t* pw, int d, uint64_t* acc,
+                   void* stream);
+/* out_c[j] = sum_{a<B} X_c[Bj+a] * T_a[(Bj+a)/tq] with tables T_a at
+ * tabs + a*tab_stride (words): level-B vectors from the base log. */
+int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N,
+                  int64_t n, int64_t ks, int64_t ls, const uint64_t* tabs,
+                  int64_t tab_stride, int64_t tq, int d, uint64_t* const* out,
+                  uint64_t mask, void* stream);
+/* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B public GR constants). */
+int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
+                        int64_t n, int64_t ks, int64_t ls, const uint64_t* g,
+                        int d, uint64_t* const* out, uint64_t mask,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

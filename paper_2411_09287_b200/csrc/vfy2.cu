@@ -1,0 +1,235 @@
+// Second reduction of the batch verification straight from the base-ring
+// log (verify.py:215-241 applied twice after verify.py:168-179).
+//
+// After compression and one reduction with challenge zeta_1 every level-1
+// element is a public combination of two base elements:
+//     x1_i = sum_{a<2} X_{2i+a} pw_{2i+a} w1_a,   y1_i = sum_{b<2} Y_{2i+b} w1_b
+// with the level-1 line weights w1_0 = 1 - ze_1, w1_1 = ze_1 (ze = the opened
+// even point 2 zeta).
+// The second reduction pairs (x1_{2j}, x1_{2j+1}), so with blocks of four
+// base elements 4j + a (a < 4) its folds are
+//     h(1) = sum_{a,b in {2,3}} [ sum_j s^{ab}_j pw_{4j+a} ] (x) w1_{a&1} w1_{b&1}
+//     h(2) = sum_{a,b < 4} alpha_a alpha_b [ sum_j s^{ab}_j pw_{4j+a} ] (x) w1_{a&1} w1_{b&1}
+// (alpha = -1 on the even half, 2 on the odd half), where s^{ab}_j are the
+// party's scalar leg products sum_t c_t x_t[4j+a] y_t[4j+b].  So the level
+// costs 16 scalar-times-GR accumulations per block (r3_vfy_l2_fold) and the
+// level-1 vectors are never formed; the 16 public GR weights are applied
+// to the 16 accumulators afterwards (tiny).  The level-2 vectors for the
+// dense tail are x2_j = sum_a X_{4j+a} V_a[j] with public tables
+// V_a[j] = pw_{4j+a} w1_{a&1} w2_{a>>1} (r3_vfy_line_b), y2 likewise with
+// constants.
+#include "r3_common.cuh"
+
+namespace r3 {
+
+struct Comps8 {
+  const u64* p[8];
+};
+struct Outs8 {
+  u64* p[8];
+};
+
+__device__ __forceinline__ int64_t elem_off(int64_t i, int64_t n, int64_t ks, int64_t ls) {
+  const int64_t l = i / n;
+  return (i - l * n) * ks + l * ls;
+}
+
+// acc[(a*4+b)][k] = sum_j s^{ab}_j pw[(4j+a)/n][k]; terms t < nterms:
+// s^{ab}_j = sum_t coef_t x_t[4j+a] y_t[4j+b] (elements >= N read as 0).
+template <int D>
+__global__ void __launch_bounds__(256)
+l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t c2, int64_t N, int64_t n,
+               int64_t ks, int64_t ls, const u64* __restrict__ pw, u64* __restrict__ acc_out) {
+  constexpr int RP = 256 / D;            // blocks of 4 elements in flight per CTA
+  __shared__ u64 sS[RP][16];
+  __shared__ u64 red[16][256];
+  const int k = threadIdx.x % D, rp = threadIdx.x / D;
+  const int64_t coefs[3] = {c0, c1, c2};
+  const int64_t nblk = (N + 3) / 4;
+  u64 acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0;
+  for (int64_t j0 = int64_t(blockIdx.x) * RP; j0 < nblk; j0 += int64_t(gridDim.x) * RP) {
+    const int64_t j = j0 + rp;
+    const bool live = j < nblk;
+    // the block's 16 scalar products, each computed once
+    if (live) {
+      for (int q = k; q < 16; q += D) {
+        const int a = q >> 2, b = q & 3;
+        const int64_t ia = 4 * j + a, ib = 4 * j + b;
+        u64 sv = 0;
+        if (ia < N && ib < N) {
+          const int64_t oa = elem_off(ia, n, ks, ls), ob = elem_off(ib, n, ks, ls);
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            if (t < nterms) sv += u64(coefs[t]) * (__ldg(xc.p[t] + oa) * __ldg(yc.p[t] + ob));
+        }
+        sS[rp][q] = sv;
+      }
+    }
+    __syncthreads();
+    if (live) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t ia = 4 * j + a;
+        const u64 w = ia < N ? __ldg(pw + (ia / n) * D + k) : 0ull;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a * 4 + b] += sS[rp][a * 4 + b] * w;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  if (rp == 0) {
+    for (int q = 0; q < 16; ++q) {
+      u64 v = 0;
+      for (int r = 0; r < RP; ++r) v += red[q][r * D + k];
+      atomicAdd(acc_out + q * D + k, v);
+    }
+  }
+}
+
+// out_c[j] = sum_{a<B} X_c[B j + a] * T_a[row_a(j)], T_a = tabs + a*tab_stride
+// with row_a(j) = (B j + a) / tq  (tq = B for multiplication logs, whose
+// tables hold one row per block; tq = n for dot logs sharing a power).
+template <int D>
+__global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                              const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
+  const int64_t nblk = (N + B - 1) / B;
+  const int64_t total = nblk * D;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / D;
+    const int k = int(e - j * D);
+    u64 w[4];
+    int64_t off[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t i = B * j + a;
+      const bool ok = a < B && i < N;
+      w[a] = ok ? __ldg(tabs + a * tab_stride + (i / tq) * D + k) : 0ull;
+      off[a] = ok ? elem_off(i, n, ks, ls) : -1;
+    }
+    for (int c = 0; c < ncomp; ++c) {
+      u64 v = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (off[a] >= 0) v += __ldg(xc.p[c] + off[a]) * w[a];
+      out.p[c][e] = v & mask;
+    }
+  }
+}
+
+// out_c[j] = sum_{b<B} Y_c[B j + b] * g_b  (public constants g, B x D)
+template <int D>
+__global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                                    const u64* __restrict__ g, Outs8 out, u64 mask) {
+  const int64_t nblk = (N + B - 1) / B;
+  const int64_t total = nblk * D;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / D;
+    const int k = int(e - j * D);
+    u64 gv[4];
+    int64_t off[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = B * j + b;
+      const bool ok = b < B && i < N;
+      gv[b] = ok ? __ldg(g + b * D + k) : 0ull;
+      off[b] = ok ? elem_off(i, n, ks, ls) : -1;
+    }
+    for (int c = 0; c < ncomp; ++c) {
+      u64 v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (off[b] >= 0) v += __ldg(yc.p[c] + off[b]) * gv[b];
+      out.p[c][e] = v & mask;
+    }
+  }
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+#define R3_DISPATCH_D2(d, CALL)                                 \
+  switch (d) {                                                  \
+    case 8: { constexpr int D = 8; CALL; } break;               \
+    case 16: { constexpr int D = 16; CALL; } break;             \
+    case 32: { constexpr int D = 32; CALL; } break;             \
+    case 64: { constexpr int D = 64; CALL; } break;             \
+    default: set_error("unsupported degree %d", d); return R3_ERR_ARG; \
+  }
+
+extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                              const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                              const uint64_t* pw, int d, uint64_t* acc, void* stream) {
+  if (nterms < 1 || nterms > 3 || N < 0 || n < 1) {
+    set_error("r3_vfy_l2_fold: bad arguments");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(acc, 0, size_t(16) * d * 8, s) != cudaSuccess) {
+    set_error("r3_vfy_l2_fold: memset failed");
+    return R3_ERR_CUDA;
+  }
+  if (N == 0) return R3_OK;
+  Comps8 xp{}, yp{};
+  int64_t cf[3] = {0, 0, 0};
+  for (int t = 0; t < nterms; ++t) {
+    xp.p[t] = reinterpret_cast<const u64*>(xc[t]);
+    yp.p[t] = reinterpret_cast<const u64*>(yc[t]);
+    cf[t] = coef[t];
+  }
+  const int64_t nblk = (N + 3) / 4;
+  R3_DISPATCH_D2(d, ({
+                   constexpr int RP = 256 / D;
+                   unsigned grid = grid_for((nblk + RP - 1) / RP, 1, 4);
+                   l2_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, xp, yp, cf[0], cf[1], cf[2], N, n, ks, ls,
+                                                          (const u64*)pw, (u64*)acc);
+                 }));
+  return check_launch("r3_vfy_l2_fold");
+}
+
+extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N, int64_t n, int64_t ks,
+                             int64_t ls, const uint64_t* tabs, int64_t tab_stride, int64_t tq, int d,
+                             uint64_t* const* out, uint64_t mask, void* stream) {
+  if (B < 1 || B > 4 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1) {
+    set_error("r3_vfy_line_b: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  Comps8 xp{};
+  Outs8 op{};
+  for (int c = 0; c < ncomp; ++c) {
+    xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  const int64_t total = (N + B - 1) / B * d;
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D2(d, (line_b_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
+                        B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  return check_launch("r3_vfy_line_b");
+}
+
+extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
+                                   int64_t ls, const uint64_t* g, int d, uint64_t* const* out, uint64_t mask,
+                                   void* stream) {
+  if (B < 1 || B > 4 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1) {
+    set_error("r3_vfy_line_b_const: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  Comps8 yp{};
+  Outs8 op{};
+  for (int c = 0; c < ncomp; ++c) {
+    yp.p[c] = reinterpret_cast<const u64*>(yc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  const int64_t total = (N + B - 1) / B * d;
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D2(d, (line_b_const_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
+                        B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+  return check_launch("r3_vfy_line_b_const");
+}

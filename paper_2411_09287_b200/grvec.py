@@ -199,10 +199,20 @@ def gr_embed(base, mod: GrModulus) -> torch.Tensor:
     return out
 
 
+_CONSTS: dict = {}
+
+
 def gr_const(value: int, mod: GrModulus, width: int) -> torch.Tensor:
-    out = zeros((1, mod.degree))
-    out[0, 0] = as_i64(value & ring_mask(width))
-    return out
+    """(1, d) embedded constant.  Built once per device on the host side and
+    reused: writing a python scalar into a device tensor would be a blocking
+    host->device copy on the hot path (tensors are never mutated in place)."""
+    key = (value & ring_mask(width), mod.degree, torch._C._cuda_getDevice())
+    t = _CONSTS.get(key)
+    if t is None:
+        host_v = np.zeros((1, mod.degree), dtype=np.uint64)
+        host_v[0, 0] = key[0]
+        t = _CONSTS[key] = to_device(host_v)
+    return t
 
 
 def lin(*terms, nvalid=None) -> LinOperand:
@@ -340,7 +350,7 @@ def gr_powers(r, n: int, width: int, mod: GrModulus) -> torch.Tensor:
     out = zeros((n, d))
     if n == 0:
         return out
-    out[0, 0] = 1
+    out[0:1] = gr_const(1, mod, width)
     filled = 1
     while filled < n:
         take = min(filled, n - filled)
