@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--log2n", type=int, default=22)
+    ap.add_argument("--log2n", type=int, default=24)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--R", default="auto")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
