@@ -381,18 +381,13 @@ def imad_peak_macs(torch, lib) -> float:
 
 def run_b200(args):
     import torch
-    import torch.distributed as dist
     import numpy as np
 
     from paper_2411_09287_b200 import _lib, verify
     from paper_2411_09287_b200.runtime import Session
 
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2411_09287_b200 import dist as pdist
+    rank, world, local = pdist.init("nccl")
     _lib.load()
 
     N = 1 << args.log2n
@@ -401,12 +396,11 @@ def run_b200(args):
     mulv, e2e = make_programs(N, d, R)
 
     def barrier():
-        if world > 1:
-            dist.barrier()
+        pdist.barrier()
         torch.cuda.synchronize()
 
     def step(i):
-        sess = Session(seed=1000 * rank + i, engine=args.engine)
+        sess = Session(seed=pdist.session_seed(rank, i), engine=args.engine)
         res = sess.run(mulv)
         return res
 
@@ -431,11 +425,7 @@ def run_b200(args):
     _lib.CALL_HOOK = None
     launches = _lib.load().r3_launch_count() - launches0
     assert all(res)
-    secs = t0.elapsed_time(t1) / 1e3
-    if world > 1:
-        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        secs = float(tt.item())
+    secs = pdist.max_over_ranks(t0.elapsed_time(t1) / 1e3)
     ms_per_step = secs / args.steps * 1e3
     value = N * world * args.steps / secs
 
@@ -454,17 +444,12 @@ def run_b200(args):
     for i in range(args.e2e_steps):
         out = Session(seed=70 + i).run(e2e, xh, yh)[0]
     barrier()
-    e2e_s = time.perf_counter() - e0
-    if world > 1:
-        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = pdist.max_over_ranks(time.perf_counter() - e0)
     want = (xh.numpy().view(np.uint64) * yh.numpy().view(np.uint64))
     assert np.array_equal(out.numpy().view(np.uint64), want), "e2e product mismatch"
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        pdist.finalize()
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -483,21 +468,21 @@ def run_b200(args):
                      "kernel_share_of_step": kt / secs if secs else None,
                      "peak_source": "measured in-run by r3_imad_peak (MEASURED_PEAKS.json has no "
                                     "integer peak); algorithmic work = rows*d^2 u64 MACs per launch"},
-        "e2e": {"value": N * args.e2e_steps / e2e_s, "unit": UNIT,
+        "e2e": {"value": N * world * args.e2e_steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": N * 8},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": wall,
     }
-    if args.matmul_n:
-        line["matmul"] = matmul_c3(args.matmul_n, 3)
-    if args.relu_log2n:
-        line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
+    if world == 1:  # single-GPU side measurements and the CPU baseline (rank 0, N = 1 only)
+        if args.matmul_n:
+            line["matmul"] = matmul_c3(args.matmul_n, 3)
+        if args.relu_log2n:
+            line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    pdist.finalize()
 
 
 def run_reference(args):

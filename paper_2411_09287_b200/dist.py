@@ -1,0 +1,82 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for control.
+
+A batch of multiplications with its batch verification is an independent
+protocol object, so ranks run independent sessions (weak scaling, no
+data-path collective).  Collectives are used only for the benchmark's
+barrier and its max-over-ranks timing (NCCL on GPUs, gloo in CPU tests).
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def env() -> tuple[int, int, int]:
+    """(rank, world_size, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: str | None = None) -> tuple[int, int, int]:
+    rank, world, local = env()
+    if world > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        kw = {}
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend, **kw)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def _device_for_collective() -> torch.device:
+    if dist.is_initialized() and dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def max_over_ranks(x: float) -> float:
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=_device_for_collective())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float) -> float:
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=_device_for_collective())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier() -> None:
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+
+
+def session_seed(rank: int, step: int, base: int = 1000) -> int:
+    """Distinct, reproducible session seed per (rank, step)."""
+    return base * (rank + 1) + step
+
+
+def shard(n_total: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:
+    """Contiguous [start, stop) slice of n_total units for `rank`, slice sizes
+    multiples of `align` except the last (batch sizes that keep 2^R pairs
+    inside one shard)."""
+    per = -(-n_total // world)
+    per = -(-per // align) * align
+    start = min(n_total, rank * per)
+    return start, min(n_total, start + per)
+
+
+def finalize() -> None:
+    if dist.is_initialized():
+        dist.destroy_process_group()
