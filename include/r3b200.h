@@ -91,6 +91,17 @@ int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out,
           const uint64_t* a, const int64_t* a_strides,
           const uint64_t* b, const int64_t* b_strides,
           uint64_t imm, uint64_t mask, void* stream);
+/* Contiguous 1-d form of r3_ew (n words; b == NULL uses imm): the host's
+ * hot elementwise call, no shape/stride arrays to marshal. */
+int r3_ew_flat(int op, int64_t n, uint64_t* out, const uint64_t* a,
+               const uint64_t* b, uint64_t imm, uint64_t mask, void* stream);
+/* k <= 4 contiguous length-n components in one launch: out[c] =
+ * op(a[c], b ? b[c] : imm) & mask (the fields of one party's share view --
+ * s1/s2/total/m, sharing.py:95-230 -- updated together).  Per-component
+ * b may be NULL only if the whole b array is NULL. */
+int r3_ew_multi(int op, int k, int64_t n, uint64_t* const* out,
+                const uint64_t* const* a, const uint64_t* const* b,
+                uint64_t imm, uint64_t mask, void* stream);
 /* Sign-extending right shift on width-bit patterns (grvec.arith_rshift,
  * grvec.py:43-51); t in [0, width). */
 int r3_ars(const uint64_t* a, int64_t n, int t, int width, uint64_t* out,
@@ -135,6 +146,13 @@ int r3_mul_leg(int role, int64_t n, int64_t lanes,
 int r3_gr_mul(const uint64_t* a, int64_t a_rs, const uint64_t* b, int64_t b_rs,
               uint64_t* out, int64_t rows, int d, uint64_t lowterms,
               uint64_t mask, void* stream);
+/* out[f][row] = sum_{t<nterms} a[t*k + f][row] * c[t] in GR(2^ell, d):
+ * k <= 4 fields (rows x d, contiguous), nterms <= 3 public single-element
+ * weights -- the Lagrange recombination z' = h0 l0 + h1 l1 + h2 l2 of
+ * Pi_rd (verify.py:233-236) for all of a party's fields in one launch. */
+int r3_gr_lincomb(int k, int nterms, const uint64_t* const* a,
+                  const uint64_t* const* c, uint64_t* const* out, int64_t rows,
+                  int d, uint64_t lowterms, uint64_t mask, void* stream);
 /* out[i] = s[i*s_stride] * g[i] (base scalar times GR element; the
  * reference's embedded-scalar gr_mul, identical values at d MACs/row). */
 int r3_gr_scale_rows(const uint64_t* s, int64_t s_stride,

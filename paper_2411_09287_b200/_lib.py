@@ -41,6 +41,8 @@ _SIGS = {
     "r3_prf_bits_packed": [C.POINTER(C.c_uint32), u64, C.c_int, i64, u64p, C.c_void_p],
     "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
               C.POINTER(i64), u64, u64, C.c_void_p],
+    "r3_ew_flat": [C.c_int, i64, u64p, u64p, u64p, u64, u64, C.c_void_p],
+    "r3_ew_multi": [C.c_int, C.c_int, i64, C.c_void_p, C.c_void_p, C.c_void_p, u64, u64, C.c_void_p],
     "r3_ars": [u64p, i64, C.c_int, C.c_int, u64p, C.c_void_p],
     "r3_bit_planes": [u64p, i64, C.c_int, u64p, C.c_void_p],
     "r3_count_nonequal": [u64p, u64p, i64, u64p, C.c_void_p],
@@ -49,6 +51,8 @@ _SIGS = {
     "r3_mul_leg": [C.c_int, i64, i64, u64p, i64, i64, u64p, i64, i64, u64p, i64, i64,
                    u64p, i64, i64, u64p, u64p, u64, C.c_void_p],
     "r3_gr_mul": [u64p, i64, u64p, i64, u64p, i64, C.c_int, u64, u64, C.c_void_p],
+    "r3_gr_lincomb": [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_int, u64, u64,
+                      C.c_void_p],
     "r3_gr_scale_rows": [u64p, i64, u64p, i64, u64p, i64, C.c_int, u64, C.c_void_p],
     "r3_gr_mulmat": [u64p, C.c_int, u64, u64p, C.c_void_p],
     "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
@@ -113,8 +117,13 @@ def exported_symbols() -> list[str]:
 CALL_HOOK = None
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
-    fn = getattr(load(), name)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
     if CALL_HOOK is None:
         rc = fn(*args)
     else:

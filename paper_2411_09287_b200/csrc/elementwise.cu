@@ -213,6 +213,68 @@ extern "C" int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out, cons
   return check_launch("r3_ew(strided)");
 }
 
+extern "C" int r3_ew_flat(int op, int64_t n, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                          uint64_t imm, uint64_t mask, void* stream) {
+  // contiguous fast path of r3_ew (one call, no shape/stride arrays)
+  const int64_t shape[1] = {n};
+  const int64_t st[1] = {1};
+  return r3_ew(op, 1, shape, out, a, st, b, st, imm, mask, stream);
+}
+
+struct Ptr4 {
+  const u64* p[4];
+};
+struct OutPtr4 {
+  u64* p[4];
+};
+
+// k same-length contiguous components in one launch (blockIdx.y = component):
+// the fields of one party's share view (s1, s2, total, m) move together.
+template <int OP>
+__global__ void ew_multi_kernel(int64_t n, OutPtr4 out, Ptr4 a, Ptr4 b, u64 imm, u64 mask) {
+  const int c = blockIdx.y;
+  const u64* __restrict__ pa = a.p[c];
+  const u64* __restrict__ pb = b.p[c];
+  u64* __restrict__ po = out.p[c];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    po[i] = ew_apply(OP, pa[i], pb ? pb[i] : imm) & mask;
+}
+
+extern "C" int r3_ew_multi(int op, int k, int64_t n, uint64_t* const* out, const uint64_t* const* a,
+                           const uint64_t* const* b, uint64_t imm, uint64_t mask, void* stream) {
+  if (k < 1 || k > 4 || n < 0 || op < 0 || op > R3_EW_COPY) {
+    set_error("r3_ew_multi: bad arguments (op=%d k=%d)", op, k);
+    return R3_ERR_ARG;
+  }
+  if (n == 0) return R3_OK;
+  OutPtr4 o{};
+  Ptr4 pa{}, pb{};
+  for (int c = 0; c < k; ++c) {
+    o.p[c] = reinterpret_cast<u64*>(out[c]);
+    pa.p[c] = reinterpret_cast<const u64*>(a[c]);
+    pb.p[c] = (b && op != R3_EW_COPY) ? reinterpret_cast<const u64*>(b[c]) : nullptr;
+  }
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = grid_for(n, 256, 8);
+  const unsigned gxk = (gx + k - 1) / k;
+  const dim3 grid{gxk > 0 ? gxk : 1u, unsigned(k), 1};
+  switch (op) {
+#define R3_EWM_CASE(OPC) \
+  case OPC: ew_multi_kernel<OPC><<<grid, 256, 0, s>>>(n, o, pa, pb, imm, mask); break;
+    R3_EWM_CASE(R3_EW_ADD)
+    R3_EWM_CASE(R3_EW_SUB)
+    R3_EWM_CASE(R3_EW_MUL)
+    R3_EWM_CASE(R3_EW_AND)
+    R3_EWM_CASE(R3_EW_XOR)
+    R3_EWM_CASE(R3_EW_OR)
+    R3_EWM_CASE(R3_EW_RSUB)
+    R3_EWM_CASE(R3_EW_COPY)
+#undef R3_EWM_CASE
+  }
+  return check_launch("r3_ew_multi");
+}
+
 extern "C" int r3_ars(const uint64_t* a, int64_t n, int t, int width, uint64_t* out, void* stream) {
   if (width < 1 || width > 64 || t < 0 || t >= width || n < 0) {
     set_error("r3_ars: shift %d out of range for width %d", t, width);

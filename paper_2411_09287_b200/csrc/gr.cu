@@ -585,6 +585,53 @@ __global__ void mask_rows_kernel(u64* out, int64_t n, u64 mask) {
     out[i] &= mask;
 }
 
+
+// ---------------------------------------------------------------------------
+// out[f][row] = sum_t a[t][f][row] * c[t]: a public-weighted combination of
+// up to 4 share fields in one launch (the Lagrange recombination
+// z' = h0 l0 + h1 l1 + h2 l2 of verify.py:233-236 for every field the party
+// holds).  Warp per (field, row); the T products are summed unreduced and
+// reduced once.
+// ---------------------------------------------------------------------------
+struct LincombArgs {
+  const u64* a[3][4];
+  const u64* c[3];
+  u64* out[4];
+};
+
+template <int D>
+__global__ void gr_lincomb_kernel(LincombArgs args, int k, int nterms, int64_t rows, u64 lowterms, u64 mask) {
+  constexpr int WARPS = 4;
+  __shared__ u64 sc[3][D];
+  __shared__ u64 sa[WARPS][D], sp[WARPS][2 * D], st[WARPS][2 * D + 8];
+  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) {
+    const int t = i / D;
+    sc[t][i - t * D] = t < nterms ? args.c[t][i - t * D] : 0ull;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t items = rows * k;
+  for (int64_t it = blockIdx.x * int64_t(WARPS) + w; it < items; it += int64_t(gridDim.x) * WARPS) {
+    const int f = int(it / rows);
+    const int64_t row = it - int64_t(f) * rows;
+    for (int idx = lane; idx < 2 * D; idx += 32) sp[w][idx] = 0;
+    for (int t = 0; t < nterms; ++t) {
+      __syncwarp();
+      for (int q = lane; q < D; q += 32) sa[w][q] = args.a[t][f][row * D + q];
+      __syncwarp();
+      for (int idx = lane; idx < 2 * D - 1; idx += 32) {
+        const int lo = idx - (D - 1) > 0 ? idx - (D - 1) : 0;
+        const int hi = idx < D - 1 ? idx : D - 1;
+        u64 acc = 0;
+        for (int i = lo; i <= hi; ++i) acc += sa[w][i] * sc[t][idx - i];
+        sp[w][idx] += acc;
+      }
+    }
+    __syncwarp();
+    reduce_poly_warp<D>(sp[w], st[w], lowterms, args.out[f] + row * D, mask, lane, nullptr);
+  }
+}
+
 }  // namespace r3
 
 using namespace r3;
@@ -882,4 +929,24 @@ extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* x
 #undef R3_LF_D
 #undef R3_LF
   return check_launch("r3_vfy_level_fold");
+}
+
+extern "C" int r3_gr_lincomb(int k, int nterms, const uint64_t* const* a, const uint64_t* const* c,
+                             uint64_t* const* out, int64_t rows, int d, uint64_t lowterms, uint64_t mask,
+                             void* stream) {
+  if (!valid_d(d) || k < 1 || k > 4 || nterms < 1 || nterms > 3 || rows < 0) {
+    set_error("r3_gr_lincomb: bad arguments (k=%d nterms=%d d=%d)", k, nterms, d);
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  LincombArgs args{};
+  for (int t = 0; t < nterms; ++t) {
+    args.c[t] = reinterpret_cast<const u64*>(c[t]);
+    for (int f = 0; f < k; ++f) args.a[t][f] = reinterpret_cast<const u64*>(a[t * k + f]);
+  }
+  for (int f = 0; f < k; ++f) args.out[f] = reinterpret_cast<u64*>(out[f]);
+  unsigned grid = grid_for(rows * k, 4, 16);
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (gr_lincomb_kernel<D><<<grid, 128, 0, s>>>(args, k, nterms, rows, lowterms, mask)));
+  return check_launch("r3_gr_lincomb");
 }

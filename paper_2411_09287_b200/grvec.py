@@ -67,8 +67,26 @@ def _scalar(x) -> int:
     return int(x) & ((1 << 64) - 1)
 
 
+_M64 = (1 << 64) - 1
+_Tensor = torch.Tensor
+
+
 def ew(op: int, a, b, mask: int) -> torch.Tensor:
     """out = op(a, b) & mask with numpy-style broadcasting (<= 4 dims)."""
+    # fast path: contiguous device tensors of one shape, or tensor (op) int
+    if type(a) is _Tensor and a.is_cuda and a.is_contiguous():
+        tb = type(b)
+        if tb is _Tensor:
+            if b.shape == a.shape and b.is_contiguous():
+                out = torch.empty(a.shape, dtype=torch.int64, device=a.device)
+                call("r3_ew_flat", op, a.numel(), out.data_ptr(), a.data_ptr(), b.data_ptr(), 0,
+                     mask & _M64, stream())
+                return out
+        elif tb is int or b is None:
+            out = torch.empty(a.shape, dtype=torch.int64, device=a.device)
+            call("r3_ew_flat", COPY if b is None else op, a.numel(), out.data_ptr(), a.data_ptr(),
+                 None, 0 if b is None else b & _M64, mask & _M64, stream())
+            return out
     if _is_scalar(a) and not _is_scalar(b):
         inv = {ADD: ADD, MUL: MUL, AND: AND, XOR: XOR, OR: OR, SUB: RSUB}
         return ew(inv[op], b, a, mask)
@@ -474,3 +492,60 @@ def u64_gemm(pairs, M: int, N: int, width: int = 64, addend: torch.Tensor | None
          ptr(addend.contiguous()) if addend is not None else None, 1 if sub else 0,
          ptr(out), ring_mask(width), stream())
     return out
+
+
+_PTRS12 = C.c_void_p * 12
+
+
+def ew_fields(op: int, a: list, b, mask: int) -> list:
+    """[op(a_c, b_c) & mask] for up to 4 same-shape contiguous tensors in one
+    launch (b: list of tensors, one int for all, or None for a copy).
+    Components that do not qualify fall back to one ew call each."""
+    k = len(a)
+    bl = b if isinstance(b, list) else None
+    ok = 0 < k <= 4
+    if ok:
+        shape = a[0].shape
+        for c in range(k):
+            t = a[c]
+            if type(t) is not _Tensor or t.shape != shape or not t.is_contiguous() or not t.is_cuda:
+                ok = False
+                break
+            if bl is not None:
+                u = bl[c]
+                if type(u) is not _Tensor or u.shape != shape or not u.is_contiguous():
+                    ok = False
+                    break
+        if ok and bl is None and b is not None and type(b) is not int:
+            ok = False
+    if not ok:
+        return [ew(op, a[c], bl[c] if bl is not None else b, mask) for c in range(k)]
+    n = a[0].numel()
+    outs = [torch.empty(shape, dtype=torch.int64, device=a[0].device) for _ in range(k)]
+    arr = _PTRS12(*[o.data_ptr() for o in outs], *([None] * (4 - k)),
+                  *[t.data_ptr() for t in a], *([None] * (4 - k)),
+                  *([u.data_ptr() for u in bl] if bl is not None else [None] * k), *([None] * (4 - k)))
+    base = C.addressof(arr)
+    call("r3_ew_multi", COPY if b is None else op, k, n, base, base + 32, base + 64 if bl is not None else None,
+         0 if (b is None or bl is not None) else b & _M64, mask & _M64, stream())
+    return outs
+
+
+def gr_lincomb(terms: list, coeffs: list, width: int, mod: GrModulus) -> list:
+    """[sum_t terms[t][f] * coeffs[t] for each field f] in GR(2^width, d):
+    terms[t] is a list of k <= 4 same-shape (rows, d) tensors, coeffs[t] one
+    public element; one launch for all fields (r3_gr_lincomb)."""
+    d = mod.degree
+    nterms, k = len(terms), len(terms[0])
+    shape = terms[0][0].shape
+    flat = [t.reshape(-1, d).contiguous() for row in terms for t in row]
+    cs = [c.reshape(-1)[:d].contiguous() if isinstance(c, torch.Tensor) else to_device(c).reshape(-1)[:d]
+          for c in coeffs]
+    rows = flat[0].shape[0]
+    outs = [torch.empty(shape, dtype=torch.int64, device=flat[0].device) for _ in range(k)]
+    pa = (C.c_void_p * (nterms * k))(*[t.data_ptr() for t in flat])
+    pc = (C.c_void_p * nterms)(*[c.data_ptr() for c in cs])
+    po = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    call("r3_gr_lincomb", k, nterms, C.addressof(pa), C.addressof(pc), C.addressof(po), rows, d,
+         mod.lowterms_mask, ring_mask(width), stream())
+    return outs

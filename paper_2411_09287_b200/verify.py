@@ -184,6 +184,41 @@ def _opened_key(party, value: torch.Tensor):
     return ("rec", party._ids.get("rec", 0))
 
 
+class _Quad:
+    """Public per-level values derived from the opened even point ze:
+    Lagrange weights for z' = z l0 + h1 (l1 - l0) + h2 l2 (h0 = z - h1
+    folded in) and the line-evaluation matrices of (1 - ze) and ze."""
+
+    def __init__(self, ze: torch.Tensor, gr: Ring, check: bool):
+        l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=check)
+        self.w = (l0, grvec.sub(l1, l0, gr.ell), l2)
+        self.one_m = grvec.sub(grvec.gr_const(1, gr.mod, gr.ell), ze, gr.ell)
+        self.M_one_m = grvec.gr_mulmat(self.one_m, gr.mod) if gr.d >= 8 else None
+        self.M_ze = grvec.gr_mulmat(ze, gr.mod) if gr.d >= 8 else None
+
+
+def _quad(party, ze: torch.Tensor, gr: Ring) -> _Quad:
+    key = ("quad", gr.ell, gr.d, _opened_key(party, ze))
+    return _public(party, key, lambda: _Quad(ze, gr, party.sess.eager_checks))
+
+
+def _recombine(party, z: MVal, h1: MVal, h2: MVal, q: _Quad, gr: Ring) -> MVal:
+    """z' = (z - h1) l0 + h1 l1 + h2 l2 (verify.py:233-236) over every
+    field the three views share, one launch."""
+    names = [f for f in ("s1", "s2", "total")
+             if all(getattr(v.mask, f) is not None for v in (z, h1, h2))]
+    terms = [[getattr(v.mask, f) for f in names] for v in (z, h1, h2)]
+    with_m = z.m is not None
+    if with_m:
+        for row, v in zip(terms, (z, h1, h2)):
+            row.append(v.m)
+    outs = grvec.gr_lincomb(terms, list(q.w), gr.ell, gr.mod)
+    vals = dict(zip(names, outs))
+    mask = AShare(gr, z.mask.role, p0_halves=z.mask.p0_halves and h1.mask.p0_halves and h2.mask.p0_halves,
+                  **vals)
+    return MVal(mask, outs[-1] if with_m else None)
+
+
 def _powers(party, r: torch.Tensor, n: int, gr: Ring) -> torch.Tensor:
     key = ("pow", gr.ell, gr.d, _opened_key(party, r), n)
     return _public(party, key, lambda: grvec.gr_powers(r, n, gr.ell, gr.mod))
@@ -321,10 +356,8 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     h1f, h2f = _l1_folds(party, comp, pw, gr)
     h1 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h1f)
     h2 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h2f)
-    h0 = z - h1
     ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
-    z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
+    z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
     if R >= 2 and gr.d >= 8:
         return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
@@ -380,10 +413,8 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     rows = (n1 + 1) // 2
     h1 = _gr_dot_folded(party, gr, rows, fold(W1))
     h2 = _gr_dot_folded(party, gr, rows, fold(W2))
-    h0 = z1 - h1
     ze2 = _open_challenge(party, chal.zetas[1].scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze2, gr.ell, gr.mod, check=party.sess.eager_checks)
-    z2 = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
+    z2 = _recombine(party, z1, h1, h2, _quad(party, ze2, gr), gr)
     tabs, kappa, tq, stride = _l2_tables(party, pw, comp.n, w1, ze2, gr)
     nb = (comp.N + 3) // 4
     xo = {k: empty((nb, gr.d)) for k in comp.x}
@@ -583,12 +614,10 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
         fold2 = _level_folds(role, X, Y, "f2", rows, gr)
     h1 = _gr_dot_folded(party, gr, rows, fold1)
     h2 = _gr_dot_folded(party, gr, rows, fold2)
-    h0 = z - h1
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
-    z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
-    one_m = grvec.sub(grvec.gr_const(1, gr.mod, gr.ell), ze, gr.ell)
-    Ms = (grvec.gr_mulmat(one_m, gr.mod) if gr.d == 64 else None, grvec.gr_mulmat(ze, gr.mod))
+    q = _quad(party, ze, gr)
+    z_out = _recombine(party, z, h1, h2, q, gr)
+    Ms = (q.M_one_m if gr.d == 64 else None, q.M_ze)
     out = lambda V, k: _line_eval(V[k], Ms, gr)
     mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
                                   p0_halves=v.mask.p0_halves),
@@ -607,10 +636,8 @@ def _reduce_dimension_small(party, xs, ys, z, gr, zeta):
     g2 = g1.scale_pub(2) - g0
     h1 = _gr_dot(party, f1, g1, gr)
     h2 = _gr_dot(party, f2, g2, gr)
-    h0 = z - h1
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
-    l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=party.sess.eager_checks)
-    z_out = h0.scale_gr(l0) + h1.scale_gr(l1) + h2.scale_gr(l2)
+    z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
     xs_out = f0 + (f1 - f0).scale_gr(ze)
     ys_out = g0 + (g1 - g0).scale_gr(ze)
     return xs_out, ys_out, z_out
@@ -645,12 +672,23 @@ def _levels_done(R: int, gr: Ring) -> int:
     return min(R, 1)
 
 
+def _cat_mvals(vals: list, dim: int = 0) -> MVal:
+    """One torch.cat per field for the whole list (MVal.concat / _map
+    semantics: a field survives only if every view has it)."""
+    if len(vals) == 1:
+        return vals[0]
+    first = vals[0].mask
+    fields = {}
+    for f in ("s1", "s2", "total"):
+        parts = [getattr(v.mask, f) for v in vals]
+        fields[f] = None if any(t is None for t in parts) else torch.cat(parts, dim=dim)
+    mask = AShare(first.ring, first.role, p0_halves=all(v.mask.p0_halves for v in vals), **fields)
+    ms = [v.m for v in vals]
+    return MVal(mask, None if ms[0] is None else torch.cat(ms, dim=dim))
+
+
 def _concat_all(recs, pick):
-    out = None
-    for r in recs:
-        v = pick(r)
-        out = v if out is None else out.concat(v)
-    return out
+    return _cat_mvals([pick(r) for r in recs])
 
 
 def _verify_tail(party, xs, ys, z, gr, ctx: Challenges, R: int, start: int = 0) -> bool:
@@ -711,14 +749,7 @@ def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
 def _concat_lanes(vals: list) -> MVal:
     """Concatenate (n, L_b) dot-log operands along the lane axis, which is the
     lane-major consolidation order of verify.py:195-201."""
-    if len(vals) == 1:
-        return vals[0]
-    cat = lambda *a: torch.cat(a, dim=1)
-    out = vals[0]
-    for v in vals[1:]:
-        out = MVal(out.mask._map(lambda a, b: cat(a, b), v.mask),
-                   None if out.m is None else cat(out.m, v.m))
-    return out
+    return _cat_mvals(vals, dim=1)
 
 
 def verify_session(party, d: int, R: int | str = "auto", profile: str = "lan") -> dict:

@@ -22,3 +22,19 @@ for name, (p, a) in progs.items():
     gc.garbage.clear()
     gc.set_debug(0)
     gc.enable()
+
+# keystream draws made by only one holder (they stay in prg_shared until
+# run() returns)
+class Rec(dict):
+    def clear(self):
+        if self:
+            print("   leftover draws", len(self), "bytes", sum(t.numel() * 8 for t in self.values()),
+                  sorted({(k[1], k[2]) for k in self})[:6], flush=True)
+        super().clear()
+for name, (p, a) in progs.items():
+    s = Session(seed=1)
+    s.prg_shared = Rec()
+    for party in s.parties:
+        pass
+    print(name)
+    s.run(p, *a)
