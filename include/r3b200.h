@@ -251,6 +251,17 @@ int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N,
                      const uint64_t* b, int d, uint64_t* const* out,
                      uint64_t mask, void* stream);
 
+/* One pass over the power table for a multiplication log (n = 1, base
+ * components contiguous): the z power sum of r3_vfy_powsum (nz <= 2
+ * components, stride zs, masked), the 16 level-2 accumulators of
+ * r3_vfy_l2_fold (acc, 16 x d, unmasked) and the level-1 folds of
+ * r3_vfy_l1_fold derived from them (h1, h2, masked) -- verify.py:168-179
+ * + 215-241 at k = 0, 1.  Same terms/coefficients as r3_vfy_l2_fold. */
+int r3_vfy_base_fold(int nterms, const int64_t* coef,
+                     const uint64_t* const* xc, const uint64_t* const* yc,
+                     int nz, const uint64_t* const* zc, int64_t zs, int64_t N,
+                     const uint64_t* pw, int d, uint64_t* acc, uint64_t* h1,
+                     uint64_t* h2, uint64_t* zsum, uint64_t mask, void* stream);
 /* Second reduction straight from the base log (vfy2.cu): for blocks of four
  * elements 4j+a, acc[(a*4+b)] = sum_j s^{ab}_j pw[(4j+a)/n] with the party's
  * scalar leg products s^{ab}_j = sum_t coef_t x_t[4j+a] y_t[4j+b]; 16 x d

@@ -149,6 +149,168 @@ __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int6
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// One pass over the power table for a multiplication log (n = 1): the z
+// power sum (r3_vfy_powsum), the 16 level-2 accumulators (r3_vfy_l2_fold)
+// and, derived from those, the level-1 folds (r3_vfy_l1_fold):
+//   h1(level 1) = acc[1][1] + acc[3][3]
+//   h2(level 1) = sum_{pair (e,o) in {(0,1),(2,3)}} 4acc[o][o] - 2acc[o][e] - 2acc[e][o] + acc[e][e]
+// (pairs (4j, 4j+1), (4j+2, 4j+3) of level 1 are the a-pairs of block j).
+// None of the accumulators depends on the level-1 challenge, so the table is
+// streamed once per party instead of three times.
+//
+// Warp-tiled: a warp owns TB = 32 consecutive blocks of 4 elements.  Phase A:
+// lane L forms block L's 16 scalar leg products and its z values into
+// warp-private shared memory.  Phase B: the warp walks the 128 power rows of
+// the tile, each lane holding KPL coefficients (D >= 32) or one coefficient
+// of one of 32/D rows (D < 32), multiply-accumulating broadcast scalars.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256)
+base_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t c2, int nz, Comps8 zc,
+                 int64_t zs, int64_t N, const u64* __restrict__ pw, u64* __restrict__ acc_out,
+                 u64* __restrict__ z_out) {
+  constexpr int KPL = D >= 32 ? D / 32 : 1;
+  constexpr int RPS = D >= 32 ? 1 : 32 / D;
+  constexpr int TB = 32;
+  constexpr int W = 8;
+  __shared__ u64 sS[W][16][TB];
+  __shared__ u64 sZ[W][8][TB];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = D >= 32 ? 0 : lane / D;
+  const int kb = D >= 32 ? lane : lane % D;
+  const int64_t coefs[3] = {c0, c1, c2};
+  u64 acc[16][KPL], zacc[2][KPL];
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) acc[q][c] = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) zacc[q][c] = 0;
+  const int64_t nblk = (N + 3) / 4;
+  const int64_t ntiles = (nblk + TB - 1) / TB;
+  for (int64_t tile = int64_t(blockIdx.x) * W + w; tile < ntiles; tile += int64_t(gridDim.x) * W) {
+    {  // phase A: block j = tile*TB + lane
+      const int64_t i0 = 4 * (tile * TB + lane);
+      u64 s[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) s[q] = 0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        if (t < nterms) {
+          u64 xv[4], yv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const bool ok = i0 + a < N;
+            xv[a] = ok ? __ldg(xc.p[t] + i0 + a) : 0ull;
+            yv[a] = ok ? __ldg(yc.p[t] + i0 + a) : 0ull;
+          }
+          const u64 cf = u64(coefs[t]);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const u64 cx = cf * xv[a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) s[a * 4 + b] += cx * yv[b];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sS[w][q][lane] = s[q];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c < nz) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            sZ[w][c * 4 + a][lane] = i0 + a < N ? __ldg(zc.p[c] + (i0 + a) * zs) : 0ull;
+        }
+      }
+    }
+    __syncwarp();
+    // phase B
+    for (int e0 = 0; e0 < TB; e0 += RPS) {
+      const int e = e0 + r;
+      const int64_t ib = 4 * (tile * TB + e);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t i = ib + a;
+        u64 wv[KPL];
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) wv[c] = i < N ? __ldg(pw + i * D + kb + 32 * c) : 0ull;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const u64 sv = sS[w][a * 4 + b][e];
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) acc[a * 4 + b][c] += sv * wv[c];
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q < nz) {
+            const u64 zv = sZ[w][q * 4 + a][e];
+#pragma unroll
+            for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wv[c];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // lanes holding the same coefficient of different rows (D < 32)
+#pragma unroll
+  for (int off = D; off < 32; off <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q][0] += __shfl_xor_sync(0xffffffffu, acc[q][0], off);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) zacc[q][0] += __shfl_xor_sync(0xffffffffu, zacc[q][0], off);
+  }
+  // across the CTA's warps, then one atomic per coefficient
+  __syncthreads();
+  u64* red = &sS[0][0][0];  // W * 16 * TB = 4096 words >= W * D
+  const int nslots = 16 + nz;
+  for (int q = 0; q < nslots; ++q) {
+    if (r == 0) {
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        u64 v = 0;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq)
+          if (qq == q) v = acc[qq][c];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq)
+          if (16 + qq == q) v = zacc[qq][c];
+        red[w * D + kb + 32 * c] = v;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < D; k += blockDim.x) {
+      u64 v = 0;
+#pragma unroll
+      for (int ww = 0; ww < W; ++ww) v += red[ww * D + k];
+      if (q < 16)
+        atomicAdd(acc_out + q * D + k, v);
+      else
+        atomicAdd(z_out + (q - 16) * D + k, v);
+    }
+    __syncthreads();
+  }
+}
+
+// level-1 folds from the 16 accumulators (see base_fold_kernel); masks z.
+__global__ void base_fold_finish_kernel(int d, int nz, const u64* __restrict__ acc, u64* __restrict__ h1,
+                                        u64* __restrict__ h2, u64* __restrict__ z, u64 mask) {
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    const u64* A = acc + k;
+#define ACC(a, b) A[((a) * 4 + (b)) * d]
+    h1[k] = (ACC(1, 1) + ACC(3, 3)) & mask;
+    h2[k] = (4 * ACC(1, 1) - 2 * ACC(1, 0) - 2 * ACC(0, 1) + ACC(0, 0) + 4 * ACC(3, 3) - 2 * ACC(3, 2) -
+             2 * ACC(2, 3) + ACC(2, 2)) & mask;
+#undef ACC
+    for (int c = 0; c < nz; ++c) z[c * d + k] &= mask;
+  }
+}
+
 }  // namespace r3
 
 using namespace r3;
@@ -232,4 +394,40 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   R3_DISPATCH_D2(d, (line_b_const_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
                         B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
   return check_launch("r3_vfy_line_b_const");
+}
+
+extern "C" int r3_vfy_base_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                                const uint64_t* const* yc, int nz, const uint64_t* const* zc, int64_t zs,
+                                int64_t N, const uint64_t* pw, int d, uint64_t* acc, uint64_t* h1, uint64_t* h2,
+                                uint64_t* zsum, uint64_t mask, void* stream) {
+  if (nterms < 1 || nterms > 3 || nz < 0 || nz > 2 || N < 0 || zs < 1) {
+    set_error("r3_vfy_base_fold: bad arguments");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(acc, 0, size_t(16) * d * 8, s) != cudaSuccess ||
+      (nz > 0 && cudaMemsetAsync(zsum, 0, size_t(nz) * d * 8, s) != cudaSuccess)) {
+    set_error("r3_vfy_base_fold: memset failed");
+    return R3_ERR_CUDA;
+  }
+  Comps8 xp{}, yp{}, zp{};
+  int64_t cf[3] = {0, 0, 0};
+  for (int t = 0; t < nterms; ++t) {
+    xp.p[t] = reinterpret_cast<const u64*>(xc[t]);
+    yp.p[t] = reinterpret_cast<const u64*>(yc[t]);
+    cf[t] = coef[t];
+  }
+  for (int c = 0; c < nz; ++c) zp.p[c] = reinterpret_cast<const u64*>(zc[c]);
+  if (N > 0) {
+    const int64_t ntiles = ((N + 3) / 4 + 31) / 32;
+    R3_DISPATCH_D2(d, ({
+                     unsigned grid = grid_for((ntiles + 7) / 8, 1, 2);
+                     base_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, xp, yp, cf[0], cf[1], cf[2], nz, zp, zs, N,
+                                                              (const u64*)pw, (u64*)acc, (u64*)zsum);
+                   }));
+    int rc = check_launch("r3_vfy_base_fold");
+    if (rc) return rc;
+  }
+  base_fold_finish_kernel<<<1, 64, 0, s>>>(d, nz, (const u64*)acc, (u64*)h1, (u64*)h2, (u64*)zsum, mask);
+  return check_launch("r3_vfy_base_fold(finish)");
 }

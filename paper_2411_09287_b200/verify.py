@@ -319,6 +319,24 @@ def _l1_folds(party, comp: _Compressed, pw: torch.Tensor, gr: Ring):
     return h1, h2
 
 
+def _base_fold(party, comp: _Compressed, zcomps: list, z_stride: int, pw: torch.Tensor, gr: Ring):
+    """r3_vfy_base_fold: (zsum (nz, 1, d), acc (16, d), h1 fold, h2 fold)."""
+    terms = _role_terms(party.role)
+    d = gr.d
+    coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+    xs = _ptrs([comp.x[t[1]] for t in terms])
+    ys = _ptrs([comp.y[t[2]] for t in terms])
+    zp = _ptrs(zcomps)
+    zsum = empty((len(zcomps), 1, d))
+    acc = empty((16, d))
+    h1 = empty((1, d))
+    h2 = empty((1, d))
+    call("r3_vfy_base_fold", len(terms), C.addressof(coef), C.addressof(xs), C.addressof(ys), len(zcomps),
+         C.addressof(zp), z_stride, comp.N, ptr(pw), d, ptr(acc), ptr(h1), ptr(h2), ptr(zsum), gr.mask,
+         stream())
+    return zsum, acc, h1, h2
+
+
 def _powsum(comps: list, stride: int, lanes: int, pw: torch.Tensor, gr: Ring) -> torch.Tensor:
     out = empty((len(comps), 1, gr.d))
     call("r3_vfy_powsum", len(comps), _ptrs(comps), stride, lanes, ptr(pw), gr.d, ptr(out),
@@ -349,17 +367,25 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     zc = _components(zs, party.role)
     zc = {k: t.reshape(-1) if t.dim() == 1 else t for k, t in zc.items()}
     names = list(zc)
-    zsum = _powsum([zc[k] for k in names], z_stride, z_lanes, pw, gr)
+    base_acc = None
+    if (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
+            and len(names) <= 2):
+        # one pass over the table: z power sum, level-2 accumulators and the
+        # level-1 folds derived from them
+        zsum, base_acc, h1f, h2f = _base_fold(party, comp, [zc[k] for k in names], z_stride, pw, gr)
+    else:
+        zsum = _powsum([zc[k] for k in names], z_stride, z_lanes, pw, gr)
     z = _mval_from({k: zsum[i] for i, k in enumerate(names)}, gr, party.role)
     if R == 0:
         return _materialise(comp, pw, gr, party.role), z
-    h1f, h2f = _l1_folds(party, comp, pw, gr)
+    if base_acc is None:
+        h1f, h2f = _l1_folds(party, comp, pw, gr)
     h1 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h1f)
     h2 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h2f)
     ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
     z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
     if R >= 2 and gr.d >= 8:
-        return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal)
+        return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
     tq = 2 if comp.n == 1 else comp.n
     half = (comp.N + 1) // 2
@@ -395,18 +421,19 @@ def _l2_weights(party, ze1: torch.Tensor, gr: Ring):
 
 
 def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: torch.Tensor,
-                             z1: MVal, gr: Ring, chal: Challenges):
+                             z1: MVal, gr: Ring, chal: Challenges, acc: torch.Tensor | None = None):
     """The second Pi_rd (verify.py:215-241 at k = 1) computed from the base
     log: 16 scalar-weighted power sums per party (r3_vfy_l2_fold) replace the
     level-1 vectors and their d^2 inner products; the level-2 vectors for the
     dense tail are written straight from the base shares (r3_vfy_line_b)."""
     role = party.role
-    terms = _role_terms(role)
-    coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
-    acc = empty((16, gr.d))
-    call("r3_vfy_l2_fold", len(terms), coef, _ptrs([comp.x[t[1]] for t in terms]),
-         _ptrs([comp.y[t[2]] for t in terms]), comp.N, comp.n, comp.ks, comp.ls, ptr(pw), gr.d,
-         ptr(acc), stream())
+    if acc is None:
+        terms = _role_terms(role)
+        coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+        acc = empty((16, gr.d))
+        call("r3_vfy_l2_fold", len(terms), coef, _ptrs([comp.x[t[1]] for t in terms]),
+             _ptrs([comp.y[t[2]] for t in terms]), comp.N, comp.n, comp.ks, comp.ls, ptr(pw), gr.d,
+             ptr(acc), stream())
     W1, W2, w1 = _l2_weights(party, ze1, gr)
     fold = lambda W: _dotsum_terms([([(1, acc, 16)], [(1, W, 16)])], 16, gr)
     n1 = (comp.N + 1) // 2

@@ -153,3 +153,60 @@ def test_u64_gemm_tc_exact(cuda, M, K, N):
                  (grvec.limb_tiles_a(Yd, 1, Xd, -1), grvec.limb_tiles_b(Vd, 1, Wd, 3), K)]
         got2 = host(grvec.u64_gemm(pairs, M, N, addend=Zd, sub=True))
         np.testing.assert_array_equal(got2, want2)
+
+
+@pytest.mark.parametrize("d,N", [(64, 4096 + 37), (16, 3001), (8, 515), (32, 128)])
+def test_base_fold_matches_definitions(cuda, d, N):
+    """r3_vfy_base_fold (one pass over the power table) against the level-1
+    folds, level-2 accumulators and z power sum written out from their
+    definitions (verify.py:168-179 + 215-241), per role's leg terms."""
+    import ctypes as C
+    from paper_2411_09287_b200 import grvec, host, _lib
+    rng = np.random.default_rng(N * 7 + d)
+    pw = _rand(rng, (N, d))
+    M = np.uint64(2**64 - 1)
+    for role, terms in ((0, [(1, 0, 0)]), (1, [(-1, 0, 1), (-1, 1, 0)]),
+                        (2, [(1, 0, 0), (-1, 0, 1), (-1, 1, 0)])):
+        comps_x = [_rand(rng, (N,)) for _ in range(2)]
+        comps_y = [_rand(rng, (N,)) for _ in range(2)]
+        zc = [_rand(rng, (N,)) for _ in range(1 if role == 0 else 2)]
+        with np.errstate(over="ignore"):
+            pad = lambda a: np.concatenate([a, np.zeros(((-N) % 4,) + a.shape[1:], np.uint64)])
+            P = pad(pw)
+            X = [pad(a) for a in comps_x]
+            Y = [pad(a) for a in comps_y]
+            acc = np.zeros((16, d), np.uint64)
+            for a in range(4):
+                for b in range(4):
+                    sab = np.zeros(len(P) // 4, np.uint64)
+                    for cf, xi, yi in terms:
+                        sab += np.uint64(cf % 2**64) * X[xi][a::4] * Y[yi][b::4]
+                    acc[a * 4 + b] = (sab[:, None] * P[a::4]).sum(axis=0)
+            # level 1 by definition: pairs (2q, 2q+1), g2 = 2 y_o - y_e
+            h1 = np.zeros(d, np.uint64)
+            h2 = np.zeros(d, np.uint64)
+            for cf, xi, yi in terms:
+                c = np.uint64(cf % 2**64)
+                xe, xo = X[xi][0::2], X[xi][1::2]
+                ye, yo = Y[yi][0::2], Y[yi][1::2]
+                g2 = np.uint64(2) * yo - ye
+                h1 += ((c * xo * yo)[:, None] * P[1::2]).sum(axis=0)
+                h2 += ((c * np.uint64(2) * xo * g2)[:, None] * P[1::2]).sum(axis=0)
+                h2 -= ((c * xe * g2)[:, None] * P[0::2]).sum(axis=0)
+            zs = [(z[:, None] * pw).sum(axis=0) for z in zc]
+        D = lambda a: grvec.dev(a)
+        dx, dy, dz, dpw = [D(a) for a in comps_x], [D(a) for a in comps_y], [D(a) for a in zc], D(pw)
+        coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+        xs = (C.c_void_p * len(terms))(*[dx[t[1]].data_ptr() for t in terms])
+        ys = (C.c_void_p * len(terms))(*[dy[t[2]].data_ptr() for t in terms])
+        zp = (C.c_void_p * len(dz))(*[t.data_ptr() for t in dz])
+        g_acc, g_h1, g_h2 = grvec.zeros((16, d)), grvec.zeros((1, d)), grvec.zeros((1, d))
+        g_z = grvec.zeros((len(dz), 1, d))
+        _lib.call("r3_vfy_base_fold", len(terms), C.addressof(coef), C.addressof(xs), C.addressof(ys),
+                  len(dz), C.addressof(zp), 1, N, dpw.data_ptr(), d, g_acc.data_ptr(), g_h1.data_ptr(),
+                  g_h2.data_ptr(), g_z.data_ptr(), (1 << 64) - 1, _lib.stream())
+        np.testing.assert_array_equal(host(g_acc), acc, err_msg=f"acc role {role}")
+        np.testing.assert_array_equal(host(g_h1)[0], h1, err_msg=f"h1 role {role}")
+        np.testing.assert_array_equal(host(g_h2)[0], h2, err_msg=f"h2 role {role}")
+        for c in range(len(dz)):
+            np.testing.assert_array_equal(host(g_z)[c, 0], zs[c], err_msg=f"z{c} role {role}")
