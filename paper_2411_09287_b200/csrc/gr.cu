@@ -892,6 +892,12 @@ extern "C" int r3_vfy_l1_line_y(int ncomp, const uint64_t* const* yc, int64_t N,
   return check_launch("r3_vfy_l1_line_y");
 }
 
+// tensor-core form of the d = 64 level fold (lf_tc.cu), used from this many
+// row pairs up; smaller levels stay on the CUDA cores
+int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64_t* ya, const uint64_t* yb,
+                  int64_t N, uint64_t* acc1, uint64_t* acc2, cudaStream_t s);
+constexpr int64_t kLevelFoldTcMinPairs = 4096;
+
 extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* xb, const uint64_t* ya,
                                  const uint64_t* yb, int64_t N, int d, uint64_t* acc1, uint64_t* acc2,
                                  void* stream) {
@@ -902,6 +908,9 @@ extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* x
   }
   if (N == 0) return R3_OK;
   cudaStream_t s = as_stream(stream);
+  const uintptr_t align = uintptr_t(xa) | uintptr_t(xb) | uintptr_t(ya) | uintptr_t(yb);
+  if (d == 64 && (N + 1) / 2 >= kLevelFoldTcMinPairs && (align & 15) == 0)
+    return level_fold_tc(role, xa, xb, ya, yb, N, acc1, acc2, s);
   LevelArrays la{(const u64*)xa, (const u64*)xb, (const u64*)ya, (const u64*)yb};
   const int64_t npairs = (N + 1) / 2;
   int64_t blocks = kNumSMs;

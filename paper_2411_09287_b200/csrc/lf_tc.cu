@@ -1,0 +1,290 @@
+// Dense-level verification folds on the tensor cores (d = 64).
+//
+// One reduction level (verify.py:215-241) needs, per party, the leg folds
+//   h(1) = sum_i  x_o(i) (x) y_o(i)          h(2) = sum_i  t_x(i) (x) t_y(i)
+// over row pairs i = (2i, 2i+1) = (e, o), with t = 2o - e and (x) the
+// unreduced polynomial product, summed over the party's leg terms
+// (gates.py:100-106).  Writing P_uv[a][b] = sum_i u_x(i)[a] v_y(i)[b] for
+// u, v in {e, o}:
+//   h(1)[c] = sum_{a+b=c} P_oo[a][b]
+//   h(2)[c] = sum_{a+b=c} (4 P_oo - 2 P_oe - 2 P_eo + P_ee)[a][b]
+// and [P_ee P_eo; P_oe P_oo] is ONE matrix product X^T Y with X, Y the
+// component arrays viewed as (pairs x 128): M = 128 (both halves of x),
+// N = 64 (one half of y per CTA), K = pairs.  Both operands are MN-major in
+// that view (features contiguous), so the loaders only split u64 words into
+// byte-limb planes -- no transposition.  Each u64 product runs as the 36
+// limb MMAs (kind::i8, p + q <= 7) accumulated per diagonal p + q in 8 TMEM
+// accumulators (8 x 64 of the 512 columns); a CTA's K range is <= 16384
+// pairs so every diagonal is exact mod 2^32 where it matters (tc.cu).  The
+// epilogue recombines the diagonals in u64, applies the (u, v) weights and
+// folds the anti-diagonals into the 2d-1 output words.
+//
+// Work item = (leg term, K chunk, y half).  Warps 0-3: epilogue (TMEM lane
+// quadrants); warps 4-15: loaders (global u64 -> limb planes in shared
+// memory, B operand = c0 Y0 + c1 Y1 formed on the fly); warp 16: MMA issuer.
+#include "tc_common.cuh"
+
+namespace r3 {
+
+constexpr int LF_BM = 128, LF_BN = 64, LF_BK = 32;
+constexpr int LF_A_PLANE = LF_BM * LF_BK;        // 4 KB
+constexpr int LF_B_PLANE = LF_BN * LF_BK;        // 2 KB
+constexpr int LF_A_TILE = 8 * LF_A_PLANE;        // 32 KB
+constexpr int LF_B_TILE = 8 * LF_B_PLANE;        // 16 KB
+constexpr int LF_STAGES = 4;
+constexpr int LF_LOADERS = 12 * 32;              // 256 A tasks + 128 B tasks per k-block
+constexpr int LF_THREADS = 4 * 32 + LF_LOADERS + 32;
+constexpr int LF_RED = 2 * 128 * 8;              // h1/h2 anti-diagonal sums
+constexpr int LF_SMEM = LF_STAGES * (LF_A_TILE + LF_B_TILE) + LF_RED + 256;
+constexpr int64_t LF_MAX_K = 16384;              // exact-accumulation bound (pairs per item)
+
+struct LfTerm {
+  const u64* a;    // x component (rows x 64)
+  const u64* b0;   // y = c0*b0 + c1*b1
+  const u64* b1;
+  u64 c0, c1;
+};
+
+struct LfArgs {
+  LfTerm t[2];
+  int nterms;
+  int64_t rows, npairs, kc, nchunks;
+};
+
+// 16 u64 -> 8 planes of 16 bytes (byte i of each value)
+__device__ __forceinline__ void lf_split16(const u64 (&v)[16], uint4 (&out)[8]) {
+  uint32_t w[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    w[2 * q] = uint32_t(v[q]);
+    w[2 * q + 1] = uint32_t(v[q] >> 32);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int hiw = i >> 2, bi = i & 3;
+    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
+    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
+    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
+    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
+  }
+}
+
+__device__ __forceinline__ void lf_named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(LF_THREADS, 1)
+level_fold_tc_kernel(LfArgs args, u64* __restrict__ acc1, u64* __restrict__ acc2) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + LF_STAGES * LF_A_TILE;
+  u64* red1 = reinterpret_cast<u64*>(smem + LF_STAGES * (LF_A_TILE + LF_B_TILE));
+  u64* red2 = red1 + 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LF_STAGES * (LF_A_TILE + LF_B_TILE) + LF_RED);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + LF_STAGES;
+  uint64_t* tfull = bars + 2 * LF_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // work item
+  const int64_t item = blockIdx.x;
+  const int half = int(item & 1);
+  const int64_t chunk = (item >> 1) % args.nchunks;
+  const int term = int((item >> 1) / args.nchunks);
+  const LfTerm T = args.t[term];
+  const int64_t p0 = chunk * args.kc;
+  const int64_t p1 = min(args.npairs, p0 + args.kc);
+  const int64_t nkb = (p1 - p0 + LF_BK - 1) / LF_BK;
+
+  if (threadIdx.x < 256) red1[threadIdx.x] = 0;  // red1 and red2 (contiguous)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LF_STAGES; ++s) {
+      mbar_init(&full[s], LF_LOADERS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 4 && warp < 16) {
+    // ---------------- loaders
+    const int lt = threadIdx.x - 128;
+    const bool isA = lt < 256;
+    const int k = lt & 31;
+    const int c = isA ? (lt >> 5) : ((lt - 256) >> 5);   // 16-feature chunk
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+      if (kb >= LF_STAGES) mbar_wait(&empty[stage], ph ^ 1);
+      const int64_t p = p0 + kb * LF_BK + k;
+      u64 v[16];
+      if (isA) {
+        // pair row p: features 0..63 = row 2p, 64..127 = row 2p+1
+        const bool ok = p < p1 && (c < 4 || 2 * p + 1 < args.rows);
+        const u64* src = T.a + p * 128 + c * 16;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          ulonglong2 x = ok ? __ldg(reinterpret_cast<const ulonglong2*>(src + q)) : make_ulonglong2(0, 0);
+          v[q] = x.x;
+          v[q + 1] = x.y;
+        }
+      } else {
+        const int64_t row = 2 * p + half;
+        const bool ok = p < p1 && row < args.rows;
+        const u64* s0 = T.b0 + row * 64 + c * 16;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          ulonglong2 x = ok ? __ldg(reinterpret_cast<const ulonglong2*>(s0 + q)) : make_ulonglong2(0, 0);
+          v[q] = T.c0 * x.x;
+          v[q + 1] = T.c0 * x.y;
+        }
+        if (T.b1) {
+          const u64* s1 = T.b1 + row * 64 + c * 16;
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+            ulonglong2 x = ok ? __ldg(reinterpret_cast<const ulonglong2*>(s1 + q)) : make_ulonglong2(0, 0);
+            v[q] += T.c1 * x.x;
+            v[q + 1] += T.c1 * x.y;
+          }
+        }
+      }
+      uint4 pk[8];
+      lf_split16(v, pk);
+      // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
+      uint8_t* dst = isA ? sA + stage * LF_A_TILE : sB + stage * LF_B_TILE;
+      const int plane = isA ? LF_A_PLANE : LF_B_PLANE;
+      const uint32_t off = uint32_t(c * 512 + k * 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * plane + off) = pk[i];
+      fence_async_smem();
+      mbar_arrive(&full[stage]);
+      if (++stage == LF_STAGES) {
+        stage = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 16) {
+    // ---------------- MMA issuer
+    constexpr uint32_t IDESC = idesc_u8(LF_BM, LF_BN) | (1u << 15) | (1u << 16);  // A, B MN-major
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full[stage], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sA + stage * LF_A_TILE);
+        const uint32_t b0 = smem_u32(sB + stage * LF_B_TILE);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+#pragma unroll
+          for (int i = 0; i <= s; ++i) {
+            const uint64_t ad = umma_desc(a0 + i * LF_A_PLANE, 128, 512);
+            const uint64_t bd = umma_desc(b0 + (s - i) * LF_B_PLANE, 128, 512);
+            mma_u8(tmem + uint32_t(s * LF_BN), ad, bd, IDESC, (kb == 0 && i == 0) ? 0u : 1u);
+          }
+        }
+        mma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == LF_STAGES) {
+        stage = 0;
+        ph ^= 1;
+      }
+    }
+    if (lane == 0) mma_commit(tfull);
+    __syncwarp();
+  } else if (warp < 4) {
+    // ---------------- epilogue: TMEM lane m = feature (u, a) of x
+    if (nkb > 0) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+      const int m = warp * 32 + lane;
+      const int u = m >> 6, a = m & 63;
+      const u64 w2 = (u == 0 && half == 0) ? 1ull : (u == 1 && half == 1) ? 4ull : u64(-2ll);
+      const bool to_h1 = u == 1 && half == 1;
+      const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < LF_BN; c0 += 8) {
+        uint32_t v[8][8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * LF_BN + c0), v[s]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          u64 P = 0;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) P += u64(v[s][q]) << (8 * s);
+          const int cidx = a + c0 + q;
+          atomicAdd(reinterpret_cast<unsigned long long*>(red2 + cidx), (unsigned long long)(w2 * P));
+          if (to_h1) atomicAdd(reinterpret_cast<unsigned long long*>(red1 + cidx), (unsigned long long)P);
+        }
+      }
+      tc_fence_before();
+      lf_named_sync(1, 128);
+      const int t = threadIdx.x;
+      if (t < 127) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(acc2 + t), (unsigned long long)red2[t]);
+        if (half == 1) atomicAdd(reinterpret_cast<unsigned long long*>(acc1 + t), (unsigned long long)red1[t]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+// Called by r3_vfy_level_fold for d == 64 (same contract).
+int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64_t* ya, const uint64_t* yb,
+                  int64_t N, uint64_t* acc1, uint64_t* acc2, cudaStream_t s) {
+  LfArgs args{};
+  const u64 M1 = ~0ull;  // -1
+  auto A = [](const uint64_t* p) { return reinterpret_cast<const u64*>(p); };
+  if (role == 0) {
+    args.t[0] = {A(xa), A(ya), nullptr, 1, 0};
+    args.nterms = 1;
+  } else if (role == 1) {  // -(m_x s_y) - (s_x m_y)
+    args.t[0] = {A(xa), A(yb), nullptr, M1, 0};
+    args.t[1] = {A(xb), A(ya), nullptr, M1, 0};
+    args.nterms = 2;
+  } else {  // m_x (m_y - s_y) - s_x m_y
+    args.t[0] = {A(xa), A(ya), A(yb), 1, M1};
+    args.t[1] = {A(xb), A(ya), nullptr, M1, 0};
+    args.nterms = 2;
+  }
+  args.rows = N;
+  args.npairs = (N + 1) / 2;
+  int64_t nchunks = (args.npairs + LF_MAX_K - 1) / LF_MAX_K;
+  const int64_t per_chunk_items = 2 * args.nterms;
+  const int64_t waves = (nchunks * per_chunk_items + kNumSMs - 1) / kNumSMs;
+  int64_t want = waves * kNumSMs / per_chunk_items;  // fill the last wave
+  const int64_t min_kc = 8 * LF_BK;
+  if (want * min_kc > args.npairs) want = (args.npairs + min_kc - 1) / min_kc;
+  if (want > nchunks) nchunks = want;
+  int64_t kc = (args.npairs + nchunks - 1) / nchunks;
+  kc = (kc + LF_BK - 1) / LF_BK * LF_BK;
+  nchunks = (args.npairs + kc - 1) / kc;
+  args.kc = kc;
+  args.nchunks = nchunks;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(level_fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LF_SMEM);
+    attr = true;
+  }
+  const unsigned grid = unsigned(nchunks * per_chunk_items);
+  level_fold_tc_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(args, (u64*)acc1, (u64*)acc2);
+  return check_launch("r3_vfy_level_fold(tc)");
+}

@@ -94,7 +94,7 @@ def test_gr_matmul2_tc_line_eval(cuda, rows):
     np.testing.assert_array_equal(host(out1), ogr.mul(X, z, 64, 64))
 
 
-@pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 40001), (16, 1000), (32, 77)])
+@pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
 def test_level_fold_matches_oracle(cuda, d, N):
     """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
     (verify.py:220-230 + gates.py:100-106) restated with oracle/gr.py."""
