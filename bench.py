@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-kernel", default="r3_vfy_level_fold")
+    ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--matmul-n", type=int, default=4096)
     return ap.parse_args()
@@ -289,8 +289,11 @@ def matmul_c3(n: int, steps: int) -> dict:
         party.freeze_logs()
         return rec(party, z, "z").cpu() if open_out else None
 
+    from paper_2411_09287_b200 import _lib
     out = Session(seed=3).run(prog, True)[0]
     torch.cuda.synchronize()
+    timer = KernelTimer("r3_u64_gemm_tc")
+    _lib.CALL_HOOK = timer.hook
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
@@ -298,7 +301,10 @@ def matmul_c3(n: int, steps: int) -> dict:
         Session(seed=30 + i).run(prog, False)
     b.record()
     torch.cuda.synchronize()
+    _lib.CALL_HOOK = None
     sec = a.elapsed_time(b) / 1e3 / steps
+    gemm_s = timer.seconds()
+    peak8 = int8_peak_ops(torch)
     # probabilistic truncation: |open - X W / 2^16| <= 1 ulp on sampled entries
     rs = np.random.default_rng(5)
     idx = rs.integers(0, n, (64, 2))
@@ -312,6 +318,14 @@ def matmul_c3(n: int, steps: int) -> dict:
     return {"n": n, "ms_per_matmul": sec * 1e3, "matmuls_per_s": 1 / sec,
             "u64_macs_per_s": u64_macs / sec, "int8_tops_equiv": 2 * 36 * u64_macs / sec / 1e12,
             "check": "64 sampled outputs within 1 ulp of trunc(XW)",
+            "gemm_roofline": {"bound": "tensor", "kernel": "r3_u64_gemm_tc",
+                              "achieved": timer.work / gemm_s / 1e12 if gemm_s else None,
+                              "peak": peak8 / 1e12, "unit": "int8 TOP/s",
+                              "frac": timer.work / gemm_s / peak8 if gemm_s else None,
+                              "launches": timer.launches,
+                              "kernel_share_of_step": gemm_s / steps / sec,
+                              "peak_source": "measured in-run: cuBLASLt int8 torch._int_mm 8192^3 (dense)",
+                              "work": "2 x 36 limb MACs x M x N x sum(K) per launch"},
             "scope": "PRE (masks, trunc_prepare 2^24 lanes, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online)"}
 
 
@@ -344,8 +358,16 @@ class KernelTimer:
 
 
 def work_of(name, args) -> int:
-    """Algorithmic u64 multiply-accumulates of one call (rows x d^2 for the
-    GR contractions)."""
+    """Algorithmic work of one call: bytes moved for the HBM-bound tensor-core
+    line evaluations (r3_gr_matmul2_tc reads nops rows of 512 B and writes one
+    per output row), u64 multiply-accumulates for the CUDA-core
+    GR contractions."""
+    if name == "r3_gr_matmul2_tc":
+        p1, nv0, nv1, rows = args[3], int(args[2]), int(args[5]), int(args[9])
+        return 512 * (rows + min(nv0, rows) + (min(nv1, rows) if p1 else 0))
+    if name == "r3_u64_gemm_tc":
+        npairs, K, M, N = int(args[0]), args[3], int(args[4]), int(args[5])
+        return 2 * 36 * M * N * sum(int(K[p]) for p in range(npairs))
     if name == "r3_vfy_level_fold":
         # per pair: h(1) and h(2), one outer product each for P0, two for P1/P2
         role, N, d = args[0], args[5], args[6]
@@ -358,6 +380,41 @@ def work_of(name, args) -> int:
         rows, d = args[5], args[6]
         return int(rows) * int(d) * int(d)
     return 0
+
+
+KERNEL_BOUND = {
+    "r3_gr_matmul2_tc": ("hbm", "GB/s", 1e9),
+    "r3_vfy_level_fold": ("int-alu", "Tu64MAC/s", 1e12),
+    "r3_gr_matmul": ("int-alu", "Tu64MAC/s", 1e12),
+    "r3_gr_dotsum": ("int-alu", "Tu64MAC/s", 1e12),
+}
+
+
+def hbm_peak() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    except (OSError, KeyError, ValueError):
+        return 6.65e12, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def int8_peak_ops(torch) -> float:
+    """Measured dense int8 tensor throughput (cuBLASLt torch._int_mm, 8192^3)."""
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t().contiguous().t()
+    torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) / 1e3))
+    return best
 
 
 def imad_peak_macs(torch, lib) -> float:
@@ -431,7 +488,14 @@ def run_b200(args):
 
     # roofline of the dominant kernel, timed live in the region above
     kt = timer.seconds()
-    peak = imad_peak_macs(torch, _lib)
+    bound, r_unit, scale = KERNEL_BOUND.get(args.profile_kernel, ("int-alu", "Tu64MAC/s", 1e12))
+    if bound == "hbm":
+        peak, peak_src = hbm_peak()
+        work_desc = "algorithmic bytes = 512 B x (rows written + rows read per operand) per launch"
+    else:
+        peak = imad_peak_macs(torch, _lib)
+        peak_src = "measured in-run by r3_imad_peak (MEASURED_PEAKS.json has no integer peak)"
+        work_desc = "algorithmic work = rows*d^2 u64 MACs per launch"
     achieved = timer.work / kt if kt else 0.0
 
     # end-to-end: host inputs in pinned memory, opened product back to host
@@ -461,13 +525,12 @@ def run_b200(args):
                    "N_per_gpu": N, "ell": 64, "d": d, "R": R, "engine": args.engine,
                    "l2": f"inputs larger than L2 ({N * 8 * 12 / 2**20:.0f} MiB of shares per step)",
                    "parallelism": f"weak dp{world}: independent sessions per rank"},
-        "roofline": {"bound": "int-alu", "kernel": args.profile_kernel,
-                     "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tu64MAC/s",
+        "roofline": {"bound": bound, "kernel": args.profile_kernel,
+                     "achieved": achieved / scale, "peak": peak / scale, "unit": r_unit,
                      "frac": achieved / peak if peak else None, "traffic": None,
                      "launches": timer.launches, "kernel_s_per_step": kt / args.steps,
                      "kernel_share_of_step": kt / secs if secs else None,
-                     "peak_source": "measured in-run by r3_imad_peak (MEASURED_PEAKS.json has no "
-                                    "integer peak); algorithmic work = rows*d^2 u64 MACs per launch"},
+                     "peak_source": peak_src + "; " + work_desc},
         "e2e": {"value": N * world * args.e2e_steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": N * 8},
         "gpu_launches": int(launches),

@@ -12,8 +12,9 @@
 // r3_gr_matmul2_tc: out[r] = P0[r] . M0 (+ P1[r] . M1) for GR(2^64, 64) rows
 // -- the "many elements times one public element" contraction of the
 // verification (line evaluations f0 (1 - zeta) + f1 zeta, power tables).
-// M = 64 x 64, so K = N = 64: per 128-row tile and operand 72 MMAs of
-// 128 x 64 x 32 into 8 x 64 TMEM columns (the full 512-column TMEM).
+// M = 64 x 64, so K = N = 64: per 128-row tile and operand 24 MMAs (the 36
+// limb products of both K-halves, N-concatenated) into 8 x 64 TMEM columns
+// (the full 512-column TMEM).
 //
 // smem operands use the canonical K-major no-swizzle layout: 8-row x 16-byte
 // core matrices, core (g, kc) at (kc * G + g) * 128 bytes (G = rows / 8), so
@@ -22,60 +23,77 @@
 
 namespace r3 {
 constexpr int TC_ROWS = 128;        // MMA M
-constexpr int TC_D = 64;            // GR degree = K = N
-constexpr int A_PLANE = TC_ROWS * TC_D;   // bytes per limb plane of A (8 KB)
-constexpr int B_PLANE = TC_D * TC_D;      // bytes per limb plane of B (4 KB)
+constexpr int TC_D = 64;            // GR degree = K = N of one limb product
+constexpr int TC_KH = 32;           // K per unit (one MMA K-step of kind::i8)
 
 // ---------------------------------------------------------------------------
-// Warp-specialised pipelined form: out = P0 . M0 (+ P1 . M1)
+// Pipelined form: out = P0 . M0 (+ P1 . M1).  A unit is (tile of 128 rows,
+// operand, K-half): 128 x 32 u64 = 32 KB of HBM, moved by two TMA tile loads
+// (16 u64 x 128 rows each, 128-byte swizzle so the converters read it
+// bank-conflict free) into a raw stage, split into 8 byte-limb planes
+// (128 x 32 B, K-major no-swizzle core matrices) by the converter warps, and
+// consumed by 12 MMAs: limb plane i of A times the N-concatenated limb planes
+// [B_0 .. B_{7-i}] of the public matrix (N = 64 (8 - i), split at 256), whose
+// column block j lands on diagonal i + j of the TMEM accumulator (diagonal s
+// at columns 64 s).  Each A plane is read by the tensor core once per unit
+// instead of once per (i, j) limb product.
 //   warps 0-3   epilogue: TMEM diagonals -> u64 recombination -> global
-//   warps 4-11  loaders : 16 consecutive u64 of a row -> 8 limb planes (smem)
-//   warp 12     MMA issue (one elected lane)
-// Two operand stages (one per operand of a tile, or consecutive tiles) are
-// ping-ponged through mbarriers; the 512 TMEM columns hold the 8 diagonal
-// accumulators of one 128 x 64 tile.
+//   warps 4-11  converters: raw stage -> limb planes
+//   warp 12     TMA producer (one elected lane)
+//   warp 13     MMA issuer (one elected lane)
 // ---------------------------------------------------------------------------
-constexpr int W_EPI = 4, W_LOAD = 8;
-constexpr int WS_THREADS = (W_EPI + W_LOAD + 1) * 32;
-constexpr int STAGE_BYTES = 8 * A_PLANE;                 // 64 KB: one operand tile in limbs
-constexpr int WS_SMEM = 2 * STAGE_BYTES + 2 * 8 * B_PLANE + 128;
-
-struct RowOperand {
-  const u64* p;
-  int64_t rs;
-  int64_t nvalid;
-};
-
+constexpr int W_EPI = 4, W_CONV = 8;
+constexpr int WS_THREADS = (W_EPI + W_CONV + 2) * 32;
+constexpr int RAW_STAGES = 3, LIMB_STAGES = 2;
+constexpr int RAW_BYTES = TC_ROWS * TC_KH * 8;           // 32 KB
+constexpr int LIMB_PLANE = TC_ROWS * TC_KH;              // 4 KB
+constexpr int LIMB_BYTES = 8 * LIMB_PLANE;               // 32 KB
+constexpr int BALL_ROWS = 8 * TC_D;                      // 512 = 8 limb planes of N
+constexpr int BALL_BYTES = BALL_ROWS * TC_D;             // 32 KB per operand
+constexpr int OFF_LIMB = RAW_STAGES * RAW_BYTES;
+constexpr int OFF_B = OFF_LIMB + LIMB_STAGES * LIMB_BYTES;
+constexpr int OFF_BAR = OFF_B + 2 * BALL_BYTES;
+constexpr int WS_SMEM = OFF_BAR + 128 + 1024;            // + alignment slack
 
 __global__ void __launch_bounds__(WS_THREADS, 1)
-gr_matmul2_tc_kernel(RowOperand P0, RowOperand P1, int nops, const u64* __restrict__ M0,
-                     const u64* __restrict__ M1, u64* __restrict__ out, int64_t rows, u64 mask) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA[2] = {smem, smem + STAGE_BYTES};
-  uint8_t* sB[2] = {smem + 2 * STAGE_BYTES, smem + 2 * STAGE_BYTES + 8 * B_PLANE};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE_BYTES + 16 * B_PLANE);
-  uint64_t* full = bars;        // [2] loaders -> MMA
-  uint64_t* empty = bars + 2;   // [2] MMA -> loaders
-  uint64_t* tfull = bars + 4;   // MMA -> epilogue
-  uint64_t* tempty = bars + 5;  // epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                     int nops, const u64* __restrict__ M0, const u64* __restrict__ M1, u64* __restrict__ out,
+                     int64_t rows, u64 mask) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sRaw = smem;
+  uint8_t* sLimb = smem + OFF_LIMB;
+  uint8_t* sB = smem + OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* raw_full = bars;                       // [3] TMA -> converters
+  uint64_t* raw_empty = bars + 3;                  // [3] converters -> TMA
+  uint64_t* limb_full = bars + 6;                  // [2] converters -> MMA
+  uint64_t* limb_empty = bars + 8;                 // [2] MMA -> converters
+  uint64_t* tfull = bars + 10;                     // MMA -> epilogue
+  uint64_t* tempty = bars + 11;                    // epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // B operands: B_j[n][k] = limb j of M[k][n]
+  // B_all[op]: row n' = 64 j + n holds limb j of column n of M (K = 64 bytes)
   for (int op = 0; op < nops; ++op) {
     const u64* M = op ? M1 : M0;
+    uint8_t* dst = sB + op * BALL_BYTES;
     for (int e = tid; e < TC_D * TC_D; e += WS_THREADS) {
       const int k = e / TC_D, n = e % TC_D;
       const u64 v = M[e];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sB[op][j * B_PLANE + core_off(n, k, TC_D / 8)] = uint8_t(v >> (8 * j));
+      for (int j = 0; j < 8; ++j) dst[core_off(j * TC_D + n, k, BALL_ROWS / 8)] = uint8_t(v >> (8 * j));
     }
   }
   if (tid == 0) {
-    mbar_init(&full[0], W_LOAD * 32);
-    mbar_init(&full[1], W_LOAD * 32);
-    mbar_init(&empty[0], 1);
-    mbar_init(&empty[1], 1);
+    for (int i = 0; i < RAW_STAGES; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], W_CONV * 32);
+    }
+    for (int i = 0; i < LIMB_STAGES; ++i) {
+      mbar_init(&limb_full[i], W_CONV * 32);
+      mbar_init(&limb_empty[i], 1);
+    }
     mbar_init(tfull, 1);
     mbar_init(tempty, W_EPI * 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -90,54 +108,46 @@ gr_matmul2_tc_kernel(RowOperand P0, RowOperand P1, int nops, const u64* __restri
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nunits = my_tiles * nops * 2;
 
-  if (warp >= W_EPI && warp < W_EPI + W_LOAD) {
-    // ------------------------------ loaders
-    // Flat stream of units (tile, operand, half): the loads of unit u+1 are in
-    // flight while unit u is split into limb planes (register double buffer).
-    const int ltid = tid - W_EPI * 32;
-    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    const int64_t nunits = my_tiles * nops * 2;
-    uint32_t w[2][32];
-    auto load_unit = [&](int64_t u, uint32_t (&dst)[32]) {
-      const int64_t t = blockIdx.x + (u / (2 * nops)) * gridDim.x;
-      const int op = int((u >> 1) % nops), h = int(u & 1);
-      const RowOperand P = op ? P1 : P0;
-      const int task = ltid + h * W_LOAD * 32;
-      const int r = task & (TC_ROWS - 1), k0 = (task >> 7) * 16;
-      const int64_t row = t * TC_ROWS + r;
-      if (row < rows && row < P.nvalid) {
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(P.p + row * P.rs + k0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          ulonglong2 v = __ldg(src + q);
-          dst[4 * q + 0] = uint32_t(v.x);
-          dst[4 * q + 1] = uint32_t(v.x >> 32);
-          dst[4 * q + 2] = uint32_t(v.y);
-          dst[4 * q + 3] = uint32_t(v.y >> 32);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) dst[q] = 0;
+  if (warp == W_EPI + W_CONV) {
+    // ------------------------------ TMA producer
+    if (lane == 0) {
+      for (int64_t u = 0; u < nunits; ++u) {
+        const int st = int(u % RAW_STAGES);
+        if (u >= RAW_STAGES) mbar_wait(&raw_empty[st], uint32_t((u / RAW_STAGES - 1) & 1));
+        const int64_t t = blockIdx.x + (u / (2 * nops)) * gridDim.x;
+        const int op = int((u >> 1) % nops), h = int(u & 1);
+        const CUtensorMap* map = op ? &tm1 : &tm0;
+        uint8_t* dst = sRaw + st * RAW_BYTES;
+        mbar_expect_tx(&raw_full[st], RAW_BYTES);
+        tma_load_2d(dst, map, h * TC_KH, int(t * TC_ROWS), &raw_full[st]);
+        tma_load_2d(dst + RAW_BYTES / 2, map, h * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
       }
-    };
-    int stage = 0;
-    uint32_t ephase0 = 0, ephase1 = 0;
-    int used0 = 0, used1 = 0;
-    // a unit with h == 0 opens a stage, h == 1 closes it; units come in pairs
-    auto process = [&](int h, const uint32_t (&x)[32]) {
-      if (h == 0) {
-        if (stage == 0) {
-          if (used0) { mbar_wait(&empty[0], ephase0); ephase0 ^= 1; }
-          used0 = 1;
-        } else {
-          if (used1) { mbar_wait(&empty[1], ephase1); ephase1 ^= 1; }
-          used1 = 1;
-        }
+    }
+    __syncwarp();
+  } else if (warp >= W_EPI && warp < W_EPI + W_CONV) {
+    // ------------------------------ converters: thread = (row r, 16-u64 box c)
+    const int ct = tid - W_EPI * 32;
+    const int r = ct & (TC_ROWS - 1), c = ct >> 7;
+    const int sw = r & 7;
+    for (int64_t u = 0; u < nunits; ++u) {
+      const int st = int(u % RAW_STAGES), ls = int(u % LIMB_STAGES);
+      mbar_wait(&raw_full[st], uint32_t((u / RAW_STAGES) & 1));
+      const uint8_t* src = sRaw + st * RAW_BYTES + c * (RAW_BYTES / 2) + r * 128;
+      uint32_t x[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + ((q ^ sw) << 4));
+        x[4 * q + 0] = v.x;
+        x[4 * q + 1] = v.y;
+        x[4 * q + 2] = v.z;
+        x[4 * q + 3] = v.w;
       }
-      const int task = ltid + h * W_LOAD * 32;
-      const int r = task & (TC_ROWS - 1), k0 = (task >> 7) * 16;
-      uint8_t* dst = (stage ? sA[1] : sA[0]) + core_off(r, k0, TC_ROWS / 8);
+      mbar_arrive(&raw_empty[st]);
+      if (u >= LIMB_STAGES) mbar_wait(&limb_empty[ls], uint32_t((u / LIMB_STAGES - 1) & 1));
+      uint8_t* dst = sLimb + ls * LIMB_BYTES + core_off(r, c * 16, TC_ROWS / 8);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int hiw = i >> 2, bi = i & 3;
@@ -146,66 +156,48 @@ gr_matmul2_tc_kernel(RowOperand P0, RowOperand P1, int nops, const u64* __restri
         pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
         pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
         pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
-        *reinterpret_cast<uint4*>(dst + i * A_PLANE) = pk;
+        *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk;
       }
-      if (h == 1) {
-        fence_async_smem();
-        mbar_arrive(&full[stage]);
-        stage ^= 1;
-      }
-    };
-    if (nunits > 0) load_unit(0, w[0]);
-#pragma unroll 1
-    for (int64_t u = 0; u < nunits; u += 2) {
-      load_unit(u + 1, w[1]);                     // nunits is even
-      process(0, w[0]);
-      if (u + 2 < nunits) load_unit(u + 2, w[0]);
-      process(1, w[1]);
+      fence_async_smem();
+      mbar_arrive(&limb_full[ls]);
     }
-  } else if (warp == W_EPI + W_LOAD) {
+  } else if (warp == W_EPI + W_CONV + 1) {
     // ------------------------------ MMA issuer
-    constexpr uint32_t IDESC = idesc_u8(TC_ROWS, TC_D);
-    int stage = 0;
-    uint32_t fphase[2] = {0, 0};
     uint32_t tphase = 0;
-    bool first_tile = true;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      if (!first_tile) {
+    for (int64_t u = 0; u < nunits; ++u) {
+      const int ls = int(u % LIMB_STAGES);
+      const int op = int((u >> 1) % nops), h = int(u & 1);
+      const bool tile_first = (u % (2 * nops)) == 0;
+      const bool tile_last = (u % (2 * nops)) == 2 * nops - 1;
+      if (tile_first && u > 0) {
         mbar_wait(tempty, tphase);
         tphase ^= 1;
       }
-      first_tile = false;
+      mbar_wait(&limb_full[ls], uint32_t((u / LIMB_STAGES) & 1));
       tc_fence_after();
-      for (int op = 0; op < nops; ++op) {
-        mbar_wait(&full[stage], fphase[stage]);
-        fphase[stage] ^= 1;
-        tc_fence_after();
-        if (lane == 0) {
-#pragma unroll 1
-          for (int s = 0; s < 8; ++s) {
-            const uint32_t d_tmem = tmem + uint32_t(s * TC_D);
-            for (int i = 0; i <= s; ++i) {
-              const int j = s - i;
-              for (int kk = 0; kk < TC_D; kk += 32) {
-                const uint32_t a_addr = smem_u32(sA[stage] + i * A_PLANE) + uint32_t((kk >> 4) * (TC_ROWS / 8) * 128);
-                const uint32_t b_addr = smem_u32(sB[op] + j * B_PLANE) + uint32_t((kk >> 4) * (TC_D / 8) * 128);
-                const uint64_t ad = umma_desc(a_addr, (TC_ROWS / 8) * 128, 128);
-                const uint64_t bd = umma_desc(b_addr, (TC_D / 8) * 128, 128);
-                const bool acc = op > 0 || i > 0 || kk > 0;
-                mma_u8(d_tmem, ad, bd, IDESC, acc ? 1u : 0u);
-              }
-            }
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sLimb + ls * LIMB_BYTES);
+        // K-half h = core columns 2h, 2h+1 of B_all (LBO = 64 groups x 128 B)
+        const uint32_t b0 = smem_u32(sB + op * BALL_BYTES) + uint32_t(2 * h * (BALL_ROWS / 8) * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint64_t ad = umma_desc(a0 + i * LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
+          const int ncols = TC_D * (8 - i);
+#pragma unroll
+          for (int n0 = 0; n0 < ncols; n0 += 256) {
+            const int nn = ncols - n0 < 256 ? ncols - n0 : 256;
+            const uint64_t bd = umma_desc(b0 + uint32_t((n0 / 8) * 128), (BALL_ROWS / 8) * 128, 128);
+            const bool acc = !(tile_first && i == 0);
+            mma_u8(tmem + uint32_t(TC_D * i + n0), ad, bd, idesc_u8(TC_ROWS, nn), acc ? 1u : 0u);
           }
-          mma_commit(&empty[stage]);
-          if (op == nops - 1) mma_commit(tfull);
         }
-        __syncwarp();
-        stage ^= 1;
+        mma_commit(&limb_empty[ls]);
+        if (tile_last) mma_commit(tfull);
       }
+      __syncwarp();
     }
   } else if (warp < W_EPI) {
-    // ------------------------------ epilogue: warp e reads TMEM lane quadrant
-    // e % 4 (rows) and column half e / 4; 8 columns x 8 diagonals per batch
+    // ------------------------------ epilogue: warp e reads TMEM lane quadrant e
     uint32_t phase = 0;
     const int quad = warp & 3;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -244,6 +236,33 @@ gr_matmul2_tc_kernel(RowOperand P0, RowOperand P1, int nops, const u64* __restri
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------
+// host: tensor maps (driver entry point fetched through the runtime, so the
+// library needs no -lcuda)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_rows_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t rs_words, int box_rows, int width) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  cuuint64_t dims[2] = {cuuint64_t(width), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(rs_words * 8)};
+  cuuint32_t box[2] = {16u, cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace r3
 
 using namespace r3;
@@ -251,22 +270,53 @@ using namespace r3;
 extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, const uint64_t* p1, int64_t rs1,
                                 int64_t nv1, const uint64_t* M0, const uint64_t* M1, uint64_t* out, int64_t rows,
                                 uint64_t mask, void* stream) {
-  if (!p0 || !M0 || rows < 0 || ((rs0 | rs1) & 1) || ((uintptr_t(p0) | uintptr_t(p1)) & 15)) {
+  if (!p0 || !M0 || rows < 0 || ((rs0 | rs1) & 1) || ((uintptr_t(p0) | uintptr_t(p1)) & 15) ||
+      (p1 && !M1)) {
     set_error("r3_gr_matmul2_tc: bad arguments (need 16-byte aligned rows)");
     return R3_ERR_ARG;
   }
   if (rows == 0) return R3_OK;
+  if (rows > (int64_t(1) << 31) - TC_ROWS) {
+    set_error("r3_gr_matmul2_tc: rows %lld exceed the TMA coordinate range", (long long)rows);
+    return R3_ERR_ARG;
+  }
+  // operands with no valid rows contribute zero: drop them
+  const uint64_t* P[2] = {p0, p1};
+  const uint64_t* Ms[2] = {M0, M1};
+  int64_t rs[2] = {rs0, rs1}, nv[2] = {nv0 < rows ? nv0 : rows, nv1 < rows ? nv1 : rows};
+  int nops = 0;
+  const uint64_t* Pk[2];
+  const uint64_t* Mk[2];
+  int64_t rsk[2], nvk[2];
+  for (int q = 0; q < 2; ++q) {
+    if (P[q] && nv[q] > 0) {
+      Pk[nops] = P[q];
+      Mk[nops] = Ms[q];
+      rsk[nops] = rs[q] > 0 ? rs[q] : TC_D;
+      nvk[nops] = nv[q];
+      ++nops;
+    }
+  }
+  if (nops == 0) {
+    cudaMemsetAsync(out, 0, size_t(rows) * TC_D * 8, as_stream(stream));
+    return check_launch("r3_gr_matmul2_tc(zero)");
+  }
+  CUtensorMap tm[2];
+  for (int q = 0; q < nops; ++q) {
+    if (!make_rows_tmap(&tm[q], Pk[q], nvk[q], rsk[q], TC_ROWS)) {
+      set_error("r3_gr_matmul2_tc: cuTensorMapEncodeTiled failed");
+      return R3_ERR_CUDA;
+    }
+  }
+  if (nops == 1) tm[1] = tm[0];
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gr_matmul2_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
     attr = true;
   }
-  RowOperand a{reinterpret_cast<const u64*>(p0), rs0, nv0};
-  RowOperand b{reinterpret_cast<const u64*>(p1), rs1, nv1};
-  const int nops = p1 ? 2 : 1;
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
   const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
-  gr_matmul2_tc_kernel<<<grid, WS_THREADS, WS_SMEM, as_stream(stream)>>>(a, b, nops, (const u64*)M0,
-                                                                          (const u64*)M1, (u64*)out, rows, mask);
+  gr_matmul2_tc_kernel<<<grid, WS_THREADS, WS_SMEM, as_stream(stream)>>>(
+      tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc");
 }

@@ -3,6 +3,8 @@
 // form: 8-row x 16-byte core matrices).
 #pragma once
 
+#include <cuda.h>
+
 #include "r3_common.cuh"
 
 namespace r3 {
@@ -108,5 +110,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+
+// 2-D TMA tile load (tensor map in kernel-parameter space) completing on bar.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Host: tensor map over `rows` rows of `width` u64 (row stride rs_words,
+// 16-byte aligned), box = 16 u64 x box_rows rows, 128-byte swizzle (16-byte
+// chunk j of smem row r lands at chunk j ^ (r & 7)); rows past `rows` read
+// as zero.
+bool make_rows_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t rs_words, int box_rows,
+                    int width = 64);
 
 }  // namespace r3

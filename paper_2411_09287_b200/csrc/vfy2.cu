@@ -94,7 +94,9 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 // out_c[j] = sum_{a<B} X_c[B j + a] * T_a[row_a(j)], T_a = tabs + a*tab_stride
 // with row_a(j) = (B j + a) / tq  (tq = B for multiplication logs, whose
 // tables hold one row per block; tq = n for dot logs sharing a power).
-template <int D>
+// ONE: a multiplication log (n == 1, tq == B): element i sits at i * ls and
+// the table row of block j is j -- no 64-bit divisions in the hot loop.
+template <int D, bool ONE>
 __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
   const int64_t nblk = (N + B - 1) / B;
@@ -108,8 +110,9 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
     for (int a = 0; a < 4; ++a) {
       const int64_t i = B * j + a;
       const bool ok = a < B && i < N;
-      w[a] = ok ? __ldg(tabs + a * tab_stride + (i / tq) * D + k) : 0ull;
-      off[a] = ok ? elem_off(i, n, ks, ls) : -1;
+      const int64_t row = ONE ? j : i / tq;
+      w[a] = ok ? __ldg(tabs + a * tab_stride + row * D + k) : 0ull;
+      off[a] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
     for (int c = 0; c < ncomp; ++c) {
       u64 v = 0;
@@ -122,7 +125,7 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
 }
 
 // out_c[j] = sum_{b<B} Y_c[B j + b] * g_b  (public constants g, B x D)
-template <int D>
+template <int D, bool ONE>
 __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                                     const u64* __restrict__ g, Outs8 out, u64 mask) {
   const int64_t nblk = (N + B - 1) / B;
@@ -137,7 +140,7 @@ __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int6
       const int64_t i = B * j + b;
       const bool ok = b < B && i < N;
       gv[b] = ok ? __ldg(g + b * D + k) : 0ull;
-      off[b] = ok ? elem_off(i, n, ks, ls) : -1;
+      off[b] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
     for (int c = 0; c < ncomp; ++c) {
       u64 v = 0;
@@ -370,8 +373,13 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
   }
   const int64_t total = (N + B - 1) / B * d;
   cudaStream_t s = as_stream(stream);
-  R3_DISPATCH_D2(d, (line_b_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
-                        B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  if (n == 1 && tq == B) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  } else {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, false><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  }
   return check_launch("r3_vfy_line_b");
 }
 
@@ -391,8 +399,13 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   }
   const int64_t total = (N + B - 1) / B * d;
   cudaStream_t s = as_stream(stream);
-  R3_DISPATCH_D2(d, (line_b_const_kernel<D><<<grid_for(total, 256), 256, 0, s>>>(
-                        B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+  if (n == 1) {
+    R3_DISPATCH_D2(d, (line_b_const_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+  } else {
+    R3_DISPATCH_D2(d, (line_b_const_kernel<D, false><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+  }
   return check_launch("r3_vfy_line_b_const");
 }
 

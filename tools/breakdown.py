@@ -24,12 +24,20 @@ def main():
     ap.add_argument("--log2n", type=int, default=22)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--engine", default="coop")
+    ap.add_argument("--prog", default="mulv", choices=["mulv", "relu", "relu-exec"])
     a = ap.parse_args()
     N = 1 << a.log2n
     R = verify.pick_r(N, 64, a.d)
-    mulv, _ = bench.make_programs(N, a.d, R)
+    if a.prog == "mulv":
+        mulv, _ = bench.make_programs(N, a.d, R)
+        args = ()
+    else:
+        import numpy as np
+        mulv = bench.make_relu_program(N, a.d)
+        xv = np.trunc(np.random.default_rng(1).normal(0, 4, N) * 2 ** 16).astype(np.int64)
+        args = (torch.from_numpy(xv).pin_memory(), a.prog == "relu")
     for i in range(2):
-        Session(seed=i, engine=a.engine).run(mulv)
+        Session(seed=i, engine=a.engine).run(mulv, *args)
     torch.cuda.synchronize()
     ev = []
 
@@ -47,7 +55,7 @@ def main():
     w0 = time.perf_counter()
     t0.record()
     _lib.CALL_HOOK = hook
-    Session(seed=99, engine=a.engine).run(mulv)
+    Session(seed=99, engine=a.engine).run(mulv, *args)
     _lib.CALL_HOOK = None
     t1.record()
     torch.cuda.synchronize()
@@ -59,7 +67,7 @@ def main():
         tot[name] += s.elapsed_time(e)
         cnt[name] += 1
     busy = sum(tot.values())
-    print(f"N=2^{a.log2n} d={a.d} R={R}: step {step:.1f} ms (wall {wall*1e3:.1f} ms), "
+    print(f"{a.prog} N=2^{a.log2n} d={a.d} R={R}: step {step:.1f} ms (wall {wall*1e3:.1f} ms), "
           f"library GPU time {busy:.1f} ms in {len(ev)} calls")
     for k, v in tot.most_common():
         print(f"  {k:24s} {v:9.2f} ms {100 * v / step:5.1f}%  calls={cnt[k]}")
