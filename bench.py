@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--matmul-n", type=int, default=4096)
+    ap.add_argument("--mlp-batch", type=int, default=4096)
+    ap.add_argument("--mlp-verified-batch", type=int, default=64)
+    ap.add_argument("--lenet-batch", type=int, default=1024)
+    ap.add_argument("--lenet-verified-batch", type=int, default=8)
     return ap.parse_args()
 
 
@@ -329,6 +333,71 @@ def matmul_c3(n: int, steps: int) -> dict:
             "scope": "PRE (masks, trunc_prepare 2^24 lanes, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online)"}
 
 
+def _plain_forward(model, imgs):
+    """float64 forward pass of the model (conv via the same patch maps)."""
+    import numpy as np
+    from paper_2411_09287_b200 import ppml
+    outs = []
+    for img in imgs:
+        cur, shape, wi = img.reshape(-1), model.input_shape, 0
+        for lay, out_shape in zip(model.layers, model.shapes()):
+            if lay.kind == "fc":
+                W = model.weights[wi].reshape(lay.params["dout"], lay.params["din"])
+                wi += 1
+                cur = W @ cur
+            elif lay.kind == "conv":
+                idx = ppml.conv_indices(shape, lay.params)
+                W = model.weights[wi].reshape(lay.params["out"], -1)
+                wi += 1
+                cur = (W @ np.concatenate([cur, [0.0]])[idx]).reshape(-1)
+            elif lay.kind == "relu":
+                cur = np.maximum(cur, 0)
+            else:
+                idx = ppml._pool_indices(shape, lay.params["win"])
+                cur = cur[idx].max(axis=0)
+            shape = out_shape
+        outs.append(cur)
+    return np.array(outs)
+
+
+def ppml_rates(name: str, batch: int, verified_batch: int) -> dict:
+    """BASELINE configs 4 / 5: batched private inference through
+    ppml.infer_batch (model owner P1, data owner P2, k = 16, d = 16, R auto),
+    synthetic MNIST-shaped images normal(0, 1) from default_rng(0) and
+    random-init weights.  Exec = PRE + ONLINE (no
+    verification), verified = with verify_session before the scores open."""
+    import numpy as np
+    import torch
+    from paper_2411_09287_b200 import ppml
+    from paper_2411_09287_b200.runtime import Session
+    model = (ppml.secureml_model if name == "mlp" else ppml.lenet28_model)(np.random.default_rng(0))
+    out = {"model": "SecureML MLP 784-128-128-10" if name == "mlp" else "LeNet-5 (28x28, pad 2)",
+           "unit": "images/s", "k": 16, "d": 16, "R": "auto"}
+    for check, B in ((False, batch), (True, verified_batch)):
+        if not B:
+            continue
+        imgs = np.random.default_rng(0).normal(0, 1, (B, int(np.prod(model.input_shape))))
+        cfg = ppml.InferConfig(check=check)
+        prog = lambda party: ppml.infer_batch(party, model, imgs, cfg)
+        Session(seed=1).run(prog)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = Session(seed=2).run(prog)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        scores = ppml.decode(res[0][0], 16).reshape(B, -1)
+        err = float(np.abs(scores - _plain_forward(model, imgs)).max())
+        assert err < 0.05, f"{name} scores off by {err}"
+        if check:
+            assert all(res[0][1].values()), "verification rejected"
+        key = "verified" if check else "exec"
+        out[key] = B / dt
+        out[key + "_batch"] = B
+        out[key + "_ms"] = dt * 1e3
+        out[key + "_max_abs_err_vs_float"] = err
+    return out
+
+
 class KernelTimer:
     """CUDA events around every launch of one library entry point, on the
     launching (current) stream."""
@@ -542,6 +611,10 @@ def run_b200(args):
             line["matmul"] = matmul_c3(args.matmul_n, 3)
         if args.relu_log2n:
             line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
+        if args.mlp_batch:
+            line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
+        if args.lenet_batch:
+            line["lenet"] = ppml_rates("lenet", args.lenet_batch, args.lenet_verified_batch)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
     print(json.dumps(line), flush=True)

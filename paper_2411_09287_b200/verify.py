@@ -39,7 +39,7 @@ from ._lib import call, empty, ptr, stream, to_host
 from .gates import dot_finish, dot_prepare, prepare_gate
 from .rings import ConfigError, modulus_for_degree
 from .sharing import AShare, MVal, Ring, rec, shc_random
-from .transport import AUX, OFFLINE, PAYLOAD, Phase
+from .transport import AUX, OFFLINE, PAYLOAD, HarnessError, Phase
 
 CHALLENGE_KINDS = ("mul.arith", "dot.arith", "mul.bool")
 DEFAULT_R_MAX = 24
@@ -732,8 +732,14 @@ def _require_ctx(party, key: str) -> Challenges:
     return party.verify_ctx[key]
 
 
+def _require_kept_logs(party) -> None:
+    if any(log.discard for log in party.logs.values()):
+        raise HarnessError("gate logs were discarded (Party.discard_logs); nothing to verify")
+
+
 def batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None = None) -> bool:
     """Verify every logged multiplication of the given base ring."""
+    _require_kept_logs(party)
     kind = "bool" if base_ell == 1 else "arith"
     log = party.logs[kind]
     if not log.muls:
@@ -753,6 +759,7 @@ def batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None
 
 def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     """Verify every logged inner-product gate of the given base ring."""
+    _require_kept_logs(party)
     kind = "bool" if base_ell == 1 else "arith"
     log = party.logs[kind]
     if not log.dots:
@@ -784,6 +791,7 @@ def verify_session(party, d: int, R: int | str = "auto", profile: str = "lan") -
     if party.phase is not Phase.POST:
         raise ConfigError("verification runs in the postprocessing phase")
     party.freeze_logs()
+    _require_kept_logs(party)
     results: dict[str, bool] = {}
     for kind, base_ell in (("arith", party.ell), ("bool", 1)):
         log = party.logs[kind]

@@ -22,6 +22,7 @@ def build(pkg_name: str) -> SimpleNamespace:
     sharing = importlib.import_module(f"{pkg_name}.sharing")
     transport = importlib.import_module(f"{pkg_name}.transport")
     nonlinear = importlib.import_module(f"{pkg_name}.nonlinear")
+    ppml = importlib.import_module(f"{pkg_name}.ppml")
     Ring, MVal = sharing.Ring, sharing.MVal
     Phase = transport.Phase
     shc_random, shc_input, rec = sharing.shc_random, sharing.shc_input, sharing.rec
@@ -253,9 +254,159 @@ def build(pkg_name: str) -> SimpleNamespace:
         party.freeze_logs()
         return {"z": z, "open": rec(party, z, "z")}
 
+
+    def _model(name):
+        if name == "snn":
+            return ppml.snn_model(np.random.default_rng(0))
+        if name == "mlp_tiny":
+            m = ppml.ModelSpec((1, 4, 4), [ppml.Layer("fc", dict(din=16, dout=8)), ppml.Layer("relu"),
+                                           ppml.Layer("fc", dict(din=8, dout=4)), ppml.Layer("relu"),
+                                           ppml.Layer("fc", dict(din=4, dout=3))])
+            rng = np.random.default_rng(1)
+            m.weights = [rng.normal(0, 0.3, 128), rng.normal(0, 0.4, 32), rng.normal(0, 0.5, 12)]
+            return m
+        if name == "conv_tiny":
+            m = ppml.ModelSpec((1, 6, 6), [
+                ppml.Layer("conv", dict(out=2, kh=3, kw=3, sh=1, sw=1, pad=1)), ppml.Layer("relu"),
+                ppml.Layer("maxpool", dict(win=2)), ppml.Layer("fc", dict(din=18, dout=3))])
+            rng = np.random.default_rng(2)
+            m.weights = [rng.normal(0, 0.3, 18), rng.normal(0, 0.3, 54)]
+            return m
+        raise ValueError(name)
+
+    def _images(model, batch, seed):
+        n_in = int(np.prod(model.input_shape))
+        return np.random.default_rng(seed).normal(0, 1, (batch, n_in))
+
+    def infer1(party, model_name, img_seed, d=16, check=True):
+        """ppml.infer on one image (ppml.py:291-409), the reference's own API."""
+        model = _model(model_name)
+        img = _images(model, 1, img_seed)[0]
+        cfg = ppml.InferConfig(d=d, check=check)
+        scores, verdicts = ppml.infer(party, model, img, cfg)
+        return {"scores": scores, "verdicts": verdicts}
+
+    def _batched_idx(lay, shape, B):
+        """(K, lanes) gather indices of a batched layer (image-major lanes;
+        conv lanes (b, oc, p) as the reference orders one image's)."""
+        n_img = int(np.prod(shape))
+        if lay.kind == "fc":
+            din, dout = lay.params["din"], lay.params["dout"]
+            b, o = np.meshgrid(np.arange(B), np.arange(dout), indexing="ij")
+            i = np.arange(din)[:, None]
+            return b.reshape(1, -1) * din + i, o.reshape(1, -1) * din + i
+        idx = ppml.conv_indices(shape, lay.params)
+        K, P = idx.shape
+        out = lay.params["out"]
+        b, oc, p = np.meshgrid(np.arange(B), np.arange(out), np.arange(P), indexing="ij")
+        b, oc, p = b.reshape(-1), oc.reshape(-1), p.reshape(-1)
+        raw = idx[:, p]
+        xi = np.where(raw == n_img, B * n_img, b[None, :] * n_img + raw)
+        wi = oc[None, :] * K + np.arange(K)[:, None]
+        return xi, wi
+
+    def _gmask(m, idx):
+        return m._map(lambda a: np.concatenate([np.asarray(a), np.zeros(1, np.uint64)])[idx])
+
+    def infer_batch_gathered(party, model_name, img_seed, batch, d=16, check=True):
+        """BASELINE configs 4-5 in the reference's own primitives: ppml.infer
+        (ppml.py:291-409) with every per-image lane count scaled by the batch,
+        each linear layer one gathered Pi_dot (ppml.py:412-427)."""
+        model = _model(model_name)
+        imgs = _images(model, batch, img_seed)
+        cfg = ppml.InferConfig(d=d, check=check)
+        ring = Ring(party.ell)
+        shapes = model.shapes()
+        B = batch
+        party.enter_phase(Phase.PRE)
+        n_in = int(np.prod(model.input_shape))
+        img_mask = shc_input_mask(party, cfg.data_owner, B * n_in, ring)
+        w_masks = [shc_input_mask(party, cfg.model_owner, model.weight_count(l), ring)
+                   if model.weight_count(l) else None for l in model.layers]
+        plans, cur_mask, cur_shape = [], img_mask, model.input_shape
+        for li, lay in enumerate(model.layers):
+            lanes = B * int(np.prod(shapes[li]))
+            if lay.kind in ("conv", "fc"):
+                tr = gates.trunc_prepare(party, lanes, cfg.k, ring)
+                xi, wi = _batched_idx(lay, cur_shape, B)
+                gate = None
+                if cur_mask is not None:
+                    gate = gates.dot_prepare(party, _gmask(cur_mask, xi), _gmask(w_masks[li], wi), lanes,
+                                             out_mask=tr.rx_mask)
+                plans.append(("dot", tr, gate, (xi, wi)))
+                cur_mask = tr.rz_mask
+            elif lay.kind == "relu":
+                mat = nonlinear.relu_prepare(party, cur_mask, lanes, ring) if cur_mask is not None else None
+                plans.append(("relu", mat, None, None))
+                cur_mask = None
+            else:
+                plans.append(("maxpool", None, None, None))
+                cur_mask = None
+            cur_shape = shapes[li]
+        if check:
+            verify.prepare_verification(party, d=d)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        vals = ppml.encode(imgs.reshape(-1), cfg.k, ring.ell) if party.role == cfg.data_owner else None
+        cur = shc_input_online(party, cfg.data_owner, vals, img_mask, B * n_in, ring, "image")
+        weights, nw = [], 0
+        for li, lay in enumerate(model.layers):
+            n = model.weight_count(lay)
+            if not n:
+                weights.append(None)
+                continue
+            wv = ppml.encode(model.weights[nw], cfg.k, ring.ell) if party.role == cfg.model_owner else None
+            nw += 1
+            weights.append(shc_input_online(party, cfg.model_owner, wv, w_masks[li], n, ring, f"w{li}"))
+        party.round_barrier()
+        cur_shape = model.input_shape
+        for li, lay in enumerate(model.layers):
+            lanes = B * int(np.prod(shapes[li]))
+            kind, mat, gate, ix = plans[li]
+            if kind == "dot":
+                xi, wi = ix
+                gv = lambda v, idx: MVal(_gmask(v.mask, idx), None if v.m is None else
+                                         np.concatenate([np.asarray(v.m), np.zeros(1, np.uint64)])[idx])
+                xs, ws = gv(cur, xi), gv(weights[li], wi)
+                if gate is None:
+                    gate = gates.dot_prepare(party, xs.mask, ws.mask, lanes, out_mask=mat.rx_mask)
+                prod = gates.dot_finish(party, gate, xs, ws)
+                party.round_barrier()
+                cur = gates.trunc_online(party, prod, mat)
+            elif kind == "relu":
+                if mat is None:
+                    mat = nonlinear.relu_prepare(party, cur.mask, lanes, ring)
+                cur = nonlinear.relu_online(party, cur, mat)
+                party.round_barrier()
+            else:
+                base = ppml._pool_indices(cur_shape, lay.params["win"])
+                n_img = int(np.prod(cur_shape))
+                idx = (np.arange(B)[None, :, None] * n_img + base[:, None, :]).reshape(base.shape[0], -1)
+                cur = nonlinear.maxpool_online(party, ppml._gather(cur, idx), ring)
+                party.round_barrier()
+            cur_shape = shapes[li]
+        party.enter_phase(Phase.POST)
+        verdicts = {}
+        if check:
+            verdicts = verify.verify_session(party, d=d, R="auto")
+            if not all(verdicts.values()):
+                party.abort(f"verification failed before output reveal: {verdicts}")
+        else:
+            party.freeze_logs()
+        return {"scores": rec(party, cur, "scores"), "verdicts": verdicts}
+
+    def infer_batch(party, model_name, img_seed, batch, d=16, check=True):
+        """paper_2411_09287_b200 only: ppml.infer_batch (GEMM-form layers);
+        must reproduce infer_batch_gathered's golden run exactly."""
+        model = _model(model_name)
+        imgs = _images(model, batch, img_seed)
+        scores, verdicts = ppml.infer_batch(party, model, imgs, ppml.InferConfig(d=d, check=check))
+        return {"scores": scores, "verdicts": verdicts}
+
     return SimpleNamespace(matmul_gemm=matmul_gemm, mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
                            trunc=trunc, trunc_verify=trunc_verify, dotv=dotv, relu=relu,
-                           a2b_roundtrip=a2b_roundtrip, matmul=matmul)
+                           a2b_roundtrip=a2b_roundtrip, matmul=matmul, infer1=infer1,
+                           infer_batch_gathered=infer_batch_gathered, infer_batch=infer_batch)
 
 
 # ---------------------------------------------------------------------------
@@ -302,6 +453,12 @@ CASES = [
     ("a2b_roundtrip_ell8", "a2b_roundtrip", (list(range(16)), 8), {}, {"seed": 0, "ell": 8}),
     ("matmul_8x8x8", "matmul", _mat_inputs(8, 8, 8, 3), {}, {"seed": 3}),
     ("matmul_12x16x10", "matmul", _mat_inputs(12, 16, 10, 4), {}, {"seed": 4}),
+    ("infer1_mlp_tiny", "infer1", ("mlp_tiny", 5), {}, {"seed": 5}),
+    ("infer1_conv_tiny", "infer1", ("conv_tiny", 6), {}, {"seed": 6}),
+    ("infer1_snn_nocheck", "infer1", ("snn", 7), {"check": False}, {"seed": 7}),
+    ("infer1_snn", "infer1", ("snn", 10), {}, {"seed": 10}),
+    ("infer_batch_mlp_tiny_b3", "infer_batch_gathered", ("mlp_tiny", 8, 3), {}, {"seed": 8}),
+    ("infer_batch_conv_tiny_b2", "infer_batch_gathered", ("conv_tiny", 9, 2), {}, {"seed": 9}),
 ]
 
 # Tamper cases: (name, program, args, injections[(site, who, delta, gate, lane)])

@@ -21,6 +21,10 @@ pytestmark = pytest.mark.gpu
 
 PKG = "paper_2411_09287_b200"
 
+# golden program (reference primitives, gathered operands) -> the B200 API
+# that must reproduce it (GEMM-form linear layers)
+GEMM_FORM = {"infer_batch_gathered": "infer_batch"}
+
 
 def _flatten(role, res, out, prefix, MVal, host):
     if isinstance(res, dict):
@@ -59,6 +63,8 @@ def run_case(name, engine="coop", prog_override=None):
         kwargs = {}
     # inputs come from the golden file where they were arrays
     args = tuple(arrays[f"arg{i}"] if f"arg{i}" in arrays else a for i, a in enumerate(args))
+    # reference-primitive programs whose B200 counterpart is a different API
+    prog_override = prog_override or GEMM_FORM.get(prog_name)
     prog = getattr(programs.build(PKG), prog_override or prog_name)
     adv = None
     if inj is not None:
