@@ -83,6 +83,22 @@ int r3_prf_ctr(const uint32_t rk[44], uint64_t first_u64, int64_t n,
 int r3_prf_bits_packed(const uint32_t rk[44], uint64_t first_u64, int nbits,
                        int64_t lanes, uint64_t* out, void* stream);
 
+/* Fused a2b ripple MSB over Z_2 for the three simulated parties (replaces
+ * the ell-2 sequential AND gates of nonlinear.py:133-160 with msb_only, each
+ * a gates.py:52-117 Pi_mul).  rk01/rk02: round keys of the ("01","sha") and
+ * ("02","sha") streams at u64 offsets o01/o02 (gate g draws out_s1, gamma_s1
+ * from 01 at o01 + 2gL, o01 + (2g+1)L and out_s2 from 02 at o02 + gL).
+ * eda[7]: (ell, lanes) edaBit rows (P0 s1, s2, total; P1 s1, m; P2 s2, m)
+ * with row_stride words between rows; delta: the opened Delta per lane.
+ * msb[7]: output MSB shares (same component order); msgs[3]: (ell-2, lanes)
+ * payloads P0->P2 gamma share, P1 leg, P2 leg; logy/logz (optional, both or
+ * neither): per-gate carry input and product output components. */
+int r3_ripple_msb(const uint32_t rk01[44], const uint32_t rk02[44], uint64_t o01,
+                  uint64_t o02, const uint64_t* delta, const uint64_t* const* eda,
+                  int64_t row_stride, int ell, int64_t lanes, uint64_t* const* msb,
+                  uint64_t* const* msgs, uint64_t* const* logy,
+                  uint64_t* const* logz, void* stream);
+
 /* ---- elementwise (grvec.py:18-40; sharing.py:95-230 linear ops) ----------
  * out[idx] = op(a[idx . a_strides], b[idx . b_strides]) over an ndim<=4 index
  * space `shape` (out contiguous).  Stride 0 broadcasts.  b == NULL uses the

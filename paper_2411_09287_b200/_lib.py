@@ -39,6 +39,8 @@ _SIGS = {
     "r3_aes128_expand": [C.c_char_p, C.POINTER(C.c_uint32)],
     "r3_prf_ctr": [C.POINTER(C.c_uint32), u64, i64, u64, C.c_int, u64p, C.c_void_p],
     "r3_prf_bits_packed": [C.POINTER(C.c_uint32), u64, C.c_int, i64, u64p, C.c_void_p],
+    "r3_ripple_msb": [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u64, u64, u64p, C.c_void_p, i64,
+                      C.c_int, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
               C.POINTER(i64), u64, u64, C.c_void_p],
     "r3_ew_flat": [C.c_int, i64, u64p, u64p, u64p, u64, u64, C.c_void_p],
