@@ -192,6 +192,12 @@ int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0,
                      const uint64_t* p1, int64_t rs1, int64_t nv1,
                      const uint64_t* M0, const uint64_t* M1, uint64_t* out,
                      int64_t rows, uint64_t mask, void* stream);
+/* d = 16 form of r3_gr_matmul2_tc (rows of 16 coefficients, M0/M1 16 x 16):
+ * both operands K-concatenate into one 32-byte kind::i8 K-step. */
+int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0,
+                     const uint64_t* p1, int64_t rs1, int64_t nv1,
+                     const uint64_t* M0, const uint64_t* M1, uint64_t* out,
+                     int64_t rows, uint64_t mask, void* stream);
 /* acc[0..2d-2] += unreduced polynomial sum_i F[i] (x) G[i] (the inner
  * products of reduce_dimension / check_inner_product, verify.py:154-161,
  * gates.dot_finish.fold over GR). acc must be zeroed by the caller before the

@@ -182,6 +182,7 @@ level_fold_tc_kernel(const __grid_constant__ LfArgs args, u64* __restrict__ acc1
           for (int q = 0; q < 16; ++q) v[q] += T.c1 * w[q];
         }
       }
+      fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
       mbar_arrive(&raw_empty[st]);
       if (!ok) {
 #pragma unroll

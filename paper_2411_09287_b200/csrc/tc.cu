@@ -145,6 +145,7 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
         x[4 * q + 2] = v.z;
         x[4 * q + 3] = v.w;
       }
+      fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
       mbar_arrive(&raw_empty[st]);
       if (u >= LIMB_STAGES) mbar_wait(&limb_empty[ls], uint32_t((u / LIMB_STAGES - 1) & 1));
       uint8_t* dst = sLimb + ls * LIMB_BYTES + core_off(r, c * 16, TC_ROWS / 8);
@@ -237,6 +238,190 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
 }
 
 // ---------------------------------------------------------------------------
+// d = 16: out = P0 . M0 (+ P1 . M1) with K = 16 per operand, so the two
+// operands K-concatenate into ONE kind::i8 K-step of 32: a unit is a tile of
+// 128 rows, raw = two TMA boxes (P0's and P1's 16 coefficients of the rows),
+// B = [M0; M1] limb planes N-concatenated (row n' = 16 j + n, K = 32 bytes).
+// 8 MMAs of N = 16 (8 - i) per tile into 8 x 16 = 128 TMEM columns.
+// ---------------------------------------------------------------------------
+constexpr int T16_D = 16;
+constexpr int T16_RAW = TC_ROWS * 2 * T16_D * 8;          // 32 KB (two 16 KB boxes)
+constexpr int T16_LIMB_PLANE = TC_ROWS * 2 * T16_D;       // 4 KB (128 rows x 32 B)
+constexpr int T16_LIMB = 8 * T16_LIMB_PLANE;              // 32 KB
+constexpr int T16_BROWS = 8 * T16_D;                      // 128
+constexpr int T16_B = T16_BROWS * 2 * T16_D;              // 4 KB
+constexpr int T16_RAW_STAGES = 3, T16_LIMB_STAGES = 2;
+constexpr int T16_OFF_LIMB = T16_RAW_STAGES * T16_RAW;
+constexpr int T16_OFF_B = T16_OFF_LIMB + T16_LIMB_STAGES * T16_LIMB;
+constexpr int T16_OFF_BAR = T16_OFF_B + T16_B;
+constexpr int T16_SMEM = T16_OFF_BAR + 128 + 1024;
+constexpr int T16_EPI = 4, T16_CONV = 8;
+constexpr int T16_THREADS = (T16_EPI + T16_CONV + 2) * 32;
+
+__global__ void __launch_bounds__(T16_THREADS, 1)
+gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                       int nops, const u64* __restrict__ M0, const u64* __restrict__ M1, u64* __restrict__ out,
+                       int64_t rows, u64 mask) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sRaw = smem;
+  uint8_t* sLimb = smem + T16_OFF_LIMB;
+  uint8_t* sB = smem + T16_OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T16_OFF_BAR);
+  uint64_t* raw_full = bars;         // [3]
+  uint64_t* raw_empty = bars + 3;    // [3]
+  uint64_t* limb_full = bars + 6;    // [2]
+  uint64_t* limb_empty = bars + 8;   // [2]
+  uint64_t* tfull = bars + 10;
+  uint64_t* tempty = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // B: row n' = 16 j + n, k < 16 from M0, k >= 16 from M1 (zero if absent)
+  for (int e = tid; e < 2 * T16_D * T16_D; e += T16_THREADS) {
+    const int k = e / T16_D, n = e % T16_D;
+    const u64 v = k < T16_D ? M0[k * T16_D + n] : (nops > 1 ? M1[(k - T16_D) * T16_D + n] : 0ull);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sB[core_off(j * T16_D + n, k, T16_BROWS / 8)] = uint8_t(v >> (8 * j));
+  }
+  if (tid == 0) {
+    for (int i = 0; i < T16_RAW_STAGES; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], T16_CONV * 32);
+    }
+    for (int i = 0; i < T16_LIMB_STAGES; ++i) {
+      mbar_init(&limb_full[i], T16_CONV * 32);
+      mbar_init(&limb_empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, T16_EPI * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t nunits = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  if (warp == T16_EPI + T16_CONV) {
+    // ------------------------------ TMA producer
+    if (lane == 0) {
+      for (int64_t u = 0; u < nunits; ++u) {
+        const int st = int(u % T16_RAW_STAGES);
+        if (u >= T16_RAW_STAGES) mbar_wait(&raw_empty[st], uint32_t((u / T16_RAW_STAGES - 1) & 1));
+        const int y = int((blockIdx.x + u * gridDim.x) * TC_ROWS);
+        uint8_t* dst = sRaw + st * T16_RAW;
+        mbar_expect_tx(&raw_full[st], uint32_t(nops * (T16_RAW / 2)));
+        tma_load_2d(dst, &tm0, 0, y, &raw_full[st]);
+        if (nops > 1) tma_load_2d(dst + T16_RAW / 2, &tm1, 0, y, &raw_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= T16_EPI && warp < T16_EPI + T16_CONV) {
+    // ------------------------------ converters: thread = (row r, operand box c)
+    const int ct = tid - T16_EPI * 32;
+    const int r = ct & (TC_ROWS - 1), c = ct >> 7;
+    const int sw = r & 7;
+    for (int64_t u = 0; u < nunits; ++u) {
+      const int st = int(u % T16_RAW_STAGES), ls = int(u % T16_LIMB_STAGES);
+      mbar_wait(&raw_full[st], uint32_t((u / T16_RAW_STAGES) & 1));
+      uint32_t x[32];
+      if (c < nops) {
+        const uint8_t* src = sRaw + st * T16_RAW + c * (T16_RAW / 2) + r * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 v = *reinterpret_cast<const uint4*>(src + ((q ^ sw) << 4));
+          x[4 * q + 0] = v.x;
+          x[4 * q + 1] = v.y;
+          x[4 * q + 2] = v.z;
+          x[4 * q + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) x[q] = 0;
+      }
+      fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
+      mbar_arrive(&raw_empty[st]);
+      if (u >= T16_LIMB_STAGES) mbar_wait(&limb_empty[ls], uint32_t((u / T16_LIMB_STAGES - 1) & 1));
+      uint8_t* dst = sLimb + ls * T16_LIMB + core_off(r, c * 16, TC_ROWS / 8);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int hiw = i >> 2, bi = i & 3;
+        uint4 pk;
+        pk.x = gather_byte(x[0 + hiw], x[2 + hiw], x[4 + hiw], x[6 + hiw], bi);
+        pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
+        pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
+        pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
+        *reinterpret_cast<uint4*>(dst + i * T16_LIMB_PLANE) = pk;
+      }
+      fence_async_smem();
+      mbar_arrive(&limb_full[ls]);
+    }
+  } else if (warp == T16_EPI + T16_CONV + 1) {
+    // ------------------------------ MMA issuer
+    for (int64_t u = 0; u < nunits; ++u) {
+      const int ls = int(u % T16_LIMB_STAGES);
+      if (u > 0) mbar_wait(tempty, uint32_t((u - 1) & 1));
+      mbar_wait(&limb_full[ls], uint32_t((u / T16_LIMB_STAGES) & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sLimb + ls * T16_LIMB);
+        const uint32_t b0 = smem_u32(sB);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint64_t ad = umma_desc(a0 + i * T16_LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
+          const uint64_t bd = umma_desc(b0, (T16_BROWS / 8) * 128, 128);
+          mma_u8(tmem + uint32_t(T16_D * i), ad, bd, idesc_u8(TC_ROWS, T16_D * (8 - i)), i ? 1u : 0u);
+        }
+        mma_commit(&limb_empty[ls]);
+        mma_commit(tfull);
+      }
+      __syncwarp();
+    }
+  } else if (warp < T16_EPI) {
+    // ------------------------------ epilogue: warp e = TMEM lane quadrant e
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    for (int64_t u = 0; u < nunits; ++u) {
+      mbar_wait(tfull, uint32_t(u & 1));
+      tc_fence_after();
+      const int64_t row = (blockIdx.x + u * gridDim.x) * TC_ROWS + warp * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < T16_D; c0 += 8) {
+        uint32_t v[8][8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * T16_D + c0), v[s]);
+        tmem_wait_ld();
+        u64 acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          u64 a = 0;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) a += u64(v[s][q]) << (8 * s);
+          acc[q] = a & mask;
+        }
+        if (row < rows) {
+          ulonglong2* o = reinterpret_cast<ulonglong2*>(out + row * T16_D + c0);
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) o[q >> 1] = make_ulonglong2(acc[q], acc[q + 1]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
 // host: tensor maps (driver entry point fetched through the runtime, so the
 // library needs no -lcuda)
 // ---------------------------------------------------------------------------
@@ -319,4 +504,56 @@ extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, co
   gr_matmul2_tc_kernel<<<grid, WS_THREADS, WS_SMEM, as_stream(stream)>>>(
       tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc");
+}
+
+extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, const uint64_t* p1, int64_t rs1,
+                                  int64_t nv1, const uint64_t* M0, const uint64_t* M1, uint64_t* out,
+                                  int64_t rows, uint64_t mask, void* stream) {
+  if (!p0 || !M0 || rows < 0 || ((rs0 | rs1) & 1) || ((uintptr_t(p0) | uintptr_t(p1)) & 15) || (p1 && !M1)) {
+    set_error("r3_gr_matmul2_tc16: bad arguments (need 16-byte aligned rows)");
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  if (rows > (int64_t(1) << 31) - TC_ROWS) {
+    set_error("r3_gr_matmul2_tc16: rows %lld exceed the TMA coordinate range", (long long)rows);
+    return R3_ERR_ARG;
+  }
+  const uint64_t* P[2] = {p0, p1};
+  const uint64_t* Ms[2] = {M0, M1};
+  int64_t rs[2] = {rs0, rs1}, nv[2] = {nv0 < rows ? nv0 : rows, nv1 < rows ? nv1 : rows};
+  int nops = 0;
+  const uint64_t* Pk[2];
+  const uint64_t* Mk[2];
+  int64_t rsk[2], nvk[2];
+  for (int q = 0; q < 2; ++q) {
+    if (P[q] && nv[q] > 0) {
+      Pk[nops] = P[q];
+      Mk[nops] = Ms[q];
+      rsk[nops] = rs[q] > 0 ? rs[q] : T16_D;
+      nvk[nops] = nv[q];
+      ++nops;
+    }
+  }
+  if (nops == 0) {
+    cudaMemsetAsync(out, 0, size_t(rows) * T16_D * 8, as_stream(stream));
+    return check_launch("r3_gr_matmul2_tc16(zero)");
+  }
+  CUtensorMap tm[2];
+  for (int q = 0; q < nops; ++q) {
+    if (!make_rows_tmap(&tm[q], Pk[q], nvk[q], rsk[q], TC_ROWS, T16_D)) {
+      set_error("r3_gr_matmul2_tc16: cuTensorMapEncodeTiled failed");
+      return R3_ERR_CUDA;
+    }
+  }
+  if (nops == 1) tm[1] = tm[0];
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gr_matmul2_tc16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T16_SMEM);
+    attr = true;
+  }
+  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  gr_matmul2_tc16_kernel<<<grid, T16_THREADS, T16_SMEM, as_stream(stream)>>>(
+      tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
+  return check_launch("r3_gr_matmul2_tc16");
 }

@@ -430,9 +430,9 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
                P1: torch.Tensor | None = None, M1: torch.Tensor | None = None,
                nvalid=(None, None), out: torch.Tensor | None = None) -> torch.Tensor:
     """out[r] = P0[r] . M0 (+ P1[r] . M1): rows of GR elements times fixed
-    elements given by their multiplication matrices.  d = 64 runs on the
-    tensor cores (r3_gr_matmul2_tc, int8 byte limbs); other degrees on the
-    CUDA-core matrix kernel.  Rows at or beyond nvalid[q] of P_q are zero."""
+    elements given by their multiplication matrices.  d = 64 and d = 16 run
+    on the tensor cores (r3_gr_matmul2_tc / _tc16, int8 byte limbs); other
+    degrees on the CUDA-core matrix kernel.  Rows at or beyond nvalid[q] of P_q are zero."""
     d = M0.shape[0]
     n0 = rows if nvalid[0] is None else nvalid[0]
     n1 = rows if nvalid[1] is None else nvalid[1]
@@ -440,14 +440,15 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
         out = empty((rows, d))
     if rows == 0:
         return out
-    if d == 64 and _tc_ok(P0) and (P1 is None or _tc_ok(P1)):
-        rs0 = P0.stride(0) if P0.shape[0] > 1 else 64
+    if d in (16, 64) and _tc_ok(P0) and (P1 is None or _tc_ok(P1)):
+        fn = "r3_gr_matmul2_tc" if d == 64 else "r3_gr_matmul2_tc16"
+        rs0 = P0.stride(0) if P0.shape[0] > 1 else d
         if P1 is not None and P1.shape[0] > 0:
-            rs1 = P1.stride(0) if P1.shape[0] > 1 else 64
-            call("r3_gr_matmul2_tc", ptr(P0), rs0, n0, ptr(P1), rs1, n1, ptr(M0), ptr(M1),
+            rs1 = P1.stride(0) if P1.shape[0] > 1 else d
+            call(fn, ptr(P0), rs0, n0, ptr(P1), rs1, n1, ptr(M0), ptr(M1),
                  ptr(out), rows, ring_mask(width), stream())
         else:
-            call("r3_gr_matmul2_tc", ptr(P0), rs0, n0, None, 0, 0, ptr(M0), None,
+            call(fn, ptr(P0), rs0, n0, None, 0, 0, ptr(M0), None,
                  ptr(out), rows, ring_mask(width), stream())
         return out
     if P1 is None or P1.shape[0] == 0:

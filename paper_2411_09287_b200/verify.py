@@ -607,10 +607,10 @@ def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring):
 
 def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:
     """f0 + (f1 - f0) * zeta (verify.py:239) = f0 . M(1 - zeta) + f1 . M(zeta):
-    one K-concatenated contraction on the tensor cores for d = 64; the CUDA
-    core form rows . M(zeta) + f0 otherwise."""
+    one K-concatenated contraction on the tensor cores for d = 64 / 16; the
+    CUDA core form rows . M(zeta) + f0 otherwise."""
     M_one_m, M_z = Ms
-    if gr.d == 64:
+    if gr.d in (16, 64):
         return grvec.rows_times(H.ev, M_one_m, H.n0, gr.ell, P1=H.od, M1=M_z,
                                 nvalid=(H.n0, H.n1))
     return grvec.gr_matmul(_lin(H.d10()), M_z, H.n0, gr.d, gr.ell, C_add=_lin(H.f0()))
@@ -644,7 +644,7 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
     q = _quad(party, ze, gr)
     z_out = _recombine(party, z, h1, h2, q, gr)
-    Ms = (q.M_one_m if gr.d == 64 else None, q.M_ze)
+    Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
     out = lambda V, k: _line_eval(V[k], Ms, gr)
     mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
                                   p0_halves=v.mask.p0_halves),

@@ -58,40 +58,50 @@ def test_gr_mul_and_powers_match_oracle(cuda):
                                       ogr.powers(r, 300, 64, d))
 
 
-@pytest.mark.parametrize("rows", [1, 128, 129, 5000, 70001])
-def test_gr_matmul2_tc_line_eval(cuda, rows):
+@pytest.mark.parametrize("d,rows", [(64, 1), (64, 128), (64, 129), (64, 5000), (64, 70001),
+                                    (16, 1), (16, 255), (16, 4097), (16, 300001)])
+def test_gr_matmul2_tc_line_eval(cuda, d, rows):
     """Pipelined tensor-core contraction: f0 + (f1 - f0) z = f0.M(1-z) + f1.M(z),
-    with even/odd row views and the odd-length zero pad (verify.py:220-240)."""
+    with even/odd row views and the odd-length zero pad (verify.py:220-240);
+    d = 64 (r3_gr_matmul2_tc) and d = 16 (r3_gr_matmul2_tc16)."""
     from oracle import gr as ogr
     from paper_2411_09287_b200 import grvec, host, _lib
     from paper_2411_09287_b200.rings import modulus_for_degree
-    mod = modulus_for_degree(64)
-    rng = np.random.default_rng(rows + 7)
-    X = _rand(rng, (rows, 64))
-    z = _rand(rng, (1, 64))
+    mod = modulus_for_degree(d)
+    fn = "r3_gr_matmul2_tc" if d == 64 else "r3_gr_matmul2_tc16"
+    rng = np.random.default_rng(rows + 7 + d)
+    X = _rand(rng, (rows, d))
+    z = _rand(rng, (1, d))
     Xd = grvec.dev(X)
-    one = np.zeros((1, 64), dtype=np.uint64)
+    one = np.zeros((1, d), dtype=np.uint64)
     one[0, 0] = 1
     with np.errstate(over="ignore"):
         Ma = grvec.gr_mulmat(grvec.dev(one - z), mod)
     Mb = grvec.gr_mulmat(grvec.dev(z), mod)
     n0, n1 = (rows + 1) // 2, rows // 2
     ev, od = Xd[0::2], Xd[1::2]
-    out = grvec.empty((n0, 64))
-    _lib.call("r3_gr_matmul2_tc", ev.data_ptr(), ev.stride(0), n0, od.data_ptr() if n1 else Xd.data_ptr(),
-              od.stride(0) if n1 > 1 else 128, n1, Ma.data_ptr(), Mb.data_ptr(), out.data_ptr(), n0,
+    out = grvec.empty((n0, d))
+    _lib.call(fn, ev.data_ptr(), ev.stride(0), n0, od.data_ptr() if n1 else Xd.data_ptr(),
+              od.stride(0) if n1 > 1 else 2 * d, n1, Ma.data_ptr(), Mb.data_ptr(), out.data_ptr(), n0,
               (1 << 64) - 1, _lib.stream())
     f0 = X[0::2]
     f1 = np.zeros_like(f0)
     f1[:n1] = X[1::2]
     with np.errstate(over="ignore"):
-        want = ogr.mul(f1 - f0, z, 64, 64) + f0
+        want = ogr.mul(f1 - f0, z, 64, d) + f0
     np.testing.assert_array_equal(host(out), want)
     # single-operand form
-    out1 = grvec.empty((rows, 64))
-    _lib.call("r3_gr_matmul2_tc", Xd.data_ptr(), 64, rows, None, 0, 0, Mb.data_ptr(), None, out1.data_ptr(),
+    out1 = grvec.empty((rows, d))
+    _lib.call(fn, Xd.data_ptr(), d, rows, None, 0, 0, Mb.data_ptr(), None, out1.data_ptr(),
               rows, (1 << 64) - 1, _lib.stream())
-    np.testing.assert_array_equal(host(out1), ogr.mul(X, z, 64, 64))
+    np.testing.assert_array_equal(host(out1), ogr.mul(X, z, 64, d))
+    # width-1 ring (the boolean log's GR(2, d)): masked output
+    if d == 16:
+        Xb = X & np.uint64(1)
+        outb = grvec.empty((rows, d))
+        _lib.call(fn, grvec.dev(Xb).data_ptr(), d, rows, None, 0, 0, Mb.data_ptr(), None, outb.data_ptr(),
+                  rows, 1, _lib.stream())
+        np.testing.assert_array_equal(host(outb), ogr.mul(Xb, z, 64, d) & np.uint64(1))
 
 
 @pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
