@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
+    ap.add_argument("--relu-sweep-log2n", type=int, default=20)
     ap.add_argument("--matmul-n", type=int, default=4096)
     ap.add_argument("--mlp-batch", type=int, default=4096)
     ap.add_argument("--mlp-verified-batch", type=int, default=64)
@@ -195,7 +196,7 @@ def make_programs(N: int, d: int, R: int):
         if not verify.batch_verify_muls(party, 64, d=d, R=R):
             party.abort("verification failed")
         out = rec(party, z, "z")
-        return out.cpu() if party.role == 0 else None
+        return out if party.role == 0 else None
 
     return mulv, e2e
 
@@ -567,19 +568,33 @@ def run_b200(args):
         work_desc = "algorithmic work = rows*d^2 u64 MACs per launch"
     achieved = timer.work / kt if kt else 0.0
 
-    # end-to-end: host inputs in pinned memory, opened product back to host
-    rng = np.random.default_rng(rank)
-    xh = torch.from_numpy(rng.integers(0, 2**63, N, dtype=np.int64)).pin_memory()
-    yh = torch.from_numpy(rng.integers(0, 2**63, N, dtype=np.int64)).pin_memory()
-    Session(seed=7).run(e2e, xh, yh)
+    # end-to-end: host inputs in pinned memory (this rank's shard of the
+    # global batch), opened product shards gathered to rank 0 over NCCL and
+    # copied back to the host there
+    def shard_inputs(r):
+        g = np.random.default_rng(1000 + r)
+        return (g.integers(0, 2**63, N, dtype=np.int64), g.integers(0, 2**63, N, dtype=np.int64))
+    xv, yv = shard_inputs(rank)
+    xh = torch.from_numpy(xv).pin_memory()
+    yh = torch.from_numpy(yv).pin_memory()
+
+    def e2e_step(seed):
+        z = Session(seed=seed).run(e2e, xh, yh)[0]
+        full = pdist.gather_outputs(z)
+        return full.cpu() if rank == 0 else None
+
+    e2e_step(7)
     barrier()
     e0 = time.perf_counter()
     for i in range(args.e2e_steps):
-        out = Session(seed=70 + i).run(e2e, xh, yh)[0]
+        out = e2e_step(70 + i)
     barrier()
     e2e_s = pdist.max_over_ranks(time.perf_counter() - e0)
-    want = (xh.numpy().view(np.uint64) * yh.numpy().view(np.uint64))
-    assert np.array_equal(out.numpy().view(np.uint64), want), "e2e product mismatch"
+    if rank == 0:
+        got = out.numpy().view(np.uint64).reshape(world, N)
+        for r in range(world):
+            xs, ys = shard_inputs(r)
+            assert np.array_equal(got[r], xs.view(np.uint64) * ys.view(np.uint64)), "e2e product mismatch"
 
     if rank != 0:
         pdist.finalize()
@@ -593,7 +608,8 @@ def run_b200(args):
                                "(tests/test_acceptance.py:124-136), 3 parties per GPU",
                    "N_per_gpu": N, "ell": 64, "d": d, "R": R, "engine": args.engine,
                    "l2": f"inputs larger than L2 ({N * 8 * 12 / 2**20:.0f} MiB of shares per step)",
-                   "parallelism": f"weak dp{world}: independent sessions per rank"},
+                   "parallelism": f"weak dp{world}: element batch sharded, one 3-party session per rank "
+                                  f"shard, NCCL gather of opened outputs"},
         "roofline": {"bound": bound, "kernel": args.profile_kernel,
                      "achieved": achieved / scale, "peak": peak / scale, "unit": r_unit,
                      "frac": achieved / peak if peak else None, "traffic": None,
@@ -601,7 +617,9 @@ def run_b200(args):
                      "kernel_share_of_step": kt / secs if secs else None,
                      "peak_source": peak_src + "; " + work_desc},
         "e2e": {"value": N * world * args.e2e_steps / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": N * 8},
+                "h2d_bytes_per_step": 2 * N * 8 * world, "d2h_bytes_per_step": N * 8 * world,
+                "path": "per rank: pinned host shard -> Session.run (PRE, ONLINE, Pi_mulv, open) -> "
+                        "NCCL all-gather of the opened shards -> rank 0 host"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": wall,
@@ -611,6 +629,8 @@ def run_b200(args):
             line["matmul"] = matmul_c3(args.matmul_n, 3)
         if args.relu_log2n:
             line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
+        if args.relu_sweep_log2n:
+            line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 1)
         if args.mlp_batch:
             line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
         if args.lenet_batch:

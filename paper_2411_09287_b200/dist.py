@@ -1,9 +1,11 @@
 """Multi-GPU plumbing: one process per GPU, torch.distributed for control.
 
 A batch of multiplications with its batch verification is an independent
-protocol object, so ranks run independent sessions (weak scaling, no
-data-path collective).  Collectives are used only for the benchmark's
-barrier and its max-over-ranks timing (NCCL on GPUs, gloo in CPU tests).
+protocol object, so the element batch is sharded: each rank runs the three
+parties over its contiguous shard (weak scaling) and the only data-path
+collective is the final gather of the opened outputs to rank 0 (NCCL
+all-gather over NVLink; gloo in the CPU tests).  Other collectives are the
+benchmark's barrier and max-over-ranks timing.
 """
 
 from __future__ import annotations
@@ -60,6 +62,21 @@ def sum_over_ranks(x: float) -> float:
 def barrier() -> None:
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()
+
+
+def gather_outputs(t: torch.Tensor) -> torch.Tensor:
+    """Concatenate every rank's equal-length opened output shard in rank
+    order (the final output reconstruction / gather of the sharded batch).
+    One all-gather into a preallocated buffer; world 1 returns t itself."""
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return t
+    world = dist.get_world_size()
+    src = t.reshape(-1).contiguous()
+    if dist.get_backend() == "nccl" and not src.is_cuda:
+        src = src.cuda()
+    out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src)
+    return out
 
 
 def session_seed(rank: int, step: int, base: int = 1000) -> int:

@@ -26,6 +26,10 @@ def _worker(rank, world, port, q):
     # every rank verifies its own independent batch with the CPU oracle
     from oracle import mpc
     res = mpc.mulv(seed=dist.session_seed(r, 0), lanes=64, d=16, R=2)
+    # final output gather of the sharded batch: rank order, equal shards
+    import torch
+    full = dist.gather_outputs(torch.arange(4, dtype=torch.int64) + 100 * rank)
+    assert full.tolist() == [0, 1, 2, 3, 100, 101, 102, 103]
     dist.barrier()
     q.put((rank, slow, total, sorted(seeds), res.verdict, int(res.z[1]["m"][0])))
     dist.finalize()
