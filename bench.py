@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--R", default="auto")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--engine", default="coop", choices=["coop", "threads"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to test the N > 1 path on fewer GPUs than ranks")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -514,7 +516,7 @@ def run_b200(args):
     from paper_2411_09287_b200.runtime import Session
 
     from paper_2411_09287_b200 import dist as pdist
-    rank, world, local = pdist.init("nccl")
+    rank, world, local = pdist.init(args.dist_backend)
     _lib.load()
 
     N = 1 << args.log2n

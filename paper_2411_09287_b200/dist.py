@@ -23,18 +23,25 @@ def env() -> tuple[int, int, int]:
 
 
 def init(backend: str | None = None) -> tuple[int, int, int]:
+    """Join the process group; one GPU per local rank (gloo runs may
+    oversubscribe GPUs for testing: local ranks wrap around the devices)."""
     rank, world, local = env()
+    dev = local
+    if torch.cuda.is_available() and backend == "gloo":
+        dev = local % torch.cuda.device_count()
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         kw = {}
         if backend == "nccl":
-            torch.cuda.set_device(local)
-            kw["device_id"] = torch.device("cuda", local)
+            torch.cuda.set_device(dev)
+            kw["device_id"] = torch.device("cuda", dev)
+        elif torch.cuda.is_available():
+            torch.cuda.set_device(dev)
         dist.init_process_group(backend, **kw)
     elif torch.cuda.is_available():
-        torch.cuda.set_device(local)
-    return rank, world, local
+        torch.cuda.set_device(dev)
+    return rank, world, dev
 
 
 def _device_for_collective() -> torch.device:
@@ -72,8 +79,11 @@ def gather_outputs(t: torch.Tensor) -> torch.Tensor:
         return t
     world = dist.get_world_size()
     src = t.reshape(-1).contiguous()
-    if dist.get_backend() == "nccl" and not src.is_cuda:
-        src = src.cuda()
+    if dist.get_backend() == "nccl":
+        if not src.is_cuda:
+            src = src.cuda()
+    else:
+        src = src.cpu()
     out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
     dist.all_gather_into_tensor(out, src)
     return out
