@@ -284,6 +284,17 @@ int r3_vfy_base_fold(int nterms, const int64_t* coef,
                      int nz, const uint64_t* const* zc, int64_t zs, int64_t N,
                      const uint64_t* pw, int d, uint64_t* acc, uint64_t* h1,
                      uint64_t* h2, uint64_t* zsum, uint64_t mask, void* stream);
+/* r3_vfy_base_fold for np <= 3 parties in ONE pass over the power table
+ * (party q's operands at xc/yc[3q + t], zc[2q + c], coef[3q + t]; outputs
+ * acc/h1/h2/zsum[q]).  Blocks of the np parties on the same table rows are
+ * adjacent, so the table streams from HBM once. */
+int r3_vfy_base_fold_multi(int np, const int* nterms, const int64_t* coef,
+                           const uint64_t* const* xc, const uint64_t* const* yc,
+                           const int* nz, const uint64_t* const* zc,
+                           const int64_t* zs, int64_t N, const uint64_t* pw, int d,
+                           uint64_t* const* acc, uint64_t* const* h1,
+                           uint64_t* const* h2, uint64_t* const* zsum,
+                           uint64_t mask, void* stream);
 /* Second reduction straight from the base log (vfy2.cu): for blocks of four
  * elements 4j+a, acc[(a*4+b)] = sum_j s^{ab}_j pw[(4j+a)/n] with the party's
  * scalar leg products s^{ab}_j = sum_t coef_t x_t[4j+a] y_t[4j+b]; 16 x d

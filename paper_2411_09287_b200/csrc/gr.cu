@@ -280,11 +280,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// pairs per pipeline stage: every (4x4 tile, pair-group) thread busy
+__host__ __device__ constexpr int lf_bk(int D) { return D == 16 ? 32 : 8; }
+
 template <int D, int ROLE>
 __global__ void __launch_bounds__(512, 1)
 level_fold_kernel(LevelArrays A, int64_t N, int64_t pairs_per_block, u64* __restrict__ out1, u64* __restrict__ out2) {
   constexpr int NARR = ROLE == 0 ? 2 : 4;  // xa, ya (+ xb, yb)
-  constexpr int BK = 8;                    // pairs per stage
+  constexpr int BK = lf_bk(D);             // pairs per stage
   constexpr int STAGES = 3;
   constexpr int ROWW = 2 * D;              // odd + even row, in words
   constexpr int STAGE_WORDS = NARR * BK * ROWW;
@@ -452,8 +455,13 @@ struct OutPtrs {
   u64* p[8];
 };
 
+// i / n for i >= 0: a shift for power-of-two n (uniform branch)
+__device__ __forceinline__ int64_t qdiv64(int64_t i, int64_t n) {
+  return (n & (n - 1)) == 0 ? (i >> (__ffsll(n) - 1)) : i / n;
+}
+
 __device__ __forceinline__ int64_t comp_off(int64_t i, int64_t n, int64_t ks, int64_t ls) {
-  int64_t l = i / n;
+  int64_t l = qdiv64(i, n);
   return (i - l * n) * ks + l * ls;
 }
 
@@ -515,8 +523,8 @@ l1_fold_kernel(int nterms, const int64_t* __restrict__ coef_dev, CompPtrs xc, Co
         c2e -= cf * (x0 * g2);
       }
     }
-    const u64 w0 = __ldg(pw + (i0 / n) * D + k);
-    const u64 w1 = has1 ? __ldg(pw + (i1 / n) * D + k) : 0ull;
+    const u64 w0 = __ldg(pw + qdiv64(i0, n) * D + k);
+    const u64 w1 = has1 ? __ldg(pw + qdiv64(i1, n) * D + k) : 0ull;
     h1 += c1 * w1;
     h2 += c2o * w1 + c2e * w0;
   }
@@ -546,8 +554,8 @@ __global__ void l1_line_x_kernel(int ncomp, CompPtrs xc, int64_t N, int64_t n, i
     const int k = int(e - j * D);
     const int64_t i0 = 2 * j, i1 = 2 * j + 1;
     const bool has1 = i1 < N;
-    const u64 a = __ldg(A + (i0 / tq) * D + k);
-    const u64 b = has1 ? __ldg(B + (i1 / tq) * D + k) : 0ull;
+    const u64 a = __ldg(A + qdiv64(i0, tq) * D + k);
+    const u64 b = has1 ? __ldg(B + qdiv64(i1, tq) * D + k) : 0ull;
     const int64_t o0 = comp_off(i0, n, ks, ls);
     const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
     for (int c = 0; c < ncomp; ++c) {
@@ -916,12 +924,12 @@ extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* x
   int64_t blocks = kNumSMs;
   int64_t per = (npairs + blocks - 1) / blocks;
   if (per < 32) per = 32;
-  per = (per + 7) / 8 * 8;
+  per = (per + lf_bk(d) - 1) / lf_bk(d) * lf_bk(d);
   blocks = (npairs + per - 1) / per;
 #define R3_LF(DD, RR)                                                                                   \
   {                                                                                                     \
     constexpr int NARR = RR == 0 ? 2 : 4;                                                               \
-    const size_t smem = size_t(3 * NARR * 8 * 2 * DD + 4 * DD) * 8;                                     \
+    const size_t smem = size_t(3 * NARR * lf_bk(DD) * 2 * DD + 4 * DD) * 8;                             \
     static bool attr = false;                                                                           \
     if (!attr) {                                                                                        \
       cudaFuncSetAttribute(level_fold_kernel<DD, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \

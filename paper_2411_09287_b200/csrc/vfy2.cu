@@ -29,8 +29,14 @@ struct Outs8 {
   u64* p[8];
 };
 
+// i / n for i >= 0: a shift when n is a power of two (dot logs of ell-bit
+// inner products, n = 64), the 64-bit division otherwise (uniform branch)
+__device__ __forceinline__ int64_t qdiv(int64_t i, int64_t n) {
+  return (n & (n - 1)) == 0 ? (i >> (__ffsll(n) - 1)) : i / n;
+}
+
 __device__ __forceinline__ int64_t elem_off(int64_t i, int64_t n, int64_t ks, int64_t ls) {
-  const int64_t l = i / n;
+  const int64_t l = qdiv(i, n);
   return (i - l * n) * ks + l * ls;
 }
 
@@ -72,7 +78,7 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int64_t ia = 4 * j + a;
-        const u64 w = ia < N ? __ldg(pw + (ia / n) * D + k) : 0ull;
+        const u64 w = ia < N ? __ldg(pw + qdiv(ia, n) * D + k) : 0ull;
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a * 4 + b] += sS[rp][a * 4 + b] * w;
       }
@@ -110,7 +116,7 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
     for (int a = 0; a < 4; ++a) {
       const int64_t i = B * j + a;
       const bool ok = a < B && i < N;
-      const int64_t row = ONE ? j : i / tq;
+      const int64_t row = ONE ? j : qdiv(i, tq);
       w[a] = ok ? __ldg(tabs + a * tab_stride + row * D + k) : 0ull;
       off[a] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
@@ -169,11 +175,35 @@ __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int6
 // the tile, each lane holding KPL coefficients (D >= 32) or one coefficient
 // of one of 32/D rows (D < 32), multiply-accumulating broadcast scalars.
 // ---------------------------------------------------------------------------
+// One party's operands of the base fold.  Several parties share one launch:
+// block b works for party b % np on tile slice b / np, so the np blocks that
+// stream the same power-table rows are adjacent (co-resident) and the table
+// is read from HBM once for all parties (L2 hits for the others).
+struct BaseFoldParty {
+  Comps8 xc, yc, zc;
+  int64_t coef[3];
+  int nterms, nz;
+  int64_t zs;
+  u64* acc_out;
+  u64* z_out;
+};
+struct BaseFoldArgs {
+  BaseFoldParty p[3];
+  int np;
+};
+
 template <int D>
 __global__ void __launch_bounds__(256)
-base_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t c2, int nz, Comps8 zc,
-                 int64_t zs, int64_t N, const u64* __restrict__ pw, u64* __restrict__ acc_out,
-                 u64* __restrict__ z_out) {
+base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64* __restrict__ pw) {
+  const BaseFoldParty& P = args.p[blockIdx.x % args.np];
+  const int nterms = P.nterms, nz = P.nz;
+  const int64_t zs = P.zs;
+  const Comps8& xc = P.xc;
+  const Comps8& yc = P.yc;
+  const Comps8& zc = P.zc;
+  u64* __restrict__ acc_out = P.acc_out;
+  u64* __restrict__ z_out = P.z_out;
+  const int64_t slice = blockIdx.x / args.np, nslices = gridDim.x / args.np;
   constexpr int KPL = D >= 32 ? D / 32 : 1;
   constexpr int RPS = D >= 32 ? 1 : 32 / D;
   constexpr int TB = 32;
@@ -183,7 +213,7 @@ base_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = D >= 32 ? 0 : lane / D;
   const int kb = D >= 32 ? lane : lane % D;
-  const int64_t coefs[3] = {c0, c1, c2};
+  const int64_t coefs[3] = {P.coef[0], P.coef[1], P.coef[2]};
   u64 acc[16][KPL], zacc[2][KPL];
 #pragma unroll
   for (int q = 0; q < 16; ++q)
@@ -195,7 +225,7 @@ base_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64
     for (int c = 0; c < KPL; ++c) zacc[q][c] = 0;
   const int64_t nblk = (N + 3) / 4;
   const int64_t ntiles = (nblk + TB - 1) / TB;
-  for (int64_t tile = int64_t(blockIdx.x) * W + w; tile < ntiles; tile += int64_t(gridDim.x) * W) {
+  for (int64_t tile = slice * W + w; tile < ntiles; tile += nslices * W) {
     {  // phase A: block j = tile*TB + lane
       const int64_t i0 = 4 * (tile * TB + lane);
       u64 s[16];
@@ -409,38 +439,85 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   return check_launch("r3_vfy_line_b_const");
 }
 
-extern "C" int r3_vfy_base_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
-                                const uint64_t* const* yc, int nz, const uint64_t* const* zc, int64_t zs,
-                                int64_t N, const uint64_t* pw, int d, uint64_t* acc, uint64_t* h1, uint64_t* h2,
-                                uint64_t* zsum, uint64_t mask, void* stream) {
-  if (nterms < 1 || nterms > 3 || nz < 0 || nz > 2 || N < 0 || zs < 1) {
-    set_error("r3_vfy_base_fold: bad arguments");
-    return R3_ERR_ARG;
+static int base_fold_launch(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                            const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                            const int64_t* zs, int64_t N, const uint64_t* pw, int d, uint64_t* const* acc,
+                            uint64_t* const* h1, uint64_t* const* h2, uint64_t* const* zsum, uint64_t mask,
+                            cudaStream_t s) {
+  BaseFoldArgs args{};
+  args.np = np;
+  for (int q = 0; q < np; ++q) {
+    if (nterms[q] < 1 || nterms[q] > 3 || nz[q] < 0 || nz[q] > 2 || zs[q] < 1) {
+      set_error("r3_vfy_base_fold: bad arguments");
+      return R3_ERR_ARG;
+    }
+    if (cudaMemsetAsync(acc[q], 0, size_t(16) * d * 8, s) != cudaSuccess ||
+        (nz[q] > 0 && cudaMemsetAsync(zsum[q], 0, size_t(nz[q]) * d * 8, s) != cudaSuccess)) {
+      set_error("r3_vfy_base_fold: memset failed");
+      return R3_ERR_CUDA;
+    }
+    BaseFoldParty& P = args.p[q];
+    P.nterms = nterms[q];
+    P.nz = nz[q];
+    P.zs = zs[q];
+    for (int t = 0; t < nterms[q]; ++t) {
+      P.xc.p[t] = reinterpret_cast<const u64*>(xc[3 * q + t]);
+      P.yc.p[t] = reinterpret_cast<const u64*>(yc[3 * q + t]);
+      P.coef[t] = coef[3 * q + t];
+    }
+    for (int c = 0; c < nz[q]; ++c) P.zc.p[c] = reinterpret_cast<const u64*>(zc[2 * q + c]);
+    P.acc_out = reinterpret_cast<u64*>(acc[q]);
+    P.z_out = reinterpret_cast<u64*>(zsum[q]);
   }
-  cudaStream_t s = as_stream(stream);
-  if (cudaMemsetAsync(acc, 0, size_t(16) * d * 8, s) != cudaSuccess ||
-      (nz > 0 && cudaMemsetAsync(zsum, 0, size_t(nz) * d * 8, s) != cudaSuccess)) {
-    set_error("r3_vfy_base_fold: memset failed");
-    return R3_ERR_CUDA;
-  }
-  Comps8 xp{}, yp{}, zp{};
-  int64_t cf[3] = {0, 0, 0};
-  for (int t = 0; t < nterms; ++t) {
-    xp.p[t] = reinterpret_cast<const u64*>(xc[t]);
-    yp.p[t] = reinterpret_cast<const u64*>(yc[t]);
-    cf[t] = coef[t];
-  }
-  for (int c = 0; c < nz; ++c) zp.p[c] = reinterpret_cast<const u64*>(zc[c]);
   if (N > 0) {
     const int64_t ntiles = ((N + 3) / 4 + 31) / 32;
     R3_DISPATCH_D2(d, ({
-                     unsigned grid = grid_for((ntiles + 7) / 8, 1, 2);
-                     base_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, xp, yp, cf[0], cf[1], cf[2], nz, zp, zs, N,
-                                                              (const u64*)pw, (u64*)acc, (u64*)zsum);
+                     unsigned slices = grid_for((ntiles + 7) / 8, 1, 2);
+                     base_fold_kernel<D><<<slices * np, 256, 0, s>>>(args, N, (const u64*)pw);
                    }));
     int rc = check_launch("r3_vfy_base_fold");
     if (rc) return rc;
   }
-  base_fold_finish_kernel<<<1, 64, 0, s>>>(d, nz, (const u64*)acc, (u64*)h1, (u64*)h2, (u64*)zsum, mask);
-  return check_launch("r3_vfy_base_fold(finish)");
+  for (int q = 0; q < np; ++q) {
+    base_fold_finish_kernel<<<1, 64, 0, s>>>(d, nz[q], (const u64*)acc[q], (u64*)h1[q], (u64*)h2[q],
+                                             (u64*)zsum[q], mask);
+    int rc = check_launch("r3_vfy_base_fold(finish)");
+    if (rc) return rc;
+  }
+  return R3_OK;
+}
+
+extern "C" int r3_vfy_base_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                                const uint64_t* const* yc, int nz, const uint64_t* const* zc, int64_t zs,
+                                int64_t N, const uint64_t* pw, int d, uint64_t* acc, uint64_t* h1, uint64_t* h2,
+                                uint64_t* zsum, uint64_t mask, void* stream) {
+  if (N < 0 || nterms < 1 || nterms > 3 || nz < 0 || nz > 2) {
+    set_error("r3_vfy_base_fold: bad arguments");
+    return R3_ERR_ARG;
+  }
+  int64_t cf[3] = {0, 0, 0};
+  const uint64_t* xs[3] = {nullptr, nullptr, nullptr};
+  const uint64_t* ys[3] = {nullptr, nullptr, nullptr};
+  const uint64_t* zz[2] = {nullptr, nullptr};
+  for (int t = 0; t < nterms; ++t) {
+    cf[t] = coef[t];
+    xs[t] = xc[t];
+    ys[t] = yc[t];
+  }
+  for (int c = 0; c < nz; ++c) zz[c] = zc[c];
+  return base_fold_launch(1, &nterms, cf, xs, ys, &nz, zz, &zs, N, pw, d, &acc, &h1, &h2, &zsum, mask,
+                          as_stream(stream));
+}
+
+extern "C" int r3_vfy_base_fold_multi(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                                      const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                                      const int64_t* zs, int64_t N, const uint64_t* pw, int d,
+                                      uint64_t* const* acc, uint64_t* const* h1, uint64_t* const* h2,
+                                      uint64_t* const* zsum, uint64_t mask, void* stream) {
+  if (np < 1 || np > 3 || N < 0) {
+    set_error("r3_vfy_base_fold_multi: bad arguments");
+    return R3_ERR_ARG;
+  }
+  return base_fold_launch(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, d, acc, h1, h2, zsum, mask,
+                          as_stream(stream));
 }

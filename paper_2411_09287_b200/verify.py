@@ -320,21 +320,38 @@ def _l1_folds(party, comp: _Compressed, pw: torch.Tensor, gr: Ring):
 
 
 def _base_fold(party, comp: _Compressed, zcomps: list, z_stride: int, pw: torch.Tensor, gr: Ring):
-    """r3_vfy_base_fold: (zsum (nz, 1, d), acc (16, d), h1 fold, h2 fold)."""
-    terms = _role_terms(party.role)
+    """r3_vfy_base_fold: (zsum (nz, 1, d), acc (16, d), h1 fold, h2 fold).
+    Honest coop sessions run the three parties' folds in one launch that
+    streams the public power table once (r3_vfy_base_fold_multi)."""
+    mine = {"terms": _role_terms(party.role), "x": comp.x, "y": comp.y, "z": zcomps}
     d = gr.d
-    coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
-    xs = _ptrs([comp.x[t[1]] for t in terms])
-    ys = _ptrs([comp.y[t[2]] for t in terms])
-    zp = _ptrs(zcomps)
-    zsum = empty((len(zcomps), 1, d))
-    acc = empty((16, d))
-    h1 = empty((1, d))
-    h2 = empty((1, d))
-    call("r3_vfy_base_fold", len(terms), C.addressof(coef), C.addressof(xs), C.addressof(ys), len(zcomps),
-         C.addressof(zp), z_stride, comp.N, ptr(pw), d, ptr(acc), ptr(h1), ptr(h2), ptr(zsum), gr.mask,
-         stream())
-    return zsum, acc, h1, h2
+
+    def folds(slots):
+        roles = sorted(slots)
+        np_ = len(roles)
+        nterms = (C.c_int * np_)(*[len(slots[r]["terms"]) for r in roles])
+        nz = (C.c_int * np_)(*[len(slots[r]["z"]) for r in roles])
+        coef = (C.c_int64 * (3 * np_))()
+        xs, ys, zp = (C.c_void_p * (3 * np_))(), (C.c_void_p * (3 * np_))(), (C.c_void_p * (2 * np_))()
+        out = {}
+        for q, r in enumerate(roles):
+            sl = slots[r]
+            for t, (cf, xk, yk) in enumerate(sl["terms"]):
+                coef[3 * q + t], xs[3 * q + t], ys[3 * q + t] = cf, ptr(sl["x"][xk]), ptr(sl["y"][yk])
+            for c, zt in enumerate(sl["z"]):
+                zp[2 * q + c] = ptr(zt)
+            out[r] = (empty((len(sl["z"]), 1, d)), empty((16, d)), empty((1, d)), empty((1, d)))
+        zs = (C.c_int64 * np_)(*([z_stride] * np_))
+        arrs = [(C.c_void_p * np_)(*[ptr(out[r][i]) for r in roles]) for i in range(4)]
+        call("r3_vfy_base_fold_multi", np_, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+             C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zs), comp.N, ptr(pw), d,
+             C.addressof(arrs[1]), C.addressof(arrs[2]), C.addressof(arrs[3]), C.addressof(arrs[0]),
+             gr.mask, stream())
+        return out
+
+    if _joint_ok(party):
+        return party.sess.joint(("bfold", party.next_id("_joint.bfold")), party.role, mine, folds)
+    return folds({party.role: mine})[party.role]
 
 
 def _powsum(comps: list, stride: int, lanes: int, pw: torch.Tensor, gr: Ring) -> torch.Tensor:
@@ -443,15 +460,42 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     ze2 = _open_challenge(party, chal.zetas[1].scale_pub(2), "vfy.zeta")
     z2 = _recombine(party, z1, h1, h2, _quad(party, ze2, gr), gr)
     tabs, kappa, tq, stride = _l2_tables(party, pw, comp.n, w1, ze2, gr)
-    nb = (comp.N + 3) // 4
-    xo = {k: empty((nb, gr.d)) for k in comp.x}
-    yo = {k: empty((nb, gr.d)) for k in comp.y}
-    xk, yk = list(comp.x), list(comp.y)
-    call("r3_vfy_line_b", 4, len(xk), _ptrs([comp.x[k] for k in xk]), comp.N, comp.n, comp.ks,
-         comp.ls, ptr(tabs), stride, tq, gr.d, _ptrs([xo[k] for k in xk]), gr.mask, stream())
-    call("r3_vfy_line_b_const", 4, len(yk), _ptrs([comp.y[k] for k in yk]), comp.N, comp.n,
-         comp.ks, comp.ls, ptr(kappa), gr.d, _ptrs([yo[k] for k in yk]), gr.mask, stream())
-    return (_mval_from(xo, gr, role), _mval_from(yo, gr, role)), z2
+    geo = (comp.N, comp.n, comp.ks, comp.ls)
+
+    def level2_vectors(slots):
+        """One r3_vfy_line_b / _const launch over the components of every
+        party in `slots` (the public tables are streamed once for all)."""
+        nb = (comp.N + 3) // 4
+        out = {}
+        for side, fn, arg in (("x", "r3_vfy_line_b", None), ("y", "r3_vfy_line_b_const", None)):
+            srcs = [(r, k, t) for r, sl in sorted(slots.items()) for k, t in sl[side].items()]
+            dst = [empty((nb, gr.d)) for _ in srcs]
+            for c0 in range(0, len(srcs), 8):
+                part, pdst = srcs[c0:c0 + 8], dst[c0:c0 + 8]
+                if side == "x":
+                    call(fn, 4, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs), stride, tq,
+                         gr.d, _ptrs(pdst), gr.mask, stream())
+                else:
+                    call(fn, 4, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(kappa), gr.d,
+                         _ptrs(pdst), gr.mask, stream())
+            for (r, k, _), o in zip(srcs, dst):
+                out.setdefault(r, {"x": {}, "y": {}})[side][k] = o
+        return out
+
+    mine = {"x": comp.x, "y": comp.y}
+    if _joint_ok(party):
+        res = party.sess.joint(("l2vec", party.next_id("_joint.l2vec")), role, mine, level2_vectors)
+    else:
+        res = level2_vectors({role: mine})[role]
+    return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z2
+
+
+def _joint_ok(party) -> bool:
+    """Honest coop sessions may batch the three simulated parties' local
+    kernels into one launch (Session.joint)."""
+    from .transport import CoopRouter
+    sess = party.sess
+    return sess.joint_enabled and isinstance(sess.router, CoopRouter)
 
 
 def _l2_tables(party, pw: torch.Tensor, dot_n: int, w1, ze2: torch.Tensor, gr: Ring):

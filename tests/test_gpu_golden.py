@@ -45,7 +45,7 @@ def _flatten(role, res, out, prefix, MVal, host):
     out["arrays"][f"p{role}.{prefix}"] = host(res)
 
 
-def run_case(name, engine="coop", prog_override=None):
+def run_case(name, engine="coop", prog_override=None, joint=True):
     import programs
     from paper_2411_09287_b200 import host
     from paper_2411_09287_b200.runtime import Session
@@ -71,7 +71,7 @@ def run_case(name, engine="coop", prog_override=None):
         site, who, delta, gate, lane = inj
         adv = AdversaryConfig(corrupted=who, injections=[Injection(site, delta=delta, gate=gate, lane=lane)])
     sess = Session(seed=sess_kw.get("seed", 0), ell=sess_kw.get("ell", 64), adversary=adv,
-                   keep_messages=True, engine=engine)
+                   keep_messages=True, engine=engine, joint=joint)
     log = []
 
     def hook(frm, to, phase, label, arr, cls, ring):
@@ -117,11 +117,25 @@ def test_golden_case(cuda, name):
         np.testing.assert_array_equal(out["arrays"][k].reshape(v.shape), v, err_msg=k)
 
 
-def test_golden_coop_message_order(cuda):
-    """The coop engine reproduces the reference's global message order."""
-    meta, _a, sess, _l, _o, _s = run_case("mulv_64_d16_R2")
+@pytest.mark.parametrize("name", ["mulv_64_d16_R2", "relu_64"])
+def test_golden_coop_message_order(cuda, name):
+    """With gate-by-gate scheduling (joint=False) the coop engine reproduces
+    the reference's global message order; joint kernels (the default) keep
+    every per-sender sequence (test_golden_case) but interleave differently."""
+    meta, _a, sess, _l, _o, _s = run_case(name, joint=False)
     msgs = [[f, t, p.value, lab, nb, c] for (f, t, p, lab, nb, c) in sess.transcript.messages]
     assert msgs == meta["messages"]
+
+
+@pytest.mark.parametrize("name", ["relu_64", "infer1_conv_tiny", "mulv_1024_d64_R7"])
+def test_golden_without_joint_kernels(cuda, name):
+    """The gate-by-gate path (joint=False) matches the same golden runs."""
+    meta, arrays, sess, log, out, status = run_case(name, joint=False)
+    assert status == meta["status"]
+    assert _per_sender(log) == _per_sender([tuple(x) for x in meta["payloads"]])
+    want = {k: v for k, v in arrays.items() if not k.startswith("arg")}
+    for k, v in want.items():
+        np.testing.assert_array_equal(out["arrays"][k].reshape(v.shape), v, err_msg=k)
 
 
 def test_golden_threads_engine(cuda):
