@@ -262,31 +262,41 @@ base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64
       }
     }
     __syncwarp();
-    // phase B
-    for (int e0 = 0; e0 < TB; e0 += RPS) {
-      const int e = e0 + r;
+    // phase B: the 4 power rows of element block e (plus the next block's,
+    // prefetched into registers) -- keeps several row loads in flight
+    u64 wcur[4][KPL], wnxt[4][KPL];
+    auto load_rows = [&](int e, u64 (&wv)[4][KPL]) {
       const int64_t ib = 4 * (tile * TB + e);
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int64_t i = ib + a;
-        u64 wv[KPL];
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < KPL; ++c) wv[c] = i < N ? __ldg(pw + i * D + kb + 32 * c) : 0ull;
+        for (int c = 0; c < KPL; ++c) wv[a][c] = ib + a < N ? __ldg(pw + (ib + a) * D + kb + 32 * c) : 0ull;
+    };
+    load_rows(r, wcur);
+    for (int e0 = 0; e0 < TB; e0 += RPS) {
+      const int e = e0 + r;
+      if (e0 + RPS < TB) load_rows(e + RPS, wnxt);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const u64 sv = sS[w][a * 4 + b][e];
 #pragma unroll
-          for (int c = 0; c < KPL; ++c) acc[a * 4 + b][c] += sv * wv[c];
+          for (int c = 0; c < KPL; ++c) acc[a * 4 + b][c] += sv * wcur[a][c];
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           if (q < nz) {
             const u64 zv = sZ[w][q * 4 + a][e];
 #pragma unroll
-            for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wv[c];
+            for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wcur[a][c];
           }
         }
       }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) wcur[a][c] = wnxt[a][c];
     }
     __syncwarp();
   }
