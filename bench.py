@@ -336,6 +336,23 @@ def matmul_c3(n: int, steps: int) -> dict:
             "scope": "PRE (masks, trunc_prepare 2^24 lanes, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online)"}
 
 
+def ref_cpu_measured(*keys) -> dict | None:
+    """The unmodified reference's own CPU timings for the configs the oracle
+    port does not cover, measured in the build container by
+    tools/ref_cpu_timing.py (profiles/ref_cpu_timing.json; the Python
+    reference cannot travel to the GPU box)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ref_cpu_timing.json")) as f:
+            j = json.load(f)
+    except (OSError, ValueError):
+        return None
+    out = {k: j["results"][k] for k in keys if k in j["results"]}
+    out["host"] = j["host"]
+    out["source"] = "profiles/ref_cpu_timing.json (tools/ref_cpu_timing.py, build container, reference " \
+                    "pkg/src/ring3pc run unmodified, one single-threaded session)"
+    return out
+
+
 def _plain_forward(model, imgs):
     """float64 forward pass of the model (conv via the same patch maps)."""
     import numpy as np
@@ -631,12 +648,16 @@ def run_b200(args):
             line["matmul"] = matmul_c3(args.matmul_n, 3)
         if args.relu_log2n:
             line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
+            line["relu"]["reference_cpu_measured"] = ref_cpu_measured(
+                "relu_exec_4096", "relu_exec_16384", "relu_verified_4096")
         if args.relu_sweep_log2n:
             line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 1)
         if args.mlp_batch:
             line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
+            line["mlp"]["reference_cpu_measured"] = ref_cpu_measured("mlp_exec_1", "mlp_verified_1")
         if args.lenet_batch:
             line["lenet"] = ppml_rates("lenet", args.lenet_batch, args.lenet_verified_batch)
+            line["lenet"]["reference_cpu_measured"] = ref_cpu_measured("lenet28_exec_1")
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
     print(json.dumps(line), flush=True)
