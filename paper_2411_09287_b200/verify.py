@@ -36,7 +36,7 @@ import torch
 
 from . import grvec
 from ._lib import call, empty, ptr, stream, to_host
-from .gates import dot_finish, dot_prepare, prepare_gate
+from .gates import MatmulBatchRec, dot_finish, dot_prepare, prepare_gate
 from .rings import ConfigError, modulus_for_degree
 from .sharing import AShare, MVal, Ring, rec, shc_random
 from .transport import AUX, OFFLINE, PAYLOAD, HarnessError, Phase
@@ -812,6 +812,8 @@ def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     gr = Ring(base_ell, modulus_for_degree(d))
     if R > len(ctx.zetas):
         raise ConfigError(f"R={R} exceeds prepared challenge budget {len(ctx.zetas)}")
+    if _structured_dots_ok(log.dots, gr):
+        return _verify_dots_structured(party, log.dots, gr, ctx, R)
     ns = {b.n for b in log.dots}
     if len(ns) != 1:
         xs, ys, z = consolidate_dot_triples(party, log.dots, gr, ctx)
@@ -822,6 +824,214 @@ def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     comp = _compressed_from_log(xs, ys, party.role, n)
     (xv, yv), z = _compress_reduce_first(party, comp, zs, comp.N // n, 1, gr, ctx, R)
     return _verify_tail(party, xv, yv, z, gr, ctx, R, start=_levels_done(R, gr))
+
+
+# ---------------------------------------------------------------------------
+# structured Pi_bsv for GEMM-form linear layers
+# ---------------------------------------------------------------------------
+
+class _FCBatch:
+    """A GEMM-form dot batch (gates.MatmulBatchRec: lane l at GEMM index
+    perm[l] = m N + n, dot index i < K) inside the consolidated vector of
+    consolidate_dot_triples (verify.py:182-212): element (l, i) is
+    r^(P + l) X[m, i] on the x side and W[i, n] on the y side.  For the
+    linear layers the lane index splits additively, l = a(m) + c(n) (FC:
+    a = mN, c = n; conv: a = b out P + p, c = oc P), so
+        x[(l), i] = r^P r^a(m) r^c(n) X[m, i].
+    Line evaluations act on the dot index only, so after k reductions (while
+    K stays even, i.e. pairs never straddle a lane) the level vectors keep
+    this form with X_k (M x K/2^k) and W_k (K/2^k x N) GR matrices, and
+    every leg fold factorises exactly in GR:
+        sum_{l,j} r^(P+l) X'[m,j] W'[j,n] = r^P sum_j (sum_m r^a(m) X'[m,j]) (sum_n r^c(n) W'[j,n]).
+    The level costs (M + N) K_k GR products instead of M N K_k."""
+
+    @staticmethod
+    def split(rec):
+        """(a, c) with lane l = a[m] + c[n] for every lane, or None."""
+        M, N = rec.M, rec.N
+        if rec.perm is None:
+            dev = rec.z.m.device if rec.z.m is not None else rec.z.mask.total.device
+            return torch.arange(M, device=dev) * N, torch.arange(N, device=dev)
+        perm = rec.perm
+        lanes = torch.empty_like(perm)
+        lanes[perm] = torch.arange(perm.numel(), device=perm.device)   # gemm index -> lane
+        L = lanes.reshape(M, N)
+        a, c = L[:, 0] - L[0, 0], L[0, :]
+        if not bool((L == a[:, None] + c[None, :]).all()):
+            return None
+        return a, c
+
+    def __init__(self, rec, role: int, gr: Ring, P: int, pw: torch.Tensor, split):
+        self.M, self.K, self.N, self.P = rec.M, rec.K, rec.N, P
+        d = gr.d
+        xc, yc = _components(rec.X, role), _components(rec.W, role)
+        self.X = {k: grvec.gr_embed(t.reshape(-1).contiguous(), gr.mod).reshape(self.M, self.K, d)
+                  for k, t in xc.items()}
+        self.Wt = {k: grvec.gr_embed(t.reshape(self.K, self.N).t().contiguous().reshape(-1), gr.mod)
+                   .reshape(self.N, self.K, d) for k, t in yc.items()}
+        a, c = split
+        self.RM = pw[a].contiguous()
+        self.RN = pw[c].contiguous()
+        self.rP = pw[P:P + 1]
+        # lane l -> (m, n) and its power r^(P + l), for materialisation
+        self.pw_lanes = pw[P:P + self.M * self.N]
+        perm = rec.perm if rec.perm is not None else torch.arange(self.M * self.N, device=pw.device)
+        self.lane_m, self.lane_n = perm // self.N, perm % self.N
+
+    def length(self) -> int:
+        return self.M * self.N * self.K
+
+    def structured(self) -> bool:
+        return self.K % 2 == 0
+
+    @staticmethod
+    def _weighted_colsum(R: torch.Tensor, A: torch.Tensor, gr: Ring) -> torch.Tensor:
+        """out[j] = sum_r R[r] A[r, j] over GR: (J, d)."""
+        rows, J, d = A.shape
+        prod = grvec.gr_mul(A.reshape(rows * J, d), R.repeat_interleave(J, dim=0), gr.ell, gr.mod)
+        return grvec.sum_axis0(prod.reshape(rows, J * d), gr.ell).reshape(J, d)
+
+    def folds(self, role: int, gr: Ring):
+        """(fold h(1), fold h(2)) of this batch for the party's leg terms."""
+        def sides(T):
+            out = {}
+            for k, t in T.items():
+                od, ev = t[:, 1::2], t[:, 0::2]
+                t2 = grvec.sub(grvec.add(od, od, gr.ell), ev, gr.ell)
+                out[k] = (od.contiguous(), t2)
+            return out
+        xs, ys = sides(self.X), sides(self.Wt)
+        res = []
+        for h in (0, 1):
+            U = {k: self._weighted_colsum(self.RM, v[h], gr) for k, v in xs.items()}
+            V = {k: self._weighted_colsum(self.RN, v[h], gr) for k, v in ys.items()}
+            if role == 0:
+                terms = [(U["total"], V["total"])]
+            elif role == 1:
+                terms = [(grvec.vneg(U["m"], gr.ell), V["s1"]), (grvec.vneg(U["s1"], gr.ell), V["m"])]
+            else:
+                terms = [(U["m"], grvec.sub(V["m"], V["s2"], gr.ell)), (grvec.vneg(U["s2"], gr.ell), V["m"])]
+            acc = None
+            for a, b in terms:
+                t = grvec.gr_dot(a, b, gr.ell, gr.mod)
+                acc = t if acc is None else grvec.add(acc, t, gr.ell)
+            res.append(grvec.gr_mul(acc, self.rP, gr.ell, gr.mod))
+        return res[0], res[1]
+
+    def reduce(self, Ms, gr: Ring) -> None:
+        d = gr.d
+        half = lambda t, rows: _line_eval(_Halves(t.reshape(-1, d)), Ms, gr).reshape(rows, -1, d)
+        self.X = {k: half(t, self.M) for k, t in self.X.items()}
+        self.Wt = {k: half(t, self.N) for k, t in self.Wt.items()}
+        self.K //= 2
+
+    def materialise(self, gr: Ring):
+        """The batch's level vectors in the reference layout (lane-major)."""
+        K, d = self.K, gr.d
+        p_rep = self.pw_lanes.repeat_interleave(K, dim=0)
+        xo = {k: grvec.gr_mul(t[self.lane_m].reshape(-1, d), p_rep, gr.ell, gr.mod) for k, t in self.X.items()}
+        yo = {k: t[self.lane_n].reshape(-1, d).contiguous() for k, t in self.Wt.items()}
+        return xo, yo
+
+    def to_dense(self, gr: Ring) -> "_DenseBatch":
+        xo, yo = self.materialise(gr)
+        return _DenseBatch.from_arrays(xo, yo)
+
+
+class _DenseBatch:
+    """Any other dot batch, materialised as consolidate_dot_triples does."""
+
+    @classmethod
+    def from_arrays(cls, x: dict, y: dict) -> "_DenseBatch":
+        obj = cls.__new__(cls)
+        obj.x, obj.y = x, y
+        return obj
+
+    def __init__(self, b, role: int, gr: Ring, P: int, pw: torch.Tensor):
+        p = pw[P:P + b.lanes]
+        flat = lambda t: t.transpose(0, 1).contiguous().reshape(-1)
+        p_rep = p.repeat_interleave(b.n, dim=0)
+        # lifted scalars times GR powers: d MACs per element (gr_scale_rows)
+        self.x = {k: grvec.gr_scale_rows(flat(t), p_rep, gr.ell) for k, t in _components(b.xs, role).items()}
+        del p_rep
+        self.y = {k: grvec.gr_embed(flat(t), gr.mod) for k, t in _components(b.ys, role).items()}
+
+    def length(self) -> int:
+        return next(iter(self.x.values())).shape[0]
+
+    def structured(self) -> bool:
+        return self.length() % 2 == 0
+
+    def folds(self, role: int, gr: Ring):
+        fused = _level_folds_fused(role, self.x, self.y, gr)
+        if fused is not None:
+            return fused
+        X = {k: _Halves(t) for k, t in self.x.items()}
+        Y = {k: _Halves(t) for k, t in self.y.items()}
+        rows = next(iter(X.values())).n0
+        return _level_folds(role, X, Y, "f1", rows, gr), _level_folds(role, X, Y, "f2", rows, gr)
+
+    def reduce(self, Ms, gr: Ring) -> None:
+        self.x = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.x.items()}
+        self.y = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.y.items()}
+
+    def materialise(self, gr: Ring):
+        return self.x, self.y
+
+
+def _structured_dots_ok(batches, gr: Ring) -> bool:
+    return gr.d >= 8 and any(isinstance(b, MatmulBatchRec) and b.K % 2 == 0 for b in batches)
+
+
+def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -> bool:
+    """Pi_bsv (verify.py:182-212) + R x Pi_rd + Pi_vdot with GEMM-form
+    batches kept factorised (_FCBatch) while their dot dimension stays even;
+    the remaining levels run on the materialised vector.  Every value
+    (folds, messages, verdict) equals the reference's."""
+    role = party.role
+    r = _open_challenge(party, ctx.r, "vfy.r")
+    total = sum(b.lanes for b in batches)
+    pw = _powers(party, r, total, gr)
+    parts, z_acc, pos = [], None, 0
+    for b in batches:
+        p = pw[pos:pos + b.lanes]
+        zl = _lift(b.z, gr)
+        zg = _sum_lanes(MVal(zl.mask._map(lambda a: grvec.gr_mul(a, p, gr.ell, gr.mod)),
+                             None if zl.m is None else grvec.gr_mul(zl.m, p, gr.ell, gr.mod)), gr)
+        z_acc = zg if z_acc is None else z_acc + zg
+        split = _FCBatch.split(b) if isinstance(b, MatmulBatchRec) else None
+        if split is not None:
+            parts.append(_FCBatch(b, role, gr, pos, pw, split))
+        else:
+            parts.append(_DenseBatch(b, role, gr, pos, pw))
+        pos += b.lanes
+    z = z_acc
+    k = 0
+    while k < R:
+        # a factorised batch whose dot dimension turned odd continues dense
+        parts = [pt.to_dense(gr) if isinstance(pt, _FCBatch) and not pt.structured()
+                 and pt.length() % 2 == 0 else pt for pt in parts]
+        if not all(pt.structured() for pt in parts):
+            break
+        folds = [pt.folds(role, gr) for pt in parts]
+        fold1, fold2 = folds[0]
+        for f1, f2 in folds[1:]:
+            fold1, fold2 = grvec.add(fold1, f1, gr.ell), grvec.add(fold2, f2, gr.ell)
+        rows = sum(pt.length() for pt in parts) // 2
+        h1 = _gr_dot_folded(party, gr, rows, fold1)
+        h2 = _gr_dot_folded(party, gr, rows, fold2)
+        ze = _open_challenge(party, ctx.zetas[k].scale_pub(2), "vfy.zeta")
+        q = _quad(party, ze, gr)
+        z = _recombine(party, z, h1, h2, q, gr)
+        Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
+        for pt in parts:
+            pt.reduce(Ms, gr)
+        k += 1
+    mats = [pt.materialise(gr) for pt in parts]
+    xs = _mval_from({c: torch.cat([m[0][c] for m in mats]) for c in mats[0][0]}, gr, role)
+    ys = _mval_from({c: torch.cat([m[1][c] for m in mats]) for c in mats[0][1]}, gr, role)
+    del parts, mats
+    return _verify_tail(party, xs, ys, z, gr, ctx, R, start=k)
 
 
 def _concat_lanes(vals: list) -> MVal:

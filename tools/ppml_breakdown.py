@@ -1,0 +1,47 @@
+"""Per-entry-point GPU time of one batched private-inference session.
+    python tools/ppml_breakdown.py mlp|lenet BATCH [check]"""
+import collections
+import os
+import sys
+import time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_2411_09287_b200 import _lib, ppml  # noqa: E402
+from paper_2411_09287_b200.runtime import Session  # noqa: E402
+
+name, B = sys.argv[1], int(sys.argv[2])
+check = len(sys.argv) > 3
+model = (ppml.secureml_model if name == "mlp" else ppml.lenet28_model)(np.random.default_rng(0))
+imgs = np.random.default_rng(0).normal(0, 1, (B, int(np.prod(model.input_shape))))
+cfg = ppml.InferConfig(check=check)
+prog = lambda party: ppml.infer_batch(party, model, imgs, cfg)
+Session(seed=1).run(prog)
+torch.cuda.synchronize()
+ev = []
+
+
+def hook(nm, args, run):
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    rc = run()
+    e.record()
+    ev.append((nm, s, e))
+    return rc
+
+
+_lib.CALL_HOOK = hook
+t0 = time.perf_counter()
+Session(seed=2).run(prog)
+torch.cuda.synchronize()
+wall = time.perf_counter() - t0
+_lib.CALL_HOOK = None
+tot, cnt = collections.Counter(), collections.Counter()
+for nm, s, e in ev:
+    tot[nm] += s.elapsed_time(e)
+    cnt[nm] += 1
+print(f"{name} B={B} check={check}: wall {wall * 1e3:.1f} ms, library GPU {sum(tot.values()):.1f} ms in {len(ev)} calls,"
+      f" peak mem {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB")
+for k, v in tot.most_common(14):
+    print(f"  {k:26s} {v:9.2f} ms  calls={cnt[k]}")
