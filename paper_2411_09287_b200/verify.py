@@ -939,30 +939,35 @@ class _FCBatch:
 
 
 class _DenseBatch:
-    """Any other dot batch, materialised as consolidate_dot_triples does."""
+    """Any other dot batch (n, L) of the consolidated vector.  Level 0 is
+    never lifted: its folds come straight from the base log
+    (r3_vfy_l1_fold over the batch's power rows) and the first line
+    evaluation writes the dense level-1 rows from the base shares and the
+    public tables r^(P+l) (1 - ze), r^(P+l) ze (r3_vfy_l1_line_x / _y), as
+    _compress_reduce_first does for a whole equal-n log."""
 
     @classmethod
     def from_arrays(cls, x: dict, y: dict) -> "_DenseBatch":
         obj = cls.__new__(cls)
-        obj.x, obj.y = x, y
+        obj.x, obj.y, obj.base = x, y, None
         return obj
 
     def __init__(self, b, role: int, gr: Ring, P: int, pw: torch.Tensor):
-        p = pw[P:P + b.lanes]
-        flat = lambda t: t.transpose(0, 1).contiguous().reshape(-1)
-        p_rep = p.repeat_interleave(b.n, dim=0)
-        # lifted scalars times GR powers: d MACs per element (gr_scale_rows)
-        self.x = {k: grvec.gr_scale_rows(flat(t), p_rep, gr.ell) for k, t in _components(b.xs, role).items()}
-        del p_rep
-        self.y = {k: grvec.gr_embed(flat(t), gr.mod) for k, t in _components(b.ys, role).items()}
+        self.base = _compressed_from_log(b.xs, b.ys, role, b.n)
+        self.pw = pw[P:P + b.lanes]
+        self.x = self.y = None
 
     def length(self) -> int:
+        if self.base is not None:
+            return self.base.N
         return next(iter(self.x.values())).shape[0]
 
     def structured(self) -> bool:
         return self.length() % 2 == 0
 
-    def folds(self, role: int, gr: Ring):
+    def folds(self, role: int, gr: Ring, party=None):
+        if self.base is not None:
+            return _l1_folds(party, self.base, self.pw, gr)
         fused = _level_folds_fused(role, self.x, self.y, gr)
         if fused is not None:
             return fused
@@ -971,12 +976,35 @@ class _DenseBatch:
         rows = next(iter(X.values())).n0
         return _level_folds(role, X, Y, "f1", rows, gr), _level_folds(role, X, Y, "f2", rows, gr)
 
-    def reduce(self, Ms, gr: Ring) -> None:
+    def reduce(self, Ms, gr: Ring, party=None, ze=None) -> None:
+        if self.base is not None:
+            comp = self.base
+            A, B, one_m = _line_tables(party, None, self.pw, comp.n, ze, gr)
+            half = (comp.N + 1) // 2
+            xk, yk = list(comp.x), list(comp.y)
+            self.x = {k: empty((half, gr.d)) for k in xk}
+            self.y = {k: empty((half, gr.d)) for k in yk}
+            call("r3_vfy_l1_line_x", len(xk), _ptrs([comp.x[k] for k in xk]), comp.N, comp.n, comp.ks,
+                 comp.ls, ptr(A), ptr(B), comp.n, gr.d, _ptrs([self.x[k] for k in xk]), gr.mask, stream())
+            call("r3_vfy_l1_line_y", len(yk), _ptrs([comp.y[k] for k in yk]), comp.N, comp.n, comp.ks,
+                 comp.ls, ptr(one_m), ptr(ze), gr.d, _ptrs([self.y[k] for k in yk]), gr.mask, stream())
+            self.base = None
+            return
         self.x = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.x.items()}
         self.y = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.y.items()}
 
     def materialise(self, gr: Ring):
+        if self.base is not None:
+            return _materialise_dense(self.base, self.pw, gr)
         return self.x, self.y
+
+
+def _materialise_dense(comp: "_Compressed", pw: torch.Tensor, gr: Ring):
+    flat = lambda t: t.transpose(0, 1).contiguous().reshape(-1)
+    p_rep = pw.repeat_interleave(comp.n, dim=0)
+    xo = {k: grvec.gr_scale_rows(flat(t), p_rep, gr.ell) for k, t in comp.x.items()}
+    yo = {k: grvec.gr_embed(flat(t), gr.mod) for k, t in comp.y.items()}
+    return xo, yo
 
 
 def _structured_dots_ok(batches, gr: Ring) -> bool:
@@ -1013,7 +1041,8 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
                  and pt.length() % 2 == 0 else pt for pt in parts]
         if not all(pt.structured() for pt in parts):
             break
-        folds = [pt.folds(role, gr) for pt in parts]
+        folds = [pt.folds(role, gr, party) if isinstance(pt, _DenseBatch) else pt.folds(role, gr)
+                 for pt in parts]
         fold1, fold2 = folds[0]
         for f1, f2 in folds[1:]:
             fold1, fold2 = grvec.add(fold1, f1, gr.ell), grvec.add(fold2, f2, gr.ell)
@@ -1025,7 +1054,10 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
         z = _recombine(party, z, h1, h2, q, gr)
         Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
         for pt in parts:
-            pt.reduce(Ms, gr)
+            if isinstance(pt, _DenseBatch):
+                pt.reduce(Ms, gr, party, ze)
+            else:
+                pt.reduce(Ms, gr)
         k += 1
     mats = [pt.materialise(gr) for pt in parts]
     xs = _mval_from({c: torch.cat([m[0][c] for m in mats]) for c in mats[0][0]}, gr, role)
