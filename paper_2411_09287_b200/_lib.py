@@ -185,7 +185,9 @@ def to_device(x) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         if x.is_cuda:
             return x
-        return x.to(torch.int64).to(device(), non_blocking=False)
+        # pinned host buffers copy asynchronously on the current stream (the
+        # kernels that consume the copy are ordered after it on that stream)
+        return x.to(torch.int64).to(device(), non_blocking=x.is_pinned())
     arr = np.asarray(x)
     if arr.dtype != np.uint64:
         if arr.dtype.kind in "iu":
