@@ -288,6 +288,18 @@ int r3_vfy_base_fold(int nterms, const int64_t* coef,
  * (party q's operands at xc/yc[3q + t], zc[2q + c], coef[3q + t]; outputs
  * acc/h1/h2/zsum[q]).  Blocks of the np parties on the same table rows are
  * adjacent, so the table streams from HBM once. */
+/* Base fold against the table pw4[j] = r^(4j) (one row per block of four
+ * elements): raw accumulators acc'[a*4+b] = sum_j s^{ab}_j r^(4j) (16 x d)
+ * and zraw[c*4+a] = sum_j z_c[4j+a] r^(4j); the caller multiplies by r^a
+ * and derives the level-1 folds with r3_vfy_base_fold_finish. */
+int r3_vfy_base_fold_q4(int np, const int* nterms, const int64_t* coef,
+                        const uint64_t* const* xc, const uint64_t* const* yc,
+                        const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                        int64_t N, const uint64_t* pw4, int d, uint64_t* const* acc,
+                        uint64_t* const* zraw, void* stream);
+/* h1/h2 level-1 folds from the 16 accumulators; masks the nz z sums. */
+int r3_vfy_base_fold_finish(int d, int nz, const uint64_t* acc, uint64_t* h1,
+                            uint64_t* h2, uint64_t* zsum, uint64_t mask, void* stream);
 int r3_vfy_base_fold_multi(int np, const int* nterms, const int64_t* coef,
                            const uint64_t* const* xc, const uint64_t* const* yc,
                            const int* nz, const uint64_t* const* zc,

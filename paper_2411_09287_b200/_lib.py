@@ -78,6 +78,9 @@ _SIGS = {
     "r3_vfy_base_fold_multi": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p, u64, C.c_void_p],
+    "r3_vfy_base_fold_q4": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                            C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
+    "r3_vfy_base_fold_finish": [C.c_int, C.c_int, u64p, u64p, u64p, u64p, u64, C.c_void_p],
     "r3_vfy_l2_fold": [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i64,
                        i64, i64, i64, u64p, C.c_int, u64p, C.c_void_p],
     "r3_vfy_line_b": [C.c_int, C.c_int, C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, i64, i64,

@@ -192,7 +192,11 @@ struct BaseFoldArgs {
   int np;
 };
 
-template <int D>
+// Q4: pw holds r^(4j) (one row per block of four elements) instead of every
+// power; the kernel then accumulates acc'[a][b] = sum_j s^{ab}_j r^(4j) and
+// z'[c][a] = sum_j z_c[4j+a] r^(4j) (z_out laid out (nz, 4, D)), and the
+// caller multiplies by r^a -- a quarter of the table traffic.
+template <int D, bool Q4>
 __global__ void __launch_bounds__(256)
 base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64* __restrict__ pw) {
   const BaseFoldParty& P = args.p[blockIdx.x % args.np];
@@ -214,13 +218,14 @@ base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64
   const int r = D >= 32 ? 0 : lane / D;
   const int kb = D >= 32 ? lane : lane % D;
   const int64_t coefs[3] = {P.coef[0], P.coef[1], P.coef[2]};
-  u64 acc[16][KPL], zacc[2][KPL];
+  constexpr int NZS = Q4 ? 8 : 2;   // z accumulator slots
+  u64 acc[16][KPL], zacc[NZS][KPL];
 #pragma unroll
   for (int q = 0; q < 16; ++q)
 #pragma unroll
     for (int c = 0; c < KPL; ++c) acc[q][c] = 0;
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
+  for (int q = 0; q < NZS; ++q)
 #pragma unroll
     for (int c = 0; c < KPL; ++c) zacc[q][c] = 0;
   const int64_t nblk = (N + 3) / 4;
@@ -262,41 +267,72 @@ base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64
       }
     }
     __syncwarp();
-    // phase B: the 4 power rows of element block e (plus the next block's,
-    // prefetched into registers) -- keeps several row loads in flight
-    u64 wcur[4][KPL], wnxt[4][KPL];
-    auto load_rows = [&](int e, u64 (&wv)[4][KPL]) {
-      const int64_t ib = 4 * (tile * TB + e);
+    if constexpr (Q4) {
+      // phase B (Q4): one table row r^(4j) per element block, prefetched
+      u64 wcur[KPL], wnxt[KPL];
+      auto load_row = [&](int e, u64 (&wv)[KPL]) {
+        const int64_t j = tile * TB + e;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int c = 0; c < KPL; ++c) wv[c] = j < nblk ? __ldg(pw + j * D + kb + 32 * c) : 0ull;
+      };
+      load_row(r, wcur);
+      for (int e0 = 0; e0 < TB; e0 += RPS) {
+        const int e = e0 + r;
+        if (e0 + RPS < TB) load_row(e + RPS, wnxt);
 #pragma unroll
-        for (int c = 0; c < KPL; ++c) wv[a][c] = ib + a < N ? __ldg(pw + (ib + a) * D + kb + 32 * c) : 0ull;
-    };
-    load_rows(r, wcur);
-    for (int e0 = 0; e0 < TB; e0 += RPS) {
-      const int e = e0 + r;
-      if (e0 + RPS < TB) load_rows(e + RPS, wnxt);
+        for (int q = 0; q < 16; ++q) {
+          const u64 sv = sS[w][q][e];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const u64 sv = sS[w][a * 4 + b][e];
-#pragma unroll
-          for (int c = 0; c < KPL; ++c) acc[a * 4 + b][c] += sv * wcur[a][c];
+          for (int c = 0; c < KPL; ++c) acc[q][c] += sv * wcur[c];
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (q < nz) {
-            const u64 zv = sZ[w][q * 4 + a][e];
+        for (int q = 0; q < 8; ++q) {
+          if (q < 4 * nz) {
+            const u64 zv = sZ[w][q][e];
 #pragma unroll
-            for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wcur[a][c];
+            for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wcur[c];
           }
         }
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) wcur[c] = wnxt[c];
       }
+    } else {
+      // phase B: the 4 power rows of element block e (plus the next block's,
+      // prefetched into registers) -- keeps several row loads in flight
+      u64 wcur[4][KPL], wnxt[4][KPL];
+      auto load_rows = [&](int e, u64 (&wv)[4][KPL]) {
+        const int64_t ib = 4 * (tile * TB + e);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < KPL; ++c) wcur[a][c] = wnxt[a][c];
+          for (int c = 0; c < KPL; ++c) wv[a][c] = ib + a < N ? __ldg(pw + (ib + a) * D + kb + 32 * c) : 0ull;
+      };
+      load_rows(r, wcur);
+      for (int e0 = 0; e0 < TB; e0 += RPS) {
+        const int e = e0 + r;
+        if (e0 + RPS < TB) load_rows(e + RPS, wnxt);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const u64 sv = sS[w][a * 4 + b][e];
+#pragma unroll
+            for (int c = 0; c < KPL; ++c) acc[a * 4 + b][c] += sv * wcur[a][c];
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (q < nz) {
+              const u64 zv = sZ[w][q * 4 + a][e];
+#pragma unroll
+              for (int c = 0; c < KPL; ++c) zacc[q][c] += zv * wcur[a][c];
+            }
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < KPL; ++c) wcur[a][c] = wnxt[a][c];
+      }
     }
     __syncwarp();
   }
@@ -306,12 +342,12 @@ base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64
 #pragma unroll
     for (int q = 0; q < 16; ++q) acc[q][0] += __shfl_xor_sync(0xffffffffu, acc[q][0], off);
 #pragma unroll
-    for (int q = 0; q < 2; ++q) zacc[q][0] += __shfl_xor_sync(0xffffffffu, zacc[q][0], off);
+    for (int q = 0; q < NZS; ++q) zacc[q][0] += __shfl_xor_sync(0xffffffffu, zacc[q][0], off);
   }
   // across the CTA's warps, then one atomic per coefficient
   __syncthreads();
   u64* red = &sS[0][0][0];  // W * 16 * TB = 4096 words >= W * D
-  const int nslots = 16 + nz;
+  const int nslots = 16 + (Q4 ? 4 : 1) * nz;
   for (int q = 0; q < nslots; ++q) {
     if (r == 0) {
 #pragma unroll
@@ -321,7 +357,7 @@ base_fold_kernel(const __grid_constant__ BaseFoldArgs args, int64_t N, const u64
         for (int qq = 0; qq < 16; ++qq)
           if (qq == q) v = acc[qq][c];
 #pragma unroll
-        for (int qq = 0; qq < 2; ++qq)
+        for (int qq = 0; qq < NZS; ++qq)
           if (16 + qq == q) v = zacc[qq][c];
         red[w * D + kb + 32 * c] = v;
       }
@@ -453,7 +489,7 @@ static int base_fold_launch(int np, const int* nterms, const int64_t* coef, cons
                             const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
                             const int64_t* zs, int64_t N, const uint64_t* pw, int d, uint64_t* const* acc,
                             uint64_t* const* h1, uint64_t* const* h2, uint64_t* const* zsum, uint64_t mask,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool q4 = false) {
   BaseFoldArgs args{};
   args.np = np;
   for (int q = 0; q < np; ++q) {
@@ -462,7 +498,7 @@ static int base_fold_launch(int np, const int* nterms, const int64_t* coef, cons
       return R3_ERR_ARG;
     }
     if (cudaMemsetAsync(acc[q], 0, size_t(16) * d * 8, s) != cudaSuccess ||
-        (nz[q] > 0 && cudaMemsetAsync(zsum[q], 0, size_t(nz[q]) * d * 8, s) != cudaSuccess)) {
+        (nz[q] > 0 && cudaMemsetAsync(zsum[q], 0, size_t(nz[q]) * (q4 ? 4 : 1) * d * 8, s) != cudaSuccess)) {
       set_error("r3_vfy_base_fold: memset failed");
       return R3_ERR_CUDA;
     }
@@ -483,11 +519,15 @@ static int base_fold_launch(int np, const int* nterms, const int64_t* coef, cons
     const int64_t ntiles = ((N + 3) / 4 + 31) / 32;
     R3_DISPATCH_D2(d, ({
                      unsigned slices = grid_for((ntiles + 7) / 8, 1, 2);
-                     base_fold_kernel<D><<<slices * np, 256, 0, s>>>(args, N, (const u64*)pw);
+                     if (q4)
+                       base_fold_kernel<D, true><<<slices * np, 256, 0, s>>>(args, N, (const u64*)pw);
+                     else
+                       base_fold_kernel<D, false><<<slices * np, 256, 0, s>>>(args, N, (const u64*)pw);
                    }));
     int rc = check_launch("r3_vfy_base_fold");
     if (rc) return rc;
   }
+  if (q4) return R3_OK;   // raw r^(4j) accumulators: the caller applies r^a and finishes
   for (int q = 0; q < np; ++q) {
     base_fold_finish_kernel<<<1, 64, 0, s>>>(d, nz[q], (const u64*)acc[q], (u64*)h1[q], (u64*)h2[q],
                                              (u64*)zsum[q], mask);
@@ -517,6 +557,25 @@ extern "C" int r3_vfy_base_fold(int nterms, const int64_t* coef, const uint64_t*
   for (int c = 0; c < nz; ++c) zz[c] = zc[c];
   return base_fold_launch(1, &nterms, cf, xs, ys, &nz, zz, &zs, N, pw, d, &acc, &h1, &h2, &zsum, mask,
                           as_stream(stream));
+}
+
+extern "C" int r3_vfy_base_fold_q4(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                                   const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                                   const int64_t* zs, int64_t N, const uint64_t* pw4, int d,
+                                   uint64_t* const* acc, uint64_t* const* zraw, void* stream) {
+  if (np < 1 || np > 3 || N < 0) {
+    set_error("r3_vfy_base_fold_q4: bad arguments");
+    return R3_ERR_ARG;
+  }
+  return base_fold_launch(np, nterms, coef, xc, yc, nz, zc, zs, N, pw4, d, acc, nullptr, nullptr, zraw, 0,
+                          as_stream(stream), true);
+}
+
+extern "C" int r3_vfy_base_fold_finish(int d, int nz, const uint64_t* acc, uint64_t* h1, uint64_t* h2,
+                                       uint64_t* zsum, uint64_t mask, void* stream) {
+  base_fold_finish_kernel<<<1, 64, 0, as_stream(stream)>>>(d, nz, (const u64*)acc, (u64*)h1, (u64*)h2,
+                                                           (u64*)zsum, mask);
+  return check_launch("r3_vfy_base_fold_finish");
 }
 
 extern "C" int r3_vfy_base_fold_multi(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,

@@ -224,6 +224,17 @@ def _powers(party, r: torch.Tensor, n: int, gr: Ring) -> torch.Tensor:
     return _public(party, key, lambda: grvec.gr_powers(r, n, gr.ell, gr.mod))
 
 
+def _powers4(party, r: torch.Tensor, n4: int, gr: Ring):
+    """(r^(4j) for j < n4, r^0..r^3): the table of every fourth power and the
+    four in-block offsets (pw[4j + a] = pw4[j] r^a)."""
+    key = ("pow4", gr.ell, gr.d, _opened_key(party, r), n4)
+
+    def build():
+        rpow = grvec.gr_powers(r, 5, gr.ell, gr.mod)
+        return grvec.gr_powers(rpow[4:5], n4, gr.ell, gr.mod), rpow[:4].contiguous()
+    return _public(party, key, build)
+
+
 def _line_tables(party, r, pw: torch.Tensor, dot_n: int, ze: torch.Tensor, gr: Ring):
     """Public level-1 tables A = pw (1 - ze), B = pw ze.  For multiplication
     logs (dot_n == 1) only even powers feed A and odd powers feed B."""
@@ -354,6 +365,55 @@ def _base_fold(party, comp: _Compressed, zcomps: list, z_stride: int, pw: torch.
     return folds({party.role: mine})[party.role]
 
 
+def _base_fold_q4(party, comp: _Compressed, zcomps: list, z_stride: int, q4, gr: Ring):
+    """_base_fold against the r^(4j) table (r3_vfy_base_fold_q4): the raw
+    accumulators sum_j s^{ab}_j r^(4j) and sum_j z[4j+a] r^(4j) are taken
+    times r^a here, then the level-1 folds follow (r3_vfy_base_fold_finish)."""
+    pw4, rpow = q4
+    mine = {"terms": _role_terms(party.role), "x": comp.x, "y": comp.y, "z": zcomps}
+    d = gr.d
+    r_acc = rpow.repeat_interleave(4, dim=0)          # row a*4 + b -> r^a
+
+    def folds(slots):
+        roles = sorted(slots)
+        np_ = len(roles)
+        nterms = (C.c_int * np_)(*[len(slots[r]["terms"]) for r in roles])
+        nz = (C.c_int * np_)(*[len(slots[r]["z"]) for r in roles])
+        coef = (C.c_int64 * (3 * np_))()
+        xs, ys, zp = (C.c_void_p * (3 * np_))(), (C.c_void_p * (3 * np_))(), (C.c_void_p * (2 * np_))()
+        raw = {}
+        for q, r in enumerate(roles):
+            sl = slots[r]
+            for t, (cf, xk, yk) in enumerate(sl["terms"]):
+                coef[3 * q + t], xs[3 * q + t], ys[3 * q + t] = cf, ptr(sl["x"][xk]), ptr(sl["y"][yk])
+            for c, zt in enumerate(sl["z"]):
+                zp[2 * q + c] = ptr(zt)
+            raw[r] = (empty((16, d)), empty((max(1, len(sl["z"])) * 4, d)))
+        zs = (C.c_int64 * np_)(*([z_stride] * np_))
+        arrs = [(C.c_void_p * np_)(*[ptr(raw[r][i]) for r in roles]) for i in range(2)]
+        call("r3_vfy_base_fold_q4", np_, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+             C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zs), comp.N, ptr(pw4), d,
+             C.addressof(arrs[0]), C.addressof(arrs[1]), stream())
+        out = {}
+        for r in roles:
+            acc_raw, z_raw = raw[r]
+            nzr = len(slots[r]["z"])
+            acc = grvec.gr_mul(acc_raw, r_acc, gr.ell, gr.mod)
+            zsum = empty((nzr, 1, d))
+            if nzr:
+                zc = grvec.gr_mul(z_raw[:4 * nzr], rpow.repeat(nzr, 1), gr.ell, gr.mod)
+                for c in range(nzr):
+                    zsum[c] = grvec.sum_axis0(zc[4 * c:4 * c + 4], gr.ell, keepdims=True)
+            h1, h2 = empty((1, d)), empty((1, d))
+            call("r3_vfy_base_fold_finish", d, nzr, ptr(acc), ptr(h1), ptr(h2), ptr(zsum), gr.mask, stream())
+            out[r] = (zsum, acc, h1, h2)
+        return out
+
+    if _joint_ok(party):
+        return party.sess.joint(("bfold4", party.next_id("_joint.bfold4")), party.role, mine, folds)
+    return folds({party.role: mine})[party.role]
+
+
 def _powsum(comps: list, stride: int, lanes: int, pw: torch.Tensor, gr: Ring) -> torch.Tensor:
     out = empty((len(comps), 1, gr.d))
     call("r3_vfy_powsum", len(comps), _ptrs(comps), stride, lanes, ptr(pw), gr.d, ptr(out),
@@ -380,17 +440,19 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     k = 0); returns dense level-1 (xs, ys, z)."""
     r = _open_challenge(party, chal.r, "vfy.r")
     n_pw = (comp.N + comp.n - 1) // comp.n
-    pw = _powers(party, r, n_pw, gr)
     zc = _components(zs, party.role)
     zc = {k: t.reshape(-1) if t.dim() == 1 else t for k, t in zc.items()}
     names = list(zc)
-    base_acc = None
+    base_acc = q4 = pw = None
     if (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
             and len(names) <= 2):
-        # one pass over the table: z power sum, level-2 accumulators and the
-        # level-1 folds derived from them
-        zsum, base_acc, h1f, h2f = _base_fold(party, comp, [zc[k] for k in names], z_stride, pw, gr)
+        # one pass over the table r^(4j): z power sum, level-2 accumulators
+        # and the level-1 folds derived from them; the full power table is
+        # never built (every later table is r^(4j) times a constant)
+        q4 = _powers4(party, r, (comp.N + 3) // 4, gr)
+        zsum, base_acc, h1f, h2f = _base_fold_q4(party, comp, [zc[k] for k in names], z_stride, q4, gr)
     else:
+        pw = _powers(party, r, n_pw, gr)
         zsum = _powsum([zc[k] for k in names], z_stride, z_lanes, pw, gr)
     z = _mval_from({k: zsum[i] for i, k in enumerate(names)}, gr, party.role)
     if R == 0:
@@ -402,7 +464,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
     z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
     if R >= 2 and gr.d >= 8:
-        return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc)
+        return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc, q4)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
     tq = 2 if comp.n == 1 else comp.n
     half = (comp.N + 1) // 2
@@ -438,7 +500,8 @@ def _l2_weights(party, ze1: torch.Tensor, gr: Ring):
 
 
 def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: torch.Tensor,
-                             z1: MVal, gr: Ring, chal: Challenges, acc: torch.Tensor | None = None):
+                             z1: MVal, gr: Ring, chal: Challenges, acc: torch.Tensor | None = None,
+                             q4=None):
     """The second Pi_rd (verify.py:215-241 at k = 1) computed from the base
     log: 16 scalar-weighted power sums per party (r3_vfy_l2_fold) replace the
     level-1 vectors and their d^2 inner products; the level-2 vectors for the
@@ -459,7 +522,10 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     h2 = _gr_dot_folded(party, gr, rows, fold(W2))
     ze2 = _open_challenge(party, chal.zetas[1].scale_pub(2), "vfy.zeta")
     z2 = _recombine(party, z1, h1, h2, _quad(party, ze2, gr), gr)
-    tabs, kappa, tq, stride = _l2_tables(party, pw, comp.n, w1, ze2, gr)
+    if q4 is not None:
+        tabs, kappa, tq, stride = _l2_tables_q4(party, q4, w1, ze2, gr)
+    else:
+        tabs, kappa, tq, stride = _l2_tables(party, pw, comp.n, w1, ze2, gr)
     geo = (comp.N, comp.n, comp.ks, comp.ls)
 
     def level2_vectors(slots):
@@ -517,6 +583,25 @@ def _l2_tables(party, pw: torch.Tensor, dot_n: int, w1, ze2: torch.Tensor, gr: R
                 M = grvec.gr_mulmat(kappa[a:a + 1], gr.mod)
                 grvec.rows_times(src, M, src.shape[0], gr.ell, out=tabs[a, :src.shape[0]])
         return tabs, kappa, (4 if dot_n == 1 else dot_n), rows * gr.d
+    return _public(party, key, build)
+
+
+def _l2_tables_q4(party, q4, w1, ze2: torch.Tensor, gr: Ring):
+    """_l2_tables for multiplication logs from the r^(4j) table:
+    V_a[j] = pw[4j + a] kappa_a = pw4[j] (r^a kappa_a)."""
+    pw4, rpow = q4
+    key = ("l2t4", gr.ell, gr.d, id(pw4), pw4.shape[0], _opened_key(party, ze2))
+
+    def build():
+        one = grvec.gr_const(1, gr.mod, gr.ell)
+        w2 = (grvec.sub(one, ze2, gr.ell), ze2)
+        kappa = torch.cat([grvec.gr_mul(w1[a & 1], w2[a >> 1], gr.ell, gr.mod) for a in range(4)])
+        rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
+        rows = pw4.shape[0]
+        tabs = grvec.zeros((4, rows, gr.d))
+        for a in range(4):
+            grvec.rows_times(pw4, grvec.gr_mulmat(rk[a:a + 1], gr.mod), rows, gr.ell, out=tabs[a])
+        return tabs, kappa, 4, rows * gr.d
     return _public(party, key, build)
 
 
