@@ -1,0 +1,303 @@
+// Base fold of a multiplication log on the tensor cores (d = 64), all
+// simulated parties in one pass over the r^(4j) table.
+//
+// The first two reductions of Pi_mulv come straight from the base log
+// (vfy2.cu): per party and block j of four elements the 16 scalar leg
+// products s^{ab}_j = sum_t c_t x_t[4j+a] y_t[4j+b] and the z values
+// z_c[4j+a] are weighted by the public row r^(4j):
+//     acc'[p][a*4+b] = sum_j s^{ab}_j r^(4j),   zraw[p][c*4+a] = sum_j z_c[4j+a] r^(4j).
+// That is ONE matrix product A^T B over the blocks j, with A's 128 columns
+// the features (party p: 32 p + q, q < 16 the s products, 16 + c*4 + a the
+// z values) and B the table rows (N = 64 coefficients), computed as the 36
+// byte-limb products of kind::i8 MMAs (12 per K-step, N-concatenated), as in
+// the level fold (lf_tc.cu).  The converter warps compute the s products
+// from the base shares and split them into limb planes; B arrives by TMA.
+// A CTA's K range is <= 16384 blocks (exact low diagonals, tc.cu).  The
+// epilogue recombines each feature row and adds it to its party's output.
+#include "tc_common.cuh"
+
+namespace r3 {
+
+constexpr int BF_BK = 32;                       // blocks j per K-step
+constexpr int BF_A_PLANE = 128 * BF_BK;         // 4 KB
+constexpr int BF_B_PLANE = 64 * BF_BK;          // 2 KB
+constexpr int BF_A_TILE = 8 * BF_A_PLANE;       // 32 KB
+constexpr int BF_B_TILE = 8 * BF_B_PLANE;       // 16 KB
+constexpr int BF_BOX = 16 * 8 * BF_BK;          // TMA box: 16 u64 x 32 rows = 4 KB
+constexpr int BF_RAW = 4 * BF_BOX;              // one K-step of table rows: 16 KB
+constexpr int BF_STAGES = 3;
+constexpr int BF_CONV = 12 * 32;                // 256 A tasks + 128 B tasks per K-step
+constexpr int BF_THREADS = 4 * 32 + BF_CONV + 2 * 32;
+constexpr int BF_OFF_LIMB = BF_STAGES * BF_RAW;
+constexpr int BF_OFF_BAR = BF_OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
+constexpr int BF_SMEM = BF_OFF_BAR + 256 + 1024;
+constexpr int64_t BF_MAX_K = 16384;
+
+struct BfParty {
+  const u64* x[3];
+  const u64* y[3];
+  const u64* z[2];
+  u64 coef[3];
+  int nterms, nz;
+  int64_t zs;
+  u64* acc;    // 16 x 64
+  u64* zraw;   // (4 nz) x 64
+};
+
+struct BfArgs {
+  CUtensorMap pw4;
+  BfParty p[3];
+  int np;
+  int64_t N, nblk, kc;
+};
+
+__device__ __forceinline__ void bf_split16(const u64 (&v)[16], uint4 (&out)[8]) {
+  uint32_t w[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    w[2 * q] = uint32_t(v[q]);
+    w[2 * q + 1] = uint32_t(v[q] >> 32);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int hiw = i >> 2, bi = i & 3;
+    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
+    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
+    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
+    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
+  }
+}
+
+__global__ void __launch_bounds__(BF_THREADS, 1)
+base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sRaw = smem;
+  uint8_t* sA = smem + BF_OFF_LIMB;
+  uint8_t* sB = sA + BF_STAGES * BF_A_TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BF_OFF_BAR);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = bars + BF_STAGES;
+  uint64_t* full = bars + 2 * BF_STAGES;
+  uint64_t* empty = bars + 3 * BF_STAGES;
+  uint64_t* tfull = bars + 4 * BF_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int64_t j0 = int64_t(blockIdx.x) * args.kc;
+  const int64_t j1 = min(args.nblk, j0 + args.kc);
+  const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < BF_STAGES; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 128);
+      mbar_init(&full[s], BF_CONV);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4 + 12) {
+    // ---------------- TMA producer: table rows j of the K-step
+    if (lane == 0) {
+      for (int64_t kb = 0; kb < nkb; ++kb) {
+        const int st = int(kb % BF_STAGES);
+        if (kb >= BF_STAGES) mbar_wait(&raw_empty[st], uint32_t((kb / BF_STAGES - 1) & 1));
+        const int y = int(j0 + kb * BF_BK);
+        mbar_expect_tx(&raw_full[st], uint32_t(BF_RAW));
+        for (int c = 0; c < 4; ++c) tma_load_2d(sRaw + st * BF_RAW + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 16) {
+    // ---------------- converters: thread = (block k of the K-step, 16-feature chunk c)
+    const int lt = threadIdx.x - 128;
+    const bool isA = lt < 256;
+    const int k = lt & 31;
+    const int c = isA ? (lt >> 5) : ((lt - 256) >> 5);
+    const int p = c >> 1, h = c & 1;
+    const bool live = isA && p < args.np;
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+      const int st = int(kb % BF_STAGES);
+      const int64_t j = j0 + kb * BF_BK + k;
+      const bool ok = j < j1;
+      u64 v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = 0;
+      if (isA) {
+        if (live && ok) {
+          const BfParty& P = args.p[p];
+          const int64_t i0 = 4 * j;
+          if (h == 0) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              if (t >= P.nterms) break;
+              u64 xv[4], yv[4];
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                const bool in = i0 + a < args.N;
+                xv[a] = in ? __ldg(P.x[t] + i0 + a) : 0ull;
+                yv[a] = in ? __ldg(P.y[t] + i0 + a) : 0ull;
+              }
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                const u64 cx = P.coef[t] * xv[a];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) v[a * 4 + b] += cx * yv[b];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int cz = 0; cz < 2; ++cz) {
+              if (cz < P.nz) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                  v[cz * 4 + a] = i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
+              }
+            }
+          }
+        }
+      } else {
+        mbar_wait(&raw_full[st], uint32_t((kb / BF_STAGES) & 1));
+        const uint8_t* row = sRaw + st * BF_RAW + c * BF_BOX + k * 128;
+        const int sw = k & 7;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(row + ((q ^ sw) << 4));
+          v[2 * q] = x.x;
+          v[2 * q + 1] = x.y;
+        }
+        fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
+        mbar_arrive(&raw_empty[st]);
+      }
+      uint4 pk[8];
+      bf_split16(v, pk);
+      if (kb >= BF_STAGES) mbar_wait(&empty[st], uint32_t((kb / BF_STAGES - 1) & 1));
+      // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
+      uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * BF_B_TILE;
+      const int plane = isA ? BF_A_PLANE : BF_B_PLANE;
+      const uint32_t off = uint32_t(c * 512 + k * 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * plane + off) = pk[i];
+      fence_async_smem();
+      mbar_arrive(&full[st]);
+    }
+  } else if (warp == 4 + 12 + 1) {
+    // ---------------- MMA issuer (as lf_tc: 12 N-concatenated limb MMAs per K-step)
+    constexpr uint32_t IDESC_M128 = idesc_u8(128, 0) | (1u << 15) | (1u << 16);
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+      const int st = int(kb % BF_STAGES);
+      mbar_wait(&full[st], uint32_t((kb / BF_STAGES) & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sA + st * BF_A_TILE);
+        const uint32_t b0 = smem_u32(sB + st * BF_B_TILE);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint64_t ad = umma_desc(a0 + i * BF_A_PLANE, 128, 512);
+#pragma unroll
+          for (int n0 = 0; n0 < 64 * (8 - i); n0 += 256) {
+            const int nn = 64 * (8 - i) - n0 < 256 ? 64 * (8 - i) - n0 : 256;
+            const uint64_t bd = umma_desc(b0 + uint32_t(n0 / 16) * 512, 128, 512);
+            mma_u8(tmem + uint32_t(i * 64 + n0), ad, bd, IDESC_M128 | (uint32_t(nn >> 3) << 17),
+                   (kb == 0 && i == 0) ? 0u : 1u);
+          }
+        }
+        mma_commit(&empty[st]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) mma_commit(tfull);
+    __syncwarp();
+  } else if (warp < 4) {
+    // ---------------- epilogue: TMEM lane f = feature (party f / 32, slot f % 32)
+    if (nkb > 0) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+      const int f = warp * 32 + lane;
+      const int p = f >> 5, q = f & 31;
+      const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
+      u64* dst = nullptr;
+      if (live) dst = q < 16 ? args.p[p].acc + q * 64 : args.p[p].zraw + (q - 16) * 64;
+      const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        uint32_t v[8][8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * 64 + c0), v[s]);
+        tmem_wait_ld();
+        if (live) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            u64 P = 0;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) P += u64(v[s][e]) << (8 * s);
+            atomicAdd(reinterpret_cast<unsigned long long*>(dst + c0 + e), (unsigned long long)P);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace r3
+
+using namespace r3;
+
+// d = 64 form of r3_vfy_base_fold_q4 (same contract); -1 if not applicable.
+int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                    int64_t N, const uint64_t* pw4, uint64_t* const* acc, uint64_t* const* zraw,
+                    cudaStream_t s) {
+  const int64_t nblk = (N + 3) / 4;
+  if (nblk < 4096 || (uintptr_t(pw4) & 15)) return -1;
+  BfArgs args{};
+  args.np = np;
+  args.N = N;
+  args.nblk = nblk;
+  for (int q = 0; q < np; ++q) {
+    BfParty& P = args.p[q];
+    P.nterms = nterms[q];
+    P.nz = nz[q];
+    P.zs = zs[q];
+    for (int t = 0; t < nterms[q]; ++t) {
+      P.x[t] = reinterpret_cast<const u64*>(xc[3 * q + t]);
+      P.y[t] = reinterpret_cast<const u64*>(yc[3 * q + t]);
+      P.coef[t] = u64(coef[3 * q + t]);
+    }
+    for (int c = 0; c < nz[q]; ++c) P.z[c] = reinterpret_cast<const u64*>(zc[2 * q + c]);
+    P.acc = reinterpret_cast<u64*>(acc[q]);
+    P.zraw = reinterpret_cast<u64*>(zraw[q]);
+  }
+  if (!make_rows_tmap(&args.pw4, pw4, nblk, 64, BF_BK, 64)) {
+    set_error("r3_vfy_base_fold_q4(tc): cuTensorMapEncodeTiled failed");
+    return R3_ERR_CUDA;
+  }
+  int64_t items = (nblk + BF_MAX_K - 1) / BF_MAX_K;
+  if (items < kNumSMs) items = kNumSMs;
+  int64_t kc = (nblk + items - 1) / items;
+  kc = (kc + BF_BK - 1) / BF_BK * BF_BK;
+  items = (nblk + kc - 1) / kc;
+  args.kc = kc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(base_fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BF_SMEM);
+    attr = true;
+  }
+  base_fold_tc_kernel<<<unsigned(items), BF_THREADS, BF_SMEM, s>>>(args);
+  return check_launch("r3_vfy_base_fold_q4(tc)");
+}

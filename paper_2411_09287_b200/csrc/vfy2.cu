@@ -485,6 +485,11 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   return check_launch("r3_vfy_line_b_const");
 }
 
+int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                    int64_t N, const uint64_t* pw4, uint64_t* const* acc, uint64_t* const* zraw,
+                    cudaStream_t s);
+
 static int base_fold_launch(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
                             const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
                             const int64_t* zs, int64_t N, const uint64_t* pw, int d, uint64_t* const* acc,
@@ -514,6 +519,11 @@ static int base_fold_launch(int np, const int* nterms, const int64_t* coef, cons
     for (int c = 0; c < nz[q]; ++c) P.zc.p[c] = reinterpret_cast<const u64*>(zc[2 * q + c]);
     P.acc_out = reinterpret_cast<u64*>(acc[q]);
     P.z_out = reinterpret_cast<u64*>(zsum[q]);
+  }
+  if (N > 0 && q4 && d == 64) {
+    // tensor-core form (bf_tc.cu) for large logs
+    int rc = base_fold_q4_tc(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, acc, zsum, s);
+    if (rc >= 0) return rc;
   }
   if (N > 0) {
     const int64_t ntiles = ((N + 3) / 4 + 31) / 32;
