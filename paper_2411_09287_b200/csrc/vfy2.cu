@@ -102,30 +102,43 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 // tables hold one row per block; tq = n for dot logs sharing a power).
 // ONE: a multiplication log (n == 1, tq == B): element i sits at i * ls and
 // the table row of block j is j -- no 64-bit divisions in the hot loop.
+// Two coefficients per thread (128-bit table loads and output stores); the
+// component loop is unrolled over the 8 slots so the pointer arrays stay in
+// registers / parameter space.
 template <int D, bool ONE>
 __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
+  constexpr int H = D / 2;
   const int64_t nblk = (N + B - 1) / B;
-  const int64_t total = nblk * D;
+  const int64_t total = nblk * H;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / D;
-    const int k = int(e - j * D);
-    u64 w[4];
+    const int64_t j = e / H;
+    const int k = 2 * int(e - j * H);
+    ulonglong2 w[4];
     int64_t off[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int64_t i = B * j + a;
       const bool ok = a < B && i < N;
       const int64_t row = ONE ? j : qdiv(i, tq);
-      w[a] = ok ? __ldg(tabs + a * tab_stride + row * D + k) : 0ull;
+      w[a] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * tab_stride + row * D + k))
+                : make_ulonglong2(0ull, 0ull);
       off[a] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
-    for (int c = 0; c < ncomp; ++c) {
-      u64 v = 0;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (off[a] >= 0) v += __ldg(xc.p[c] + off[a]) * w[a];
-      out.p[c][e] = v & mask;
+    for (int c = 0; c < 8; ++c) {
+      if (c < ncomp) {
+        u64 v0 = 0, v1 = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          if (off[a] >= 0) {
+            const u64 xv = __ldg(xc.p[c] + off[a]);
+            v0 += xv * w[a].x;
+            v1 += xv * w[a].y;
+          }
+        }
+        *reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k) = make_ulonglong2(v0 & mask, v1 & mask);
+      }
     }
   }
 }
@@ -134,26 +147,35 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
 template <int D, bool ONE>
 __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                                     const u64* __restrict__ g, Outs8 out, u64 mask) {
+  constexpr int H = D / 2;
   const int64_t nblk = (N + B - 1) / B;
-  const int64_t total = nblk * D;
+  const int64_t total = nblk * H;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / D;
-    const int k = int(e - j * D);
-    u64 gv[4];
+    const int64_t j = e / H;
+    const int k = 2 * int(e - j * H);
+    ulonglong2 gv[4];
     int64_t off[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t i = B * j + b;
       const bool ok = b < B && i < N;
-      gv[b] = ok ? __ldg(g + b * D + k) : 0ull;
+      gv[b] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(g + b * D + k)) : make_ulonglong2(0ull, 0ull);
       off[b] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
-    for (int c = 0; c < ncomp; ++c) {
-      u64 v = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (off[b] >= 0) v += __ldg(yc.p[c] + off[b]) * gv[b];
-      out.p[c][e] = v & mask;
+    for (int c = 0; c < 8; ++c) {
+      if (c < ncomp) {
+        u64 v0 = 0, v1 = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (off[b] >= 0) {
+            const u64 yv = __ldg(yc.p[c] + off[b]);
+            v0 += yv * gv[b].x;
+            v1 += yv * gv[b].y;
+          }
+        }
+        *reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k) = make_ulonglong2(v0 & mask, v1 & mask);
+      }
     }
   }
 }
@@ -447,7 +469,7 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
     xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
     op.p[c] = reinterpret_cast<u64*>(out[c]);
   }
-  const int64_t total = (N + B - 1) / B * d;
+  const int64_t total = (N + B - 1) / B * (d / 2);
   cudaStream_t s = as_stream(stream);
   if (n == 1 && tq == B) {
     R3_DISPATCH_D2(d, (line_b_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
@@ -473,7 +495,7 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
     yp.p[c] = reinterpret_cast<const u64*>(yc[c]);
     op.p[c] = reinterpret_cast<u64*>(out[c]);
   }
-  const int64_t total = (N + B - 1) / B * d;
+  const int64_t total = (N + B - 1) / B * (d / 2);
   cudaStream_t s = as_stream(stream);
   if (n == 1) {
     R3_DISPATCH_D2(d, (line_b_const_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
