@@ -244,15 +244,19 @@ def relu_rates(N: int, d: int, steps: int) -> dict:
     xh = torch.from_numpy(xv).pin_memory()
     want = np.where(xv >= 0, xv, 0)
     prog = make_relu_program(N, d)
-    out = {"N": N, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s"}
+    out = {"N": N, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s",
+           "timing": f"median of {steps} sessions after 2 warm-up sessions, wall clock incl. host"}
     for check in (False, True):
-        Session(seed=1).run(prog, xh, check)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        for w in range(2):                      # warm-up (allocator, tables)
+            Session(seed=1 + w).run(prog, xh, check)
+        times = []
         for i in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             res = Session(seed=10 + i).run(prog, xh, check)
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / steps
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        dt = statistics.median(times)
         got = res[0].cpu().numpy()
         assert np.array_equal(got, want), "relu output mismatch"
         out["verified" if check else "exec"] = N / dt
@@ -653,11 +657,11 @@ def run_b200(args):
         if args.matmul_n:
             line["matmul"] = matmul_c3(args.matmul_n, 3)
         if args.relu_log2n:
-            line["relu"] = relu_rates(1 << args.relu_log2n, 16, 2)
+            line["relu"] = relu_rates(1 << args.relu_log2n, 16, 5)
             line["relu"]["reference_cpu_measured"] = ref_cpu_measured(
                 "relu_exec_4096", "relu_exec_16384", "relu_verified_4096")
         if args.relu_sweep_log2n:
-            line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 1)
+            line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 3)
         if args.mlp_batch:
             line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
             line["mlp"]["reference_cpu_measured"] = ref_cpu_measured("mlp_exec_1", "mlp_verified_1")

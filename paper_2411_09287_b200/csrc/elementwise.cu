@@ -230,13 +230,32 @@ struct OutPtr4 {
 
 // k same-length contiguous components in one launch (blockIdx.y = component):
 // the fields of one party's share view (s1, s2, total, m) move together.
+template <typename T>
+__device__ __forceinline__ T pick4(const T (&p)[4], int c) {
+  // select without dynamic indexing (keeps the parameter arrays out of local memory)
+  return c == 0 ? p[0] : c == 1 ? p[1] : c == 2 ? p[2] : p[3];
+}
+
 template <int OP>
 __global__ void ew_multi_kernel(int64_t n, OutPtr4 out, Ptr4 a, Ptr4 b, u64 imm, u64 mask) {
   const int c = blockIdx.y;
-  const u64* __restrict__ pa = a.p[c];
-  const u64* __restrict__ pb = b.p[c];
-  u64* __restrict__ po = out.p[c];
+  const u64* __restrict__ pa = pick4(a.p, c);
+  const u64* __restrict__ pb = pick4(b.p, c);
+  u64* __restrict__ po = pick4(out.p, c);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const bool vec = ((uintptr_t(pa) | uintptr_t(pb) | uintptr_t(po)) & 15) == 0;
+  if (vec) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(pa)[i];
+      const ulonglong2 y = pb ? reinterpret_cast<const ulonglong2*>(pb)[i] : make_ulonglong2(imm, imm);
+      reinterpret_cast<ulonglong2*>(po)[i] =
+          make_ulonglong2(ew_apply(OP, x.x, y.x) & mask, ew_apply(OP, x.y, y.y) & mask);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+      po[n - 1] = ew_apply(OP, pa[n - 1], pb ? pb[n - 1] : imm) & mask;
+    return;
+  }
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     po[i] = ew_apply(OP, pa[i], pb ? pb[i] : imm) & mask;
 }

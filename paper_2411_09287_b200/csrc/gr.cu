@@ -482,7 +482,9 @@ powsum_kernel(int ncomp, CompPtrs comps, int64_t stride, int64_t lanes, const u6
     for (int c = 0; c < 8; ++c)
       if (c < ncomp) acc[c] += __ldg(comps.p[c] + l * stride) * w;
   }
-  for (int c = 0; c < ncomp; ++c) red[c][threadIdx.x] = acc[c];
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < ncomp) red[c][threadIdx.x] = acc[c];
   __syncthreads();
   if (rp == 0) {
     for (int c = 0; c < ncomp; ++c) {
@@ -558,10 +560,13 @@ __global__ void l1_line_x_kernel(int ncomp, CompPtrs xc, int64_t N, int64_t n, i
     const u64 b = has1 ? __ldg(B + qdiv64(i1, tq) * D + k) : 0ull;
     const int64_t o0 = comp_off(i0, n, ks, ls);
     const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
-    for (int c = 0; c < ncomp; ++c) {
-      u64 x0 = __ldg(xc.p[c] + o0);
-      u64 x1 = has1 ? __ldg(xc.p[c] + o1) : 0ull;
-      out.p[c][e] = (x0 * a + x1 * b) & mask;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < ncomp) {
+        u64 x0 = __ldg(xc.p[c] + o0);
+        u64 x1 = has1 ? __ldg(xc.p[c] + o1) : 0ull;
+        out.p[c][e] = (x0 * a + x1 * b) & mask;
+      }
     }
   }
 }
@@ -580,10 +585,13 @@ __global__ void l1_line_y_kernel(int ncomp, CompPtrs yc, int64_t N, int64_t n, i
     const u64 av = a[k], bv = b[k];
     const int64_t o0 = comp_off(i0, n, ks, ls);
     const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
-    for (int c = 0; c < ncomp; ++c) {
-      u64 y0 = __ldg(yc.p[c] + o0);
-      u64 y1 = has1 ? __ldg(yc.p[c] + o1) : 0ull;
-      out.p[c][e] = (y0 * av + y1 * bv) & mask;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < ncomp) {
+        u64 y0 = __ldg(yc.p[c] + o0);
+        u64 y1 = has1 ? __ldg(yc.p[c] + o1) : 0ull;
+        out.p[c][e] = (y0 * av + y1 * bv) & mask;
+      }
     }
   }
 }
