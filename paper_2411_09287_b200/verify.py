@@ -107,11 +107,27 @@ def prepare_verification(party, d: int, r_max: int = DEFAULT_R_MAX) -> None:
     ctx = {}
     for kind in CHALLENGE_KINDS:
         gr = Ring(1 if kind.endswith("bool") else party.ell, mod)
-        ctx[kind] = Challenges(
-            r=shc_random(party, 1, gr, seal=True),
-            alpha=shc_random(party, 1, gr, seal=True),
-            zetas=[shc_random(party, 1, gr, seal=True) for _ in range(r_max)])
+        ch = _sealed_block(party, 2 + r_max, gr)
+        ctx[kind] = Challenges(r=ch[0], alpha=ch[1], zetas=ch[2:])
     party.verify_ctx = ctx
+
+
+def _sealed_block(party, count: int, gr: Ring) -> list:
+    """`count` consecutive shc_random(party, 1, gr, seal=True) values
+    (sharing.py:316-321) with one keystream draw per pairwise stream: each
+    stream's offsets advance exactly as `count` single draws would (P0 "01"
+    then "02" per value, m from "12"), so every share is identical."""
+    role = party.role
+    draw = lambda pair, dom: party.prg(pair, dom).draw_gr(count, gr.ell, gr.mod)
+    if role == 0:
+        s1, s2 = draw("01", "sha"), draw("02", "sha")
+        tot = grvec.add(s1, s2, gr.ell)
+        return [MVal(AShare(gr, 0, s1=s1[k:k + 1], s2=s2[k:k + 1], total=tot[k:k + 1]), None, sealed=True)
+                for k in range(count)]
+    half = "s1" if role == 1 else "s2"
+    h = draw("01" if role == 1 else "02", "sha")
+    m = draw("12", "sha.m")
+    return [MVal(AShare(gr, role, **{half: h[k:k + 1]}), m[k:k + 1], sealed=True) for k in range(count)]
 
 
 # ---------------------------------------------------------------------------
