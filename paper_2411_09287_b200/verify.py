@@ -460,13 +460,19 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     zc = {k: t.reshape(-1) if t.dim() == 1 else t for k, t in zc.items()}
     names = list(zc)
     base_acc = q4 = pw = None
-    if (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
-            and len(names) <= 2):
-        # one pass over the table r^(4j): z power sum, level-2 accumulators
-        # and the level-1 folds derived from them; the full power table is
-        # never built (every later table is r^(4j) times a constant)
+    base_ok = (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
+               and len(names) <= 2)
+    if base_ok and gr.d == 64:
+        # one pass over the table r^(4j) on the tensor cores: z power sum,
+        # level-2 accumulators and the level-1 folds derived from them; the
+        # full power table is never built (every later table is r^(4j)
+        # times a constant)
         q4 = _powers4(party, r, (comp.N + 3) // 4, gr)
         zsum, base_acc, h1f, h2f = _base_fold_q4(party, comp, [zc[k] for k in names], z_stride, q4, gr)
+    elif base_ok:
+        # CUDA-core degrees: the same pass over the full power table
+        pw = _powers(party, r, n_pw, gr)
+        zsum, base_acc, h1f, h2f = _base_fold(party, comp, [zc[k] for k in names], z_stride, pw, gr)
     else:
         pw = _powers(party, r, n_pw, gr)
         zsum = _powsum([zc[k] for k in names], z_stride, z_lanes, pw, gr)
