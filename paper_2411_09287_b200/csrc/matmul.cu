@@ -96,9 +96,13 @@ __global__ void limb_tiles_b_kernel(const u64* __restrict__ p0, u64 c0, const u6
     split16(v, pk);
     const int64_t nb = n / MM_BN, kb = (kc * 16) / MM_BK;
     uint8_t* tile = dst + (nb * KB + kb) * MM_B_TILE;
-    const uint32_t off = core_off(int(n % MM_BN), int((kc * 16) % MM_BK), MM_BN / 8);
+    // the 8 planes stacked as one 512-row K-major matrix (row 64 j + n), so a
+    // limb MMA can take the planes B_0..B_{7-i} as one N-concatenated operand
 #pragma unroll
-    for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(tile + i * MM_B_PLANE + off) = pk[i];
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t off = core_off(i * MM_BN + int(n % MM_BN), int((kc * 16) % MM_BK), 8 * MM_BN / 8);
+      *reinterpret_cast<uint4*>(tile + off) = pk[i];
+    }
   }
 }
 
@@ -167,7 +171,6 @@ u64_gemm_tc_kernel(GemmPairs P, int64_t M, int64_t N, const u64* __restrict__ ad
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
-    constexpr uint32_t IDESC = idesc_u8(MM_BM, MM_BN);
     int stage = 0;
     uint32_t ph[MM_STAGES] = {0, 0, 0, 0};
     uint32_t tph = 0;
@@ -188,13 +191,17 @@ u64_gemm_tc_kernel(GemmPairs P, int64_t M, int64_t N, const u64* __restrict__ ad
           if (lane == 0) {
             const uint32_t a0 = smem_u32(sA + stage * MM_A_TILE);
             const uint32_t b0 = smem_u32(sB + stage * MM_B_TILE);
+            // limb plane i of A against B_0..B_{7-i} N-concatenated: column
+            // block j lands on diagonal i + j (12 MMAs per K step, not 36)
 #pragma unroll
-            for (int s = 0; s < 8; ++s) {
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t ad = umma_desc(a0 + i * MM_A_PLANE, (MM_BM / 8) * 128, 128);
 #pragma unroll
-              for (int i = 0; i <= s; ++i) {
-                const uint64_t ad = umma_desc(a0 + i * MM_A_PLANE, (MM_BM / 8) * 128, 128);
-                const uint64_t bd = umma_desc(b0 + (s - i) * MM_B_PLANE, (MM_BN / 8) * 128, 128);
-                mma_u8(tmem + uint32_t(s * MM_BN), ad, bd, IDESC, (fresh && i == 0) ? 0u : 1u);
+              for (int n0 = 0; n0 < MM_BN * (8 - i); n0 += 256) {
+                const int nn = MM_BN * (8 - i) - n0 < 256 ? MM_BN * (8 - i) - n0 : 256;
+                const uint64_t bd = umma_desc(b0 + uint32_t((n0 / 8) * 128), (8 * MM_BN / 8) * 128, 128);
+                mma_u8(tmem + uint32_t(i * MM_BN + n0), ad, bd, idesc_u8(MM_BM, nn),
+                       (fresh && i == 0) ? 0u : 1u);
               }
             }
             mma_commit(&empty[stage]);
