@@ -102,42 +102,55 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 // tables hold one row per block; tq = n for dot logs sharing a power).
 // ONE: a multiplication log (n == 1, tq == B): element i sits at i * ls and
 // the table row of block j is j -- no 64-bit divisions in the hot loop.
-// Two coefficients per thread (128-bit table loads and output stores); the
+// CPT coefficients per thread (128-bit table loads and output stores: 2 for
+// d >= 32, 4 for d = 16 so the broadcast share loads serve more output); the
 // component loop is unrolled over the 8 slots so the pointer arrays stay in
 // registers / parameter space.
+template <int D>
+__host__ __device__ constexpr int lb_cpt() { return D == 16 ? 4 : 2; }
+
 template <int D, bool ONE>
 __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
-  constexpr int H = D / 2;
+  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = e / H;
-    const int k = 2 * int(e - j * H);
-    ulonglong2 w[4];
+    const int k = CPT * int(e - j * H);
+    ulonglong2 w[4][V];
     int64_t off[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int64_t i = B * j + a;
       const bool ok = a < B && i < N;
       const int64_t row = ONE ? j : qdiv(i, tq);
-      w[a] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * tab_stride + row * D + k))
-                : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        w[a][q] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * tab_stride + row * D + k) + q)
+                     : make_ulonglong2(0ull, 0ull);
       off[a] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (c < ncomp) {
-        u64 v0 = 0, v1 = 0;
+        ulonglong2 v[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) v[q] = make_ulonglong2(0ull, 0ull);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           if (off[a] >= 0) {
             const u64 xv = __ldg(xc.p[c] + off[a]);
-            v0 += xv * w[a].x;
-            v1 += xv * w[a].y;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              v[q].x += xv * w[a][q].x;
+              v[q].y += xv * w[a][q].y;
+            }
           }
         }
-        *reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k) = make_ulonglong2(v0 & mask, v1 & mask);
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k)[q] = make_ulonglong2(v[q].x & mask, v[q].y & mask);
       }
     }
   }
@@ -147,34 +160,43 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
 template <int D, bool ONE>
 __global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                                     const u64* __restrict__ g, Outs8 out, u64 mask) {
-  constexpr int H = D / 2;
+  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = e / H;
-    const int k = 2 * int(e - j * H);
-    ulonglong2 gv[4];
+    const int k = CPT * int(e - j * H);
+    ulonglong2 gv[4][V];
     int64_t off[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t i = B * j + b;
       const bool ok = b < B && i < N;
-      gv[b] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(g + b * D + k)) : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        gv[b][q] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(g + b * D + k) + q) : make_ulonglong2(0ull, 0ull);
       off[b] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (c < ncomp) {
-        u64 v0 = 0, v1 = 0;
+        ulonglong2 v[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) v[q] = make_ulonglong2(0ull, 0ull);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           if (off[b] >= 0) {
             const u64 yv = __ldg(yc.p[c] + off[b]);
-            v0 += yv * gv[b].x;
-            v1 += yv * gv[b].y;
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              v[q].x += yv * gv[b][q].x;
+              v[q].y += yv * gv[b][q].y;
+            }
           }
         }
-        *reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k) = make_ulonglong2(v0 & mask, v1 & mask);
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k)[q] = make_ulonglong2(v[q].x & mask, v[q].y & mask);
       }
     }
   }
@@ -469,7 +491,7 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
     xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
     op.p[c] = reinterpret_cast<u64*>(out[c]);
   }
-  const int64_t total = (N + B - 1) / B * (d / 2);
+  const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
   if (n == 1 && tq == B) {
     R3_DISPATCH_D2(d, (line_b_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
@@ -495,7 +517,7 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
     yp.p[c] = reinterpret_cast<const u64*>(yc[c]);
     op.p[c] = reinterpret_cast<u64*>(out[c]);
   }
-  const int64_t total = (N + B - 1) / B * (d / 2);
+  const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
   if (n == 1) {
     R3_DISPATCH_D2(d, (line_b_const_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
