@@ -86,3 +86,25 @@ def test_model_file_roundtrip(tmp_path):
     assert [(l.kind, l.params) for l in back.layers] == [(l.kind, l.params) for l in m.layers]
     for a, b in zip(back.weights, m.weights):
         np.testing.assert_array_equal(a, b)
+
+
+def test_lane_split_of_conv_and_fc_batches():
+    """verify._FCBatch.split: lane l = a(m) + c(n) for the GEMM-form layers
+    (FC lanes m N + n; conv lanes (b, oc, p) at GEMM (b P + p, oc))."""
+    from types import SimpleNamespace
+    import torch
+    from paper_2411_09287_b200.verify import _FCBatch
+    z = SimpleNamespace(m=torch.zeros(1), mask=SimpleNamespace(total=torch.zeros(1)))
+    M, N = 6, 4
+    a, c = _FCBatch.split(SimpleNamespace(M=M, N=N, perm=None, z=z))
+    assert (a[:, None] + c[None, :]).reshape(-1).tolist() == list(range(M * N))
+    B, out, P = 3, 4, 5                        # conv: M = B P, N = out
+    lb, loc, lp = np.meshgrid(np.arange(B), np.arange(out), np.arange(P), indexing="ij")
+    perm = torch.as_tensor(((lb * P + lp) * out + loc).reshape(-1))
+    a, c = _FCBatch.split(SimpleNamespace(M=B * P, N=out, perm=perm, z=z))
+    L = (a[:, None] + c[None, :]).reshape(-1)           # lane of each GEMM index
+    assert sorted(L.tolist()) == list(range(B * out * P))
+    assert torch.equal(L[perm], torch.arange(B * out * P))
+    # a lane order that does not split additively is rejected
+    bad = torch.randperm(M * N, generator=torch.Generator().manual_seed(1))
+    assert _FCBatch.split(SimpleNamespace(M=M, N=N, perm=bad, z=z)) is None
