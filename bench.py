@@ -55,9 +55,9 @@ def parse():
     ap.add_argument("--relu-sweep-log2n", type=int, default=20)
     ap.add_argument("--matmul-n", type=int, default=4096)
     ap.add_argument("--mlp-batch", type=int, default=4096)
-    ap.add_argument("--mlp-verified-batch", type=int, default=1024)
+    ap.add_argument("--mlp-verified-batch", type=int, default=4096)
     ap.add_argument("--lenet-batch", type=int, default=1024)
-    ap.add_argument("--lenet-verified-batch", type=int, default=32)
+    ap.add_argument("--lenet-verified-batch", type=int, default=64)
     return ap.parse_args()
 
 

@@ -1063,18 +1063,33 @@ class _DenseBatch:
         self.base = _compressed_from_log(b.xs, b.ys, role, b.n)
         self.pw = pw[P:P + b.lanes]
         self.x = self.y = None
+        self.level = 0          # base-form levels: 0 (l1 folds), 1 (l2 folds from 16 accumulators)
+        self.ze1 = None
 
     def length(self) -> int:
         if self.base is not None:
-            return self.base.N
+            return (self.base.N + self.level) >> self.level if self.level else self.base.N
         return next(iter(self.x.values())).shape[0]
 
     def structured(self) -> bool:
         return self.length() % 2 == 0
 
     def folds(self, role: int, gr: Ring, party=None):
-        if self.base is not None:
+        if self.base is not None and self.level == 0:
             return _l1_folds(party, self.base, self.pw, gr)
+        if self.base is not None:
+            # level 1 from the base log: 16 scalar-weighted power sums, then
+            # the public weights of the level-1 line (vfy2.cu)
+            comp = self.base
+            terms = _role_terms(role)
+            coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+            acc = empty((16, gr.d))
+            call("r3_vfy_l2_fold", len(terms), coef, _ptrs([comp.x[t[1]] for t in terms]),
+                 _ptrs([comp.y[t[2]] for t in terms]), comp.N, comp.n, comp.ks, comp.ls, ptr(self.pw),
+                 gr.d, ptr(acc), stream())
+            W1, W2, self.w1 = _l2_weights(party, self.ze1, gr)   # ze1 is the latest opening here
+            fold = lambda W: _dotsum_terms([([(1, acc, 16)], [(1, W, 16)])], 16, gr)
+            return fold(W1), fold(W2)
         fused = _level_folds_fused(role, self.x, self.y, gr)
         if fused is not None:
             return fused
@@ -1084,24 +1099,56 @@ class _DenseBatch:
         return _level_folds(role, X, Y, "f1", rows, gr), _level_folds(role, X, Y, "f2", rows, gr)
 
     def reduce(self, Ms, gr: Ring, party=None, ze=None) -> None:
-        if self.base is not None:
-            comp = self.base
-            A, B, one_m = _line_tables(party, None, self.pw, comp.n, ze, gr)
-            half = (comp.N + 1) // 2
+        comp = self.base
+        if comp is not None and self.level == 0 and comp.N % 4 == 0 and gr.d >= 8:
+            self.ze1, self.level = ze, 1      # stay in base form for the next level
+            return
+        if comp is not None and self.level == 1:
+            # level-2 rows straight from the base shares (r3_vfy_line_b)
+            tabs, kappa, tq, stride = _l2_tables(party, self.pw, comp.n, self.w1, ze, gr)
+            nb = (comp.N + 3) // 4
             xk, yk = list(comp.x), list(comp.y)
-            self.x = {k: empty((half, gr.d)) for k in xk}
-            self.y = {k: empty((half, gr.d)) for k in yk}
-            call("r3_vfy_l1_line_x", len(xk), _ptrs([comp.x[k] for k in xk]), comp.N, comp.n, comp.ks,
-                 comp.ls, ptr(A), ptr(B), comp.n, gr.d, _ptrs([self.x[k] for k in xk]), gr.mask, stream())
-            call("r3_vfy_l1_line_y", len(yk), _ptrs([comp.y[k] for k in yk]), comp.N, comp.n, comp.ks,
-                 comp.ls, ptr(one_m), ptr(ze), gr.d, _ptrs([self.y[k] for k in yk]), gr.mask, stream())
+            self.x = {k: empty((nb, gr.d)) for k in xk}
+            self.y = {k: empty((nb, gr.d)) for k in yk}
+            geo = (comp.N, comp.n, comp.ks, comp.ls)
+            call("r3_vfy_line_b", 4, len(xk), _ptrs([comp.x[k] for k in xk]), *geo, ptr(tabs), stride, tq,
+                 gr.d, _ptrs([self.x[k] for k in xk]), gr.mask, stream())
+            call("r3_vfy_line_b_const", 4, len(yk), _ptrs([comp.y[k] for k in yk]), *geo, ptr(kappa), gr.d,
+                 _ptrs([self.y[k] for k in yk]), gr.mask, stream())
             self.base = None
+            return
+        if comp is not None:
+            self._write_level1(party, gr, ze, _line_tables(party, None, self.pw, comp.n, ze, gr))
             return
         self.x = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.x.items()}
         self.y = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.y.items()}
 
-    def materialise(self, gr: Ring):
+    def _write_level1(self, party, gr: Ring, ze, tables) -> None:
+        """Level-1 rows from the base shares and the tables r^(P+l) (1 - ze),
+        r^(P+l) ze (r3_vfy_l1_line_x / _y)."""
+        comp = self.base
+        A, B, one_m = tables
+        half = (comp.N + 1) // 2
+        xk, yk = list(comp.x), list(comp.y)
+        self.x = {k: empty((half, gr.d)) for k in xk}
+        self.y = {k: empty((half, gr.d)) for k in yk}
+        call("r3_vfy_l1_line_x", len(xk), _ptrs([comp.x[k] for k in xk]), comp.N, comp.n, comp.ks,
+             comp.ls, ptr(A), ptr(B), comp.n, gr.d, _ptrs([self.x[k] for k in xk]), gr.mask, stream())
+        call("r3_vfy_l1_line_y", len(yk), _ptrs([comp.y[k] for k in yk]), comp.N, comp.n, comp.ks,
+             comp.ls, ptr(one_m), ptr(ze), gr.d, _ptrs([self.y[k] for k in yk]), gr.mask, stream())
+        self.base = None
+
+    def materialise(self, gr: Ring, party=None):
         if self.base is not None:
+            if self.level == 1:
+                # the loop stopped between the two base levels: write level 1
+                # (tables built here, uncached: ze1 is not the latest opening)
+                one = grvec.gr_const(1, gr.mod, gr.ell)
+                one_m = grvec.sub(one, self.ze1, gr.ell)
+                A = grvec.gr_mul(self.pw, one_m, gr.ell, gr.mod)
+                B = grvec.gr_mul(self.pw, self.ze1, gr.ell, gr.mod)
+                self._write_level1(party, gr, self.ze1, (A, B, one_m))
+                return self.x, self.y
             return _materialise_dense(self.base, self.pw, gr)
         return self.x, self.y
 
@@ -1166,7 +1213,7 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
             else:
                 pt.reduce(Ms, gr)
         k += 1
-    mats = [pt.materialise(gr) for pt in parts]
+    mats = [pt.materialise(gr, party) if isinstance(pt, _DenseBatch) else pt.materialise(gr) for pt in parts]
     xs = _mval_from({c: torch.cat([m[0][c] for m in mats]) for c in mats[0][0]}, gr, role)
     ys = _mval_from({c: torch.cat([m[1][c] for m in mats]) for c in mats[0][1]}, gr, role)
     del parts, mats
