@@ -160,6 +160,7 @@ class Clocks:
 
 def make_programs(N: int, d: int, R: int):
     from paper_2411_09287_b200 import gates, verify
+    from paper_2411_09287_b200._lib import StagedInput
     from paper_2411_09287_b200.sharing import (Ring, rec, shc_input_mask, shc_input_online,
                                                shc_random)
     from paper_2411_09287_b200.transport import Phase
@@ -184,14 +185,17 @@ def make_programs(N: int, d: int, R: int):
         product opened and copied back to the host."""
         ring = Ring(64)
         party.enter_phase(Phase.PRE)
+        # owners start their input copies now (side stream), overlapping PRE
+        xs = StagedInput(xh) if party.role == 0 else None
+        ys = StagedInput(yh) if party.role == 1 else None
         xm = shc_input_mask(party, 0, N, ring)
         ym = shc_input_mask(party, 1, N, ring)
         g = gates.mul_prepare(party, xm, ym, N)
         verify.prepare_verification(party, d=d, r_max=max(R, 1))
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
-        x = shc_input_online(party, 0, xh if party.role == 0 else None, xm, N, ring, "x")
-        y = shc_input_online(party, 1, yh if party.role == 1 else None, ym, N, ring, "y")
+        x = shc_input_online(party, 0, xs, xm, N, ring, "x")
+        y = shc_input_online(party, 1, ys, ym, N, ring, "y")
         z = gates.mul_finish(party, g, x, y)
         party.round_barrier()
         party.enter_phase(Phase.POST)

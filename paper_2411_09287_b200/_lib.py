@@ -182,9 +182,39 @@ def zeros(shape, dev=None) -> torch.Tensor:
     return torch.zeros(shape, dtype=torch.int64, device=dev or device())
 
 
+_copy_streams: dict = {}
+
+
+class StagedInput:
+    """A host input whose host->device copy is started early on a side copy
+    stream (e.g. at the start of preprocessing, overlapping the copy with
+    the PRE-phase kernels); consumers on the compute stream wait on its
+    event.  Pass it wherever a host input is accepted (shc_input_online)."""
+
+    def __init__(self, host):
+        dev = device()
+        st = _copy_streams.get(dev.index)
+        if st is None:
+            st = _copy_streams[dev.index] = torch.cuda.Stream(dev)
+        if not isinstance(host, torch.Tensor):
+            host = torch.from_numpy(np.ascontiguousarray(np.asarray(host).astype(np.uint64).view(np.int64)))
+        with torch.cuda.stream(st):
+            self._t = host.to(torch.int64).to(dev, non_blocking=host.is_pinned())
+            self._event = torch.cuda.Event()
+            self._event.record(st)
+
+    def get(self) -> torch.Tensor:
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self._event)
+        self._t.record_stream(cur)
+        return self._t
+
+
 def to_device(x) -> torch.Tensor:
     """Host (numpy uint64 / python ints / CPU tensor) -> device int64 tensor.
     Device tensors pass through unchanged."""
+    if isinstance(x, StagedInput):
+        return x.get()
     if isinstance(x, torch.Tensor):
         if x.is_cuda:
             return x
