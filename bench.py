@@ -491,6 +491,21 @@ KERNEL_BOUND = {
 }
 
 
+def ncu_traffic(kernel: str) -> dict:
+    """DRAM bytes of one ncu --set full capture of the kernel against that
+    launch's algorithmic bytes (profiles/r01_traffic.json): traffic well
+    above the algorithmic bytes would mean re-reads."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            j = json.load(f)
+        k = j["r3::gr_matmul2_tc_kernel" if kernel == "r3_gr_matmul2_tc" else kernel]
+        return {"traffic": k["dram_read_bytes"] + k["dram_write_bytes"],
+                "traffic_algorithmic": k.get("algorithmic_bytes"),
+                "traffic_launch": k.get("launch"), "traffic_source": j.get("source")}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
+
+
 def hbm_peak() -> tuple[float, str]:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -652,7 +667,7 @@ def run_b200(args):
                                   f"shard, NCCL gather of opened outputs"},
         "roofline": {"bound": bound, "kernel": args.profile_kernel,
                      "achieved": achieved / scale, "peak": peak / scale, "unit": r_unit,
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, **ncu_traffic(args.profile_kernel),
                      "launches": timer.launches, "kernel_s_per_step": kt / args.steps,
                      "kernel_share_of_step": kt / secs if secs else None,
                      "peak_source": peak_src + "; " + work_desc},
