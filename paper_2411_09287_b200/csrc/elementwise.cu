@@ -7,6 +7,8 @@
 // gates._pair_sum (gates.py:41-49).  Contiguous same-shape operands take a
 // 128-bit vectorised path; anything else goes through a strided <=4-d index
 // walk (stride 0 broadcasts, mirroring numpy broadcasting in the reference).
+#include <algorithm>
+
 #include "r3_common.cuh"
 
 namespace r3 {
@@ -64,6 +66,22 @@ __global__ void ew_strided_kernel(int op, int64_t n, Shape4 sh, u64* __restrict_
     }
     u64 bv = b ? b[ob] : imm;
     out[i] = ew_apply(op, a[oa], bv) & mask;
+  }
+}
+
+// 2-D broadcast without index division: blockIdx.y = row (row-constant /
+// column-vector operands such as the edaBits weights -2^(i+1), (ell, lanes))
+__global__ void ew_2d_kernel(int op, int64_t R, int64_t L, u64* __restrict__ out, const u64* __restrict__ a,
+                             int64_t as0, int64_t as1, const u64* __restrict__ b, int64_t bs0, int64_t bs1,
+                             u64 imm, u64 mask) {
+  for (int64_t r = blockIdx.y; r < R; r += gridDim.y) {
+    const u64* ar = a + r * as0;
+    const u64* br = b ? b + r * bs0 : nullptr;
+    u64* orow = out + r * L;
+    for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < L; l += int64_t(gridDim.x) * blockDim.x) {
+      const u64 bv = br ? br[l * bs1] : imm;
+      orow[l] = ew_apply(op, ar[l * as1], bv) & mask;
+    }
   }
 }
 
@@ -200,6 +218,21 @@ extern "C" int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out, cons
     }
 #undef R3_EW_CASE
     return check_launch("r3_ew(vec)");
+  }
+  // 2-D (or 2-D after dropping leading unit dims): row-wise kernel
+  {
+    int k0 = 0;
+    while (k0 < ndim - 2 && shape[k0] == 1) ++k0;
+    if (ndim - k0 == 2) {
+      const int64_t R = shape[k0], L = shape[k0 + 1];
+      const unsigned gy = unsigned(R < 65535 ? R : 65535);
+      const int64_t want = (int64_t(kNumSMs) * 8 + gy - 1) / gy;
+      const unsigned gx = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, (L + 255) / 256)));
+      ew_2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(op, R, L, (u64*)out, (const u64*)a, a_strides[k0],
+                                                a_strides[k0 + 1], (const u64*)b, b ? b_strides[k0] : 0,
+                                                b ? b_strides[k0 + 1] : 0, imm, mask);
+      return check_launch("r3_ew(2d)");
+    }
   }
   Shape4 sh;
   for (int k = 0; k < 4; ++k) {
