@@ -23,6 +23,7 @@ def build(pkg_name: str) -> SimpleNamespace:
     transport = importlib.import_module(f"{pkg_name}.transport")
     nonlinear = importlib.import_module(f"{pkg_name}.nonlinear")
     ppml = importlib.import_module(f"{pkg_name}.ppml")
+    circuit = importlib.import_module(f"{pkg_name}.circuit")
     Ring, MVal = sharing.Ring, sharing.MVal
     Phase = transport.Phase
     shc_random, shc_input, rec = sharing.shc_random, sharing.shc_input, sharing.rec
@@ -403,7 +404,14 @@ def build(pkg_name: str) -> SimpleNamespace:
         scores, verdicts = ppml.infer_batch(party, model, imgs, ppml.InferConfig(d=d, check=check))
         return {"scores": scores, "verdicts": verdicts}
 
-    return SimpleNamespace(matmul_gemm=matmul_gemm, mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
+    def circ(party, name, d=16, R=1, check=True):
+        """tests/test_circuit.py:41-110: circuit.evaluate over a named text
+        circuit (CIRCUITS below) with its plaintext inputs."""
+        text, values = CIRCUITS[name]
+        outs, verdicts = circuit.evaluate(party, circuit.parse(text), values, d, R, check)
+        return {"outputs": np.array(outs, dtype=np.uint64), "verdicts": verdicts}
+
+    return SimpleNamespace(circ=circ, matmul_gemm=matmul_gemm, mulv=mulv, mul_inputs=mul_inputs, bool_mulv=bool_mulv,
                            trunc=trunc, trunc_verify=trunc_verify, dotv=dotv, relu=relu,
                            a2b_roundtrip=a2b_roundtrip, matmul=matmul, infer1=infer1,
                            infer_batch_gathered=infer_batch_gathered, infer_batch=infer_batch)
@@ -430,6 +438,95 @@ def _mat_inputs(M, K, N, seed):
     X = np.trunc(rng.normal(0, 1, (M, K)) * 2 ** 16).astype(np.int64).astype(np.uint64)
     W = np.trunc(rng.normal(0, 1 / 8, (K, N)) * 2 ** 16).astype(np.int64).astype(np.uint64)
     return X, W
+
+
+def _fx(v, k=8):
+    return int(v * 2 ** k) % 2 ** 64
+
+
+def random_circuit(seed: int, n_gates: int = 14, k: int = 8):
+    """Seeded random circuit over every gate kind: products feed TRUNC, and
+    RELU / MAXPOOL outputs feed later products, so those products get their
+    masks online.  Linear gates only read wires whose mask is known offline
+    (the reference's offline pass cannot propagate an online-only mask
+    through ADD / SUB / SCALE, circuit.py:176-184), and stacked operand
+    lists start with a truncation output when they hold one (the
+    reference stacks the first mask's fields, nonlinear.py:248-259, and a
+    truncation output's P0 view is sum-only)."""
+    rng = np.random.default_rng(seed)
+    lines, values, wires, wid = [], {}, [], 0
+    online_mask = set()                       # wires whose mask is set online
+    truncs = set()                            # sum-only P0 view: truncation lineage
+    sparse_first = lambda ids: sorted(ids, key=lambda w: w not in truncs)
+    for _ in range(3):
+        lines.append(f"INPUT {wid} {int(rng.integers(0, 3))}")
+        values[wid] = _fx(float(rng.normal(0, 2)), k)
+        wires.append(wid)
+        wid += 1
+    lines.append(f"CONST {wid} {_fx(0.5, k)}")
+    wires.append(wid)
+    wid += 1
+    for _ in range(n_gates):
+        op = str(rng.choice(["ADD", "SUB", "MULT", "DOTT", "SCALE", "RELU", "MAXPOOL"]))
+        pick = lambda n: [int(x) for x in rng.choice(wires, size=n)]
+        offline = [w for w in wires if w not in online_mask]
+        pick_off = lambda n: [int(x) for x in rng.choice(offline, size=n)]
+        if op in ("ADD", "SUB"):
+            a, b = pick_off(2)
+            lines.append(f"{op} {wid} {a} {b}")
+            if a in truncs or b in truncs:
+                truncs.add(wid)
+        elif op == "SCALE":
+            a = pick_off(1)[0]
+            lines.append(f"SCALE {wid} {int(rng.integers(-3, 4)) % 2 ** 64} {a}")
+            if a in truncs:
+                truncs.add(wid)
+        elif op == "RELU":
+            a = pick(1)[0]
+            lines.append(f"RELU {wid} {a}")
+            online_mask.add(wid)
+            if a in truncs:
+                truncs.add(wid)
+        elif op == "MAXPOOL":
+            n = int(rng.integers(2, 5))
+            ids = sparse_first(pick(n))
+            lines.append(f"MAXPOOL {wid} {n} " + " ".join(map(str, ids)))
+            online_mask.add(wid)
+            if ids[0] in truncs:
+                truncs.add(wid)
+        else:                                   # product then truncation
+            if op == "MULT":
+                a, b = pick(2)
+                lines.append(f"MUL {wid} {a} {b}")
+            else:
+                n = int(rng.integers(1, 4))
+                ids = sparse_first(pick(n)) + sparse_first(pick(n))
+                lines.append(f"DOT {wid} {n} " + " ".join(map(str, ids)))
+            wid += 1
+            lines.append(f"TRUNC {wid} {wid - 1} {k}")
+            truncs.add(wid)
+        wires.append(wid)
+        wid += 1
+    for w in sorted({wires[-1]} | {int(x) for x in rng.choice(wires[4:], size=3)}):
+        lines.append(f"OUTPUT {w}")
+    return "\n".join(lines), values
+
+
+CIRCUITS = {
+    # tests/test_circuit.py:41-57
+    "mixed": ("INPUT 0 0\nINPUT 1 1\nINPUT 2 2\nCONST 3 11\nMUL 4 0 1\nADD 5 4 2\nSUB 6 5 3\n"
+              "SCALE 7 3 6\nDOT 8 2 4 5 6 7\nOUTPUT 7\nOUTPUT 8", {0: 3, 1: 5, 2: 9}),
+    # tests/test_circuit.py:92-110
+    "trunc_relu_pool": ("INPUT 0 0\nINPUT 1 1\nMUL 2 0 1\nTRUNC 3 2 8\nRELU 4 3\n"
+                        "MAXPOOL 5 2 3 4\nOUTPUT 4\nOUTPUT 5", {0: _fx(-1.5), 1: _fx(2.0)}),
+    # deferred masks: products whose inputs come out of RELU / MAXPOOL
+    "deferred": ("INPUT 0 2\nINPUT 1 1\nRELU 2 0\nMUL 3 2 1\nTRUNC 4 3 8\nMAXPOOL 5 3 4 0 1\n"
+                 "DOT 6 2 5 2 1 0\nSCALE 7 0xffffffffffffffff 1\nOUTPUT 4\nOUTPUT 6\nOUTPUT 7",
+                 {0: _fx(1.25), 1: _fx(-0.75)}),
+    "add_only": ("INPUT 0 0\nINPUT 1 1\nADD 2 0 1\nOUTPUT 2", {0: 1, 1: 2}),
+    "random_a": random_circuit(101),
+    "random_b": random_circuit(202, n_gates=20),
+}
 
 
 CASES = [
@@ -461,6 +558,16 @@ CASES = [
     ("infer_batch_conv_tiny_b2", "infer_batch_gathered", ("conv_tiny", 9, 2), {}, {"seed": 9}),
 ]
 
+CASES += [
+    ("circ_mixed", "circ", ("mixed",), {}, {"seed": 31}),
+    ("circ_trunc_relu_pool", "circ", ("trunc_relu_pool",), {}, {"seed": 32}),
+    ("circ_deferred_d64", "circ", ("deferred",), {"d": 64, "R": "auto"}, {"seed": 33}),
+    ("circ_add_only_R0", "circ", ("add_only",), {"R": 0}, {"seed": 34}),
+    ("circ_random_a", "circ", ("random_a",), {}, {"seed": 35}),
+    ("circ_random_b_nocheck", "circ", ("random_b",), {"check": False}, {"seed": 36}),
+    ("circ_mixed_ell32", "circ", ("mixed",), {"R": 2}, {"seed": 37, "ell": 32}),
+]
+
 # Tamper cases: (name, program, args, injections[(site, who, delta, gate, lane)])
 TAMPER_CASES = [
     ("tamper_gamma", "mulv", (16, 16, 2), ("gamma", 0, 5, 0, 3), {"seed": 1000}),
@@ -468,5 +575,6 @@ TAMPER_CASES = [
     ("tamper_mz", "mulv", (16, 16, 2), ("mz", 1, 1, 0, 2), {"seed": 1002}),
     ("tamper_z_msb", "mulv", (64, 16, 2), ("z", 2, 1 << 63, 0, 5), {"seed": 1003}),
     ("tamper_mz_rec_abort", "mul_inputs", ([3], [4]), ("mz", 1, 1, 0, None), {"seed": 0}),
+    ("tamper_circ_gamma", "circ", ("mixed",), ("gamma", 0, 1, 0, None), {"seed": 38}),
     ("tamper_vfy_gamma", "mulv", (64, 16, 3), ("vfy.dot.gamma", 0, 11, 2, 0), {"seed": 1004}),
 ]

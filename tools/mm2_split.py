@@ -39,3 +39,5 @@ for single in (True, False):
           f"{ms:7.2f} ms {nb / ms / 1e6 if ms else 0:7.0f} GB/s")
     big = sorted(sel, reverse=True)[:3]
     print("   largest:", [(r, round(t, 3)) for r, t in big])
+    small = [(r, t) for r, t in sel if r < 148 * 128]
+    print(f"   launches under one wave: {len(small)} calls, {sum(t for _, t in small):.2f} ms")
