@@ -6,7 +6,7 @@ CUDA context); prints one JSON line with misses, the control acceptance rate
 and wall-clock seconds (the reference's bar: <= 30 misses per mode, control
 0.50 +/- 0.05, under 300 s).
 
-    python tools/soundness_mc.py [--trials 1000] [--workers 8]
+    python tools/soundness_mc.py [--trials 1000] [--workers 4]
 """
 
 import argparse
@@ -38,7 +38,7 @@ def _chunk(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--trials", type=int, default=1000)
-    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--workers", type=int, default=4)
     a = ap.parse_args()
     step = max(1, a.trials // (4 * a.workers))
     jobs = [(m, lo, min(lo + step, a.trials)) for m in ("random", "msb", "gamma", "mz", "control")
