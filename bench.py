@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--relu-sweep-log2n", type=int, default=20)
+    ap.add_argument("--mulv-sweep", default="20,22,26",
+                    help="comma list of log2 batch sizes for the config-2 sweep on one GPU ('' = off)")
     ap.add_argument("--matmul-n", type=int, default=4096)
     ap.add_argument("--mlp-batch", type=int, default=4096)
     ap.add_argument("--mlp-verified-batch", type=int, default=4096)
@@ -265,6 +267,43 @@ def relu_rates(N: int, d: int, steps: int) -> dict:
         assert np.array_equal(got, want), "relu output mismatch"
         out["verified" if check else "exec"] = N / dt
         out[("verified" if check else "exec") + "_ms"] = dt * 1e3
+    return out
+
+
+def mulv_sweep(sizes, d: int, steps: int = 3) -> dict:
+    """Config 2's sweep on one GPU: verified mults/s per batch size (same
+    program as the headline, R = pick_r), median of `steps` sessions after
+    one warm-up, with the peak device memory; a size that does not fit in
+    HBM is reported as such (2^28 is meant for 8 GPUs: 2^25 per rank)."""
+    import torch
+    from paper_2411_09287_b200 import verify
+    from paper_2411_09287_b200.runtime import Session
+    out = {"unit": UNIT, "d": d, "timing": f"median of {steps} sessions after 1 warm-up, wall clock incl. host",
+           "points": []}
+    for lg in sizes:
+        N = 1 << lg
+        R = verify.pick_r(N, 64, d)
+        prog, _ = make_programs(N, d, R)
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        try:
+            Session(seed=1).run(prog)
+            times = []
+            for i in range(steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ok = Session(seed=2 + i).run(prog)
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+            assert all(ok), "honest mulv rejected"
+        except torch.OutOfMemoryError:
+            out["points"].append({"log2n": lg, "R": R, "fits": False})
+            torch.cuda.empty_cache()
+            continue
+        dt = statistics.median(times)
+        out["points"].append({"log2n": lg, "R": R, "value": N / dt, "ms": dt * 1e3,
+                              "peak_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
+    torch.cuda.empty_cache()
     return out
 
 
@@ -688,6 +727,8 @@ def run_b200(args):
                 "relu_exec_4096", "relu_exec_16384", "relu_verified_4096")
         if args.relu_sweep_log2n:
             line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 3)
+        if args.mulv_sweep:
+            line["mulv_sweep"] = mulv_sweep([int(v) for v in args.mulv_sweep.split(",")], d)
         if args.mlp_batch:
             line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
             line["mlp"]["reference_cpu_measured"] = ref_cpu_measured("mlp_exec_1", "mlp_verified_1")

@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libr3b200.so")
+# R3B200_LIB: load an alternative in-tree build (A/B kernel experiments)
+LIB_PATH = os.environ.get("R3B200_LIB") or os.path.join(_HERE, "libr3b200.so")
 
 _lock = threading.Lock()
 _lib = None

@@ -215,12 +215,8 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
         tmem_wait_ld();
         u64 acc[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          u64 a = 0;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) a += u64(v[s][q]) << (8 * s);
-          acc[q] = a & mask;
-        }
+        for (int q = 0; q < 8; ++q)
+          acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
         if (row < rows) {
           ulonglong2* o = reinterpret_cast<ulonglong2*>(out + row * TC_D + c0);
 #pragma unroll

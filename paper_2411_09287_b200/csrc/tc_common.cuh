@@ -89,6 +89,27 @@ __device__ __forceinline__ uint32_t gather_byte(uint32_t x0, uint32_t x1, uint32
   return __byte_perm(lo, hi, 0x5410);
 }
 
+// sum_s d[s] 2^(8 s) mod 2^64 for the 8 diagonal accumulators of one output,
+// in 32-bit halves: diagonals 0-3 straddle the word boundary (one carry
+// chain), diagonals 4-7 only reach the high word.
+__device__ __forceinline__ uint64_t recombine8(const uint32_t d0, const uint32_t d1, const uint32_t d2,
+                                               const uint32_t d3, const uint32_t d4, const uint32_t d5,
+                                               const uint32_t d6, const uint32_t d7) {
+  uint32_t lo, hi;
+  asm("{\n\t"
+      "add.cc.u32 %0, %2, %3;\n\t"
+      "addc.u32 %1, %4, 0;\n\t"
+      "add.cc.u32 %0, %0, %5;\n\t"
+      "addc.u32 %1, %1, %6;\n\t"
+      "add.cc.u32 %0, %0, %7;\n\t"
+      "addc.u32 %1, %1, %8;\n\t"
+      "}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(d0), "r"(d1 << 8), "r"(d1 >> 24), "r"(d2 << 16), "r"(d2 >> 16), "r"(d3 << 24), "r"(d3 >> 8));
+  hi += d4 + (d5 << 8) + (d6 << 16) + (d7 << 24);
+  return (uint64_t(hi) << 32) | lo;
+}
+
 // core-matrix byte offset of (row, k) in a K-major no-swizzle tile with G row groups
 __device__ __forceinline__ uint32_t core_off(int row, int k, int G) {
   return uint32_t((((k >> 4) * G + (row >> 3)) << 7) + ((row & 7) << 4) + (k & 15));
