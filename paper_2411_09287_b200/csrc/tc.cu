@@ -12,9 +12,9 @@
 // r3_gr_matmul2_tc: out[r] = P0[r] . M0 (+ P1[r] . M1) for GR(2^64, 64) rows
 // -- the "many elements times one public element" contraction of the
 // verification (line evaluations f0 (1 - zeta) + f1 zeta, power tables).
-// M = 64 x 64, so K = N = 64: per 128-row tile and operand 24 MMAs (the 36
-// limb products of both K-halves, N-concatenated) into 8 x 64 TMEM columns
-// (the full 512-column TMEM).
+// M = 64 x 64, so K = N = 64: per 128-row tile, operand and output-column
+// half 16 MMAs (the 36 limb products of both K-halves, N-concatenated) into
+// 8 x 32 TMEM columns; the two halves double-buffer the 512-column TMEM.
 //
 // smem operands use the canonical K-major no-swizzle layout: 8-row x 16-byte
 // core matrices, core (g, kc) at (kc * G + g) * 128 bytes (G = rows / 8), so
@@ -27,75 +27,92 @@ constexpr int TC_D = 64;            // GR degree = K = N of one limb product
 constexpr int TC_KH = 32;           // K per unit (one MMA K-step of kind::i8)
 
 // ---------------------------------------------------------------------------
-// Pipelined form: out = P0 . M0 (+ P1 . M1).  A unit is (tile of 128 rows,
-// operand, K-half): 128 x 32 u64 = 32 KB of HBM, moved by two TMA tile loads
-// (16 u64 x 128 rows each, 128-byte swizzle so the converters read it
-// bank-conflict free) into a raw stage, split into 8 byte-limb planes
-// (128 x 32 B, K-major no-swizzle core matrices) by the converter warps, and
-// consumed by 12 MMAs: limb plane i of A times the N-concatenated limb planes
-// [B_0 .. B_{7-i}] of the public matrix (N = 64 (8 - i), split at 256), whose
-// column block j lands on diagonal i + j of the TMEM accumulator (diagonal s
-// at columns 64 s).  Each A plane is read by the tensor core once per unit
-// instead of once per (i, j) limb product.
-//   warps 0-3   epilogue: TMEM diagonals -> u64 recombination -> global
-//   warps 4-11  converters: raw stage -> limb planes
-//   warp 12     TMA producer (one elected lane)
-//   warp 13     MMA issuer (one elected lane)
+// out = P0 . M0 (+ P1 . M1).  A unit is (tile of 128 rows, operand, K-half):
+// 128 x 32 u64 = 32 KB of HBM, moved by two TMA tile loads (16 u64 x 128
+// rows each, 128-byte swizzle so the converters read it bank-conflict
+// free), split into 8 byte-limb planes (128 x 32 B, K-major no-swizzle core
+// matrices) by the converter warps, and consumed by MMAs that multiply limb
+// plane i of A by the N-concatenated limb planes [B_0 .. B_{7-i}] of the
+// public matrix, whose column block j lands on diagonal i + j of the TMEM
+// accumulator.  Each A plane is read by the tensor core once per unit and
+// output half instead of once per (i, j) limb product.
 // ---------------------------------------------------------------------------
 constexpr int W_EPI = 4, W_CONV = 8;
 constexpr int WS_THREADS = (W_EPI + W_CONV + 2) * 32;
-constexpr int RAW_STAGES = 3, LIMB_STAGES = 2;
 constexpr int RAW_BYTES = TC_ROWS * TC_KH * 8;           // 32 KB
 constexpr int LIMB_PLANE = TC_ROWS * TC_KH;              // 4 KB
-constexpr int LIMB_BYTES = 8 * LIMB_PLANE;               // 32 KB
 constexpr int BALL_ROWS = 8 * TC_D;                      // 512 = 8 limb planes of N
 constexpr int BALL_BYTES = BALL_ROWS * TC_D;             // 32 KB per operand
-constexpr int OFF_LIMB = RAW_STAGES * RAW_BYTES;
-constexpr int OFF_B = OFF_LIMB + LIMB_STAGES * LIMB_BYTES;
-constexpr int OFF_BAR = OFF_B + 2 * BALL_BYTES;
-constexpr int WS_SMEM = OFF_BAR + 128 + 1024;            // + alignment slack
+
+// ---------------------------------------------------------------------------
+// Double-buffered TMEM.  The accumulators of a 128 x 64 output tile would
+// fill all 512 TMEM columns, so the epilogue (bound by TMEM reads: 256 KB
+// per tile) and the next tile's MMAs would run one after the other.  A tile
+// is computed as two column halves (output columns 32 h .. 32 h + 31),
+// each with its own 256-column accumulator (diagonal s at 256 h + 32 s): the
+// epilogue drains half 0 while the MMAs of half 1 run, and half 1 while the
+// next tile's half 0 runs.  Both halves read the same limb planes, so a
+// tile's units stay resident until its half-1 MMAs: each stage is converted
+// IN PLACE (raw rows -> registers, converter barrier, limb planes written
+// over the raw bytes), which gives 5 stages of 32 KB in the shared memory
+// the raw + limb stages used before, and a stage is released unit by unit
+// as half 1 consumes it, so the next tile's loads start early.
+// B_all rows are ordered n' = 256 h + 32 j + (n mod 32) (half h, limb j) so
+// one half's N-concatenated limb planes are contiguous: 8 MMAs of
+// N = 32 (8 - i) per unit and half.
+//   warps 0-3   epilogue       warps 4-11  converters
+//   warp 12     TMA producer   warp 13     MMA issuer
+// ---------------------------------------------------------------------------
+constexpr int DB_STAGES = 5;
+constexpr int DB_OFF_B = DB_STAGES * RAW_BYTES;
+constexpr int DB_OFF_BAR = DB_OFF_B + 2 * BALL_BYTES;
+constexpr int DB_SMEM = DB_OFF_BAR + 256 + 1024;
+constexpr int DB_HALF = TC_D / 2;                        // output columns per half
+
+__device__ __forceinline__ void conv_named_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(W_CONV * 32) : "memory");
+}
 
 __global__ void __launch_bounds__(WS_THREADS, 1)
-gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
                      int nops, const u64* __restrict__ M0, const u64* __restrict__ M1, u64* __restrict__ out,
                      int64_t rows, u64 mask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sRaw = smem;
-  uint8_t* sLimb = smem + OFF_LIMB;
-  uint8_t* sB = smem + OFF_B;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* raw_full = bars;                       // [3] TMA -> converters
-  uint64_t* raw_empty = bars + 3;                  // [3] converters -> TMA
-  uint64_t* limb_full = bars + 6;                  // [2] converters -> MMA
-  uint64_t* limb_empty = bars + 8;                 // [2] MMA -> converters
-  uint64_t* tfull = bars + 10;                     // MMA -> epilogue
-  uint64_t* tempty = bars + 11;                    // epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint8_t* sStage = smem;
+  uint8_t* sB = smem + DB_OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DB_OFF_BAR);
+  uint64_t* raw_full = bars;                       // [S] TMA -> converters
+  uint64_t* limb_full = bars + DB_STAGES;          // [S] converters -> MMA
+  uint64_t* empty = bars + 2 * DB_STAGES;          // [S] MMA (half 1) -> TMA
+  uint64_t* tfull = bars + 3 * DB_STAGES;          // [2] MMA -> epilogue, per half
+  uint64_t* tempty = tfull + 2;                    // [2] epilogue -> MMA, per half
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // B_all[op]: row n' = 64 j + n holds limb j of column n of M (K = 64 bytes)
+  // B_all[op]: row 256 h + 32 j + c holds limb j of column 32 h + c of M
   for (int op = 0; op < nops; ++op) {
     const u64* M = op ? M1 : M0;
     uint8_t* dst = sB + op * BALL_BYTES;
     for (int e = tid; e < TC_D * TC_D; e += WS_THREADS) {
       const int k = e / TC_D, n = e % TC_D;
+      const int h = n / DB_HALF, c = n % DB_HALF;
       const u64 v = M[e];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) dst[core_off(j * TC_D + n, k, BALL_ROWS / 8)] = uint8_t(v >> (8 * j));
+      for (int j = 0; j < 8; ++j)
+        dst[core_off(256 * h + DB_HALF * j + c, k, BALL_ROWS / 8)] = uint8_t(v >> (8 * j));
     }
   }
   if (tid == 0) {
-    for (int i = 0; i < RAW_STAGES; ++i) {
+    for (int i = 0; i < DB_STAGES; ++i) {
       mbar_init(&raw_full[i], 1);
-      mbar_init(&raw_empty[i], W_CONV * 32);
-    }
-    for (int i = 0; i < LIMB_STAGES; ++i) {
       mbar_init(&limb_full[i], W_CONV * 32);
-      mbar_init(&limb_empty[i], 1);
+      mbar_init(&empty[i], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, W_EPI * 32);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);
+      mbar_init(&tempty[h], W_EPI * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -109,18 +126,19 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t nunits = my_tiles * nops * 2;
+  const int upt = 2 * nops;                        // units per tile: (operand, K-half)
+  const int64_t nunits = my_tiles * upt;
 
   if (warp == W_EPI + W_CONV) {
     // ------------------------------ TMA producer
     if (lane == 0) {
-      for (int64_t u = 0; u < nunits; ++u) {
-        const int st = int(u % RAW_STAGES);
-        if (u >= RAW_STAGES) mbar_wait(&raw_empty[st], uint32_t((u / RAW_STAGES - 1) & 1));
-        const int64_t t = blockIdx.x + (u / (2 * nops)) * gridDim.x;
-        const int op = int((u >> 1) % nops), h = int(u & 1);
+      for (int64_t g = 0; g < nunits; ++g) {
+        const int st = int(g % DB_STAGES);
+        if (g >= DB_STAGES) mbar_wait(&empty[st], uint32_t((g / DB_STAGES - 1) & 1));
+        const int64_t t = blockIdx.x + (g / upt) * gridDim.x;
+        const int op = int((g >> 1) % nops), h = int(g & 1);
         const CUtensorMap* map = op ? &tm1 : &tm0;
-        uint8_t* dst = sRaw + st * RAW_BYTES;
+        uint8_t* dst = sStage + st * RAW_BYTES;
         mbar_expect_tx(&raw_full[st], RAW_BYTES);
         tma_load_2d(dst, map, h * TC_KH, int(t * TC_ROWS), &raw_full[st]);
         tma_load_2d(dst + RAW_BYTES / 2, map, h * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
@@ -128,14 +146,15 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
     }
     __syncwarp();
   } else if (warp >= W_EPI && warp < W_EPI + W_CONV) {
-    // ------------------------------ converters: thread = (row r, 16-u64 box c)
+    // ------------------------------ converters (in place): thread = (row r, box c)
     const int ct = tid - W_EPI * 32;
     const int r = ct & (TC_ROWS - 1), c = ct >> 7;
     const int sw = r & 7;
-    for (int64_t u = 0; u < nunits; ++u) {
-      const int st = int(u % RAW_STAGES), ls = int(u % LIMB_STAGES);
-      mbar_wait(&raw_full[st], uint32_t((u / RAW_STAGES) & 1));
-      const uint8_t* src = sRaw + st * RAW_BYTES + c * (RAW_BYTES / 2) + r * 128;
+    for (int64_t g = 0; g < nunits; ++g) {
+      const int st = int(g % DB_STAGES);
+      mbar_wait(&raw_full[st], uint32_t((g / DB_STAGES) & 1));
+      uint8_t* stage = sStage + st * RAW_BYTES;
+      const uint8_t* src = stage + c * (RAW_BYTES / 2) + r * 128;
       uint32_t x[32];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -145,10 +164,8 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
         x[4 * q + 2] = v.z;
         x[4 * q + 3] = v.w;
       }
-      fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
-      mbar_arrive(&raw_empty[st]);
-      if (u >= LIMB_STAGES) mbar_wait(&limb_empty[ls], uint32_t((u / LIMB_STAGES - 1) & 1));
-      uint8_t* dst = sLimb + ls * LIMB_BYTES + core_off(r, c * 16, TC_ROWS / 8);
+      conv_named_sync();    // every raw row of the stage is in registers before any limb write
+      uint8_t* dst = stage + core_off(r, c * 16, TC_ROWS / 8);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int hiw = i >> 2, bi = i & 3;
@@ -159,72 +176,78 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
         pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
         *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk;
       }
-      fence_async_smem();
-      mbar_arrive(&limb_full[ls]);
+      fence_async_smem();   // generic limb writes -> tensor-core (async proxy) reads
+      mbar_arrive(&limb_full[st]);
     }
   } else if (warp == W_EPI + W_CONV + 1) {
     // ------------------------------ MMA issuer
-    uint32_t tphase = 0;
-    for (int64_t u = 0; u < nunits; ++u) {
-      const int ls = int(u % LIMB_STAGES);
-      const int op = int((u >> 1) % nops), h = int(u & 1);
-      const bool tile_first = (u % (2 * nops)) == 0;
-      const bool tile_last = (u % (2 * nops)) == 2 * nops - 1;
-      if (tile_first && u > 0) {
-        mbar_wait(tempty, tphase);
-        tphase ^= 1;
-      }
-      mbar_wait(&limb_full[ls], uint32_t((u / LIMB_STAGES) & 1));
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(sLimb + ls * LIMB_BYTES);
-        // K-half h = core columns 2h, 2h+1 of B_all (LBO = 64 groups x 128 B)
-        const uint32_t b0 = smem_u32(sB + op * BALL_BYTES) + uint32_t(2 * h * (BALL_ROWS / 8) * 128);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint64_t ad = umma_desc(a0 + i * LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
-          const int ncols = TC_D * (8 - i);
-#pragma unroll
-          for (int n0 = 0; n0 < ncols; n0 += 256) {
-            const int nn = ncols - n0 < 256 ? ncols - n0 : 256;
-            const uint64_t bd = umma_desc(b0 + uint32_t((n0 / 8) * 128), (BALL_ROWS / 8) * 128, 128);
-            const bool acc = !(tile_first && i == 0);
-            mma_u8(tmem + uint32_t(TC_D * i + n0), ad, bd, idesc_u8(TC_ROWS, nn), acc ? 1u : 0u);
-          }
+    uint32_t tph[2] = {0, 0};
+    for (int64_t g0 = 0; g0 < nunits; g0 += upt) {
+      for (int h = 0; h < 2; ++h) {
+        if (g0 > 0) {
+          mbar_wait(&tempty[h], tph[h]);
+          tph[h] ^= 1;
         }
-        mma_commit(&limb_empty[ls]);
-        if (tile_last) mma_commit(tfull);
+        for (int uu = 0; uu < upt; ++uu) {
+          const int64_t g = g0 + uu;
+          const int st = int(g % DB_STAGES);
+          const int op = uu >> 1, kh = uu & 1;
+          if (h == 0) mbar_wait(&limb_full[st], uint32_t((g / DB_STAGES) & 1));
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sStage + st * RAW_BYTES);
+            // K-half kh = core columns 2 kh, 2 kh + 1; half h = row groups 32 h ..
+            const uint32_t b0 = smem_u32(sB + op * BALL_BYTES) +
+                                uint32_t((2 * kh * (BALL_ROWS / 8) + 32 * h) * 128);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t ad = umma_desc(a0 + i * LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
+              const uint64_t bd = umma_desc(b0, (BALL_ROWS / 8) * 128, 128);
+              const bool acc = !(uu == 0 && i == 0);
+              mma_u8(tmem + uint32_t(256 * h + DB_HALF * i), ad, bd, idesc_u8(TC_ROWS, DB_HALF * (8 - i)),
+                     acc ? 1u : 0u);
+            }
+            if (h == 1) mma_commit(&empty[st]);
+            if (uu == upt - 1) mma_commit(&tfull[h]);
+          }
+          __syncwarp();
+        }
       }
-      __syncwarp();
     }
   } else if (warp < W_EPI) {
     // ------------------------------ epilogue: warp e reads TMEM lane quadrant e
-    uint32_t phase = 0;
+    // (16-lane x 8-column loads: 4 threads per row, so every store writes
+    // 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes)
+    uint32_t ph[2] = {0, 0};
     const int quad = warp & 3;
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(tfull, phase);
-      phase ^= 1;
-      tc_fence_after();
-      const int64_t row = t * TC_ROWS + quad * 32 + lane;
-      const uint32_t lane_base = tmem + (uint32_t(quad * 32) << 16);
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait(&tfull[h], ph[h]);
+        ph[h] ^= 1;
+        tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < TC_D; c0 += 8) {
-        uint32_t v[8][8];
+        for (int it = 0; it < 2 * (DB_HALF / 8); ++it) {
+          const int lg = it & 1, c0 = 8 * (it >> 1);
+          const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * h + c0);
+          uint32_t v[8][4];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * TC_D + c0), v[s]);
-        tmem_wait_ld();
-        u64 acc[8];
+          for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(DB_HALF * s), v[s]);
+          tmem_wait_ld();
+          u64 acc[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
-        if (row < rows) {
-          ulonglong2* o = reinterpret_cast<ulonglong2*>(out + row * TC_D + c0);
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) o[q >> 1] = make_ulonglong2(acc[q], acc[q + 1]);
+          for (int q = 0; q < 4; ++q)
+            acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
+          const int64_t row = t * TC_ROWS + quad * 32 + lg * 16 + rq;
+          const int col = DB_HALF * h + c0 + cq;
+          if (row < rows)
+            *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
+          if (row + 8 < rows)
+            *reinterpret_cast<ulonglong2*>(out + (row + 8) * TC_D + col) = make_ulonglong2(acc[2], acc[3]);
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[h]);
       }
-      tc_fence_before();
-      mbar_arrive(tempty);
     }
   }
   tc_fence_before();
@@ -238,7 +261,8 @@ gr_matmul2_tc_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
 // operands K-concatenate into ONE kind::i8 K-step of 32: a unit is a tile of
 // 128 rows, raw = two TMA boxes (P0's and P1's 16 coefficients of the rows),
 // B = [M0; M1] limb planes N-concatenated (row n' = 16 j + n, K = 32 bytes).
-// 8 MMAs of N = 16 (8 - i) per tile into 8 x 16 = 128 TMEM columns.
+// 8 MMAs of N = 16 (8 - i) per tile into 8 x 16 = 128 TMEM columns; four such
+// accumulators rotate so the MMAs of later tiles overlap the epilogue.
 // ---------------------------------------------------------------------------
 constexpr int T16_D = 16;
 constexpr int T16_RAW = TC_ROWS * 2 * T16_D * 8;          // 32 KB (two 16 KB boxes)
@@ -250,8 +274,9 @@ constexpr int T16_RAW_STAGES = 3, T16_LIMB_STAGES = 2;
 constexpr int T16_OFF_LIMB = T16_RAW_STAGES * T16_RAW;
 constexpr int T16_OFF_B = T16_OFF_LIMB + T16_LIMB_STAGES * T16_LIMB;
 constexpr int T16_OFF_BAR = T16_OFF_B + T16_B;
-constexpr int T16_SMEM = T16_OFF_BAR + 128 + 1024;
+constexpr int T16_SMEM = T16_OFF_BAR + 256 + 1024;
 constexpr int T16_EPI = 4, T16_CONV = 8;
+constexpr int T16_ACC = 4, T16_ACC_COLS = 128;            // TMEM accumulator buffers (8 x 16 columns each)
 constexpr int T16_THREADS = (T16_EPI + T16_CONV + 2) * 32;
 
 __global__ void __launch_bounds__(T16_THREADS, 1)
@@ -268,9 +293,9 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
   uint64_t* raw_empty = bars + 3;    // [3]
   uint64_t* limb_full = bars + 6;    // [2]
   uint64_t* limb_empty = bars + 8;   // [2]
-  uint64_t* tfull = bars + 10;
-  uint64_t* tempty = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* tfull = bars + 10;       // [4] one per TMEM accumulator buffer
+  uint64_t* tempty = bars + 14;      // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // B: row n' = 16 j + n, k < 16 from M0, k >= 16 from M1 (zero if absent)
@@ -289,12 +314,14 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
       mbar_init(&limb_full[i], T16_CONV * 32);
       mbar_init(&limb_empty[i], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, T16_EPI * 32);
+    for (int b = 0; b < T16_ACC; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], T16_EPI * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_async_smem();
@@ -362,8 +389,8 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
   } else if (warp == T16_EPI + T16_CONV + 1) {
     // ------------------------------ MMA issuer
     for (int64_t u = 0; u < nunits; ++u) {
-      const int ls = int(u % T16_LIMB_STAGES);
-      if (u > 0) mbar_wait(tempty, uint32_t((u - 1) & 1));
+      const int ls = int(u % T16_LIMB_STAGES), b = int(u % T16_ACC);
+      if (u >= T16_ACC) mbar_wait(&tempty[b], uint32_t((u / T16_ACC - 1) & 1));
       mbar_wait(&limb_full[ls], uint32_t((u / T16_LIMB_STAGES) & 1));
       tc_fence_after();
       if (lane == 0) {
@@ -373,48 +400,48 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
         for (int i = 0; i < 8; ++i) {
           const uint64_t ad = umma_desc(a0 + i * T16_LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
           const uint64_t bd = umma_desc(b0, (T16_BROWS / 8) * 128, 128);
-          mma_u8(tmem + uint32_t(T16_D * i), ad, bd, idesc_u8(TC_ROWS, T16_D * (8 - i)), i ? 1u : 0u);
+          mma_u8(tmem + uint32_t(T16_ACC_COLS * b + T16_D * i), ad, bd, idesc_u8(TC_ROWS, T16_D * (8 - i)),
+                 i ? 1u : 0u);
         }
         mma_commit(&limb_empty[ls]);
-        mma_commit(tfull);
+        mma_commit(&tfull[b]);
       }
       __syncwarp();
     }
   } else if (warp < T16_EPI) {
     // ------------------------------ epilogue: warp e = TMEM lane quadrant e
-    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    // (16-lane x 8-column loads: 4 threads per row, 64-byte row segments)
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t u = 0; u < nunits; ++u) {
-      mbar_wait(tfull, uint32_t(u & 1));
+      const int b = int(u % T16_ACC);
+      mbar_wait(&tfull[b], uint32_t((u / T16_ACC) & 1));
       tc_fence_after();
-      const int64_t row = (blockIdx.x + u * gridDim.x) * TC_ROWS + warp * 32 + lane;
 #pragma unroll 1
-      for (int c0 = 0; c0 < T16_D; c0 += 8) {
-        uint32_t v[8][8];
+      for (int it = 0; it < 2 * (T16_D / 8); ++it) {
+        const int lg = it & 1, c0 = 8 * (it >> 1);
+        const uint32_t taddr = tmem + (uint32_t(warp * 32 + lg * 16) << 16) + uint32_t(T16_ACC_COLS * b + c0);
+        uint32_t v[8][4];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * T16_D + c0), v[s]);
+        for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(T16_D * s), v[s]);
         tmem_wait_ld();
-        u64 acc[8];
+        u64 acc[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          u64 a = 0;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) a += u64(v[s][q]) << (8 * s);
-          acc[q] = a & mask;
-        }
-        if (row < rows) {
-          ulonglong2* o = reinterpret_cast<ulonglong2*>(out + row * T16_D + c0);
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) o[q >> 1] = make_ulonglong2(acc[q], acc[q + 1]);
-        }
+        for (int q = 0; q < 4; ++q)
+          acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
+        const int64_t row = (blockIdx.x + u * gridDim.x) * TC_ROWS + warp * 32 + lg * 16 + rq;
+        if (row < rows)
+          *reinterpret_cast<ulonglong2*>(out + row * T16_D + c0 + cq) = make_ulonglong2(acc[0], acc[1]);
+        if (row + 8 < rows)
+          *reinterpret_cast<ulonglong2*>(out + (row + 8) * T16_D + c0 + cq) = make_ulonglong2(acc[2], acc[3]);
       }
       tc_fence_before();
-      mbar_arrive(tempty);
+      mbar_arrive(&tempty[b]);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ---------------------------------------------------------------------------
@@ -490,14 +517,14 @@ extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, co
     }
   }
   if (nops == 1) tm[1] = tm[0];
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gr_matmul2_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_SMEM);
-    attr = true;
-  }
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
   const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
-  gr_matmul2_tc_kernel<<<grid, WS_THREADS, WS_SMEM, as_stream(stream)>>>(
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gr_matmul2_db_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DB_SMEM);
+    attr = true;
+  }
+  gr_matmul2_db_kernel<<<grid, WS_THREADS, DB_SMEM, as_stream(stream)>>>(
       tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc");
 }

@@ -79,6 +79,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(taddr));
 }
+// 16 TMEM lanes x 8 columns (32-bit): thread t gets lane t/4 columns 2(t%4),
+// 2(t%4)+1 in v[0..1] and lane t/4 + 8 in v[2..3] (the mma.sync C-fragment
+// pattern), so 4 consecutive threads hold one row's 8 consecutive columns.
+__device__ __forceinline__ void tmem_ld_16x256(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // byte i of each of x0..x3 (32-bit words) packed little-endian into one word
