@@ -80,6 +80,109 @@ __device__ __forceinline__ void aes_ctr_words(const RoundKeys& rk, const u32* Tl
   hi = u64(bswap32(o2)) | (u64(bswap32(o3)) << 32);
 }
 
+// ---------------------------------------------------------------------------
+// Four-table form for the bulk PRF kernels.  128 KB of dynamic shared
+// memory: region r (64 KB) holds Te(2r) and Te(2r+1); row x is 256 bytes,
+// Te(2r)[x] replicated for the 32 lanes in bytes 0..127 (word = lane) and
+// Te(2r+1)[x] in bytes 128..255.  With the tables 64 KB-aligned in the
+// shared window, a lookup address base | (x << 8) | lane * 4 (| 128 for the
+// odd table) is ONE byte permute of the state word: byte k of s to byte 1,
+// the per-thread selector to bytes 0, 2 and 3 -- so a round is
+// 16 PRMT + 16 LDS + 8 three-input XORs, with no rotates, masks or shifts
+// (the single-table form spends about 100 instructions per round).  Every
+// warp-wide lookup still hits 32 distinct banks.
+// ---------------------------------------------------------------------------
+constexpr int kAes4Bytes = 4 * 256 * 128;      // 128 KB of tables
+constexpr int kAes4Smem = kAes4Bytes + 65536;  // + room to align them to 64 KB
+constexpr int kAes4Threads = 1024;
+extern __shared__ __align__(16) uint8_t aes4_smem[];
+
+// Per-thread lookup selectors: the shared-window address of the tables is
+// aligned to 64 KB, so its high half-word rides in bytes 2-3 of the PRMT
+// operand and the permute yields the complete LDS address.
+struct Aes4Sel {
+  u32 y[4];   // table t: region base | (t & 1) * 128 | lane * 4
+};
+
+__device__ __forceinline__ Aes4Sel load_ttables4() {
+  const u32 win = u32(__cvta_generic_to_shared(aes4_smem));
+  const u32 base = (win + 65535u) & ~65535u;
+  u32* W = reinterpret_cast<u32*>(aes4_smem + (base - win));
+  for (int i = threadIdx.x; i < kAes4Bytes / 4; i += blockDim.x) {
+    const int region = i >> 14, x = (i >> 6) & 255, col = i & 63;
+    const int tbl = 2 * region + (col >> 5);
+    const u32 t = te0_of(d_sbox[x]);
+    W[i] = tbl ? __funnelshift_r(t, t, 8 * tbl) : t;
+  }
+  __syncthreads();
+  Aes4Sel sel;
+  const u32 lane4 = (threadIdx.x & 31) * 4;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) sel.y[t] = base + 65536u * u32(t >> 1) + 128u * u32(t & 1) + lane4;
+  return sel;
+}
+
+// Te(TBL)[byte BYTE of s]: one PRMT (s byte -> address byte 1, selector
+// bytes 0, 2, 3) and one LDS.
+template <int TBL, int BYTE>
+__device__ __forceinline__ u32 t4(const Aes4Sel& q, u32 s) {
+  const u32 a = __byte_perm(s, q.y[TBL], 0x7604 + 16 * BYTE);
+  u32 v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// Rounds 1..9 of AES-128 on the counter block BE128(ctr); leaves the state
+// before the final round in s0..s3.
+__device__ __forceinline__ void aes4_rounds(const RoundKeys& rk, const Aes4Sel& q, u64 ctr, u32& s0, u32& s1,
+                                            u32& s2, u32& s3) {
+  s0 = rk.w[0];
+  s1 = rk.w[1];
+  s2 = u32(ctr >> 32) ^ rk.w[2];
+  s3 = u32(ctr) ^ rk.w[3];
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    const u32 t0 = t4<0, 3>(q, s0) ^ t4<1, 2>(q, s1) ^ t4<2, 1>(q, s2) ^ t4<3, 0>(q, s3) ^
+                   rk.w[4 * r + 0];
+    const u32 t1 = t4<0, 3>(q, s1) ^ t4<1, 2>(q, s2) ^ t4<2, 1>(q, s3) ^ t4<3, 0>(q, s0) ^
+                   rk.w[4 * r + 1];
+    const u32 t2 = t4<0, 3>(q, s2) ^ t4<1, 2>(q, s3) ^ t4<2, 1>(q, s0) ^ t4<3, 0>(q, s1) ^
+                   rk.w[4 * r + 2];
+    const u32 t3 = t4<0, 3>(q, s3) ^ t4<1, 2>(q, s0) ^ t4<2, 1>(q, s1) ^ t4<3, 0>(q, s2) ^
+                   rk.w[4 * r + 3];
+    s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+  }
+}
+
+// Final-round word: S-box bytes taken from the table whose byte lane holds s
+// at that position (Te3: byte 3, Te0: byte 2, Te1: byte 1, Te2: byte 0).
+__device__ __forceinline__ u32 aes4_last(const Aes4Sel& q, u32 a, u32 b, u32 c, u32 d, u32 k) {
+  return (t4<3, 3>(q, a) & 0xff000000u) ^ (t4<0, 2>(q, b) & 0x00ff0000u) ^
+         (t4<1, 1>(q, c) & 0x0000ff00u) ^ (t4<2, 0>(q, d) & 0x000000ffu) ^ k;
+}
+
+// The two little-endian keystream words of counter block ctr.
+__device__ __forceinline__ void aes4_ctr_words(const RoundKeys& rk, const Aes4Sel& q, u64 ctr, u64& lo, u64& hi) {
+  u32 s0, s1, s2, s3;
+  aes4_rounds(rk, q, ctr, s0, s1, s2, s3);
+  const u32 o0 = aes4_last(q, s0, s1, s2, s3, rk.w[40]);
+  const u32 o1 = aes4_last(q, s1, s2, s3, s0, rk.w[41]);
+  const u32 o2 = aes4_last(q, s2, s3, s0, s1, rk.w[42]);
+  const u32 o3 = aes4_last(q, s3, s0, s1, s2, rk.w[43]);
+  lo = u64(bswap32(o0)) | (u64(bswap32(o1)) << 32);
+  hi = u64(bswap32(o2)) | (u64(bswap32(o3)) << 32);
+}
+
+// Bit 0 of both keystream words of block ctr (keystream bytes 0 and 8: the
+// top bytes of final-round words 0 and 2 -- two S-box lookups).
+__device__ __forceinline__ void aes4_ctr_bit0s(const RoundKeys& rk, const Aes4Sel& q, u64 ctr, u32& b_lo,
+                                               u32& b_hi) {
+  u32 s0, s1, s2, s3;
+  aes4_rounds(rk, q, ctr, s0, s1, s2, s3);
+  b_lo = ((t4<3, 3>(q, s0) ^ rk.w[40]) >> 24) & 1u;
+  b_hi = ((t4<3, 3>(q, s2) ^ rk.w[42]) >> 24) & 1u;
+}
+
 __device__ __forceinline__ void load_ttable(u32* T) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) T[i] = te0_of(d_sbox[i >> 5]);
   __syncthreads();

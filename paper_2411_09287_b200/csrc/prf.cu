@@ -76,6 +76,77 @@ prf_bits_packed_kernel(RoundKeys rk, u64 first, int nbits, int64_t lanes, u64* _
   }
 }
 
+// Four-table kernels (aes.cuh) for bulk draws: one 1024-thread block per SM
+// shares the 128 KB tables.
+__global__ void __launch_bounds__(kAes4Threads, 1)
+prf_ctr4_kernel(RoundKeys rk, u64 first, int64_t n, u64 mask, int mode, u64* __restrict__ out) {
+  const Aes4Sel q = load_ttables4();
+  const u64 b0 = first >> 1;
+  const u64 nb = ((first + u64(n) + 1) >> 1) - b0;
+  for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < nb; t += u64(gridDim.x) * blockDim.x) {
+    const u64 ctr = b0 + t;
+    u64 lo, hi;
+    aes4_ctr_words(rk, q, ctr, lo, hi);
+    if (mode == 1) { lo &= 1ull; hi &= 1ull; } else { lo &= mask; hi &= mask; }
+    const int64_t i0 = int64_t(2 * ctr - first);
+    if (i0 >= 0 && i0 + 1 < n && (((uintptr_t)(out + i0)) & 15) == 0) {
+      __stcs(reinterpret_cast<ulonglong2*>(out + i0), make_ulonglong2(lo, hi));
+    } else {
+      if (i0 >= 0 && i0 < n) out[i0] = lo;
+      if (i0 + 1 >= 0 && i0 + 1 < n) out[i0 + 1] = hi;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kAes4Threads, 1)
+prf_bits4_kernel(RoundKeys rk, u64 first, int nbits, int64_t lanes, u64* __restrict__ out) {
+  const Aes4Sel q = load_ttables4();
+  const bool paired = ((first | u64(lanes)) & 1) == 0;
+  const int64_t units = paired ? lanes / 2 : lanes;
+  for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < units; u += int64_t(gridDim.x) * blockDim.x) {
+    if (paired) {
+      const int64_t l = 2 * u;
+      u64 a0 = 0, a1 = 0;
+      for (int j = 0; j < nbits; ++j) {
+        const u64 w = first + u64(j) * u64(lanes) + u64(l);
+        u32 blo, bhi;
+        aes4_ctr_bit0s(rk, q, w >> 1, blo, bhi);
+        a0 |= u64(blo) << j;
+        a1 |= u64(bhi) << j;
+      }
+      *reinterpret_cast<ulonglong2*>(out + l) = make_ulonglong2(a0, a1);
+    } else {
+      u64 a = 0;
+      for (int j = 0; j < nbits; ++j) {
+        const u64 w = first + u64(j) * u64(lanes) + u64(u);
+        u32 blo, bhi;
+        aes4_ctr_bit0s(rk, q, w >> 1, blo, bhi);
+        a |= u64((w & 1) ? bhi : blo) << j;
+      }
+      out[u] = a;
+    }
+  }
+}
+
+// Bulk draws (at least this many AES blocks) take the four-table kernels;
+// smaller ones the single-table kernels (no 128 KB table fill per block).
+constexpr int64_t kAes4MinBlocks = int64_t(1) << 16;
+
+static bool aes4_init() {
+  static bool ok = [] {
+    return cudaFuncSetAttribute(prf_ctr4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(prf_bits4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) ==
+               cudaSuccess;
+  }();
+  return ok;
+}
+
+static unsigned aes4_grid(int64_t work) {
+  const int64_t g = (work + kAes4Threads - 1) / kAes4Threads;
+  return unsigned(g < kNumSMs ? g : kNumSMs);
+}
+
 }  // namespace r3
 
 using namespace r3;
@@ -148,6 +219,11 @@ extern "C" int r3_prf_ctr(const uint32_t rk[44], uint64_t first_u64, int64_t n, 
   RoundKeys k;
   memcpy(k.w, rk, sizeof(k.w));
   const int64_t nblocks = (int64_t((first_u64 + n + 1) >> 1) - int64_t(first_u64 >> 1));
+  if (nblocks >= kAes4MinBlocks && aes4_init()) {
+    prf_ctr4_kernel<<<aes4_grid(nblocks), kAes4Threads, kAes4Smem, as_stream(stream)>>>(
+        k, first_u64, n, mask, mode, reinterpret_cast<u64*>(out));
+    return check_launch("r3_prf_ctr");
+  }
   unsigned grid = grid_for(nblocks, kPrfThreads, 7);
   prf_ctr_kernel<<<grid, kPrfThreads, 0, as_stream(stream)>>>(k, first_u64, n, mask, mode,
                                                               reinterpret_cast<u64*>(out));
@@ -165,6 +241,11 @@ extern "C" int r3_prf_bits_packed(const uint32_t rk[44], uint64_t first_u64, int
   memcpy(k.w, rk, sizeof(k.w));
   const bool paired = ((first_u64 | uint64_t(lanes)) & 1) == 0;
   const int64_t units = paired ? lanes / 2 : lanes;
+  if (units * nbits >= kAes4MinBlocks && aes4_init()) {
+    prf_bits4_kernel<<<aes4_grid(units), kAes4Threads, kAes4Smem, as_stream(stream)>>>(
+        k, first_u64, nbits, lanes, reinterpret_cast<u64*>(out));
+    return check_launch("r3_prf_bits_packed");
+  }
   prf_bits_packed_kernel<<<grid_for(units, kPrfThreads, 7), kPrfThreads, 0, as_stream(stream)>>>(
       k, first_u64, nbits, lanes, reinterpret_cast<u64*>(out));
   return check_launch("r3_prf_bits_packed");

@@ -19,17 +19,47 @@ from paper_2411_09287_b200 import _lib, verify  # noqa: E402
 from paper_2411_09287_b200.runtime import Session  # noqa: E402
 
 
+def _matmul_program(n):
+    import numpy as np
+    from paper_2411_09287_b200 import gates
+    from paper_2411_09287_b200.sharing import Ring, shc_input_mask, shc_input_online
+    from paper_2411_09287_b200.transport import Phase
+    rng = np.random.default_rng(3)
+    enc = lambda a: torch.from_numpy(np.trunc(a * 2 ** 16).astype(np.int64)).pin_memory()
+    Xh, Wh = enc(rng.normal(0, 1, (n, n))), enc(rng.normal(0, 1 / 64, (n, n)))
+
+    def prog(party):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        xm = shc_input_mask(party, 2, n * n, ring)
+        wm = shc_input_mask(party, 1, n * n, ring)
+        tr = gates.trunc_prepare(party, n * n, 16, ring)
+        g = gates.matmul_prepare(party, xm, wm, n, n, n, out_mask=tr.rx_mask)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        X = shc_input_online(party, 2, Xh.reshape(-1) if party.role == 2 else None, xm, n * n, ring, "X")
+        W = shc_input_online(party, 1, Wh.reshape(-1) if party.role == 1 else None, wm, n * n, ring, "W")
+        gates.trunc_online(party, gates.matmul_finish(party, g, X, W, log=False), tr)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+    return prog
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--log2n", type=int, default=22)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--engine", default="coop")
-    ap.add_argument("--prog", default="mulv", choices=["mulv", "relu", "relu-exec"])
+    ap.add_argument("--prog", default="mulv", choices=["mulv", "relu", "relu-exec", "matmul"])
     a = ap.parse_args()
     N = 1 << a.log2n
     R = verify.pick_r(N, 64, a.d)
     if a.prog == "mulv":
         mulv, _ = bench.make_programs(N, a.d, R)
+        args = ()
+    elif a.prog == "matmul":              # config C3 at n = 2^(log2n / 2)
+        mulv = _matmul_program(1 << (a.log2n // 2))
         args = ()
     else:
         import numpy as np
