@@ -39,18 +39,19 @@ struct RippleOut {
   u64* logz[7];       // optional: gate output (mask comps, m_z for P1 / P2)
 };
 
-__device__ __forceinline__ u64 ks_bit(const RoundKeys& rk, const u32* Tl, u64 idx) {
-  u64 lo, hi;
-  aes_ctr_words(rk, Tl, idx >> 1, lo, hi);
-  return ((idx & 1) ? hi : lo) & 1ull;
+// bit 0 of stream word idx (four-table AES, aes.cuh)
+__device__ __forceinline__ u64 ks_bit(const RoundKeys& rk, const Aes4Sel& q, u64 idx) {
+  u32 blo, bhi;
+  aes4_ctr_bit0s(rk, q, idx >> 1, blo, bhi);
+  return (idx & 1) ? bhi : blo;
 }
 
-__global__ void __launch_bounds__(kPrfThreads)
+constexpr int kRippleThreads = 768;   // 24 warps: the carry state needs ~80 registers
+
+__global__ void __launch_bounds__(kRippleThreads, 1)
 ripple_msb_kernel(RoundKeys rk01, RoundKeys rk02, u64 o01, u64 o02, const u64* __restrict__ delta, RippleIn in,
                   RippleOut out, int ell, int64_t lanes, int write_log) {
-  __shared__ u32 T[256 * 32];
-  load_ttable(T);
-  const u32* Tl = T + (threadIdx.x & 31);
+  const Aes4Sel Tl = load_ttables4();
   const int64_t rs = in.row_stride;
   const int ng = ell - 2;
   for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < lanes; l += int64_t(gridDim.x) * blockDim.x) {
@@ -138,8 +139,15 @@ extern "C" int r3_ripple_msb(const uint32_t* rk01, const uint32_t* rk02, uint64_
     }
   }
   for (int q = 0; q < 3; ++q) out.msg[q] = reinterpret_cast<u64*>(msgs[q]);
-  const unsigned grid = grid_for(lanes, kPrfThreads, 4);
-  ripple_msb_kernel<<<grid, kPrfThreads, 0, as_stream(stream)>>>(k01, k02, o01, o02,
+  static const bool attr =
+      cudaFuncSetAttribute(ripple_msb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) == cudaSuccess;
+  if (!attr) {
+    set_error("r3_ripple_msb: cannot reserve %d bytes of shared memory", kAes4Smem);
+    return R3_ERR_CUDA;
+  }
+  const int64_t blocks = (lanes + kRippleThreads - 1) / kRippleThreads;
+  const unsigned grid = unsigned(blocks < kNumSMs ? blocks : kNumSMs);
+  ripple_msb_kernel<<<grid, kRippleThreads, kAes4Smem, as_stream(stream)>>>(k01, k02, o01, o02,
                                                                  reinterpret_cast<const u64*>(delta), in, out,
                                                                  ell, lanes, write_log);
   return check_launch("r3_ripple_msb");
