@@ -109,27 +109,49 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 template <int D>
 __host__ __device__ constexpr int lb_cpt() { return D == 16 ? 4 : 2; }
 
-template <int D, bool ONE>
-__global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
-                              const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
+template <int D, bool ONE, bool TAB>
+__global__ void __launch_bounds__(256, 4)
+line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+              const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
+  // Lane (row j, coefficients k..k+CPT-1); the 4 lanes of an aligned quad
+  // share j (H is a multiple of 4), lane b of a quad loads the scalar of
+  // element B j + b for every component, and the quad exchanges them by
+  // shuffles: one load per component per lane, all issued before any store.
   constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / H;
-    const int k = CPT * int(e - j * H);
-    ulonglong2 w[4][V];
-    int64_t off[4];
+  const int lane = threadIdx.x & 31, bl = lane & 3, quad0 = lane & ~3;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int k = CPT * int((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) % H);   // invariant: H | stride
+  ulonglong2 w[4][V];
+  if (!TAB) {   // public constants g (B x D): per lane, loaded once
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t i = B * j + a;
-      const bool ok = a < B && i < N;
-      const int64_t row = ONE ? j : qdiv(i, tq);
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < V; ++q)
-        w[a][q] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * tab_stride + row * D + k) + q)
-                     : make_ulonglong2(0ull, 0ull);
-      off[a] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
+        w[a][q] = a < B ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * D + k) + q) : make_ulonglong2(0ull, 0ull);
+  }
+  for (int64_t e0 = blockIdx.x * int64_t(blockDim.x) + (threadIdx.x & ~31); e0 < total; e0 += stride) {
+    const int64_t e = e0 + lane;
+    const bool live = e < total;
+    const int64_t j = e / H;
+    const int64_t i = B * j + bl;
+    const bool ok = live && bl < B && i < N;
+    const int64_t off = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : 0;
+    u64 xs[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) xs[c] = (c < ncomp && ok) ? __ldg(xc.p[c] + off) : 0ull;
+    if (TAB) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t ia = B * j + a;
+        const bool oka = live && a < B && ia < N;
+        const int64_t row = ONE ? j : qdiv(ia, tq);
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          w[a][q] = oka ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * tab_stride + row * D + k) + q)
+                        : make_ulonglong2(0ull, 0ull);
+      }
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -139,69 +161,26 @@ __global__ void line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n,
         for (int q = 0; q < V; ++q) v[q] = make_ulonglong2(0ull, 0ull);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          if (off[a] >= 0) {
-            const u64 xv = __ldg(xc.p[c] + off[a]);
+          const u64 xv = __shfl_sync(0xffffffffu, xs[c], quad0 + a);
 #pragma unroll
-            for (int q = 0; q < V; ++q) {
-              v[q].x += xv * w[a][q].x;
-              v[q].y += xv * w[a][q].y;
-            }
+          for (int q = 0; q < V; ++q) {
+            v[q].x += xv * w[a][q].x;
+            v[q].y += xv * w[a][q].y;
           }
         }
+        if (live) {
 #pragma unroll
-        for (int q = 0; q < V; ++q)
-          reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k)[q] = make_ulonglong2(v[q].x & mask, v[q].y & mask);
+          for (int q = 0; q < V; ++q)
+            __stcs(reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k) + q,
+                   make_ulonglong2(v[q].x & mask, v[q].y & mask));
+        }
       }
     }
   }
 }
 
-// out_c[j] = sum_{b<B} Y_c[B j + b] * g_b  (public constants g, B x D)
-template <int D, bool ONE>
-__global__ void line_b_const_kernel(int B, int ncomp, Comps8 yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
-                                    const u64* __restrict__ g, Outs8 out, u64 mask) {
-  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT;
-  const int64_t nblk = (N + B - 1) / B;
-  const int64_t total = nblk * H;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / H;
-    const int k = CPT * int(e - j * H);
-    ulonglong2 gv[4][V];
-    int64_t off[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t i = B * j + b;
-      const bool ok = b < B && i < N;
-#pragma unroll
-      for (int q = 0; q < V; ++q)
-        gv[b][q] = ok ? __ldg(reinterpret_cast<const ulonglong2*>(g + b * D + k) + q) : make_ulonglong2(0ull, 0ull);
-      off[b] = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : -1;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (c < ncomp) {
-        ulonglong2 v[V];
-#pragma unroll
-        for (int q = 0; q < V; ++q) v[q] = make_ulonglong2(0ull, 0ull);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (off[b] >= 0) {
-            const u64 yv = __ldg(yc.p[c] + off[b]);
-#pragma unroll
-            for (int q = 0; q < V; ++q) {
-              v[q].x += yv * gv[b][q].x;
-              v[q].y += yv * gv[b][q].y;
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < V; ++q)
-          reinterpret_cast<ulonglong2*>(out.p[c] + j * D + k)[q] = make_ulonglong2(v[q].x & mask, v[q].y & mask);
-      }
-    }
-  }
-}
-
+// out_c[j] = sum_{b<B} Y_c[B j + b] * g_b  (public constants g, B x D): the
+// TAB = false form of line_b_kernel.
 
 // ---------------------------------------------------------------------------
 // One pass over the power table for a multiplication log (n = 1): the z
@@ -494,10 +473,10 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
   if (n == 1 && tq == B) {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, true><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
   } else {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, false><<<grid_for(total, 256), 256, 0, s>>>(
+    R3_DISPATCH_D2(d, (line_b_kernel<D, false, true><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
   }
   return check_launch("r3_vfy_line_b");
@@ -520,11 +499,11 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
   if (n == 1) {
-    R3_DISPATCH_D2(d, (line_b_const_kernel<D, true><<<grid_for(total, 256), 256, 0, s>>>(
-                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, false><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
   } else {
-    R3_DISPATCH_D2(d, (line_b_const_kernel<D, false><<<grid_for(total, 256), 256, 0, s>>>(
-                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, op, mask)));
+    R3_DISPATCH_D2(d, (line_b_kernel<D, false, false><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
   }
   return check_launch("r3_vfy_line_b_const");
 }
