@@ -81,12 +81,17 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   uint64_t* full = bars + 2 * BF_STAGES;
   uint64_t* empty = bars + 3 * BF_STAGES;
   uint64_t* tfull = bars + 4 * BF_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int64_t j0 = int64_t(blockIdx.x) * args.kc;
-  const int64_t j1 = min(args.nblk, j0 + args.kc);
-  const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
+  // persistent: CTA b takes K-chunks (items) b, b + grid, ... of kc blocks;
+  // unit g enumerates (item, K-step) in that order
+  const int64_t nitems = (args.nblk + args.kc - 1) / args.kc;
+  auto item_range = [&](int64_t it, int64_t& j0, int64_t& j1) {
+    j0 = it * args.kc;
+    j1 = min(args.nblk, j0 + args.kc);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < BF_STAGES; ++s) {
@@ -96,6 +101,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -110,12 +116,19 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   if (warp == 4 + 12) {
     // ---------------- TMA producer: table rows j of the K-step
     if (lane == 0) {
-      for (int64_t kb = 0; kb < nkb; ++kb) {
-        const int st = int(kb % BF_STAGES);
-        if (kb >= BF_STAGES) mbar_wait(&raw_empty[st], uint32_t((kb / BF_STAGES - 1) & 1));
-        const int y = int(j0 + kb * BF_BK);
-        mbar_expect_tx(&raw_full[st], uint32_t(BF_RAW));
-        for (int c = 0; c < 4; ++c) tma_load_2d(sRaw + st * BF_RAW + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[st]);
+      int64_t g = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int64_t j0, j1;
+        item_range(it, j0, j1);
+        const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
+        for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
+          const int st = int(g % BF_STAGES);
+          if (g >= BF_STAGES) mbar_wait(&raw_empty[st], uint32_t((g / BF_STAGES - 1) & 1));
+          const int y = int(j0 + kb * BF_BK);
+          mbar_expect_tx(&raw_full[st], uint32_t(BF_RAW));
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d(sRaw + st * BF_RAW + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[st]);
+        }
       }
     }
     __syncwarp();
@@ -127,8 +140,14 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     const int c = isA ? (lt >> 5) : ((lt - 256) >> 5);
     const int p = c >> 1, h = c & 1;
     const bool live = isA && p < args.np;
+    int64_t g = -1;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int64_t j0, j1;
+    item_range(it, j0, j1);
+    const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
     for (int64_t kb = 0; kb < nkb; ++kb) {
-      const int st = int(kb % BF_STAGES);
+      ++g;
+      const int st = int(g % BF_STAGES);
       const int64_t j = j0 + kb * BF_BK + k;
       const bool ok = j < j1;
       u64 v[16];
@@ -168,7 +187,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           }
         }
       } else {
-        mbar_wait(&raw_full[st], uint32_t((kb / BF_STAGES) & 1));
+        mbar_wait(&raw_full[st], uint32_t((g / BF_STAGES) & 1));
         const uint8_t* row = sRaw + st * BF_RAW + c * BF_BOX + k * 128;
         const int sw = k & 7;
 #pragma unroll
@@ -182,7 +201,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       }
       uint4 pk[8];
       bf_split16(v, pk);
-      if (kb >= BF_STAGES) mbar_wait(&empty[st], uint32_t((kb / BF_STAGES - 1) & 1));
+      if (g >= BF_STAGES) mbar_wait(&empty[st], uint32_t((g / BF_STAGES - 1) & 1));
       // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
       uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * BF_B_TILE;
       const int plane = isA ? BF_A_PLANE : BF_B_PLANE;
@@ -192,12 +211,24 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       fence_async_smem();
       mbar_arrive(&full[st]);
     }
+    }
   } else if (warp == 4 + 12 + 1) {
     // ---------------- MMA issuer (as lf_tc: 12 N-concatenated limb MMAs per K-step)
     constexpr uint32_t IDESC_M128 = idesc_u8(128, 0) | (1u << 15) | (1u << 16);
+    int64_t g = -1;
+    uint32_t tph = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int64_t j0, j1;
+    item_range(it, j0, j1);
+    const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
+    if (it != blockIdx.x) {        // the epilogue has drained the previous item
+      mbar_wait(tempty, tph);
+      tph ^= 1;
+    }
     for (int64_t kb = 0; kb < nkb; ++kb) {
-      const int st = int(kb % BF_STAGES);
-      mbar_wait(&full[st], uint32_t((kb / BF_STAGES) & 1));
+      ++g;
+      const int st = int(g % BF_STAGES);
+      mbar_wait(&full[st], uint32_t((g / BF_STAGES) & 1));
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(sA + st * BF_A_TILE);
@@ -219,10 +250,13 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     }
     if (lane == 0) mma_commit(tfull);
     __syncwarp();
+    }
   } else if (warp < 4) {
     // ---------------- epilogue: TMEM lane f = feature (party f / 32, slot f % 32)
-    if (nkb > 0) {
-      mbar_wait(tfull, 0);
+    uint32_t ph = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      mbar_wait(tfull, ph);
+      ph ^= 1;
       tc_fence_after();
       const int f = warp * 32 + lane;
       const int p = f >> 5, q = f & 31;
@@ -246,6 +280,8 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(tempty);
     }
   }
   tc_fence_before();
@@ -287,17 +323,20 @@ int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64
     set_error("r3_vfy_base_fold_q4(tc): cuTensorMapEncodeTiled failed");
     return R3_ERR_CUDA;
   }
+  // K-chunks of <= BF_MAX_K blocks, a whole number of chunks per CTA of a
+  // persistent grid (no partial second wave)
   int64_t items = (nblk + BF_MAX_K - 1) / BF_MAX_K;
-  if (items < kNumSMs) items = kNumSMs;
+  items = (items + kNumSMs - 1) / kNumSMs * kNumSMs;
   int64_t kc = (nblk + items - 1) / items;
   kc = (kc + BF_BK - 1) / BF_BK * BF_BK;
   items = (nblk + kc - 1) / kc;
   args.kc = kc;
+  const unsigned grid = unsigned(items < kNumSMs ? items : kNumSMs);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(base_fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BF_SMEM);
     attr = true;
   }
-  base_fold_tc_kernel<<<unsigned(items), BF_THREADS, BF_SMEM, s>>>(args);
+  base_fold_tc_kernel<<<grid, BF_THREADS, BF_SMEM, s>>>(args);
   return check_launch("r3_vfy_base_fold_q4(tc)");
 }
