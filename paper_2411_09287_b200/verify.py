@@ -189,6 +189,23 @@ def _public(party, key, build):
         return cache[key]
 
 
+def _shared_m(party, build):
+    """The masked value m is held identically by P1 and P2 in an honest
+    session, so anything computed from m alone (line evaluations of the m
+    component) is computed once: the first of the two to arrive builds it,
+    the second takes the same tensor (value semantics: nothing writes into
+    it).  Sessions with an adversary, and the threads engine, compute per
+    party as in the reference."""
+    if party.role == 0 or not _joint_ok(party):
+        return build()
+    key = ("m", party.next_id("_shared_m"))
+    memo = party.sess.shared_m
+    if key in memo:
+        return memo.pop(key)
+    out = memo[key] = build()
+    return out
+
+
 def _opened_key(party, value: torch.Tensor):
     """Cache identity of a just-opened public value.  With eager checks (an
     adversary is configured) parties may disagree on an opening until the
@@ -556,7 +573,10 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
         nb = (comp.N + 3) // 4
         out = {}
         for side, fn, arg in (("x", "r3_vfy_line_b", None), ("y", "r3_vfy_line_b_const", None)):
-            srcs = [(r, k, t) for r, sl in sorted(slots.items()) for k, t in sl[side].items()]
+            # m is the same public value at P1 and P2 (honest joint session):
+            # one output serves both
+            srcs = [(r, k, t) for r, sl in sorted(slots.items()) for k, t in sl[side].items()
+                    if not (r == 2 and k == "m" and 1 in slots and "m" in slots[1][side])]
             dst = [empty((nb, gr.d)) for _ in srcs]
             for c0 in range(0, len(srcs), 8):
                 part, pdst = srcs[c0:c0 + 8], dst[c0:c0 + 8]
@@ -568,6 +588,8 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
                          _ptrs(pdst), gr.mask, stream())
             for (r, k, _), o in zip(srcs, dst):
                 out.setdefault(r, {"x": {}, "y": {}})[side][k] = o
+            if 2 in slots and "m" in slots[2][side] and "m" not in out.get(2, {}).get(side, {}):
+                out.setdefault(2, {"x": {}, "y": {}})[side]["m"] = out[1][side]["m"]
         return out
 
     mine = {"x": comp.x, "y": comp.y}
@@ -799,7 +821,7 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     out = lambda V, k: _line_eval(V[k], Ms, gr)
     mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
                                   p0_halves=v.mask.p0_halves),
-                           out(V, "m") if "m" in V else None)
+                           _shared_m(party, lambda: out(V, "m")) if "m" in V else None)
     return mk(X, xs), mk(Y, ys), z_out
 
 
