@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--log2n", type=int, default=22)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--engine", default="coop")
+    ap.add_argument("--top-calls", default="", help="kernel name: print its 15 slowest calls with a stack hint")
     ap.add_argument("--prog", default="mulv", choices=["mulv", "relu", "relu-exec", "matmul"])
     a = ap.parse_args()
     N = 1 << a.log2n
@@ -77,7 +78,12 @@ def main():
         s.record()
         rc = run()
         e.record()
-        ev.append((name, s, e))
+        where = ""
+        if name == a.top_calls:
+            import traceback
+            fr = [f for f in traceback.extract_stack()[:-2] if "paper_2411_09287_b200" in f.filename]
+            where = " <- ".join(f"{os.path.basename(f.filename)}:{f.lineno}:{f.name}" for f in fr[-3:][::-1])
+        ev.append((name, s, e, where, [x for x in args if isinstance(x, int)][:4]))
         return rc
 
     t0 = torch.cuda.Event(enable_timing=True)
@@ -93,7 +99,7 @@ def main():
     step = t0.elapsed_time(t1)
     tot = collections.Counter()
     cnt = collections.Counter()
-    for name, s, e in ev:
+    for name, s, e, _w, _a in ev:
         tot[name] += s.elapsed_time(e)
         cnt[name] += 1
     busy = sum(tot.values())
@@ -101,6 +107,19 @@ def main():
           f"library GPU time {busy:.1f} ms in {len(ev)} calls")
     for k, v in tot.most_common():
         print(f"  {k:24s} {v:9.2f} ms {100 * v / step:5.1f}%  calls={cnt[k]}")
+    if a.top_calls:
+        sites = collections.Counter()
+        for name, s, e, w, ia in ev:
+            if name == a.top_calls:
+                sites[w] += s.elapsed_time(e)
+        print(f"{a.top_calls} by call site:")
+        for w, v in sites.most_common(15):
+            print(f"  {v:8.3f} ms  {w}")
+        calls = sorted(((s.elapsed_time(e), w, ia) for name, s, e, w, ia in ev if name == a.top_calls),
+                       key=lambda t: -t[0])
+        print(f"{a.top_calls} slowest calls (int args):")
+        for t, w, ia in calls[:12]:
+            print(f"  {t:8.3f} ms  {ia}  {w.split(' <- ')[-1] if w else ''}")
 
 
 if __name__ == "__main__":

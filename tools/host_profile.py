@@ -17,3 +17,4 @@ torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(25)
+st.sort_stats("cumulative").print_stats(60)
