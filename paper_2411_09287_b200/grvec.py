@@ -365,7 +365,7 @@ def gr_powers(r, n: int, width: int, mod: GrModulus) -> torch.Tensor:
     each doubling round is one rows . M_step matrix product."""
     d = mod.degree
     r = r.reshape(1, d)
-    out = zeros((n, d))
+    out = empty((n, d))          # every row is written by the doubling rounds
     if n == 0:
         return out
     out[0:1] = gr_const(1, mod, width)

@@ -620,12 +620,14 @@ def _l2_tables(party, pw: torch.Tensor, dot_n: int, w1, ze2: torch.Tensor, gr: R
         kappa = torch.cat([grvec.gr_mul(w1[a & 1], w2[a >> 1], gr.ell, gr.mod) for a in range(4)])
         P = pw.shape[0]
         rows = (P + 3) // 4 if dot_n == 1 else P
-        tabs = grvec.zeros((4, rows, gr.d))
+        tabs = grvec.empty((4, rows, gr.d))
         for a in range(4):
             src = pw[a::4] if dot_n == 1 else pw
             if src.shape[0]:
                 M = grvec.gr_mulmat(kappa[a:a + 1], gr.mod)
                 grvec.rows_times(src, M, src.shape[0], gr.ell, out=tabs[a, :src.shape[0]])
+            if src.shape[0] < rows:
+                tabs[a, src.shape[0]:].zero_()      # only the rows past the log are padding
         return tabs, kappa, (4 if dot_n == 1 else dot_n), rows * gr.d
     return _public(party, key, build)
 
@@ -642,7 +644,7 @@ def _l2_tables_q4(party, q4, w1, ze2: torch.Tensor, gr: Ring):
         kappa = torch.cat([grvec.gr_mul(w1[a & 1], w2[a >> 1], gr.ell, gr.mod) for a in range(4)])
         rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
         rows = pw4.shape[0]
-        tabs = grvec.zeros((4, rows, gr.d))
+        tabs = grvec.empty((4, rows, gr.d))        # every row is written below
         for a in range(4):
             grvec.rows_times(pw4, grvec.gr_mulmat(rk[a:a + 1], gr.mod), rows, gr.ell, out=tabs[a])
         return tabs, kappa, 4, rows * gr.d
