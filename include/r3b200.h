@@ -192,6 +192,15 @@ int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0,
                      const uint64_t* p1, int64_t rs1, int64_t nv1,
                      const uint64_t* M0, const uint64_t* M1, uint64_t* out,
                      int64_t rows, uint64_t mask, void* stream);
+/* One operand times q <= 4 public GR(2^64, 64) multiplication matrices in
+ * one pass: outs[k][r] = p[r] . Ms[k] for r < rows (rows of 64 u64 at
+ * stride rs words, 16-byte aligned).  The four level-2 tables of a
+ * verification (r^(4j) . C_a, verify.py:215-241 applied from the base log)
+ * come from one read of the r^(4j) table. */
+int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows,
+                      const uint64_t* const* Ms, uint64_t* const* outs, int q,
+                      uint64_t mask, void* stream);
+
 /* d = 16 form of r3_gr_matmul2_tc (rows of 16 coefficients, M0/M1 16 x 16):
  * both operands K-concatenate into one 32-byte kind::i8 K-step. */
 int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0,

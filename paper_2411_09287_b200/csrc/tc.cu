@@ -257,6 +257,207 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
 }
 
 // ---------------------------------------------------------------------------
+// One operand, Q <= 4 public matrices: out_q[r] = P[r] . M_q (the four
+// level-2 tables V_a = r^(4j) . C_a of one verification come from ONE pass
+// over the r^(4j) table instead of four).  Same unit / in-place stage / TMEM
+// double-buffering scheme as gr_matmul2_db_kernel; a tile's limb planes stay
+// resident for its 2 Q pieces (matrix q, output-column half h), and the
+// 4 x 32 KB of B planes leave room for 3 stages.
+// ---------------------------------------------------------------------------
+constexpr int MQ_MAX = 4;
+constexpr int MQ_STAGES = 3;
+constexpr int MQ_OFF_B = MQ_STAGES * RAW_BYTES;
+constexpr int MQ_OFF_BAR = MQ_OFF_B + MQ_MAX * BALL_BYTES;
+constexpr int MQ_SMEM = MQ_OFF_BAR + 256 + 1024;
+
+struct MqArgs {
+  const u64* M[MQ_MAX];
+  u64* out[MQ_MAX];
+  int q;
+};
+
+__global__ void __launch_bounds__(WS_THREADS, 1)
+gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ MqArgs args, int64_t rows,
+                   u64 mask) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sStage = smem;
+  uint8_t* sB = smem + MQ_OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MQ_OFF_BAR);
+  uint64_t* raw_full = bars;
+  uint64_t* limb_full = bars + MQ_STAGES;
+  uint64_t* empty = bars + 2 * MQ_STAGES;
+  uint64_t* tfull = bars + 3 * MQ_STAGES;      // [2] per TMEM buffer
+  uint64_t* tempty = tfull + 2;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Q = args.q;
+
+  for (int q = 0; q < Q; ++q) {
+    const u64* M = args.M[q];
+    uint8_t* dst = sB + q * BALL_BYTES;
+    for (int e = tid; e < TC_D * TC_D; e += WS_THREADS) {
+      const int k = e / TC_D, n = e % TC_D;
+      const int h = n / DB_HALF, c = n % DB_HALF;
+      const u64 v = M[e];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        dst[core_off(256 * h + DB_HALF * j + c, k, BALL_ROWS / 8)] = uint8_t(v >> (8 * j));
+    }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < MQ_STAGES; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&limb_full[i], W_CONV * 32);
+      mbar_init(&empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], W_EPI * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nunits = my_tiles * 2;
+  const int pieces = 2 * Q;
+
+  if (warp == W_EPI + W_CONV) {
+    // ------------------------------ TMA producer
+    if (lane == 0) {
+      for (int64_t g = 0; g < nunits; ++g) {
+        const int st = int(g % MQ_STAGES);
+        if (g >= MQ_STAGES) mbar_wait(&empty[st], uint32_t((g / MQ_STAGES - 1) & 1));
+        const int64_t t = blockIdx.x + (g >> 1) * gridDim.x;
+        const int kh = int(g & 1);
+        uint8_t* dst = sStage + st * RAW_BYTES;
+        mbar_expect_tx(&raw_full[st], RAW_BYTES);
+        tma_load_2d(dst, &tm, kh * TC_KH, int(t * TC_ROWS), &raw_full[st]);
+        tma_load_2d(dst + RAW_BYTES / 2, &tm, kh * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= W_EPI && warp < W_EPI + W_CONV) {
+    // ------------------------------ converters (in place)
+    const int ct = tid - W_EPI * 32;
+    const int r = ct & (TC_ROWS - 1), c = ct >> 7;
+    const int sw = r & 7;
+    for (int64_t g = 0; g < nunits; ++g) {
+      const int st = int(g % MQ_STAGES);
+      mbar_wait(&raw_full[st], uint32_t((g / MQ_STAGES) & 1));
+      uint8_t* stage = sStage + st * RAW_BYTES;
+      const uint8_t* src = stage + c * (RAW_BYTES / 2) + r * 128;
+      uint32_t x[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + ((q ^ sw) << 4));
+        x[4 * q + 0] = v.x;
+        x[4 * q + 1] = v.y;
+        x[4 * q + 2] = v.z;
+        x[4 * q + 3] = v.w;
+      }
+      conv_named_sync();
+      uint8_t* dst = stage + core_off(r, c * 16, TC_ROWS / 8);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int hiw = i >> 2, bi = i & 3;
+        uint4 pk;
+        pk.x = gather_byte(x[0 + hiw], x[2 + hiw], x[4 + hiw], x[6 + hiw], bi);
+        pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
+        pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
+        pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
+        *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk;
+      }
+      fence_async_smem();
+      mbar_arrive(&limb_full[st]);
+    }
+  } else if (warp == W_EPI + W_CONV + 1) {
+    // ------------------------------ MMA issuer: pieces p = (q, h), buffer p & 1
+    uint32_t tph[2] = {0, 0};
+    int64_t use = 0;                                  // pieces issued so far (buffer uses)
+    for (int64_t g0 = 0; g0 < nunits; g0 += 2) {
+      for (int p = 0; p < pieces; ++p, ++use) {
+        const int b = int(use & 1);
+        if (use >= 2) {
+          mbar_wait(&tempty[b], tph[b]);
+          tph[b] ^= 1;
+        }
+        const int q = p >> 1, h = p & 1;
+        for (int kh = 0; kh < 2; ++kh) {
+          const int64_t g = g0 + kh;
+          const int st = int(g % MQ_STAGES);
+          if (p == 0) mbar_wait(&limb_full[st], uint32_t((g / MQ_STAGES) & 1));
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sStage + st * RAW_BYTES);
+            const uint32_t b0 = smem_u32(sB + q * BALL_BYTES) + uint32_t((2 * kh * (BALL_ROWS / 8) + 32 * h) * 128);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t ad = umma_desc(a0 + i * LIMB_PLANE, (TC_ROWS / 8) * 128, 128);
+              const uint64_t bd = umma_desc(b0, (BALL_ROWS / 8) * 128, 128);
+              mma_u8(tmem + uint32_t(256 * b + DB_HALF * i), ad, bd, idesc_u8(TC_ROWS, DB_HALF * (8 - i)),
+                     (kh == 0 && i == 0) ? 0u : 1u);
+            }
+            if (p == pieces - 1) mma_commit(&empty[st]);
+            if (kh == 1) mma_commit(&tfull[b]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp < W_EPI) {
+    // ------------------------------ epilogue
+    uint32_t ph[2] = {0, 0};
+    int64_t use = 0;
+    const int quad = warp & 3;
+    const int rq = lane >> 2, cq = 2 * (lane & 3);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int p = 0; p < pieces; ++p, ++use) {
+        const int b = int(use & 1), q = p >> 1, h = p & 1;
+        mbar_wait(&tfull[b], ph[b]);
+        ph[b] ^= 1;
+        tc_fence_after();
+        u64* out = args.out[q];
+#pragma unroll 1
+        for (int it = 0; it < 2 * (DB_HALF / 8); ++it) {
+          const int lg = it & 1, c0 = 8 * (it >> 1);
+          const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * b + c0);
+          uint32_t v[8][4];
+#pragma unroll
+          for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(DB_HALF * s), v[s]);
+          tmem_wait_ld();
+          u64 acc[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            acc[j] = recombine8(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]) & mask;
+          const int64_t row = t * TC_ROWS + quad * 32 + lg * 16 + rq;
+          const int col = DB_HALF * h + c0 + cq;
+          if (row < rows)
+            *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
+          if (row + 8 < rows)
+            *reinterpret_cast<ulonglong2*>(out + (row + 8) * TC_D + col) = make_ulonglong2(acc[2], acc[3]);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
 // d = 16: out = P0 . M0 (+ P1 . M1) with K = 16 per operand, so the two
 // operands K-concatenate into ONE kind::i8 K-step of 32: a unit is a tile of
 // 128 rows, raw = two TMA boxes (P0's and P1's 16 coefficients of the rows),
@@ -579,4 +780,41 @@ extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, 
   gr_matmul2_tc16_kernel<<<grid, T16_THREADS, T16_SMEM, as_stream(stream)>>>(
       tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc16");
+}
+
+extern "C" int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows, const uint64_t* const* Ms,
+                                 uint64_t* const* outs, int q, uint64_t mask, void* stream) {
+  if (!p || !Ms || !outs || q < 1 || q > MQ_MAX || rows < 0 || (rs & 1) || (uintptr_t(p) & 15)) {
+    set_error("r3_gr_matmul_q_tc: bad arguments (1 <= q <= 4, 16-byte aligned rows)");
+    return R3_ERR_ARG;
+  }
+  if (rows == 0) return R3_OK;
+  if (rows > (int64_t(1) << 31) - TC_ROWS) {
+    set_error("r3_gr_matmul_q_tc: rows %lld exceed the TMA coordinate range", (long long)rows);
+    return R3_ERR_ARG;
+  }
+  MqArgs a{};
+  a.q = q;
+  for (int i = 0; i < q; ++i) {
+    if (!Ms[i] || !outs[i]) {
+      set_error("r3_gr_matmul_q_tc: null matrix or output");
+      return R3_ERR_ARG;
+    }
+    a.M[i] = reinterpret_cast<const u64*>(Ms[i]);
+    a.out[i] = reinterpret_cast<u64*>(outs[i]);
+  }
+  CUtensorMap tm;
+  if (!make_rows_tmap(&tm, p, rows, rs > 0 ? rs : TC_D, TC_ROWS)) {
+    set_error("r3_gr_matmul_q_tc: cuTensorMapEncodeTiled failed");
+    return R3_ERR_CUDA;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gr_matmul_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MQ_SMEM);
+    attr = true;
+  }
+  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  gr_matmul_q_kernel<<<grid, WS_THREADS, MQ_SMEM, as_stream(stream)>>>(tm, a, rows, mask);
+  return check_launch("r3_gr_matmul_q_tc");
 }

@@ -460,6 +460,22 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
                      C_add=lin((1, tmp)), out=out)
 
 
+def rows_times_multi(P: torch.Tensor, Ms: list, rows: int, width: int, outs: list) -> list:
+    """outs[k][r] = P[r] . Ms[k] for d = 64 and up to 4 matrices in one pass
+    over P (r3_gr_matmul_q_tc); other degrees / layouts one rows_times each."""
+    d = Ms[0].shape[0]
+    if d == 64 and len(Ms) <= 4 and _tc_ok(P) and all(o.is_contiguous() for o in outs):
+        if rows:
+            rs = P.stride(0) if P.shape[0] > 1 else d
+            pm = (C.c_void_p * len(Ms))(*[m.data_ptr() for m in Ms])
+            po = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+            call("r3_gr_matmul_q_tc", ptr(P), rs, rows, pm, po, len(Ms), ring_mask(width), stream())
+        return outs
+    for M, o in zip(Ms, outs):
+        rows_times(P, M, rows, width, out=o)
+    return outs
+
+
 # ---------------------------------------------------------------------------
 # u64 GEMM on the tensor cores (share-domain matmul)
 # ---------------------------------------------------------------------------

@@ -645,8 +645,8 @@ def _l2_tables_q4(party, q4, w1, ze2: torch.Tensor, gr: Ring):
         rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
         rows = pw4.shape[0]
         tabs = grvec.empty((4, rows, gr.d))        # every row is written below
-        for a in range(4):
-            grvec.rows_times(pw4, grvec.gr_mulmat(rk[a:a + 1], gr.mod), rows, gr.ell, out=tabs[a])
+        grvec.rows_times_multi(pw4, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(4)], rows, gr.ell,
+                               [tabs[a] for a in range(4)])
         return tabs, kappa, 4, rows * gr.d
     return _public(party, key, build)
 

@@ -104,6 +104,28 @@ def test_gr_matmul2_tc_line_eval(cuda, d, rows):
         np.testing.assert_array_equal(host(outb), ogr.mul(Xb, z, 64, d) & np.uint64(1))
 
 
+@pytest.mark.parametrize("rows,q", [(1, 4), (129, 4), (5000, 3), (70001, 4), (1 << 18, 2), (300, 1)])
+def test_gr_matmul_q_tc(cuda, rows, q):
+    """r3_gr_matmul_q_tc: one operand times q public matrices in one pass
+    (strided rows, partial last tile) against the oracle GR product."""
+    from oracle import gr as ogr
+    from paper_2411_09287_b200 import grvec, host
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    d = 64
+    mod = modulus_for_degree(d)
+    rng = np.random.default_rng(rows + q)
+    X = _rand(rng, (2 * rows, d))
+    zs = [_rand(rng, (1, d)) for _ in range(q)]
+    Xd = grvec.dev(X)[0::2]                       # strided rows, as the even half of a level
+    outs = [grvec.empty((rows, d)) for _ in range(q)]
+    grvec.rows_times_multi(Xd, [grvec.gr_mulmat(grvec.dev(z), mod) for z in zs], rows, 64, outs)
+    for z, o in zip(zs, outs):
+        np.testing.assert_array_equal(host(o), ogr.mul(X[0::2], z, 64, d))
+    outs63 = [grvec.empty((rows, d)) for _ in range(q)]
+    grvec.rows_times_multi(Xd, [grvec.gr_mulmat(grvec.dev(z), mod) for z in zs], rows, 63, outs63)
+    np.testing.assert_array_equal(host(outs63[-1]), ogr.mul(X[0::2], zs[-1], 64, d) & np.uint64((1 << 63) - 1))
+
+
 @pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
 def test_level_fold_matches_oracle(cuda, d, N):
     """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
