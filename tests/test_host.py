@@ -112,3 +112,40 @@ def test_reduction_rows_match_oracle_reduction():
             for _ in range(i):
                 p = gr.mul(p, xi, 64, d)
             np.testing.assert_array_equal(p[0], rows[i])
+
+
+def test_coop_scheduler_order_barriers_and_deadlock():
+    """The cooperative engine on CPU tensors: a message ring with round
+    barriers completes in the reference's round-robin order (global message
+    log P0 first), a Session.joint rendezvous hands every party its own
+    result, and a program where every party first waits on a message is a
+    deadlock (HarnessError), not a hang."""
+    import torch
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import Ring
+    from paper_2411_09287_b200.transport import HarnessError
+    ring = Ring(64)
+
+    def ring_prog(party):
+        nxt, prv = (party.role + 1) % 3, (party.role + 2) % 3
+        got = []
+        for k in range(4):
+            party.send(nxt, f"t{k}", torch.full((2,), 10 * party.role + k, dtype=torch.int64), ring)
+            got.append(int(party.recv(prv, f"t{k}", ring, 2)[0]))
+            party.round_barrier()
+        joint = party.sess.joint(("sum", 0), party.role, party.role + 1,
+                                 lambda ins: {r: sum(ins.values()) * 100 + r for r in ins})
+        return got, joint
+
+    sess = Session(seed=1, keep_messages=True)
+    res = sess.run(ring_prog)
+    assert [r[0] for r in res] == [[20, 21, 22, 23], [0, 1, 2, 3], [10, 11, 12, 13]]
+    assert [r[1] for r in res] == [600, 601, 602]
+    assert [m[0] for m in sess.transcript.messages[:3]] == [0, 1, 2]
+    assert sess.transcript.rounds[next(iter(sess.transcript.rounds))] == 4
+
+    def dead(party):
+        return party.recv((party.role + 1) % 3, "x", ring, 1)
+
+    with pytest.raises(HarnessError):
+        Session(seed=1).run(dead)
