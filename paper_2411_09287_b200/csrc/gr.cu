@@ -544,6 +544,77 @@ l1_fold_kernel(int nterms, const int64_t* __restrict__ coef_dev, CompPtrs xc, Co
   }
 }
 
+// Small degrees (d <= 16): one thread per pair.  The scalar leg products
+// of a pair are computed once (the D-threads-per-pair form above repeats
+// them in every coefficient lane) and the thread accumulates all D
+// coefficients of h(1)/h(2) from the two power rows (128-bit loads);
+// warp shuffles and one shared-memory pass reduce a block to 2 D atomics.
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+l1_fold_pair_kernel(int nterms, CompPtrs xc, CompPtrs yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
+                    const u64* __restrict__ pw, u64* __restrict__ out_h1, u64* __restrict__ out_h2,
+                    int64_t coef0, int64_t coef1, int64_t coef2, int64_t coef3) {
+  __shared__ u64 part[8][2 * D];
+  const int64_t coefs[4] = {coef0, coef1, coef2, coef3};
+  const int64_t npairs = (N + 1) / 2;
+  u64 h1[D], h2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) h1[k] = h2[k] = 0;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < npairs; j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i0 = 2 * j, i1 = 2 * j + 1;
+    const bool has1 = i1 < N;
+    const int64_t o0 = comp_off(i0, n, ks, ls);
+    const int64_t o1 = has1 ? comp_off(i1, n, ks, ls) : 0;
+    u64 c1 = 0, c2o = 0, c2e = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (t < nterms) {
+        const u64 cf = u64(coefs[t]);
+        const u64 x0 = __ldg(xc.p[t] + o0), y0 = __ldg(yc.p[t] + o0);
+        const u64 x1 = has1 ? __ldg(xc.p[t] + o1) : 0ull, y1 = has1 ? __ldg(yc.p[t] + o1) : 0ull;
+        const u64 g2 = 2 * y1 - y0;
+        c1 += cf * (x1 * y1);
+        c2o += cf * (2 * x1 * g2);
+        c2e -= cf * (x0 * g2);
+      }
+    }
+    const ulonglong2* r0 = reinterpret_cast<const ulonglong2*>(pw + qdiv64(i0, n) * D);
+    const ulonglong2* r1 = reinterpret_cast<const ulonglong2*>(pw + qdiv64(i1, n) * D);
+#pragma unroll
+    for (int q = 0; q < D / 2; ++q) {
+      const ulonglong2 w0 = __ldg(r0 + q);
+      const ulonglong2 w1 = has1 ? __ldg(r1 + q) : make_ulonglong2(0ull, 0ull);
+      h1[2 * q] += c1 * w1.x;
+      h1[2 * q + 1] += c1 * w1.y;
+      h2[2 * q] += c2o * w1.x + c2e * w0.x;
+      h2[2 * q + 1] += c2o * w1.y + c2e * w0.y;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      h1[k] += __shfl_down_sync(0xffffffffu, h1[k], off);
+      h2[k] += __shfl_down_sync(0xffffffffu, h2[k], off);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      part[warp][k] = h1[k];
+      part[warp][D + k] = h2[k];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * D) {
+    u64 v = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += part[w][threadIdx.x];
+    atomicAdd(threadIdx.x < D ? out_h1 + threadIdx.x : out_h2 + (threadIdx.x - D), v);
+  }
+}
+
 template <int D>
 __global__ void l1_line_x_kernel(int ncomp, CompPtrs xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                                  const u64* __restrict__ A, const u64* __restrict__ B, int64_t tq, OutPtrs out,
@@ -853,12 +924,22 @@ extern "C" int r3_vfy_l1_fold(int nterms, const int64_t* coef, const uint64_t* c
     cf[t] = coef[t];
   }
   const int64_t npairs = (N + 1) / 2;
-  R3_DISPATCH_D(d, ({
-                  constexpr int RP = 256 / D;
-                  unsigned grid = grid_for((npairs + RP - 1) / RP, 1, 4);
-                  l1_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, nullptr, xp, yp, N, n, ks, ls, (const u64*)pw,
-                                                         (u64*)out_h1, (u64*)out_h2, cf[0], cf[1], cf[2], cf[3]);
-                }));
+  if (d == 16 || d == 8) {
+    const unsigned grid = grid_for(npairs, 256, 4);
+    if (d == 16)
+      l1_fold_pair_kernel<16><<<grid, 256, 0, s>>>(nterms, xp, yp, N, n, ks, ls, (const u64*)pw, (u64*)out_h1,
+                                                   (u64*)out_h2, cf[0], cf[1], cf[2], cf[3]);
+    else
+      l1_fold_pair_kernel<8><<<grid, 256, 0, s>>>(nterms, xp, yp, N, n, ks, ls, (const u64*)pw, (u64*)out_h1,
+                                                  (u64*)out_h2, cf[0], cf[1], cf[2], cf[3]);
+  } else {
+    R3_DISPATCH_D(d, ({
+                    constexpr int RP = 256 / D;
+                    unsigned grid = grid_for((npairs + RP - 1) / RP, 1, 4);
+                    l1_fold_kernel<D><<<grid, 256, 0, s>>>(nterms, nullptr, xp, yp, N, n, ks, ls, (const u64*)pw,
+                                                           (u64*)out_h1, (u64*)out_h2, cf[0], cf[1], cf[2], cf[3]);
+                  }));
+  }
   int rc = check_launch("r3_vfy_l1_fold");
   if (rc) return rc;
   rc = finish_mask((u64*)out_h1, d, mask, s);
