@@ -1,3 +1,4 @@
+"""d = 16 tensor-core line evaluation against the oracle at multi-wave sizes (debug aid)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -1,3 +1,7 @@
+"""Secure-ReLU session timing with and without verification (debug aid).
+
+    python tools/relu_probe.py N
+"""
 import sys, time, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

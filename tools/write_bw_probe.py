@@ -1,3 +1,4 @@
+"""Pure-write vs copy HBM bandwidth (torch fill / copy of 8 GB) for the roofline of write-heavy kernels."""
 import torch
 x = torch.empty(1 << 30, dtype=torch.int64, device="cuda")  # 8 GB
 y = torch.empty(1 << 29, dtype=torch.int64, device="cuda")
