@@ -125,3 +125,28 @@ def test_matmul_512_trunc_against_plaintext(cuda):
     want = np.vectorize(lambda v: int(v) >> 16, otypes=[object])(exact)
     diff = np.abs(got.astype(object) - want)
     assert int(diff.max()) <= 1
+
+
+@pytest.mark.parametrize("n,lanes,d", [(64, 1 << 16, 16), (4, 1 << 18, 64)])
+def test_dot_log_at_scale_verdicts(cuda, n, lanes, d):
+    """Pi_bsv over a large dot log (the ReLU's n = 64 edaBits dots at d = 16,
+    short dots at d = 64; R = pick_r): the honest run verifies and opens
+    sum_k x_k y_k on every lane, and an additive error on one lane's leg of
+    the same log is caught."""
+    import programs
+    from paper_2411_09287_b200 import host, verify
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import reconstruct_clear
+    from paper_2411_09287_b200.transport import AbortError, AdversaryConfig, Injection
+    R = verify.pick_r(n * lanes, 64, d)
+    prog = programs.build("paper_2411_09287_b200").dotv
+    res = Session(seed=5).run(prog, n, lanes, d, R)
+    assert all(r["verdict"]["dot"] for r in res)
+    z = host(reconstruct_clear([r["z"] for r in res]))
+    assert z.shape == (lanes,)
+    adv = AdversaryConfig(corrupted=1, injections=[Injection("dot.mz", delta=3, gate=0, lane=lanes // 3)])
+    try:
+        res = Session(seed=5, adversary=adv).run(prog, n, lanes, d, R)
+    except AbortError:
+        return
+    assert not all(r["verdict"]["dot"] for r in res), "tampered dot log verified"
