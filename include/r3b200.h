@@ -201,6 +201,18 @@ int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows,
                       const uint64_t* const* Ms, uint64_t* const* outs, int q,
                       uint64_t mask, void* stream);
 
+/* Dense-level leg folds for d = 16 of up to four leg terms (several
+ * simulated parties) in one tensor-core pass: term k (x, y' = c0 y0 + c1 y1,
+ * (N, 16) row-major, y1 may be null) adds its h(1) = sum o_x (x) o_y' and
+ * h(2) = sum t_x (x) t_y' (t = 2 odd - even over row pairs) into the 31
+ * unreduced words acc1[party[k]] / acc2[party[k]] (zeroed here; parties
+ * without terms may pass null).  Same values as r3_vfy_level_fold per role
+ * (verify.py:229-231 via gates.py:92-106). */
+int r3_vfy_level_fold16_tc(int nterms, const int* party, const uint64_t* const* xs,
+                           const uint64_t* const* y0s, const uint64_t* const* y1s,
+                           const int64_t* c0, const int64_t* c1, int64_t N,
+                           uint64_t* const* acc1, uint64_t* const* acc2, void* stream);
+
 /* d = 16 form of r3_gr_matmul2_tc (rows of 16 coefficients, M0/M1 16 x 16):
  * both operands K-concatenate into one 32-byte kind::i8 K-step. */
 int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0,

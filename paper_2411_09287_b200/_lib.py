@@ -62,6 +62,9 @@ _SIGS = {
                      C.c_void_p],
     "r3_gr_matmul2_tc": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
     "r3_gr_matmul2_tc16": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
+    "r3_vfy_level_fold16_tc": [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                               C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64), i64,
+                               C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p],
     "r3_gr_matmul_q_tc": [u64p, i64, i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, u64,
                           C.c_void_p],
     "r3_limb_tiles_a": [u64p, u64, u64p, u64, i64, i64, u64p, C.c_void_p],

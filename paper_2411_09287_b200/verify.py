@@ -756,11 +756,54 @@ def _level_folds(role: int, X: dict, Y: dict, which: str, rows: int, gr: Ring) -
     return _dotsum_terms(pairs, rows, gr)
 
 
-def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring):
+_JOINT16_MIN_ROWS = 1 << 14
+
+
+def _level_folds_joint16(party, xt: dict, yt: dict, gr: Ring):
+    """d = 16 dense-level folds of all three simulated parties at once
+    (honest joint sessions): P1's and P2's four leg terms share one
+    tensor-core pass (r3_vfy_level_fold16_tc), P0's single term runs the
+    CUDA-core fold.  Each party deposits only its own component arrays and
+    takes only its own folds."""
+    role = party.role
+    names = ("total",) if role == 0 else ("m", "s1" if role == 1 else "s2")
+    mine = {"x": [xt[k].contiguous() for k in names], "y": [yt[k].contiguous() for k in names]}
+
+    def folds(slots):
+        N = slots[0]["x"][0].shape[0]
+        accs = {r: grvec.zeros((2, 2 * gr.d - 1)) for r in range(3)}
+        xa, ya = slots[0]["x"][0], slots[0]["y"][0]
+        call("r3_vfy_level_fold", 0, ptr(xa), None, ptr(ya), None, N, gr.d, ptr(accs[0][0]), ptr(accs[0][1]),
+             stream())
+        (m1x, s1x), (m1y, s1y) = slots[1]["x"], slots[1]["y"]
+        (m2x, s2x), (m2y, s2y) = slots[2]["x"], slots[2]["y"]
+        # P1: -(m_x s_y1) - (s_x1 m_y);  P2: m_x (m_y - s_y2) - s_x2 m_y
+        terms = [(1, m1x, s1y, None, -1, 0), (1, s1x, m1y, None, -1, 0),
+                 (2, m2x, m2y, s2y, 1, -1), (2, s2x, m2y, None, -1, 0)]
+        P = C.c_void_p
+        party_ids = (C.c_int * 4)(*[t[0] for t in terms])
+        xs = (P * 4)(*[t[1].data_ptr() for t in terms])
+        y0 = (P * 4)(*[t[2].data_ptr() for t in terms])
+        y1 = (P * 4)(*[None if t[3] is None else t[3].data_ptr() for t in terms])
+        c0 = (C.c_int64 * 4)(*[t[4] for t in terms])
+        c1 = (C.c_int64 * 4)(*[t[5] for t in terms])
+        a1 = (P * 3)(None, accs[1][0].data_ptr(), accs[2][0].data_ptr())
+        a2 = (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr())
+        call("r3_vfy_level_fold16_tc", 4, party_ids, xs, y0, y1, c0, c1, N, a1, a2, stream())
+        return {r: (grvec.reduce_poly(accs[r][0], gr.mod, gr.ell), grvec.reduce_poly(accs[r][1], gr.mod, gr.ell))
+                for r in range(3)}
+
+    return party.sess.joint(("fold16", party.next_id("_joint.fold16")), role, mine, folds)
+
+
+def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring, party=None):
     """Both folds of one party in one pass (r3_vfy_level_fold) when the
     component arrays are dense (N, d) rows; None -> use the dot-sum path."""
     if gr.d not in (16, 32, 64):
         return None
+    if (party is not None and gr.d == 16 and _joint_ok(party)
+            and next(iter(xt.values())).shape[0] >= _JOINT16_MIN_ROWS):
+        return _level_folds_joint16(party, xt, yt, gr)
     if role == 0:
         names = ("total", None)
     else:
@@ -808,7 +851,7 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     yt = {k: getattr(ys.mask, k) for k in names}
     if xs.m is not None:
         xt["m"], yt["m"] = xs.m, ys.m
-    fused = _level_folds_fused(role, xt, yt, gr)
+    fused = _level_folds_fused(role, xt, yt, gr, party)
     if fused is not None:
         fold1, fold2 = fused
     else:
@@ -1114,7 +1157,7 @@ class _DenseBatch:
             W1, W2, self.w1 = _l2_weights(party, self.ze1, gr)   # ze1 is the latest opening here
             fold = lambda W: _dotsum_terms([([(1, acc, 16)], [(1, W, 16)])], 16, gr)
             return fold(W1), fold(W2)
-        fused = _level_folds_fused(role, self.x, self.y, gr)
+        fused = _level_folds_fused(role, self.x, self.y, gr, party)
         if fused is not None:
             return fused
         X = {k: _Halves(t) for k, t in self.x.items()}

@@ -280,3 +280,38 @@ def test_staged_input_matches_host_input(cuda):
         np.testing.assert_array_equal(a[r][0], b[r][0])
     np.testing.assert_array_equal(a[0][0], xh.numpy().view(np.uint64) * yh.numpy().view(np.uint64))
     np.testing.assert_array_equal(a[1][1], b[1][1])
+
+
+@pytest.mark.parametrize("N", [2, 3, 1001, 40000, 1 << 18])
+def test_level_fold16_tc_matches_cuda_core(cuda, N):
+    """r3_vfy_level_fold16_tc (P1's and P2's four leg terms in one
+    tensor-core pass) equals the per-role CUDA-core r3_vfy_level_fold on the
+    same arrays, incl. odd N (zero odd tail) and a party without terms."""
+    import ctypes as C
+    import torch
+    from paper_2411_09287_b200 import _lib, grvec, host
+    d = 16
+    rng = np.random.default_rng(N)
+    arr = lambda: grvec.dev(_rand(rng, (N, d)))
+    m_x, m_y, s1x, s1y, s2x, s2y = (arr() for _ in range(6))
+
+    def core(role, xa, xb, ya, yb):
+        acc = torch.zeros((2, 2 * d - 1), dtype=torch.int64, device="cuda")
+        _lib.call("r3_vfy_level_fold", role, xa.data_ptr(), xb.data_ptr(), ya.data_ptr(), yb.data_ptr(), N, d,
+                  acc[0].data_ptr(), acc[1].data_ptr(), _lib.stream())
+        return host(acc)
+
+    want1 = core(1, m_x, s1x, m_y, s1y)
+    want2 = core(2, m_x, s2x, m_y, s2y)
+    accs = {r: torch.full((2, 2 * d - 1), 7, dtype=torch.int64, device="cuda") for r in (1, 2)}
+    terms = [(1, m_x, s1y, None, -1, 0), (1, s1x, m_y, None, -1, 0),
+             (2, m_x, m_y, s2y, 1, -1), (2, s2x, m_y, None, -1, 0)]
+    P = C.c_void_p
+    _lib.call("r3_vfy_level_fold16_tc", 4, (C.c_int * 4)(*[t[0] for t in terms]),
+              (P * 4)(*[t[1].data_ptr() for t in terms]), (P * 4)(*[t[2].data_ptr() for t in terms]),
+              (P * 4)(*[None if t[3] is None else t[3].data_ptr() for t in terms]),
+              (C.c_int64 * 4)(*[t[4] for t in terms]), (C.c_int64 * 4)(*[t[5] for t in terms]), N,
+              (P * 3)(None, accs[1][0].data_ptr(), accs[2][0].data_ptr()),
+              (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr()), _lib.stream())
+    np.testing.assert_array_equal(host(accs[1]), want1)
+    np.testing.assert_array_equal(host(accs[2]), want2)
