@@ -98,8 +98,9 @@ level_fold16_tc_kernel(const __grid_constant__ L16Args args) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int64_t item = blockIdx.x;
-  const int half = int(item & 1);                   // y terms {2 half, 2 half + 1}
-  const int64_t chunk = item >> 1;
+  const int ipc = args.nterms > 2 ? 2 : 1;          // items per chunk: y halves that hold terms
+  const int half = int(item % ipc);                 // y terms {2 half, 2 half + 1}
+  const int64_t chunk = item / ipc;
   const int64_t p0 = chunk * args.kc;
   const int64_t p1 = min(args.npairs, p0 + args.kc);
   const int64_t nkb = (p1 - p0 + L16_BK - 1) / L16_BK;
@@ -346,7 +347,7 @@ extern "C" int r3_vfy_level_fold16_tc(int nterms, const int* party, const uint64
   args.nterms = nterms;
   args.npairs = (N + 1) / 2;
   int64_t nchunks = (args.npairs + L16_MAX_K - 1) / L16_MAX_K;
-  const int64_t items_per_chunk = 2;
+  const int64_t items_per_chunk = nterms > 2 ? 2 : 1;
   const int64_t waves = (nchunks * items_per_chunk + kNumSMs - 1) / kNumSMs;
   int64_t want = waves * kNumSMs / items_per_chunk;   // fill the last wave
   const int64_t min_kc = 8 * L16_BK;

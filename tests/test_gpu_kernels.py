@@ -315,3 +315,12 @@ def test_level_fold16_tc_matches_cuda_core(cuda, N):
               (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr()), _lib.stream())
     np.testing.assert_array_equal(host(accs[1]), want1)
     np.testing.assert_array_equal(host(accs[2]), want2)
+    # P0's single term (one item per chunk)
+    acc0 = torch.full((2, 2 * d - 1), 5, dtype=torch.int64, device="cuda")
+    _lib.call("r3_vfy_level_fold16_tc", 1, (C.c_int * 1)(0), (P * 1)(s1x.data_ptr()), (P * 1)(s2y.data_ptr()),
+              (P * 1)(None), (C.c_int64 * 1)(1), (C.c_int64 * 1)(0), N,
+              (P * 3)(acc0[0].data_ptr(), None, None), (P * 3)(acc0[1].data_ptr(), None, None), _lib.stream())
+    acc_core = torch.zeros((2, 2 * d - 1), dtype=torch.int64, device="cuda")
+    _lib.call("r3_vfy_level_fold", 0, s1x.data_ptr(), None, s2y.data_ptr(), None, N, d,
+              acc_core[0].data_ptr(), acc_core[1].data_ptr(), _lib.stream())
+    np.testing.assert_array_equal(host(acc0), host(acc_core))
