@@ -150,3 +150,28 @@ def test_dot_log_at_scale_verdicts(cuda, n, lanes, d):
     except AbortError:
         return
     assert not all(r["verdict"]["dot"] for r in res), "tampered dot log verified"
+
+
+def test_mulv_d16_at_scale_honest_and_tamper(cuda):
+    """d = 16 multiplication logs large enough for the tensor-core base fold
+    (2^20 gates): the honest run verifies with z = x y, one tampered leg is
+    caught."""
+    from paper_2411_09287_b200 import host, verify
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import reconstruct_clear
+    from paper_2411_09287_b200.transport import AbortError, AdversaryConfig, Injection
+    N, d = 1 << 20, 16
+    R = verify.pick_r(N, 64, d)
+    res = Session(seed=21).run(_mulv_prog(N, d, R))
+    assert all(r[3] for r in res)
+    x = host(reconstruct_clear([r[0] for r in res]))
+    y = host(reconstruct_clear([r[1] for r in res]))
+    z = host(reconstruct_clear([r[2] for r in res]))
+    with np.errstate(over="ignore"):
+        np.testing.assert_array_equal(z, x * y)
+    adv = AdversaryConfig(corrupted=2, injections=[Injection("dot.mz", delta=1 << 40, gate=0, lane=12345)])
+    try:
+        res = Session(seed=21, adversary=adv).run(_mulv_prog(N, d, R))
+    except AbortError:
+        return
+    assert not all(r[3] for r in res), "tampered d = 16 multiplication verified"
