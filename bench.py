@@ -724,12 +724,12 @@ def run_b200(args):
                 if ev is not None:
                     ev.synchronize()
 
-    e2e_step(7, 0)
+    e2e_step(pdist.session_seed(rank, 0, stream=1), 0)
     e2e_drain()
     barrier()
     e0 = time.perf_counter()
     for i in range(args.e2e_steps):
-        out = e2e_step(70 + i, i % 2)
+        out = e2e_step(pdist.session_seed(rank, 1 + i, stream=1), i % 2)
     e2e_drain()
     barrier()
     e2e_s = pdist.max_over_ranks(time.perf_counter() - e0)

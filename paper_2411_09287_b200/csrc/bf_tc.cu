@@ -326,17 +326,13 @@ int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64
   // K-chunks of <= BF_MAX_K blocks, a whole number of chunks per CTA of a
   // persistent grid (no partial second wave)
   int64_t items = (nblk + BF_MAX_K - 1) / BF_MAX_K;
-  items = (items + kNumSMs - 1) / kNumSMs * kNumSMs;
+  items = (items + num_sms() - 1) / num_sms() * num_sms();
   int64_t kc = (nblk + items - 1) / items;
   kc = (kc + BF_BK - 1) / BF_BK * BF_BK;
   items = (nblk + kc - 1) / kc;
   args.kc = kc;
-  const unsigned grid = unsigned(items < kNumSMs ? items : kNumSMs);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(base_fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BF_SMEM);
-    attr = true;
-  }
+  const unsigned grid = unsigned(items < num_sms() ? items : num_sms());
+  ensure_smem(base_fold_tc_kernel, BF_SMEM);
   base_fold_tc_kernel<<<grid, BF_THREADS, BF_SMEM, s>>>(args);
   return check_launch("r3_vfy_base_fold_q4(tc)");
 }

@@ -226,7 +226,7 @@ extern "C" int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out, cons
     if (ndim - k0 == 2) {
       const int64_t R = shape[k0], L = shape[k0 + 1];
       const unsigned gy = unsigned(R < 65535 ? R : 65535);
-      const int64_t want = (int64_t(kNumSMs) * 8 + gy - 1) / gy;
+      const int64_t want = (int64_t(num_sms()) * 8 + gy - 1) / gy;
       const unsigned gx = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, (L + 255) / 256)));
       ew_2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(op, R, L, (u64*)out, (const u64*)a, a_strides[k0],
                                                 a_strides[k0 + 1], (const u64*)b, b ? b_strides[k0] : 0,
@@ -379,7 +379,7 @@ extern "C" int r3_sum_axis0(const uint64_t* a, int64_t n, int64_t inner, int64_t
     const int threads = inner >= 256 ? 256 : (inner >= 64 ? 64 : 32);
     const int64_t colblocks = (inner + threads - 1) / threads;
     // aim for ~8 resident blocks per SM in total
-    int64_t ychunks = (int64_t(kNumSMs) * 8 + colblocks - 1) / colblocks;
+    int64_t ychunks = (int64_t(num_sms()) * 8 + colblocks - 1) / colblocks;
     int64_t rows_per_block = (n + ychunks - 1) / ychunks;
     if (rows_per_block < 16) rows_per_block = 16;
     ychunks = (n + rows_per_block - 1) / rows_per_block;

@@ -797,12 +797,7 @@ extern "C" int r3_gr_matmul(r3_lin_operand A, const uint64_t* M, int has_c, r3_l
   case DD: {                                                                                   \
     constexpr int CG = DD / 4, RG = 256 / CG, BM = RG * 4;                                     \
     size_t smem = size_t(DD * DD + BM * DD) * 8;                                               \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
-      cudaFuncSetAttribute(gr_matmul_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                           int(smem));                                                         \
-      attr = true;                                                                             \
-    }                                                                                          \
+    ensure_smem(gr_matmul_kernel<DD>, int(smem));                                                   \
     unsigned grid = grid_for((rows + BM - 1) / BM, 1, 3);                                      \
     gr_matmul_kernel<DD><<<grid, 256, smem, s>>>(la, (const u64*)M, has_c, lc, (u64*)out, rows, \
                                                  mask);                                        \
@@ -832,7 +827,7 @@ extern "C" int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, in
     if (d == 4) gr_dotsum_small_kernel<4><<<grid, 256, 0, s>>>(lf, lg, rows, (u64*)acc);
     return check_launch("r3_gr_dotsum(small)");
   }
-  int64_t blocks = int64_t(kNumSMs) * 2;
+  int64_t blocks = int64_t(num_sms()) * 2;
   int64_t per = (rows + blocks - 1) / blocks;
   if (per < 64) per = 64;
   per = (per + 31) / 32 * 32;
@@ -841,12 +836,7 @@ extern "C" int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, in
 #define R3_DS(DD)                                                                                 \
   case DD: {                                                                                      \
     const size_t smem = size_t(4 * 32 * DD + 2 * DD) * 8;                                         \
-    static bool attr = false;                                                                     \
-    if (!attr) {                                                                                  \
-      cudaFuncSetAttribute(gr_dotsum_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                           int(smem));                                                            \
-      attr = true;                                                                                \
-    }                                                                                             \
+    ensure_smem(gr_dotsum_kernel<DD>, int(smem));                                                   \
     gr_dotsum_kernel<DD><<<unsigned(blocks), 256, smem, s>>>(lf, lg, rows, per, (u64*)acc);      \
   } break;
     R3_DS(8)
@@ -1010,7 +1000,7 @@ extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* x
     return level_fold_tc(role, xa, xb, ya, yb, N, acc1, acc2, s);
   LevelArrays la{(const u64*)xa, (const u64*)xb, (const u64*)ya, (const u64*)yb};
   const int64_t npairs = (N + 1) / 2;
-  int64_t blocks = kNumSMs;
+  int64_t blocks = num_sms();
   int64_t per = (npairs + blocks - 1) / blocks;
   if (per < 32) per = 32;
   per = (per + lf_bk(d) - 1) / lf_bk(d) * lf_bk(d);
@@ -1019,12 +1009,7 @@ extern "C" int r3_vfy_level_fold(int role, const uint64_t* xa, const uint64_t* x
   {                                                                                                     \
     constexpr int NARR = RR == 0 ? 2 : 4;                                                               \
     const size_t smem = size_t(3 * NARR * lf_bk(DD) * 2 * DD + 4 * DD) * 8;                             \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
-      cudaFuncSetAttribute(level_fold_kernel<DD, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                           int(smem));                                                                  \
-      attr = true;                                                                                      \
-    }                                                                                                   \
+    ensure_smem(level_fold_kernel<DD, RR>, int(smem));                                                  \
     level_fold_kernel<DD, RR><<<unsigned(blocks), 512, smem, s>>>(la, N, per, (u64*)acc1, (u64*)acc2); \
   }
 #define R3_LF_D(DD)                 \

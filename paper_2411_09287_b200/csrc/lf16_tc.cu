@@ -348,8 +348,8 @@ extern "C" int r3_vfy_level_fold16_tc(int nterms, const int* party, const uint64
   args.npairs = (N + 1) / 2;
   int64_t nchunks = (args.npairs + L16_MAX_K - 1) / L16_MAX_K;
   const int64_t items_per_chunk = nterms > 2 ? 2 : 1;
-  const int64_t waves = (nchunks * items_per_chunk + kNumSMs - 1) / kNumSMs;
-  int64_t want = waves * kNumSMs / items_per_chunk;   // fill the last wave
+  const int64_t waves = (nchunks * items_per_chunk + num_sms() - 1) / num_sms();
+  int64_t want = waves * num_sms() / items_per_chunk;   // fill the last wave
   const int64_t min_kc = 8 * L16_BK;
   if (want * min_kc > args.npairs) want = (args.npairs + min_kc - 1) / min_kc;
   if (want > nchunks) nchunks = want;
@@ -358,11 +358,7 @@ extern "C" int r3_vfy_level_fold16_tc(int nterms, const int* party, const uint64
   nchunks = (args.npairs + kc - 1) / kc;
   args.kc = kc;
   args.nchunks = nchunks;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(level_fold16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L16_SMEM);
-    attr = true;
-  }
+  ensure_smem(level_fold16_tc_kernel, L16_SMEM);
   level_fold16_tc_kernel<<<unsigned(nchunks * items_per_chunk), L16_THREADS, L16_SMEM, s>>>(args);
   return check_launch("r3_vfy_level_fold16_tc");
 }

@@ -328,8 +328,8 @@ int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64
   args.npairs = (N + 1) / 2;
   int64_t nchunks = (args.npairs + LF_MAX_K - 1) / LF_MAX_K;
   const int64_t per_chunk_items = 2 * args.nterms;
-  const int64_t waves = (nchunks * per_chunk_items + kNumSMs - 1) / kNumSMs;
-  int64_t want = waves * kNumSMs / per_chunk_items;  // fill the last wave
+  const int64_t waves = (nchunks * per_chunk_items + num_sms() - 1) / num_sms();
+  int64_t want = waves * num_sms() / per_chunk_items;  // fill the last wave
   const int64_t min_kc = 8 * LF_BK;
   if (want * min_kc > args.npairs) want = (args.npairs + min_kc - 1) / min_kc;
   if (want > nchunks) nchunks = want;
@@ -338,11 +338,7 @@ int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64
   nchunks = (args.npairs + kc - 1) / kc;
   args.kc = kc;
   args.nchunks = nchunks;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(level_fold_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LF_SMEM);
-    attr = true;
-  }
+  ensure_smem(level_fold_tc_kernel, LF_SMEM);
   const unsigned grid = unsigned(nchunks * per_chunk_items);
   level_fold_tc_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(args, (u64*)acc1, (u64*)acc2);
   return check_launch("r3_vfy_level_fold(tc)");

@@ -308,13 +308,9 @@ extern "C" int r3_u64_gemm_tc(int npairs, const uint8_t* const* a_tiles, const u
               (long long)ktot);
     return R3_ERR_ARG;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(u64_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MM_SMEM);
-    attr = true;
-  }
+  ensure_smem(u64_gemm_tc_kernel, MM_SMEM);
   const int64_t tiles = (M / MM_BM) * (N / MM_BN);
-  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
   u64_gemm_tc_kernel<<<grid, MM_THREADS, MM_SMEM, as_stream(stream)>>>(gp, M, N, (const u64*)addend, sub,
                                                                         (u64*)out, mask);
   return check_launch("r3_u64_gemm_tc");

@@ -133,18 +133,12 @@ prf_bits4_kernel(RoundKeys rk, u64 first, int nbits, int64_t lanes, u64* __restr
 constexpr int64_t kAes4MinBlocks = int64_t(1) << 16;
 
 static bool aes4_init() {
-  static bool ok = [] {
-    return cudaFuncSetAttribute(prf_ctr4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(prf_bits4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) ==
-               cudaSuccess;
-  }();
-  return ok;
+  return ensure_smem(prf_ctr4_kernel, kAes4Smem) && ensure_smem(prf_bits4_kernel, kAes4Smem);
 }
 
 static unsigned aes4_grid(int64_t work) {
   const int64_t g = (work + kAes4Threads - 1) / kAes4Threads;
-  return unsigned(g < kNumSMs ? g : kNumSMs);
+  return unsigned(g < num_sms() ? g : num_sms());
 }
 
 }  // namespace r3
@@ -177,8 +171,39 @@ __global__ void imad_peak_kernel(u64 seed, int iters, u64* __restrict__ sink) {
 }
 
 extern "C" int r3_imad_peak(int iters, uint64_t* sink, void* stream) {
-  imad_peak_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(0x243f6a8885a308d3ull, iters, (u64*)sink);
+  imad_peak_kernel<<<num_sms() * 8, 256, 0, as_stream(stream)>>>(0x243f6a8885a308d3ull, iters, (u64*)sink);
   return check_launch("r3_imad_peak");
+}
+
+int r3::num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+  }
+  return v;
+}
+
+bool r3::smem_attr_once(const void* func, int bytes) {
+  // (kernel, device) -> bytes already granted; a handful of entries
+  struct Entry { const void* f; int dev; int bytes; };
+  static std::mutex mu;
+  static Entry table[256];
+  static int used = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < used; ++i)
+    if (table[i].f == func && table[i].dev == dev && table[i].bytes >= bytes) return true;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (used < 256) table[used++] = {func, dev, bytes};
+  return true;
 }
 
 void r3::set_error(const char* fmt, ...) {

@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/r3b200.h"
@@ -17,7 +18,19 @@ namespace r3 {
 using u64 = unsigned long long;
 using u32 = unsigned int;
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on B200), queried once per device;
+// persistent grids and wave sizing use it.
+int num_sms();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per kernel
+// and device (the attribute is per device, and one process may drive
+// several GPUs or launch from several threads).  False if the attribute
+// could not be set.
+bool smem_attr_once(const void* func, int bytes);
+template <class F>
+inline bool ensure_smem(F* func, int bytes) {
+  return smem_attr_once(reinterpret_cast<const void*>(func), bytes);
+}
 
 // Thread-local last-error text for r3_last_error().
 void set_error(const char* fmt, ...);
@@ -40,7 +53,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline unsigned grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
   int64_t b = (work + threads - 1) / threads;
-  int64_t cap = int64_t(kNumSMs) * max_blocks_per_sm;
+  int64_t cap = int64_t(num_sms()) * max_blocks_per_sm;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return unsigned(b);

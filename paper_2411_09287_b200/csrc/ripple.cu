@@ -139,14 +139,12 @@ extern "C" int r3_ripple_msb(const uint32_t* rk01, const uint32_t* rk02, uint64_
     }
   }
   for (int q = 0; q < 3; ++q) out.msg[q] = reinterpret_cast<u64*>(msgs[q]);
-  static const bool attr =
-      cudaFuncSetAttribute(ripple_msb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAes4Smem) == cudaSuccess;
-  if (!attr) {
+  if (!ensure_smem(ripple_msb_kernel, kAes4Smem)) {
     set_error("r3_ripple_msb: cannot reserve %d bytes of shared memory", kAes4Smem);
     return R3_ERR_CUDA;
   }
   const int64_t blocks = (lanes + kRippleThreads - 1) / kRippleThreads;
-  const unsigned grid = unsigned(blocks < kNumSMs ? blocks : kNumSMs);
+  const unsigned grid = unsigned(blocks < num_sms() ? blocks : num_sms());
   ripple_msb_kernel<<<grid, kRippleThreads, kAes4Smem, as_stream(stream)>>>(k01, k02, o01, o02,
                                                                  reinterpret_cast<const u64*>(delta), in, out,
                                                                  ell, lanes, write_log);

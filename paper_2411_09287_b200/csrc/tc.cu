@@ -719,12 +719,8 @@ extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, co
   }
   if (nops == 1) tm[1] = tm[0];
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gr_matmul2_db_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DB_SMEM);
-    attr = true;
-  }
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
+  ensure_smem(gr_matmul2_db_kernel, DB_SMEM);
   gr_matmul2_db_kernel<<<grid, WS_THREADS, DB_SMEM, as_stream(stream)>>>(
       tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc");
@@ -770,13 +766,9 @@ extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, 
     }
   }
   if (nops == 1) tm[1] = tm[0];
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gr_matmul2_tc16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T16_SMEM);
-    attr = true;
-  }
+  ensure_smem(gr_matmul2_tc16_kernel, T16_SMEM);
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
   gr_matmul2_tc16_kernel<<<grid, T16_THREADS, T16_SMEM, as_stream(stream)>>>(
       tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
   return check_launch("r3_gr_matmul2_tc16");
@@ -808,13 +800,9 @@ extern "C" int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows, co
     set_error("r3_gr_matmul_q_tc: cuTensorMapEncodeTiled failed");
     return R3_ERR_CUDA;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gr_matmul_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MQ_SMEM);
-    attr = true;
-  }
+  ensure_smem(gr_matmul_q_kernel, MQ_SMEM);
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < kNumSMs ? tiles : kNumSMs);
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
   gr_matmul_q_kernel<<<grid, WS_THREADS, MQ_SMEM, as_stream(stream)>>>(tm, a, rows, mask);
   return check_launch("r3_gr_matmul_q_tc");
 }

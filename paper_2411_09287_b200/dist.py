@@ -89,9 +89,14 @@ def gather_outputs(t: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def session_seed(rank: int, step: int, base: int = 1000) -> int:
-    """Distinct, reproducible session seed per (rank, step)."""
-    return base * (rank + 1) + step
+def session_seed(rank: int, step: int, stream: int = 0) -> int:
+    """Distinct, reproducible 128-bit session seed per (stream, rank, step):
+    the three fields occupy disjoint bit ranges, so no two (rank, step)
+    pairs of any stream (warm-up, timed, end-to-end, side workloads) share
+    pairwise seeds or masks for step, rank < 2^32."""
+    if not (0 <= rank < 1 << 32 and 0 <= step < 1 << 32 and 0 <= stream < 1 << 64):
+        raise ValueError("session_seed: rank/step must be < 2^32, stream < 2^64")
+    return (stream << 64) | (rank << 32) | step
 
 
 def shard(n_total: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:

@@ -19,7 +19,10 @@ def pytest_configure(config):
 
 
 def load_golden(name: str):
-    z = np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False)
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    if not os.path.exists(path):
+        path = os.path.join(GOLDEN, "scale", f"{name}.npz")
+    z = np.load(path, allow_pickle=False)
     meta = json.loads(str(z["meta"]))
     arrays = {k: z[k] for k in z.files if k != "meta"}
     return meta, arrays
@@ -28,6 +31,10 @@ def load_golden(name: str):
 def golden_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
                   if not p.endswith("prf.npz"))
+
+
+def scale_golden_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "scale", "*.npz")))
 
 
 @pytest.fixture(scope="session")

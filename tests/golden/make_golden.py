@@ -84,7 +84,13 @@ def flatten_result(role: int, res, out: dict, prefix: str):
     raise TypeError(f"unhandled result type {type(res)} at {prefix}")
 
 
-def run_case(name, prog_name, args, kwargs, sess_kw, injection=None):
+def array_digest(a) -> str:
+    """SHA-256 of a uint64 array's little-endian words (C order); the same
+    function is applied to the GPU outputs by tests/test_gpu_golden_scale.py."""
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+
+
+def run_case(name, prog_name, args, kwargs, sess_kw, injection=None, hashed=False):
     progs = programs.build("ring3pc")
     prog = getattr(progs, prog_name)
     adv = None
@@ -118,11 +124,18 @@ def run_case(name, prog_name, args, kwargs, sess_kw, injection=None):
         "ref_seconds": dt,
     }
     arrays = dict(out["arrays"])
+    target = HERE
+    if hashed:
+        # config-scale cases: one digest + shape per array keeps the fixture small
+        meta["array_sha256"] = {k: [array_digest(v), list(v.shape)] for k, v in arrays.items()}
+        arrays = {}
+        target = os.path.join(HERE, "scale")
+        os.makedirs(target, exist_ok=True)
     # program inputs (so the GPU tests need nothing but this file)
     for i, a in enumerate(args):
         if isinstance(a, np.ndarray):
             arrays[f"arg{i}"] = a.astype(np.uint64)
-    np.savez_compressed(os.path.join(HERE, f"{name}.npz"),
+    np.savez_compressed(os.path.join(target, f"{name}.npz"),
                         meta=np.array(json.dumps(meta)), **arrays)
     return status, dt
 
@@ -157,10 +170,19 @@ def make_prf_golden():
 
 
 def main():
-    make_prf_golden()
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
+    ap.add_argument("--scale", action="store_true",
+                    help="only the config-scale cases (programs.SCALE_CASES), hashed fixtures")
     a = ap.parse_args()
+    if a.scale:
+        for name, prog, args, kwargs, sess_kw in programs.SCALE_CASES:
+            if a.only and a.only != name:
+                continue
+            st, dt = run_case(name, prog, args, kwargs, sess_kw, hashed=True)
+            print(f"{name:28s} {st:10s} {dt:7.2f}s", flush=True)
+        return
+    make_prf_golden()
     for name, prog, args, kwargs, sess_kw in programs.CASES:
         if a.only and a.only != name:
             continue

@@ -194,7 +194,7 @@ def build(pkg_name: str) -> SimpleNamespace:
         party.freeze_logs()
         return {"open": rec(party, acc, "x2"), "ea": rec(party, eda.arith, "ea")}
 
-    def matmul(party, Xv, Wv, t=16):
+    def matmul(party, Xv, Wv, t=16, check=False, d=16):
         """Share matmul + truncation as ppml.infer runs an FC layer
         (ppml.py:304-309, 320-328, 373-381, 412-427): X (M,K) owned by P2,
         W (K,N) owned by P1, gathered (K, M*N) operands, one Pi_dot with the
@@ -215,6 +215,8 @@ def build(pkg_name: str) -> SimpleNamespace:
         gw = lambda a: a[wi]
         g = gates.dot_prepare(party, xmask._map(gx), wmask._map(gw), lanes,
                               out_mask=tr.rx_mask)
+        if check:
+            verify.prepare_verification(party, d=d)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
         X = shc_input_online(party, 2, Xv.reshape(-1) if party.role == 2 else None,
@@ -227,10 +229,14 @@ def build(pkg_name: str) -> SimpleNamespace:
         party.round_barrier()
         z = gates.trunc_online(party, prod, tr)
         party.enter_phase(Phase.POST)
+        if check:
+            # ppml.py:440-445: verify every log before anything is opened
+            return {"verdict": verify.verify_session(party, d=d, R="auto"), "z": z,
+                    "open": rec(party, z, "z")}
         party.freeze_logs()
         return {"z": z, "open": rec(party, z, "z")}
 
-    def matmul_gemm(party, Xv, Wv, t=16):
+    def matmul_gemm(party, Xv, Wv, t=16, check=False, d=16):
         """The matmul program through the GEMM-form gate API
         (paper_2411_09287_b200 only: gates.matmul_prepare / matmul_finish);
         must reproduce the gathered-dot golden run exactly."""
@@ -242,6 +248,8 @@ def build(pkg_name: str) -> SimpleNamespace:
         wmask = shc_input_mask(party, 1, K * N, ring)
         tr = gates.trunc_prepare(party, M * N, t, ring)
         g = gates.matmul_prepare(party, xmask, wmask, M, K, N, out_mask=tr.rx_mask)
+        if check:
+            verify.prepare_verification(party, d=d)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
         X = shc_input_online(party, 2, Xv.reshape(-1) if party.role == 2 else None,
@@ -252,6 +260,9 @@ def build(pkg_name: str) -> SimpleNamespace:
         party.round_barrier()
         z = gates.trunc_online(party, prod, tr)
         party.enter_phase(Phase.POST)
+        if check:
+            return {"verdict": verify.verify_session(party, d=d, R="auto"), "z": z,
+                    "open": rec(party, z, "z")}
         party.freeze_logs()
         return {"z": z, "open": rec(party, z, "z")}
 
@@ -577,4 +588,18 @@ TAMPER_CASES = [
     ("tamper_mz_rec_abort", "mul_inputs", ([3], [4]), ("mz", 1, 1, 0, None), {"seed": 0}),
     ("tamper_circ_gamma", "circ", ("mixed",), ("gamma", 0, 1, 0, None), {"seed": 38}),
     ("tamper_vfy_gamma", "mulv", (64, 16, 3), ("vfy.dot.gamma", 0, 11, 2, 0), {"seed": 1004}),
+]
+
+
+# Config-scale cases: sizes where every multi-stage kernel
+# pipeline wraps (the d = 64 tensor-core base fold runs >= 4 K-steps per CTA,
+# the d = 16 joint level folds see >= 2^14 dense rows, the factorised
+# Pi_bsv runs six structured levels).  The reference takes tens of seconds
+# per case, so their fixtures keep a SHA-256 per array instead of the raw
+# words (tests/golden/scale/*.npz, make_golden.py --scale).
+SCALE_CASES = [
+    ("mulv_65536_d64_auto", "mulv", (65536, 64, 0), {"auto": True}, {"seed": 41}),
+    ("relu_4096_d16_auto", "relu", (_relu_inputs(4096, 2),), {}, {"seed": 42}),
+    ("mulv_40000_d16_auto", "mulv", (40000, 16, 0), {"auto": True}, {"seed": 43}),
+    ("matmul_v_24x64x40", "matmul", _mat_inputs(24, 64, 40, 5), {"check": True}, {"seed": 44}),
 ]

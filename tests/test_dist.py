@@ -52,6 +52,18 @@ def test_gloo_world2_plumbing():
     assert v0 and v1 and z0 != z1
 
 
+def test_session_seeds_are_collision_free():
+    from paper_2411_09287_b200.dist import session_seed
+    seen = {}
+    for stream in range(3):
+        for rank in range(8):
+            for step in list(range(1200)) + [2**32 - 1]:
+                s = session_seed(rank, step, stream)
+                assert s not in seen, (stream, rank, step, seen.get(s))
+                assert s < 2**128
+                seen[s] = (stream, rank, step)
+
+
 def test_shard_plan():
     from paper_2411_09287_b200.dist import shard
     parts = [shard(1000, 3, r, align=8) for r in range(3)]

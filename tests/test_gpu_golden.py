@@ -53,7 +53,7 @@ def run_case(name, engine="coop", prog_override=None, joint=True):
     from paper_2411_09287_b200.transport import AbortError, AdversaryConfig, Injection, DIGEST
 
     meta, arrays = load_golden(name)
-    spec = {c[0]: c for c in programs.CASES}
+    spec = {c[0]: c for c in programs.CASES + programs.SCALE_CASES}
     tspec = {c[0]: c for c in programs.TAMPER_CASES}
     if name in spec:
         _, prog_name, args, kwargs, sess_kw = spec[name]

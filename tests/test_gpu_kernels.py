@@ -324,3 +324,71 @@ def test_level_fold16_tc_matches_cuda_core(cuda, N):
     _lib.call("r3_vfy_level_fold", 0, s1x.data_ptr(), None, s2y.data_ptr(), None, N, d,
               acc_core[0].data_ptr(), acc_core[1].data_ptr(), _lib.stream())
     np.testing.assert_array_equal(host(acc0), host(acc_core))
+
+
+@pytest.mark.parametrize("N", [(1 << 16) + 37, 1 << 20])
+@pytest.mark.parametrize("joint", [True, False])
+def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
+    """r3_vfy_base_fold_q4 on the tensor cores (bf_tc.cu, d = 64) -- the
+    headline's base fold -- against its definition
+        acc'[a*4+b] = sum_j s^{ab}_j pw4[j],  zraw[c*4+a] = sum_j z_c[4j+a] pw4[j]
+    with s^{ab}_j = sum_t coef_t x_t[4j+a] y_t[4j+b] (verify.py:168-179 +
+    215-241 restated per block of four).  At these sizes every CTA of the
+    persistent grid runs >= 4 (2^16 + 37) and 56 (2^20) 32-block K-steps, so
+    the 3-stage TMA / mbarrier ring wraps many times; N = 2^16 + 37 also has
+    a ragged last block.  joint=True is the honest-session form (all three
+    parties' features in one pass), joint=False one launch per party."""
+    import ctypes as C
+    from paper_2411_09287_b200 import grvec, host, _lib
+    d = 64
+    rng = np.random.default_rng(N + 3)
+    nblk = (N + 3) // 4
+    pw4 = _rand(rng, (nblk, d))
+    roles = {0: [(1, 0, 0)], 1: [(-1, 0, 1), (-1, 1, 0)], 2: [(1, 0, 0), (-1, 0, 1), (-1, 1, 0)]}
+    data, want = {}, {}
+    for role, terms in roles.items():
+        xs = [_rand(rng, (N,)) for _ in range(2)]
+        ys = [_rand(rng, (N,)) for _ in range(2)]
+        zs = [_rand(rng, (N,)) for _ in range(1 if role == 0 else 2)]
+        data[role] = (terms, xs, ys, zs)
+        pad = lambda a: np.concatenate([a, np.zeros((-N) % 4, np.uint64)]).reshape(nblk, 4)
+        X, Y, Z = [pad(a) for a in xs], [pad(a) for a in ys], [pad(a) for a in zs]
+        with np.errstate(over="ignore"):
+            S = np.zeros((nblk, 16), np.uint64)
+            for cf, xi, yi in terms:
+                S += np.uint64(cf % 2**64) * (X[xi][:, :, None] * Y[yi][:, None, :]).reshape(nblk, 16)
+            acc = S.T @ pw4
+            zr = np.concatenate([z.T @ pw4 for z in Z]) if Z else np.zeros((4, d), np.uint64)
+        want[role] = (acc, zr)
+    D = grvec.dev
+    dev = {r: ([D(a) for a in v[1]], [D(a) for a in v[2]], [D(a) for a in v[3]]) for r, v in data.items()}
+    dpw4 = D(pw4)
+
+    def launch(rs):
+        P = C.c_void_p
+        n = len(rs)
+        nterms = (C.c_int * n)(*[len(roles[r]) for r in rs])
+        nz = (C.c_int * n)(*[len(dev[r][2]) for r in rs])
+        coef = (C.c_int64 * (3 * n))()
+        xs, ys, zp = (P * (3 * n))(), (P * (3 * n))(), (P * (2 * n))()
+        outs = {}
+        for q, r in enumerate(rs):
+            for t, (cf, xi, yi) in enumerate(roles[r]):
+                coef[3 * q + t], xs[3 * q + t], ys[3 * q + t] = cf, dev[r][0][xi].data_ptr(), dev[r][1][yi].data_ptr()
+            for c, zt in enumerate(dev[r][2]):
+                zp[2 * q + c] = zt.data_ptr()
+            # garbage-filled outputs: the entry point must initialise them
+            outs[r] = (grvec.dev(np.full((16, d), 0xDEADBEEF, np.uint64)),
+                       grvec.dev(np.full((4 * len(dev[r][2]), d), 0xDEADBEEF, np.uint64)))
+        zstr = (C.c_int64 * n)(*([1] * n))
+        acc = (P * n)(*[outs[r][0].data_ptr() for r in rs])
+        zr = (P * n)(*[outs[r][1].data_ptr() for r in rs])
+        _lib.call("r3_vfy_base_fold_q4", n, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+                  C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zstr), N, dpw4.data_ptr(), d,
+                  C.addressof(acc), C.addressof(zr), _lib.stream())
+        return outs
+
+    outs = launch([0, 1, 2]) if joint else {r: launch([r])[r] for r in roles}
+    for r in roles:
+        np.testing.assert_array_equal(host(outs[r][0]), want[r][0], err_msg=f"acc role {r}")
+        np.testing.assert_array_equal(host(outs[r][1]), want[r][1], err_msg=f"zraw role {r}")

@@ -1,0 +1,87 @@
+"""Session-level behaviour on the GPU: deferred digest checks abort a run
+whose openings disagree, and per-run state does not leak between runs."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mul_open_program():
+    from paper_2411_09287_b200 import gates
+    from paper_2411_09287_b200.sharing import Ring, rec, shc_input
+    from paper_2411_09287_b200.transport import Phase
+
+    def prog(party):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        party.enter_phase(Phase.ONLINE)
+        x = shc_input(party, 0, np.array([3, 5], np.uint64) if party.role == 0 else None, 2, ring, "x")
+        y = shc_input(party, 1, np.array([4, 6], np.uint64) if party.role == 1 else None, 2, ring, "y")
+        z = gates.mul(party, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        party.freeze_logs()
+        return rec(party, z, "z")
+    return prog
+
+
+def test_deferred_digest_mismatch_aborts(cuda):
+    """A payload altered in flight on an honest (deferred-check) session:
+    the mismatch is only counted on the device during the run, and run()
+    raises AbortError when it settles the counter."""
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.transport import AbortError, CoopRouter
+
+    class Tamper(CoopRouter):
+        done = False
+
+        def send(self, frm, to, phase, label, payload, cls="payload", count_bytes=None):
+            if label.startswith("h:") and not Tamper.done and hasattr(payload, "add_"):
+                payload = payload.clone()
+                payload.view(-1)[0] += 1
+                Tamper.done = True
+            return super().send(frm, to, phase, label, payload, cls, count_bytes)
+
+    sess = Session(seed=5, router_cls=Tamper)
+    assert not sess.eager_checks
+    with pytest.raises(AbortError):
+        sess.run(_mul_open_program())
+    assert Tamper.done
+    assert sess._deferred is None and sess._deferred_what == []
+    ok = Session(seed=5).run(_mul_open_program())
+    assert [int(v) for v in ok[0].cpu()] == [12, 30]
+
+
+def test_session_rerun_after_discarded_logs(cuda):
+    """A Session that ran an unverified program with discarded logs can run
+    a verified program afterwards (discard is scoped to one run)."""
+    from paper_2411_09287_b200 import gates, verify
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import Ring, shc_random
+    from paper_2411_09287_b200.transport import Phase
+
+    def unverified(party):
+        party.discard_logs()
+        return True
+
+    def verified(party):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        x = shc_random(party, 64, ring)
+        y = shc_random(party, 64, ring)
+        g = gates.mul_prepare(party, x.mask, y.mask, 64)
+        verify.prepare_verification(party, d=16, r_max=2)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        gates.mul_finish(party, g, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        return verify.batch_verify_muls(party, 64, d=16, R=2)
+
+    sess = Session(seed=9)
+    sess.run(unverified)
+    assert all(p.logs[k].discard for p in sess.parties for k in p.logs)
+    assert all(Session(seed=9).run(verified))

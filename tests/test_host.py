@@ -149,3 +149,16 @@ def test_coop_scheduler_order_barriers_and_deadlock():
 
     with pytest.raises(HarnessError):
         Session(seed=1).run(dead)
+
+
+def test_deferred_checks_refused_with_adversary():
+    """Digest checks of a session with an adversary must be eager (abort
+    points and the public-value cache key depend on it)."""
+    from paper_2411_09287_b200.rings import ConfigError
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.transport import AdversaryConfig, Injection
+    adv = AdversaryConfig(corrupted=1, injections=[Injection("mz", delta=1, gate=0, lane=0)])
+    with pytest.raises(ConfigError):
+        Session(seed=1, adversary=adv, checks="deferred")
+    assert Session(seed=1, adversary=adv).eager_checks
+    assert not Session(seed=1).eager_checks
