@@ -48,8 +48,10 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to test the N > 1 path on fewer GPUs than ranks")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-step-profile", action="store_true",
+                    help="skip the headline's per-kernel table and joint=False session")
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--relu-sweep-log2n", type=int, default=20)
@@ -64,40 +66,17 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port of the reference algorithm on host cores
+# CPU baselines: the unmodified reference on the host cores (bench_cpu.py)
 # ---------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    lanes, d, seed = args
-    from oracle import mpc
-    from oracle.verify_model import pick_r
-    R = pick_r(lanes, 64, d)
-    t0 = time.perf_counter()
-    res = mpc.mulv(seed=seed, lanes=lanes, d=d, R=R)
-    dt = time.perf_counter() - t0
-    assert res.verdict
-    return lanes, dt
-
-
-def cpu_baseline(d: int, budget_s: float) -> dict:
-    """Time the oracle port (numpy restatement of the reference's mulv path,
-    single-threaded numpy per process) on all host cores: one independent
-    session per process, throughput = total mults / wall time."""
-    import concurrent.futures as cf
-    cores = os.cpu_count() or 1
-    # size one session so each worker spends roughly budget/2 seconds
-    probe_lanes = 1 << 10
-    _, t_probe = _cpu_worker((probe_lanes, d, 1))
-    per_mult = t_probe / probe_lanes
-    lanes = 1 << max(10, min(16, int(math.log2(max(1, budget_s / 2 / per_mult)))))
-    t0 = time.perf_counter()
-    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
-        outs = list(ex.map(_cpu_worker, [(lanes, d, 100 + i) for i in range(cores)]))
-    wall = time.perf_counter() - t0
-    total = sum(o[0] for o in outs)
-    return {"value": total / wall, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cores} independent oracle-port mulv sessions x {lanes} mults, d={d}, "
-                      f"R=pick_r(lan), ell=64 (numpy restatement of ring3pc; wall {wall:.1f}s)"}
+def cpu_leg(workload: str, budget_s: float) -> dict:
+    """Same-run CPU baseline of one workload (rank 0, N = 1): the reference's
+    own program on every host core (bench_cpu.measure)."""
+    import bench_cpu
+    try:
+        return bench_cpu.measure(workload, budget_s=budget_s)
+    except Exception as e:  # noqa: BLE001 - a baseline failure must not sink the GPU line
+        return {"unavailable": f"{type(e).__name__}: {e}"[:300]}
 
 
 # ---------------------------------------------------------------------------
@@ -240,33 +219,97 @@ def make_relu_program(N: int, d: int = 16):
     return relu
 
 
-def relu_rates(N: int, d: int, steps: int) -> dict:
-    """Secure ReLU/s (execution and verified) on C1-shaped inputs."""
+def aes_blocks(sess) -> int:
+    """AES-128 blocks of keystream the session's protocol consumed: every
+    distinct pairwise stream (pair, domain) read up to its final offset
+    (both holders read the same words; the GPU generates them once)."""
+    seen = {}
+    for p in sess.parties:
+        for key, st in p._prgs.items():
+            seen[key] = max(seen.get(key, 0), st.offset)
+    return sum(-(-v // 16) for v in seen.values())
+
+
+def prf_peak_blocks(torch, lib) -> float:
+    """Measured bulk keystream rate of the PRF kernel (r3_prf_ctr, four-table
+    AES, 2^27 words = 2^26 blocks): the ceiling an AES-bound step runs
+    against (LDS-bound)."""
+    import ctypes as C
+    from paper_2411_09287_b200 import prg
+    rk = prg.round_keys(bytes(range(16)))
+    n = 1 << 27
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    lib.call("r3_prf_ctr", rk, 0, n, (1 << 64) - 1, 0, out.data_ptr(), lib.stream())
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        lib.call("r3_prf_ctr", rk, 0, n, (1 << 64) - 1, 0, out.data_ptr(), lib.stream())
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, (n // 2) / (a.elapsed_time(b) / 1e3))
+    del out
+    return best
+
+
+def relu_rates(N_total: int, d: int, steps: int, rank: int, world: int, prof: bool = True) -> dict:
+    """Secure ReLU/s (execution and verified) on C1-shaped inputs: N_total
+    lanes (normal(0, 4) fixed point, default_rng(1)) sharded over the ranks;
+    each rank runs its shard as one session (x owned by P0, relu_prepare /
+    relu_online / verify_session(d, auto) / open), the opened shards are
+    all-gathered to rank 0 and compared with max(x, 0) there.  Timing: CUDA
+    events around `steps` sessions per rank (host protocol driver included),
+    max over ranks."""
     import numpy as np
     import torch
+    from paper_2411_09287_b200 import _lib
+    from paper_2411_09287_b200 import dist as pdist
     from paper_2411_09287_b200.runtime import Session
+    n = N_total // world
     rng = np.random.default_rng(1)
-    xv = np.trunc(rng.normal(0, 4, N) * 2 ** 16).astype(np.int64)
-    xh = torch.from_numpy(xv).pin_memory()
-    want = np.where(xv >= 0, xv, 0)
-    prog = make_relu_program(N, d)
-    out = {"N": N, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s",
-           "timing": f"median of {steps} sessions after 2 warm-up sessions, wall clock incl. host"}
+    xv_all = np.trunc(rng.normal(0, 4, N_total) * 2 ** 16).astype(np.int64)
+    xh = torch.from_numpy(xv_all[rank * n:(rank + 1) * n].copy()).pin_memory()
+    want = np.where(xv_all >= 0, xv_all, 0)
+    prog = make_relu_program(n, d)
+    out = {"N": N_total, "N_per_gpu": n, "n_gpus": world, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s",
+           "timing": f"CUDA events around {steps} complete sessions per rank after 2 warm-up sessions, "
+                     f"max over ranks (host protocol driver inside the region)"}
     for check in (False, True):
+        key = "verified" if check else "exec"
         for w in range(2):                      # warm-up (allocator, tables)
-            Session(seed=1 + w).run(prog, xh, check)
-        times = []
+            Session(seed=pdist.session_seed(rank, w, stream=10)).run(prog, xh, check)
+        pdist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         for i in range(steps):
+            sess = Session(seed=pdist.session_seed(rank, 2 + i, stream=10 + check))
+            res = sess.run(prog, xh, check)
+        b.record()
+        torch.cuda.synchronize()
+        dt = pdist.max_over_ranks(a.elapsed_time(b) / 1e3 / steps)
+        full = pdist.gather_outputs(res[0])
+        if rank == 0:
+            got = full.cpu().numpy()
+            assert np.array_equal(got, want), "relu output mismatch"
+        out[key] = N_total / dt
+        out[key + "_ms"] = dt * 1e3
+        if not check:
+            out["aes_blocks_per_lane"] = aes_blocks(sess) / n
+        if prof and rank == 0:
+            # one more session under the per-call profiler (outside the timing)
+            cp = CallProfiler()
+            _lib.CALL_HOOK = cp.hook
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res = Session(seed=10 + i).run(prog, xh, check)
+            Session(seed=pdist.session_seed(rank, 99, stream=10 + check)).run(prog, xh, check)
             torch.cuda.synchronize()
-            times.append(time.perf_counter() - t0)
-        dt = statistics.median(times)
-        got = res[0].cpu().numpy()
-        assert np.array_equal(got, want), "relu output mismatch"
-        out["verified" if check else "exec"] = N / dt
-        out[("verified" if check else "exec") + "_ms"] = dt * 1e3
+            wall = time.perf_counter() - t0
+            _lib.CALL_HOOK = None
+            out[key + "_kernels"] = cp.table(wall)
+    out["check"] = "opened ReLU equals max(x, 0) on every lane (gathered on rank 0)"
     return out
 
 
@@ -307,101 +350,103 @@ def mulv_sweep(sizes, d: int, steps: int = 3) -> dict:
     return out
 
 
-def matmul_c3(n: int, steps: int) -> dict:
+def matmul_c3(n: int, steps: int, rank: int, world: int) -> dict:
     """BASELINE config C3: share-domain matmul n x n x n over Z_2^64 with
     truncation t = 16 (ppml linear-layer algebra, X owned by P2, W by P1,
     fixed-point encode(normal), default_rng(3)), through
-    gates.matmul_prepare/finish + trunc_prepare/trunc_online."""
+    gates.matmul_prepare/finish + trunc_prepare/trunc_online.  With N > 1
+    ranks the rows of X are sharded (each rank n/N x n x n against the whole
+    W) and the opened row blocks are all-gathered to rank 0."""
     import numpy as np
     import torch
-    from paper_2411_09287_b200 import gates
+    from paper_2411_09287_b200 import _lib, gates
+    from paper_2411_09287_b200 import dist as pdist
     from paper_2411_09287_b200.runtime import Session
     from paper_2411_09287_b200.sharing import Ring, rec, shc_input_mask, shc_input_online
     from paper_2411_09287_b200.transport import Phase
 
+    M = n // world
     rng = np.random.default_rng(3)
     Xf = rng.normal(0, 1, (n, n))
     Wf = rng.normal(0, 1 / 64, (n, n))
-    enc = lambda a: torch.from_numpy(np.trunc(a * 2 ** 16).astype(np.int64)).pin_memory()
-    Xh, Wh = enc(Xf), enc(Wf)
-    t_ev = {}
+    enc = lambda a: torch.from_numpy(np.ascontiguousarray(np.trunc(a * 2 ** 16).astype(np.int64))).pin_memory()
+    Xh, Wh = enc(Xf[rank * M:(rank + 1) * M]), enc(Wf)
 
     def prog(party, open_out):
         ring = Ring(64)
         party.enter_phase(Phase.PRE)
-        xm = shc_input_mask(party, 2, n * n, ring)
+        xm = shc_input_mask(party, 2, M * n, ring)
         wm = shc_input_mask(party, 1, n * n, ring)
-        tr = gates.trunc_prepare(party, n * n, 16, ring)
-        g = gates.matmul_prepare(party, xm, wm, n, n, n, out_mask=tr.rx_mask)
+        tr = gates.trunc_prepare(party, M * n, 16, ring)
+        g = gates.matmul_prepare(party, xm, wm, M, n, n, out_mask=tr.rx_mask)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
-        X = shc_input_online(party, 2, Xh.reshape(-1) if party.role == 2 else None, xm, n * n, ring, "X")
+        X = shc_input_online(party, 2, Xh.reshape(-1) if party.role == 2 else None, xm, M * n, ring, "X")
         W = shc_input_online(party, 1, Wh.reshape(-1) if party.role == 1 else None, wm, n * n, ring, "W")
         z = gates.trunc_online(party, gates.matmul_finish(party, g, X, W, log=False), tr)
         party.round_barrier()
         party.enter_phase(Phase.POST)
         party.freeze_logs()
-        return rec(party, z, "z").cpu() if open_out else None
+        return rec(party, z, "z") if open_out else None
 
-    from paper_2411_09287_b200 import _lib
-    out = Session(seed=3).run(prog, True)[0]
+    out = Session(seed=pdist.session_seed(rank, 0, stream=20)).run(prog, True)[0]
+    full = pdist.gather_outputs(out)
     torch.cuda.synchronize()
+    pdist.barrier()
     timer = KernelTimer("r3_u64_gemm_tc")
     _lib.CALL_HOOK = timer.hook
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for i in range(steps):
-        Session(seed=30 + i).run(prog, False)
+        Session(seed=pdist.session_seed(rank, 1 + i, stream=20)).run(prog, False)
     b.record()
     torch.cuda.synchronize()
     _lib.CALL_HOOK = None
-    sec = a.elapsed_time(b) / 1e3 / steps
+    sec = pdist.max_over_ranks(a.elapsed_time(b) / 1e3 / steps)
     gemm_s = timer.seconds()
-    cublas8 = int8_peak_ops(torch)
-    peak8 = max(cublas8, INT8_DENSE_NOMINAL)
-    # probabilistic truncation: |open - X W / 2^16| <= 1 ulp on sampled entries
-    rs = np.random.default_rng(5)
-    idx = rs.integers(0, n, (64, 2))
-    Xi, Wi = Xh.numpy(), Wh.numpy()
-    got = out.numpy().reshape(n, n)
-    exact = np.array([sum(int(Xi[r, k]) * int(Wi[k, c]) for k in range(n)) for r, c in idx], dtype=object)
-    want = np.array([int(v) >> 16 for v in exact], dtype=object)
-    err = max(abs(int(got[r, c]) - int(w)) for (r, c), w in zip(idx, want))
-    assert err <= 1, f"matmul+trunc off by {err}"
-    u64_macs = 5 * n ** 3     # P0 1, P1 2, P2 2 u64 GEMM MACs
-    return {"n": n, "ms_per_matmul": sec * 1e3, "matmuls_per_s": 1 / sec,
-            "u64_macs_per_s": u64_macs / sec, "int8_tops_equiv": 2 * 36 * u64_macs / sec / 1e12,
-            "check": "64 sampled outputs within 1 ulp of trunc(XW)",
-            "gemm_roofline": {"bound": "tensor", "kernel": "r3_u64_gemm_tc",
-                              "achieved": timer.work / gemm_s / 1e12 if gemm_s else None,
-                              "peak": peak8 / 1e12, "unit": "int8 TOP/s",
-                              "frac": timer.work / gemm_s / peak8 if gemm_s else None,
-                              "launches": timer.launches,
-                              "kernel_share_of_step": gemm_s / steps / sec,
-                              "cublaslt_int8_measured": cublas8 / 1e12,
-                              "peak_source": "nominal dense int8 of B200 (4.5 POPS; MEASURED_PEAKS.json has no "
-                                             "int8 entry and the in-run cuBLASLt int8 torch._int_mm 8192^3 "
-                                             "figure is below this kernel)",
-                              "work": "2 x 36 limb MACs x M x N x sum(K) per launch"},
-            "scope": "PRE (masks, trunc_prepare 2^24 lanes, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online)"}
-
-
-def ref_cpu_measured(*keys) -> dict | None:
-    """The unmodified reference's own CPU timings for the configs the oracle
-    port does not cover, measured in the build container by
-    tools/ref_cpu_timing.py (profiles/ref_cpu_timing.json; the Python
-    reference cannot travel to the GPU box)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ref_cpu_timing.json")) as f:
-            j = json.load(f)
-    except (OSError, ValueError):
-        return None
-    out = {k: j["results"][k] for k in keys if k in j["results"]}
-    out["host"] = j["host"]
-    out["source"] = "profiles/ref_cpu_timing.json (tools/ref_cpu_timing.py, build container, reference " \
-                    "pkg/src/ring3pc run unmodified, one single-threaded session)"
-    return out
+    res = {"n": n, "n_gpus": world, "rows_per_gpu": M, "ms_per_matmul": sec * 1e3, "matmuls_per_s": 1 / sec,
+           "u64_macs_per_s": n ** 3 / sec,
+           "scope": "PRE (masks, trunc_prepare, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online), "
+                    "one complete session per matmul"}
+    if rank == 0:
+        # probabilistic truncation: |open - X W / 2^16| <= 1 ulp on sampled entries
+        Xi = np.trunc(Xf * 2 ** 16).astype(np.int64)
+        Wi = np.trunc(Wf * 2 ** 16).astype(np.int64)
+        got = full.cpu().numpy().reshape(n, n)
+        rs = np.random.default_rng(5)
+        idx = rs.integers(0, n, (64, 2))
+        exact = [sum(int(Xi[r, k]) * int(Wi[k, c]) for k in range(n)) for r, c in idx]
+        err = max(abs(int(got[r, c]) - (int(v) >> 16)) for (r, c), v in zip(idx, exact))
+        assert err <= 1, f"matmul+trunc off by {err}"
+        res["check"] = "64 sampled outputs (gathered on rank 0) within 1 ulp of trunc(XW / 2^16)"
+        cublas8 = int8_peak_ops(torch)
+        peak8 = max(cublas8, INT8_DENSE_NOMINAL)
+        res["gemm_roofline"] = {
+            "bound": "tensor", "kernel": "r3_u64_gemm_tc",
+            "achieved": timer.work / gemm_s / 1e12 if gemm_s else None, "peak": peak8 / 1e12,
+            "unit": "int8 TOP/s", "frac": timer.work / gemm_s / peak8 if gemm_s else None,
+            "launches": timer.launches, "kernel_share_of_step": gemm_s / steps / sec,
+            "cublaslt_int8_measured": cublas8 / 1e12,
+            "peak_source": "nominal dense int8 of B200 (4.5 POPS; MEASURED_PEAKS.json has no int8 entry and "
+                           "the in-run cuBLASLt int8 torch._int_mm 8192^3 figure is below this kernel)",
+            "work": "2 x 36 limb MACs x M x N x sum(K) per launch"}
+        # whole-step kernel table (one more session under the per-call profiler)
+        cp = CallProfiler()
+        _lib.CALL_HOOK = cp.hook
+        t0 = time.perf_counter()
+        sess = Session(seed=pdist.session_seed(rank, 99, stream=20))
+        sess.run(prog, False)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        _lib.CALL_HOOK = None
+        res["kernels"] = cp.table(wall)
+        blocks = aes_blocks(sess)
+        res["aes_blocks"] = blocks
+        res["aes_roofline"] = {"bound": "aes", "achieved": blocks / sec / 1e9, "unit": "G AES blocks/s",
+                               "what": "keystream the session consumes (trunc_prepare bit matrices, masks) "
+                                       "over the whole matmul step"}
+    return res
 
 
 def _plain_forward(model, imgs):
@@ -431,63 +476,89 @@ def _plain_forward(model, imgs):
     return np.array(outs)
 
 
-def ppml_rates(name: str, batch: int, verified_batch: int, verified_total: int = 0) -> dict:
+def ppml_rates(name: str, batch: int, verified_batch: int, rank: int, world: int,
+               verified_total: int = 0) -> dict:
     """BASELINE configs 4 / 5: batched private inference through
     ppml.infer_batch (model owner P1, data owner P2, k = 16, d = 16, R auto),
     synthetic MNIST-shaped images normal(0, 1) from default_rng(0) and
     random-init weights.  Exec = PRE + ONLINE (no
-    verification), verified = with verify_session before the scores open."""
+    verification), verified = with verify_session before the scores open.
+    With N > 1 ranks the images are sharded (batch / N per rank, one
+    session each) and the opened scores all-gathered to rank 0, where they
+    are compared with a float forward pass."""
     import numpy as np
     import torch
-    from paper_2411_09287_b200 import ppml
+    from paper_2411_09287_b200 import _lib, ppml
+    from paper_2411_09287_b200 import dist as pdist
     from paper_2411_09287_b200.runtime import Session
     model = (ppml.secureml_model if name == "mlp" else ppml.lenet28_model)(np.random.default_rng(0))
     out = {"model": "SecureML MLP 784-128-128-10" if name == "mlp" else "LeNet-5 (28x28, pad 2)",
-           "unit": "images/s", "k": 16, "d": 16, "R": "auto"}
+           "unit": "images/s", "k": 16, "d": 16, "R": "auto", "n_gpus": world}
+    n_in = int(np.prod(model.input_shape))
     for check, B in ((False, batch), (True, verified_batch)):
         if not B:
             continue
-        imgs = np.random.default_rng(0).normal(0, 1, (B, int(np.prod(model.input_shape))))
+        b = B // world
+        imgs = np.random.default_rng(0).normal(0, 1, (B, n_in))
+        mine = imgs[rank * b:(rank + 1) * b]
         cfg = ppml.InferConfig(check=check)
-        prog = lambda party: ppml.infer_batch(party, model, imgs, cfg)
-        Session(seed=1).run(prog)
+        prog = lambda party: ppml.infer_batch(party, model, mine, cfg)
+        Session(seed=pdist.session_seed(rank, 0, stream=30 + check)).run(prog)
+        pdist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = Session(seed=2).run(prog)
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = Session(seed=pdist.session_seed(rank, 1, stream=30 + check)).run(prog)
+        e.record()
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        scores = ppml.decode(res[0][0], 16).reshape(B, -1)
-        err = float(np.abs(scores - _plain_forward(model, imgs)).max())
-        assert err < 0.05, f"{name} scores off by {err}"
+        dt = pdist.max_over_ranks(a.elapsed_time(e) / 1e3)
         if check:
             assert all(res[0][1].values()), "verification rejected"
+        full = pdist.gather_outputs(res[0][0])
         key = "verified" if check else "exec"
+        if rank == 0:
+            scores = ppml.decode(full, 16).reshape(B, -1)
+            err = float(np.abs(scores - _plain_forward(model, imgs)).max())
+            assert err < 0.05, f"{name} scores off by {err}"
+            out[key + "_max_abs_err_vs_float"] = err
+            cp = CallProfiler()
+            _lib.CALL_HOOK = cp.hook
+            t0 = time.perf_counter()
+            Session(seed=pdist.session_seed(rank, 99, stream=30 + check)).run(prog)
+            torch.cuda.synchronize()
+            _lib.CALL_HOOK = None
+            out[key + "_kernels"] = cp.table(time.perf_counter() - t0)
         out[key] = B / dt
         out[key + "_batch"] = B
         out[key + "_ms"] = dt * 1e3
-        out[key + "_max_abs_err_vs_float"] = err
     if verified_total > verified_batch > 0:
         # the config batch, verified: sequential sessions of verified_batch
-        # images (one session's gate logs for the whole config batch exceed
-        # HBM), each a complete PRE / ONLINE / verify / open run
-        imgs = np.random.default_rng(1).normal(0, 1, (verified_total, int(np.prod(model.input_shape))))
+        # images per rank, each a complete PRE / ONLINE / verify / open run
+        imgs = np.random.default_rng(1).normal(0, 1, (verified_total, n_in))
         cfg = ppml.InferConfig(check=True)
-        want = _plain_forward(model, imgs)
-        err = 0.0
+        per_rank = verified_total // world
+        lo_r = rank * per_rank
+        outs = []
+        pdist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for i, lo in enumerate(range(0, verified_total, verified_batch)):
-            part = imgs[lo:lo + verified_batch]
-            res = Session(seed=100 + i).run(lambda party: ppml.infer_batch(party, model, part, cfg))
+        for i, lo in enumerate(range(lo_r, lo_r + per_rank, verified_batch)):
+            part = imgs[lo:min(lo + verified_batch, lo_r + per_rank)]
+            res = Session(seed=pdist.session_seed(rank, 100 + i, stream=32)).run(
+                lambda party: ppml.infer_batch(party, model, part, cfg))
             assert all(res[0][1].values()), "verification rejected"
-            sc = ppml.decode(res[0][0], 16).reshape(part.shape[0], -1)
-            err = max(err, float(np.abs(sc - want[lo:lo + part.shape[0]]).max()))
+            outs.append(res[0][0])
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        assert err < 0.05, f"{name} scores off by {err}"
-        out["verified_config_batch"] = {"images": verified_total, "sessions": -(-verified_total // verified_batch),
-                                        "images_per_s": verified_total / dt, "ms": dt * 1e3,
-                                        "max_abs_err_vs_float": err}
+        dt = pdist.max_over_ranks(time.perf_counter() - t0)
+        full = pdist.gather_outputs(torch.cat(outs))
+        if rank == 0:
+            sc = ppml.decode(full, 16).reshape(verified_total, -1)
+            err = float(np.abs(sc - _plain_forward(model, imgs)).max())
+            assert err < 0.05, f"{name} scores off by {err}"
+            out["verified_config_batch"] = {"images": verified_total,
+                                            "sessions_per_gpu": -(-per_rank // verified_batch),
+                                            "images_per_s": verified_total / dt, "ms": dt * 1e3,
+                                            "max_abs_err_vs_float": err}
     return out
 
 
@@ -519,14 +590,66 @@ class KernelTimer:
         return sum(a.elapsed_time(b) for a, b in self.events) / 1e3
 
 
+class CallProfiler:
+    """CUDA events around EVERY library call (side workloads, outside the
+    timed regions): per-entry-point device time, launches and algorithmic
+    work, for the kernel tables and rooflines of the side configs."""
+
+    def __init__(self):
+        self.events = {}
+        self.work = {}
+
+    def hook(self, name, args, run):
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = run()
+        b.record()
+        self.events.setdefault(name, []).append((a, b))
+        self.work[name] = self.work.get(name, 0) + work_of(name, args)
+        return rc
+
+    def seconds(self, name: str) -> float:
+        return sum(a.elapsed_time(b) for a, b in self.events.get(name, ())) / 1e3
+
+    def table(self, wall_s: float, top: int = 5) -> dict:
+        import torch
+        torch.cuda.synchronize()
+        rows = sorted(((self.seconds(n), n) for n in self.events), reverse=True)
+        busy = sum(t for t, _ in rows)
+        return {"wall_ms": wall_s * 1e3, "device_busy_ms": busy * 1e3,
+                "launches": sum(len(v) for v in self.events.values()),
+                "top": [{"entry_point": n, "ms": t * 1e3, "share_of_wall": t / wall_s if wall_s else None,
+                         "launches": len(self.events[n]), **self.roofline(n, t)} for t, n in rows[:top]]}
+
+    def roofline(self, name: str, secs: float) -> dict:
+        bound = KERNEL_BOUND.get(name)
+        if bound is None or not secs or not self.work.get(name):
+            return {}
+        kind, unit, scale = bound
+        return {"bound": kind, "achieved": self.work[name] / secs / scale, "unit": unit}
+
+
 def work_of(name, args) -> int:
     """Algorithmic work of one call: bytes moved for the HBM-bound tensor-core
     line evaluations (r3_gr_matmul2_tc reads nops rows of 512 B and writes one
     per output row), u64 multiply-accumulates for the CUDA-core
     GR contractions."""
-    if name == "r3_gr_matmul2_tc":
+    if name in ("r3_gr_matmul2_tc", "r3_gr_matmul2_tc16"):
+        w = 512 if name == "r3_gr_matmul2_tc" else 128
         p1, nv0, nv1, rows = args[3], int(args[2]), int(args[5]), int(args[9])
-        return 512 * (rows + min(nv0, rows) + (min(nv1, rows) if p1 else 0))
+        return w * (rows + min(nv0, rows) + (min(nv1, rows) if p1 else 0))
+    if name == "r3_prf_ctr":
+        return -(-int(args[2]) // 2)                       # AES blocks
+    if name == "r3_prf_bits_packed":
+        return -(-int(args[2]) * int(args[3]) // 2)        # nbits x lanes words
+    if name == "r3_ripple_msb":
+        lanes, ell = int(args[6]), int(args[7])
+        return 3 * (ell - 2) * lanes // 2                  # 3 words per gate and lane
+    if name == "r3_ew_flat":
+        n, b = int(args[1]), args[4]
+        return 8 * n * (3 if b else 2)                     # bytes
     if name == "r3_u64_gemm_tc":
         npairs, K, M, N = int(args[0]), args[3], int(args[4]), int(args[5])
         return 2 * 36 * M * N * sum(int(K[p]) for p in range(npairs))
@@ -546,6 +669,12 @@ def work_of(name, args) -> int:
 
 KERNEL_BOUND = {
     "r3_gr_matmul2_tc": ("hbm", "GB/s", 1e9),
+    "r3_gr_matmul2_tc16": ("hbm", "GB/s", 1e9),
+    "r3_ew_flat": ("hbm", "GB/s", 1e9),
+    "r3_u64_gemm_tc": ("tensor", "int8 TOP/s", 1e12),
+    "r3_prf_ctr": ("aes", "G AES blocks/s", 1e9),
+    "r3_prf_bits_packed": ("aes", "G AES blocks/s", 1e9),
+    "r3_ripple_msb": ("aes", "G AES blocks/s", 1e9),
     "r3_vfy_level_fold": ("int-alu", "Tu64MAC/s", 1e12),
     "r3_gr_matmul": ("int-alu", "Tu64MAC/s", 1e12),
     "r3_gr_dotsum": ("int-alu", "Tu64MAC/s", 1e12),
@@ -739,14 +868,70 @@ def run_b200(args):
             xs, ys = shard_inputs(r)
             assert np.array_equal(got[r], xs.view(np.uint64) * ys.view(np.uint64)), "e2e product mismatch"
 
+    # the headline step's whole-step kernel table and the per-party rate
+    # (rank 0; outside the timed region): one session under the per-call
+    # profiler, and one session with joint kernels off -- every party's
+    # local kernels launched per party, pairwise PRF draws and m-derived
+    # line evaluations still shared
+    step_kernels = per_party = None
+    if rank == 0 and not args.no_step_profile:
+        cp = CallProfiler()
+        _lib.CALL_HOOK = cp.hook
+        torch.cuda.synchronize()
+        tp = time.perf_counter()
+        Session(seed=pdist.session_seed(rank, 1 << 20)).run(mulv)
+        torch.cuda.synchronize()
+        _lib.CALL_HOOK = None
+        step_kernels = cp.table(time.perf_counter() - tp)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record()
+        ok = Session(seed=pdist.session_seed(rank, (1 << 20) + 1), joint=False).run(mulv)
+        b_ev.record()
+        torch.cuda.synchronize()
+        assert all(ok)
+        pp = a_ev.elapsed_time(b_ev) / 1e3
+        per_party = {"value": N / pp, "unit": UNIT, "ms_per_step": pp * 1e3,
+                     "what": "one session with joint kernels off (Session(joint=False)): each simulated "
+                             "party launches its own kernels; the headline's joint launches batch the "
+                             "three parties' local work, which a one-party-per-host deployment cannot"}
+
+    # side configs, every rank; sharded over the
+    # ranks, outputs all-gathered to rank 0 and checked there
+    side = {}
+    if args.matmul_n:
+        side["matmul"] = matmul_c3(args.matmul_n, 3, rank, world)
+    if args.relu_log2n:
+        side["relu"] = relu_rates(1 << args.relu_log2n, 16, 5, rank, world)
+    if args.relu_sweep_log2n:
+        # weak scaling: 2^L lanes per GPU
+        side["relu_sweep"] = relu_rates((1 << args.relu_sweep_log2n) * world, 16, 3, rank, world)
+    if args.mlp_batch:
+        side["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch, rank, world)
+    if args.lenet_batch:
+        side["lenet"] = ppml_rates("lenet", args.lenet_batch, args.lenet_verified_batch, rank, world,
+                                   args.lenet_batch)
+    if world == 1 and args.mulv_sweep:
+        side["mulv_sweep"] = mulv_sweep([int(v) for v in args.mulv_sweep.split(",")], d)
+
     if rank != 0:
         pdist.finalize()
         return
+    if "relu" in side or "relu_sweep" in side:
+        prf_peak = prf_peak_blocks(torch, _lib)
+        for key in ("relu", "relu_sweep"):
+            r = side.get(key)
+            if r and "aes_blocks_per_lane" in r:
+                ach = r["exec"] * r["aes_blocks_per_lane"]
+                r["roofline"] = {"bound": "aes", "leg": "exec", "achieved": ach / 1e9, "peak": prf_peak / 1e9,
+                                 "unit": "G AES blocks/s", "frac": ach / prf_peak,
+                                 "peak_source": "measured in-run: r3_prf_ctr bulk keystream rate (2^26 blocks)",
+                                 "work": "AES blocks of keystream the protocol consumes per lane (every "
+                                         "distinct pairwise stream up to its final offset) x lanes / exec time"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic: PRF-generated (AES-128-CTR) random shares, seed per rank/step",
+        "data": "synthetic: PRF-generated (AES-128-CTR) random shares, distinct seed per rank and step",
         "config": {"workload": "mulv: batched 3PC Pi_mul + GR(2^64,d) batch verification "
                                "(tests/test_acceptance.py:124-136), 3 parties per GPU",
                    "N_per_gpu": N, "ell": 64, "d": d, "R": R, "engine": args.engine,
@@ -768,41 +953,38 @@ def run_b200(args):
         "clocks": clk.summary(),
         "wall_s_timed": wall,
     }
-    if world == 1:  # single-GPU side measurements and the CPU baseline (rank 0, N = 1 only)
-        if args.matmul_n:
-            line["matmul"] = matmul_c3(args.matmul_n, 3)
-        if args.relu_log2n:
-            line["relu"] = relu_rates(1 << args.relu_log2n, 16, 5)
-            line["relu"]["reference_cpu_measured"] = ref_cpu_measured(
-                "relu_exec_4096", "relu_exec_16384", "relu_verified_4096")
-        if args.relu_sweep_log2n:
-            line["relu_sweep"] = relu_rates(1 << args.relu_sweep_log2n, 16, 3)
-        if args.mulv_sweep:
-            line["mulv_sweep"] = mulv_sweep([int(v) for v in args.mulv_sweep.split(",")], d)
-        if args.mlp_batch:
-            line["mlp"] = ppml_rates("mlp", args.mlp_batch, args.mlp_verified_batch)
-            line["mlp"]["reference_cpu_measured"] = ref_cpu_measured("mlp_exec_1", "mlp_verified_1")
-        if args.lenet_batch:
-            line["lenet"] = ppml_rates("lenet", args.lenet_batch, args.lenet_verified_batch, args.lenet_batch)
-            line["lenet"]["reference_cpu_measured"] = ref_cpu_measured("lenet28_exec_1")
-        if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(d, args.cpu_seconds)
+    if step_kernels is not None:
+        line["step_kernels"] = step_kernels
+        line["per_party_rate"] = per_party
+    line.update(side)
+    if world == 1 and not args.no_cpu_baseline:
+        # same-run CPU baselines (rank 0, N = 1): the unmodified reference on
+        # every host core, one leg per config
+        line["cpu_baseline"] = cpu_leg("mulv", args.cpu_seconds)
+        legs = {"relu": ("relu_exec", "relu_verified"), "matmul": ("matmul",),
+                "mlp": ("mlp_exec", "mlp_verified"), "lenet": ("lenet_exec",)}
+        for key, works in legs.items():
+            if key in line:
+                cb = {w: cpu_leg(w, args.cpu_seconds / 2) for w in works}
+                line[key]["cpu_baseline"] = cb if len(cb) > 1 else cb[works[0]]
     print(json.dumps(line), flush=True)
     pdist.finalize()
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the
-    host cores, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (the unmodified ring3pc from baseline/_ref, bench_cpu.py) on the host
+    cores, rank 0 only; each step one bounded parallel round of mulv
+    sessions.  Falls back to the oracle port if the reference is absent."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    d = args.d
-    vals = []
+    import bench_cpu
+    ex = bench_cpu.pool()
     for _ in range(args.warmup):
-        cpu_baseline(d, args.cpu_seconds / 4)
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(d, args.cpu_seconds))
+        bench_cpu.measure("mulv", budget_s=0.0, max_rounds=1, executor=ex)
+    vals = [bench_cpu.measure("mulv", budget_s=0.0, max_rounds=1, executor=ex) for _ in range(args.steps)]
+    ex.shutdown()
     v = statistics.median(x["value"] for x in vals)
     cb = dict(vals[-1])
     cb["value"] = v
@@ -810,8 +992,10 @@ def run_reference(args):
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "impl": "reference",
             "data": "synthetic: PRF-generated random shares",
-            "config": {"workload": "mulv (CPU oracle port of the reference algorithm)", "d": d,
-                       "ell": 64},
+            "config": {"workload": "mulv: batched 3PC Pi_mul + GR(2^64,d) batch verification "
+                                   "(tests/test_acceptance.py:124-136), the reference's own CPU code",
+                       "N_per_session": bench_cpu.WORKLOADS["mulv"][0], "d": args.d, "ell": 64,
+                       "R": "pick_r(lan)"},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

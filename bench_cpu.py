@@ -21,7 +21,7 @@ time of the parallel round.  Only bench.py (its cpu_baseline legs and
 from __future__ import annotations
 
 import concurrent.futures as cf
-import math
+import functools
 import multiprocessing as mp
 import os
 import platform
@@ -49,6 +49,7 @@ def host_info() -> dict:
             "python": platform.python_version(), "numpy": np.__version__}
 
 
+@functools.lru_cache(maxsize=None)
 def reference_status() -> str | None:
     """None if the unmodified reference imports from baseline/_ref, else why not."""
     if not os.path.isdir(os.path.join(REF_DIR, "ring3pc")):
@@ -215,8 +216,17 @@ def _job(args):
     return time.perf_counter() - t0
 
 
+def pool(procs: int | None = None) -> cf.ProcessPoolExecutor:
+    """A warmed-up pool of spawned worker processes (one per core by default)."""
+    procs = procs or os.cpu_count() or 1
+    ex = cf.ProcessPoolExecutor(max_workers=procs, mp_context=mp.get_context("spawn"))
+    list(ex.map(_noop, range(procs)))
+    ex.procs = procs
+    return ex
+
+
 def measure(name: str, procs: int | None = None, budget_s: float = 10.0, size: int | None = None,
-            seed0: int = 100, max_rounds: int = 64) -> dict:
+            seed0: int = 100, max_rounds: int = 64, executor: cf.ProcessPoolExecutor | None = None) -> dict:
     """Whole-host throughput of one workload: `procs` independent reference
     sessions at a time (default: every logical core), rounds repeated until
     `budget_s` of wall time has passed (at least one round)."""
@@ -228,11 +238,10 @@ def measure(name: str, procs: int | None = None, budget_s: float = 10.0, size: i
         if name != "mulv":
             return {"unavailable": why, "unit": unit}
         kind = "port"
-    procs = procs or os.cpu_count() or 1
-    ctx = mp.get_context("spawn")
-    with cf.ProcessPoolExecutor(max_workers=procs, mp_context=ctx) as ex:
-        # spin the workers up (imports) outside the timed rounds
-        list(ex.map(_noop, range(procs)))
+    own = executor is None
+    ex = pool(procs) if own else executor
+    procs = ex.procs
+    try:
         t0 = time.perf_counter()
         per = []
         rounds = 0
@@ -240,6 +249,9 @@ def measure(name: str, procs: int | None = None, budget_s: float = 10.0, size: i
             per += list(ex.map(_job, [(name, n, seed0 + rounds * procs + i, kind) for i in range(procs)]))
             rounds += 1
         wall = time.perf_counter() - t0
+    finally:
+        if own:
+            ex.shutdown()
     units = _units(name, n) * procs * rounds
     src = ("unmodified reference ring3pc from baseline/_ref, Session(engine='threads')" if kind == "reference"
            else f"oracle port oracle/mpc.py (reference not importable: {why})")
