@@ -19,6 +19,7 @@ Prints one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -58,6 +59,8 @@ def parse():
     ap.add_argument("--mulv-sweep", default="20,22,26",
                     help="comma list of log2 batch sizes for the config-2 sweep on one GPU ('' = off)")
     ap.add_argument("--matmul-n", type=int, default=4096)
+    ap.add_argument("--matmul-verified-rows", type=int, default=256,
+                    help="rows of X per verified C3 session (0 = skip the verified C3 leg)")
     ap.add_argument("--mlp-batch", type=int, default=4096)
     ap.add_argument("--mlp-verified-batch", type=int, default=4096)
     ap.add_argument("--lenet-batch", type=int, default=1024)
@@ -274,22 +277,25 @@ def relu_rates(N_total: int, d: int, steps: int, rank: int, world: int, prof: bo
     want = np.where(xv_all >= 0, xv_all, 0)
     prog = make_relu_program(n, d)
     out = {"N": N_total, "N_per_gpu": n, "n_gpus": world, "d": d, "R": "auto (pick_r, lan)", "unit": "ReLU/s",
-           "timing": f"CUDA events around {steps} complete sessions per rank after 2 warm-up sessions, "
-                     f"max over ranks (host protocol driver inside the region)"}
+           "timing": f"median of {steps} complete sessions per rank (CUDA events around each, host protocol "
+                     f"driver inside the region) after 2 warm-up sessions, max over ranks"}
     for check in (False, True):
         key = "verified" if check else "exec"
         for w in range(2):                      # warm-up (allocator, tables)
             Session(seed=pdist.session_seed(rank, w, stream=10)).run(prog, xh, check)
+        gc.collect()
         pdist.barrier()
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        times = []
         for i in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
             sess = Session(seed=pdist.session_seed(rank, 2 + i, stream=10 + check))
             res = sess.run(prog, xh, check)
-        b.record()
-        torch.cuda.synchronize()
-        dt = pdist.max_over_ranks(a.elapsed_time(b) / 1e3 / steps)
+            b.record()
+            b.synchronize()
+            times.append(a.elapsed_time(b) / 1e3)
+        dt = pdist.max_over_ranks(statistics.median(times))
         full = pdist.gather_outputs(res[0])
         if rank == 0:
             got = full.cpu().numpy()
@@ -350,7 +356,7 @@ def mulv_sweep(sizes, d: int, steps: int = 3) -> dict:
     return out
 
 
-def matmul_c3(n: int, steps: int, rank: int, world: int) -> dict:
+def matmul_c3(n: int, steps: int, rank: int, world: int, verified_rows: int = 256) -> dict:
     """BASELINE config C3: share-domain matmul n x n x n over Z_2^64 with
     truncation t = 16 (ppml linear-layer algebra, X owned by P2, W by P1,
     fixed-point encode(normal), default_rng(3)), through
@@ -359,7 +365,7 @@ def matmul_c3(n: int, steps: int, rank: int, world: int) -> dict:
     W) and the opened row blocks are all-gathered to rank 0."""
     import numpy as np
     import torch
-    from paper_2411_09287_b200 import _lib, gates
+    from paper_2411_09287_b200 import _lib, gates, verify
     from paper_2411_09287_b200 import dist as pdist
     from paper_2411_09287_b200.runtime import Session
     from paper_2411_09287_b200.sharing import Ring, rec, shc_input_mask, shc_input_online
@@ -372,21 +378,34 @@ def matmul_c3(n: int, steps: int, rank: int, world: int) -> dict:
     enc = lambda a: torch.from_numpy(np.ascontiguousarray(np.trunc(a * 2 ** 16).astype(np.int64))).pin_memory()
     Xh, Wh = enc(Xf[rank * M:(rank + 1) * M]), enc(Wf)
 
-    def prog(party, open_out):
+    def prog(party, open_out, rows=None, check=False):
+        """One session over `rows` (default: all M) rows of this rank's X
+        block; check=True logs the GEMM-form dot batch and the truncation's
+        bit dots and runs verify_session(d=16, R=auto) before opening
+        (ppml.py:440-445; the factorised Pi_bsv of verify.py section 3c)."""
+        lo, hi = rows if rows is not None else (0, M)
+        m = hi - lo
         ring = Ring(64)
         party.enter_phase(Phase.PRE)
-        xm = shc_input_mask(party, 2, M * n, ring)
+        xm = shc_input_mask(party, 2, m * n, ring)
         wm = shc_input_mask(party, 1, n * n, ring)
-        tr = gates.trunc_prepare(party, M * n, 16, ring)
-        g = gates.matmul_prepare(party, xm, wm, M, n, n, out_mask=tr.rx_mask)
+        tr = gates.trunc_prepare(party, m * n, 16, ring)
+        g = gates.matmul_prepare(party, xm, wm, m, n, n, out_mask=tr.rx_mask)
+        if check:
+            verify.prepare_verification(party, d=16)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
-        X = shc_input_online(party, 2, Xh.reshape(-1) if party.role == 2 else None, xm, M * n, ring, "X")
+        X = shc_input_online(party, 2, Xh[lo:hi].reshape(-1) if party.role == 2 else None, xm, m * n, ring, "X")
         W = shc_input_online(party, 1, Wh.reshape(-1) if party.role == 1 else None, wm, n * n, ring, "W")
-        z = gates.trunc_online(party, gates.matmul_finish(party, g, X, W, log=False), tr)
+        z = gates.trunc_online(party, gates.matmul_finish(party, g, X, W, log=check), tr)
         party.round_barrier()
         party.enter_phase(Phase.POST)
-        party.freeze_logs()
+        if check:
+            v = verify.verify_session(party, d=16, R="auto")
+            if not all(v.values()):
+                party.abort("verification failed")
+        else:
+            party.freeze_logs()
         return rec(party, z, "z") if open_out else None
 
     out = Session(seed=pdist.session_seed(rank, 0, stream=20)).run(prog, True)[0]
@@ -409,17 +428,43 @@ def matmul_c3(n: int, steps: int, rank: int, world: int) -> dict:
            "u64_macs_per_s": n ** 3 / sec,
            "scope": "PRE (masks, trunc_prepare, Gamma) + ONLINE (inputs H2D, GEMM legs, trunc_online), "
                     "one complete session per matmul"}
+    vfull = None
+    if verified_rows:
+        # verified C3: the same n x n x n matmul + truncation with every log
+        # verified, as sessions over row blocks of `verified_rows` rows (one
+        # session's truncation bit-dot log for all n^2 outputs -- 64 x 2^24
+        # logged products -- exceeds HBM in the dense verification levels)
+        blocks = [(lo, min(M, lo + verified_rows)) for lo in range(0, M, verified_rows)]
+        Session(seed=pdist.session_seed(rank, 0, stream=21)).run(prog, False, blocks[0], True)
+        torch.cuda.synchronize()
+        pdist.barrier()
+        a.record()
+        vouts = []
+        for i, blk in enumerate(blocks):
+            vouts.append(Session(seed=pdist.session_seed(rank, 1 + i, stream=21)).run(prog, True, blk, True)[0])
+        b.record()
+        torch.cuda.synchronize()
+        vsec = pdist.max_over_ranks(a.elapsed_time(b) / 1e3)
+        vfull = pdist.gather_outputs(torch.cat([v.reshape(-1) for v in vouts]))
+        res["verified"] = {"ms_per_matmul": vsec * 1e3, "matmuls_per_s": 1 / vsec,
+                           "sessions_per_gpu": len(blocks), "rows_per_session": verified_rows,
+                           "d": 16, "R": "auto", "verdict": "every session accepted (verify_session)",
+                           "scope": "per session: PRE, ONLINE, verify_session over the GEMM-form dot batch "
+                                    "(factorised Pi_bsv) and the truncation bit dots, open"}
     if rank == 0:
         # probabilistic truncation: |open - X W / 2^16| <= 1 ulp on sampled entries
         Xi = np.trunc(Xf * 2 ** 16).astype(np.int64)
         Wi = np.trunc(Wf * 2 ** 16).astype(np.int64)
-        got = full.cpu().numpy().reshape(n, n)
         rs = np.random.default_rng(5)
         idx = rs.integers(0, n, (64, 2))
         exact = [sum(int(Xi[r, k]) * int(Wi[k, c]) for k in range(n)) for r, c in idx]
-        err = max(abs(int(got[r, c]) - (int(v) >> 16)) for (r, c), v in zip(idx, exact))
-        assert err <= 1, f"matmul+trunc off by {err}"
-        res["check"] = "64 sampled outputs (gathered on rank 0) within 1 ulp of trunc(XW / 2^16)"
+        for what, t in (("exec", full), ("verified", vfull)):
+            if t is None:
+                continue
+            got = t.cpu().numpy().reshape(n, n)
+            err = max(abs(int(got[r, c]) - (int(v) >> 16)) for (r, c), v in zip(idx, exact))
+            assert err <= 1, f"matmul+trunc ({what}) off by {err}"
+        res["check"] = "64 sampled outputs (gathered on rank 0) within 1 ulp of trunc(XW / 2^16), exec and verified"
         cublas8 = int8_peak_ops(torch)
         peak8 = max(cublas8, INT8_DENSE_NOMINAL)
         res["gemm_roofline"] = {
@@ -899,7 +944,7 @@ def run_b200(args):
     # ranks, outputs all-gathered to rank 0 and checked there
     side = {}
     if args.matmul_n:
-        side["matmul"] = matmul_c3(args.matmul_n, 3, rank, world)
+        side["matmul"] = matmul_c3(args.matmul_n, 3, rank, world, args.matmul_verified_rows)
     if args.relu_log2n:
         side["relu"] = relu_rates(1 << args.relu_log2n, 16, 5, rank, world)
     if args.relu_sweep_log2n:
@@ -960,7 +1005,7 @@ def run_b200(args):
     if world == 1 and not args.no_cpu_baseline:
         # same-run CPU baselines (rank 0, N = 1): the unmodified reference on
         # every host core, one leg per config
-        line["cpu_baseline"] = cpu_leg("mulv", args.cpu_seconds)
+        line["cpu_baseline"] = cpu_leg("mulv", args.cpu_seconds / 2)
         legs = {"relu": ("relu_exec", "relu_verified"), "matmul": ("matmul",),
                 "mlp": ("mlp_exec", "mlp_verified"), "lenet": ("lenet_exec",)}
         for key, works in legs.items():

@@ -72,7 +72,7 @@ WORKLOADS = {
              "mulv (tests/test_acceptance.py:124-136): {n} mults, d=64, R=pick_r(lan), ell=64"),
     "relu_exec": (1 << 14, "ReLU/s",
                   "secure ReLU (nonlinear.py:295-319), {n} lanes, owner P0, no verification"),
-    "relu_verified": (1 << 12, "ReLU/s",
+    "relu_verified": (1 << 10, "ReLU/s",
                       "secure ReLU, {n} lanes + verify_session(d=16, R=auto)"),
     "matmul": (256, "share-matmul MACs/s",
                "share matmul {n}x{n}x{n} + truncation t=16 (ppml FC-layer algebra, gathered Pi_dot, "

@@ -45,7 +45,7 @@ def _flatten(role, res, out, prefix, MVal, host):
     out["arrays"][f"p{role}.{prefix}"] = host(res)
 
 
-def run_case(name, engine="coop", prog_override=None, joint=True):
+def run_case(name, engine="coop", prog_override=None, joint=True, pkg=PKG):
     import programs
     from paper_2411_09287_b200 import host
     from paper_2411_09287_b200.runtime import Session
@@ -65,7 +65,7 @@ def run_case(name, engine="coop", prog_override=None, joint=True):
     args = tuple(arrays[f"arg{i}"] if f"arg{i}" in arrays else a for i, a in enumerate(args))
     # reference-primitive programs whose B200 counterpart is a different API
     prog_override = prog_override or GEMM_FORM.get(prog_name)
-    prog = getattr(programs.build(PKG), prog_override or prog_name)
+    prog = getattr(programs.build(pkg), prog_override or prog_name)
     adv = None
     if inj is not None:
         site, who, delta, gate, lane = inj
@@ -153,6 +153,33 @@ def test_matmul_gemm_form_matches_gathered_golden(cuda, name):
     assert status == meta["status"]
     counters = sorted([[f, t, p.value, c, n] for (f, t, p, c), n in sess.transcript.counters.items()])
     assert counters == meta["counters"]
+    assert _per_sender(log) == _per_sender([tuple(x) for x in meta["payloads"]])
+    want = {k: v for k, v in arrays.items() if not k.startswith("arg")}
+    for k, v in want.items():
+        np.testing.assert_array_equal(out["arrays"][k].reshape(v.shape), v, err_msg=k)
+
+
+@pytest.mark.parametrize("name", ["mulv_1024_d64_R7", "relu_64", "infer1_mlp_tiny"])
+def test_golden_through_ring3pc_import_path(cuda, name):
+    """Unmodified reference-shaped programs written against `ring3pc`
+    (tests/programs.py builds them from `ring3pc.gates`, `ring3pc.verify`,
+    ...) run on the GPU through pkg/src/ring3pc and match the reference."""
+    import os
+    import sys
+    from conftest import ROOT
+    src = os.path.join(ROOT, "pkg", "src")
+    sys.path.insert(0, src)
+    try:
+        for k in [k for k in sys.modules if k == "ring3pc" or k.startswith("ring3pc.")]:
+            del sys.modules[k]
+        import ring3pc
+        assert ring3pc.__file__.startswith(src)
+        meta, arrays, sess, log, out, status = run_case(name, pkg="ring3pc")
+    finally:
+        sys.path.remove(src)
+        for k in [k for k in sys.modules if k == "ring3pc" or k.startswith("ring3pc.")]:
+            del sys.modules[k]
+    assert status == meta["status"]
     assert _per_sender(log) == _per_sender([tuple(x) for x in meta["payloads"]])
     want = {k: v for k, v in arrays.items() if not k.startswith("arg")}
     for k, v in want.items():

@@ -88,18 +88,11 @@ def test_relu_2_18_matches_plaintext(cuda):
     np.testing.assert_array_equal(out.cpu().numpy(), np.where(xv >= 0, xv, 0))
 
 
-def test_matmul_512_trunc_against_plaintext(cuda):
-    """Share matmul 512^3 + probabilistic truncation (t = 16): every opened
-    entry is within one ulp of floor(X W / 2^16) (gates.py:248-302)."""
+def _matmul_prog(n, X, W, check):
     import torch
-    from paper_2411_09287_b200 import gates
-    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200 import gates, verify
     from paper_2411_09287_b200.sharing import Ring, rec, shc_input_mask, shc_input_online
     from paper_2411_09287_b200.transport import Phase
-    n = 512
-    rng = np.random.default_rng(9)
-    X = np.trunc(rng.normal(0, 1, (n, n)) * 2 ** 16).astype(np.int64)
-    W = np.trunc(rng.normal(0, 1 / 16, (n, n)) * 2 ** 16).astype(np.int64)
 
     def prog(party):
         ring = Ring(64)
@@ -108,23 +101,62 @@ def test_matmul_512_trunc_against_plaintext(cuda):
         wm = shc_input_mask(party, 1, n * n, ring)
         tr = gates.trunc_prepare(party, n * n, 16, ring)
         g = gates.matmul_prepare(party, xm, wm, n, n, n, out_mask=tr.rx_mask)
+        if check:
+            verify.prepare_verification(party, d=16)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
         Xs = shc_input_online(party, 2, torch.from_numpy(X.reshape(-1)) if party.role == 2 else None, xm,
                               n * n, ring, "X")
         Ws = shc_input_online(party, 1, torch.from_numpy(W.reshape(-1)) if party.role == 1 else None, wm,
                               n * n, ring, "W")
-        z = gates.trunc_online(party, gates.matmul_finish(party, g, Xs, Ws, log=False), tr)
+        z = gates.trunc_online(party, gates.matmul_finish(party, g, Xs, Ws, log=check), tr)
         party.round_barrier()
         party.enter_phase(Phase.POST)
-        party.freeze_logs()
-        return rec(party, z, "z").cpu().numpy()
+        verdict = None
+        if check:
+            verdict = verify.verify_session(party, d=16, R="auto")
+        else:
+            party.freeze_logs()
+        return rec(party, z, "z").cpu().numpy(), verdict
+    return prog
 
-    got = Session(seed=2).run(prog)[0].reshape(n, n)
+
+@pytest.mark.parametrize("check", [False, True])
+def test_matmul_512_trunc_against_plaintext(cuda, check):
+    """Share matmul 512^3 + probabilistic truncation (t = 16): every opened
+    entry is within one ulp of floor(X W / 2^16) (gates.py:248-302); with
+    check=True the GEMM-form dot log (factorised Pi_bsv, nine structured
+    levels) and the truncation bit dots are verified first and accepted."""
+    from paper_2411_09287_b200.runtime import Session
+    n = 512
+    rng = np.random.default_rng(9)
+    X = np.trunc(rng.normal(0, 1, (n, n)) * 2 ** 16).astype(np.int64)
+    W = np.trunc(rng.normal(0, 1 / 16, (n, n)) * 2 ** 16).astype(np.int64)
+    got, verdict = Session(seed=2).run(_matmul_prog(n, X, W, check))[0]
+    if check:
+        assert verdict and all(verdict.values()), verdict
     exact = X.astype(object).dot(W.astype(object))
     want = np.vectorize(lambda v: int(v) >> 16, otypes=[object])(exact)
-    diff = np.abs(got.astype(object) - want)
+    diff = np.abs(got.reshape(n, n).astype(object) - want)
     assert int(diff.max()) <= 1
+
+
+@pytest.mark.parametrize("site,who", [("mz", 1), ("z", 2), ("gamma", 0)])
+def test_matmul_512_verified_tamper_aborts(cuda, site, who):
+    """One tampered lane in the 512^3 share matmul (the P1 -> P2 leg, a
+    party's local output share, or P0's Gamma deal of the GEMM gate) is
+    caught by the verified session: run() raises AbortError."""
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.transport import AbortError, AdversaryConfig, Injection
+    n = 512
+    rng = np.random.default_rng(10)
+    X = np.trunc(rng.normal(0, 1, (n, n)) * 2 ** 16).astype(np.int64)
+    W = np.trunc(rng.normal(0, 1 / 16, (n, n)) * 2 ** 16).astype(np.int64)
+    # gate ids of kind "dot": the truncation's two bit dots are dealt first
+    # (trunc_prepare), then the GEMM gate
+    adv = AdversaryConfig(corrupted=who, injections=[Injection(site, delta=1, gate=2, lane=12345)])
+    with pytest.raises(AbortError):
+        Session(seed=3, adversary=adv).run(_matmul_prog(n, X, W, True))
 
 
 @pytest.mark.parametrize("n,lanes,d", [(64, 1 << 16, 16), (4, 1 << 18, 64)])

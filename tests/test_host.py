@@ -162,3 +162,27 @@ def test_deferred_checks_refused_with_adversary():
         Session(seed=1, adversary=adv, checks="deferred")
     assert Session(seed=1, adversary=adv).eager_checks
     assert not Session(seed=1).eager_checks
+
+
+def test_ring3pc_import_path_is_the_b200_package():
+    """pkg/src/ring3pc: `import ring3pc` (the reference's import path)
+    resolves every reference submodule to the B200 implementation."""
+    import importlib
+    import sys
+    src = os.path.join(ROOT, "pkg", "src")
+    sys.path.insert(0, src)
+    try:
+        for k in [k for k in sys.modules if k == "ring3pc" or k.startswith("ring3pc.")]:
+            del sys.modules[k]
+        r = importlib.import_module("ring3pc")
+        assert r.__file__.startswith(src)
+        import paper_2411_09287_b200 as impl
+        for name in r.SUBMODULES:
+            mod = importlib.import_module(f"ring3pc.{name}")
+            assert mod is importlib.import_module(f"paper_2411_09287_b200.{name}")
+        from ring3pc.runtime import Session
+        assert Session is impl.Session and r.Phase is impl.Phase
+    finally:
+        sys.path.remove(src)
+        for k in [k for k in sys.modules if k == "ring3pc" or k.startswith("ring3pc.")]:
+            del sys.modules[k]
