@@ -111,6 +111,10 @@ int r3_ew(int op, int ndim, const int64_t* shape, uint64_t* out,
  * hot elementwise call, no shape/stride arrays to marshal. */
 int r3_ew_flat(int op, int64_t n, uint64_t* out, const uint64_t* a,
                const uint64_t* b, uint64_t imm, uint64_t mask, void* stream);
+/* out = a - b - c (op 0) or a + b + c (op 1), & mask, contiguous n words:
+ * opening a value from the three views (sharing.py:364-471) in one pass. */
+int r3_ew3(int op, int64_t n, uint64_t* out, const uint64_t* a,
+           const uint64_t* b, const uint64_t* c, uint64_t mask, void* stream);
 /* k <= 4 contiguous length-n components in one launch: out[c] =
  * op(a[c], b ? b[c] : imm) & mask (the fields of one party's share view --
  * s1/s2/total/m, sharing.py:95-230 -- updated together).  Per-component
@@ -174,6 +178,14 @@ int r3_gr_lincomb(int k, int nterms, const uint64_t* const* a,
 int r3_gr_scale_rows(const uint64_t* s, int64_t s_stride,
                      const uint64_t* g, int64_t g_rs, uint64_t* out,
                      int64_t rows, int d, uint64_t mask, void* stream);
+/* Public per-level values of one Pi_rd reduction from the opened even point
+ * ze (reference verify.py:215-241, grvec quad weights): out (4 x d) =
+ * [l0, l1 - l0, l2, 1 - ze] with u = ze >> 1, l0 = (ze-1)(u-1), l1 = ze(2-ze),
+ * l2 = u(ze-1) in GR(2^width, d) (mask = 2^width - 1); if Mo and Mz are both
+ * non-NULL also the (d x d) multiplication matrices of 1 - ze and ze.  One
+ * launch replaces the ~15 small GR operations of the reference's helper. */
+int r3_gr_quad(const uint64_t* ze, int d, uint64_t lowterms, uint64_t mask,
+               uint64_t* out, uint64_t* Mo, uint64_t* Mz, void* stream);
 /* M (d x d): row j = x^j * c mod f, so that (a * c) = a_row . M. */
 int r3_gr_mulmat(const uint64_t* c, int d, uint64_t lowterms, uint64_t* M,
                  void* stream);

@@ -45,6 +45,7 @@ _SIGS = {
     "r3_ew": [C.c_int, C.c_int, C.POINTER(i64), u64p, u64p, C.POINTER(i64), u64p,
               C.POINTER(i64), u64, u64, C.c_void_p],
     "r3_ew_flat": [C.c_int, i64, u64p, u64p, u64p, u64, u64, C.c_void_p],
+    "r3_ew3": [C.c_int, i64, u64p, u64p, u64p, u64p, u64, C.c_void_p],
     "r3_ew_multi": [C.c_int, C.c_int, i64, C.c_void_p, C.c_void_p, C.c_void_p, u64, u64, C.c_void_p],
     "r3_ars": [u64p, i64, C.c_int, C.c_int, u64p, C.c_void_p],
     "r3_bit_planes": [u64p, i64, C.c_int, u64p, C.c_void_p],
@@ -58,6 +59,7 @@ _SIGS = {
                       C.c_void_p],
     "r3_gr_scale_rows": [u64p, i64, u64p, i64, u64p, i64, C.c_int, u64, C.c_void_p],
     "r3_gr_mulmat": [u64p, C.c_int, u64, u64p, C.c_void_p],
+    "r3_gr_quad": [u64p, C.c_int, u64, u64, u64p, u64p, u64p, C.c_void_p],
     "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
                      C.c_void_p],
     "r3_gr_matmul2_tc": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],

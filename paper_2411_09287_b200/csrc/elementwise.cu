@@ -254,6 +254,28 @@ extern "C" int r3_ew_flat(int op, int64_t n, uint64_t* out, const uint64_t* a, c
   return r3_ew(op, 1, shape, out, a, st, b, st, imm, mask, stream);
 }
 
+// out = (a - b - c) & mask (op 0) or (a + b + c) & mask (op 1): the
+// reconstruction of an opened value from the three views (sharing.rec,
+// sharing.py:364-471) in one pass instead of two subtractions.
+__global__ void ew3_kernel(int op, int64_t n, u64* __restrict__ out, const u64* __restrict__ a,
+                           const u64* __restrict__ b, const u64* __restrict__ c, u64 mask) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    out[i] = (op == 0 ? a[i] - b[i] - c[i] : a[i] + b[i] + c[i]) & mask;
+}
+
+extern "C" int r3_ew3(int op, int64_t n, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                      const uint64_t* c, uint64_t mask, void* stream) {
+  if ((op != 0 && op != 1) || n < 0) {
+    set_error("r3_ew3: bad arguments");
+    return R3_ERR_ARG;
+  }
+  if (n == 0) return R3_OK;
+  ew3_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(op, n, (u64*)out, (const u64*)a,
+                                                                 (const u64*)b, (const u64*)c, mask);
+  return check_launch("r3_ew3");
+}
+
 struct Ptr4 {
   const u64* p[4];
 };

@@ -112,6 +112,88 @@ __global__ void gr_mulmat_kernel(const u64* __restrict__ c, int d, u64 lowterms,
   }
 }
 
+// Public per-level values of one reduction from the opened even point ze
+// (verify._Quad, verify.py:215-241): one warp computes
+//   u = ze >> 1,  l0 = (ze-1)(u-1),  l1 = ze(2-ze),  l2 = u(ze-1)   (mod f, width)
+// and writes out = [l0, l1 - l0, l2, 1 - ze]; with Mo/Mz non-null also the
+// multiplication matrices of (1 - ze) and ze (gr_mulmat_kernel's rows).
+template <int D>
+__device__ void warp_gr_mul(const u64* a, const u64* b, u64* p, u64* t, u64 lowterms, u64* out, u64 mask,
+                            int lane) {
+  for (int idx = lane; idx < 2 * D - 1; idx += 32) {
+    const int lo = idx - (D - 1) > 0 ? idx - (D - 1) : 0;
+    const int hi = idx < D - 1 ? idx : D - 1;
+    u64 acc = 0;
+    for (int i = lo; i <= hi; ++i) acc += a[i] * b[idx - i];
+    p[idx] = acc;
+  }
+  __syncwarp();
+  reduce_poly_warp<D>(p, t, lowterms, out, mask, lane, nullptr);
+}
+
+template <int D>
+__global__ void gr_quad_kernel(const u64* __restrict__ ze, u64 lowterms, u64 mask, u64* __restrict__ out,
+                               u64* __restrict__ Mo, u64* __restrict__ Mz) {
+  __shared__ u64 z[D], zm1[D], um1[D], tmz[D], u[D], om[D], p[2 * D], t[2 * D + 8], l0[D], l1[D];
+  const int lane = threadIdx.x;
+  for (int k = lane; k < D; k += 32) {
+    const u64 zk = ze[k];
+    const u64 e = k == 0 ? 1ull : 0ull;
+    z[k] = zk;
+    u[k] = zk >> 1;
+    zm1[k] = (zk - e) & mask;
+    um1[k] = ((zk >> 1) - e) & mask;
+    tmz[k] = (2 * e - zk) & mask;
+    om[k] = (e - zk) & mask;
+  }
+  __syncwarp();
+  warp_gr_mul<D>(zm1, um1, p, t, lowterms, l0, mask, lane);
+  warp_gr_mul<D>(z, tmz, p, t, lowterms, l1, mask, lane);
+  warp_gr_mul<D>(u, zm1, p, t, lowterms, out + 2 * D, mask, lane);
+  for (int k = lane; k < D; k += 32) {
+    out[k] = l0[k];
+    out[D + k] = (l1[k] - l0[k]) & mask;
+    out[3 * D + k] = om[k];
+  }
+  if (Mo == nullptr) return;
+  // rows j = x^j * c mod f for c = 1 - ze (Mo) and c = ze (Mz)
+  __shared__ u64 ro[D], rz[D];
+  for (int k = lane; k < D; k += 32) {
+    ro[k] = om[k];
+    rz[k] = z[k];
+  }
+  __syncwarp();
+  for (int j = 0; j < D; ++j) {
+    u64 no[(D + 31) / 32], nz[(D + 31) / 32];
+    const u64 to = ro[D - 1], tz = rz[D - 1];
+#pragma unroll
+    for (int q = 0; q < (D + 31) / 32; ++q) {
+      const int k = lane + 32 * q;
+      if (k < D) {
+        Mo[j * D + k] = ro[k];
+        Mz[j * D + k] = rz[k];
+        u64 vo = k >= 1 ? ro[k - 1] : 0, vz = k >= 1 ? rz[k - 1] : 0;
+        if ((lowterms >> k) & 1ull) {
+          vo -= to;
+          vz -= tz;
+        }
+        no[q] = vo;
+        nz[q] = vz;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < (D + 31) / 32; ++q) {
+      const int k = lane + 32 * q;
+      if (k < D) {
+        ro[k] = no[q];
+        rz[k] = nz[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // out[i] = A_i . M (+ C_i): 256 threads, 4x4 register tiles, whole M in smem.
 template <int D>
 __global__ void __launch_bounds__(256)
@@ -846,6 +928,18 @@ extern "C" int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, in
 #undef R3_DS
   }
   return check_launch("r3_gr_dotsum");
+}
+
+extern "C" int r3_gr_quad(const uint64_t* ze, int d, uint64_t lowterms, uint64_t mask, uint64_t* out,
+                          uint64_t* Mo, uint64_t* Mz, void* stream) {
+  if (d < 1 || d > 64 || (d & (d - 1)) || ((Mo == nullptr) != (Mz == nullptr))) {
+    set_error("r3_gr_quad: bad arguments (d %d)", d);
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (gr_quad_kernel<D><<<1, 32, 0, s>>>((const u64*)ze, lowterms, mask, (u64*)out, (u64*)Mo,
+                                                        (u64*)Mz)));
+  return check_launch("r3_gr_quad");
 }
 
 extern "C" int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms, uint64_t* out, uint64_t mask,

@@ -126,6 +126,18 @@ def sub(a, b, width: int = 64):
     return ew(SUB, a, b, ring_mask(width))
 
 
+def sub3(a, b, c, width: int = 64):
+    """(a - b - c) & mask in one launch for same-shape contiguous device
+    tensors (r3_ew3); broadcasting / strided operands take two subtractions."""
+    if (type(a) is _Tensor and type(b) is _Tensor and type(c) is _Tensor and a.shape == b.shape == c.shape
+            and a.is_contiguous() and b.is_contiguous() and c.is_contiguous() and a.is_cuda):
+        out = torch.empty(a.shape, dtype=torch.int64, device=a.device)
+        call("r3_ew3", 0, a.numel(), out.data_ptr(), a.data_ptr(), b.data_ptr(), c.data_ptr(),
+             ring_mask(width), stream())
+        return out
+    return sub(sub(a, b, width), c, width)
+
+
 def mul(a, b, width: int = 64):
     return ew(MUL, a, b, ring_mask(width))
 
@@ -405,6 +417,20 @@ def gr_quad_coeffs(z_even, width: int, mod: GrModulus, check: bool = True):
     l1 = gr_mul(z_even, sub(two, z_even, width), width, mod)
     l2 = gr_mul(u, sub(z_even, one, width), width, mod)
     return l0, l1, l2
+
+
+def gr_quad(z_even, width: int, mod: GrModulus, mats: bool = True, check: bool = True):
+    """((l0, l1 - l0, l2), 1 - z, (M(1 - z), M(z)) or None) in one launch
+    (r3_gr_quad): gr_quad_coeffs plus the line-evaluation operands."""
+    if check:
+        _check_even(z_even)
+    d = mod.degree
+    out = empty((4, d))
+    Mo = empty((d, d)) if mats else None
+    Mz = empty((d, d)) if mats else None
+    call("r3_gr_quad", ptr(z_even.reshape(-1, d)[0].contiguous()), d, mod.lowterms_mask, ring_mask(width),
+         ptr(out), ptr(Mo), ptr(Mz), stream())
+    return (out[0:1], out[1:2], out[2:3]), out[3:4], ((Mo, Mz) if mats else None)
 
 
 def _shr1(a):

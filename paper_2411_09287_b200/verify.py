@@ -223,11 +223,10 @@ class _Quad:
     folded in) and the line-evaluation matrices of (1 - ze) and ze."""
 
     def __init__(self, ze: torch.Tensor, gr: Ring, check: bool):
-        l0, l1, l2 = grvec.gr_quad_coeffs(ze, gr.ell, gr.mod, check=check)
-        self.w = (l0, grvec.sub(l1, l0, gr.ell), l2)
-        self.one_m = grvec.sub(grvec.gr_const(1, gr.mod, gr.ell), ze, gr.ell)
-        self.M_one_m = grvec.gr_mulmat(self.one_m, gr.mod) if gr.d >= 8 else None
-        self.M_ze = grvec.gr_mulmat(ze, gr.mod) if gr.d >= 8 else None
+        # one launch (r3_gr_quad): the weights, 1 - ze and, for d >= 8, the
+        # multiplication matrices of 1 - ze and ze
+        self.w, self.one_m, mats = grvec.gr_quad(ze, gr.ell, gr.mod, mats=gr.d >= 8, check=check)
+        self.M_one_m, self.M_ze = mats if mats is not None else (None, None)
 
 
 def _quad(party, ze: torch.Tensor, gr: Ring) -> _Quad:

@@ -392,3 +392,36 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
     for r in roles:
         np.testing.assert_array_equal(host(outs[r][0]), want[r][0], err_msg=f"acc role {r}")
         np.testing.assert_array_equal(host(outs[r][1]), want[r][1], err_msg=f"zraw role {r}")
+
+
+@pytest.mark.parametrize("width", [64, 1])
+def test_gr_quad_matches_step_by_step(cuda, width):
+    """r3_gr_quad (one launch) equals the reference-shaped helper chain it
+    replaces: gr_quad_coeffs (Lagrange weights at an even point), 1 - ze and
+    the multiplication matrices of 1 - ze and ze, for every degree."""
+    from paper_2411_09287_b200 import grvec, host
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    rng = np.random.default_rng(width)
+    for d in (1, 2, 4, 8, 16, 32, 64):
+        mod = modulus_for_degree(d)
+        z = rng.integers(0, 2**64, (1, d), dtype=np.uint64) & np.uint64((1 << width) - 1)
+        ze = grvec.dev((z * np.uint64(2)) & np.uint64((2**64 - 1) if width == 64 else 1))
+        l0, l1, l2 = grvec.gr_quad_coeffs(ze, width, mod)
+        (w0, w1, w2), one_m, mats = grvec.gr_quad(ze, width, mod, mats=True)
+        np.testing.assert_array_equal(host(w0), host(l0), err_msg=f"l0 d={d}")
+        np.testing.assert_array_equal(host(w1), host(grvec.sub(l1, l0, width)), err_msg=f"l1-l0 d={d}")
+        np.testing.assert_array_equal(host(w2), host(l2), err_msg=f"l2 d={d}")
+        om = grvec.sub(grvec.gr_const(1, mod, width), ze, width)
+        np.testing.assert_array_equal(host(one_m), host(om), err_msg=f"1-ze d={d}")
+        np.testing.assert_array_equal(host(mats[0]), host(grvec.gr_mulmat(om, mod)), err_msg=f"M(1-ze) d={d}")
+        np.testing.assert_array_equal(host(mats[1]), host(grvec.gr_mulmat(ze, mod)), err_msg=f"M(ze) d={d}")
+
+
+def test_ew3_matches_two_subtractions(cuda):
+    from paper_2411_09287_b200 import grvec, host
+    rng = np.random.default_rng(3)
+    for n in (1, 64, 4099, 1 << 20):
+        a, b, c = (grvec.dev(rng.integers(0, 2**64, n, dtype=np.uint64)) for _ in range(3))
+        for w in (64, 1, 37):
+            np.testing.assert_array_equal(host(grvec.sub3(a, b, c, w)),
+                                          host(grvec.sub(grvec.sub(a, b, w), c, w)))

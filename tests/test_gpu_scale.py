@@ -115,6 +115,8 @@ def _matmul_prog(n, X, W, check):
         verdict = None
         if check:
             verdict = verify.verify_session(party, d=16, R="auto")
+            if not all(verdict.values()):
+                party.abort("verification failed")   # ppml.py:440-445: never open after a failed check
         else:
             party.freeze_logs()
         return rec(party, z, "z").cpu().numpy(), verdict
