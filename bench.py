@@ -613,13 +613,15 @@ class KernelTimer:
 
     def __init__(self, name: str):
         self.name = name
+        # the batched form of an entry point launches the same kernel
+        self.names = {name, name + "_multi"}
         self.events = []
         self.work = 0
         self.launches = 0
 
     def hook(self, name, args, run):
         import torch
-        if name != self.name:
+        if name not in self.names:
             return run()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -685,6 +687,10 @@ def work_of(name, args) -> int:
         w = 512 if name == "r3_gr_matmul2_tc" else 128
         p1, nv0, nv1, rows = args[3], int(args[2]), int(args[5]), int(args[9])
         return w * (rows + min(nv0, rows) + (min(nv1, rows) if p1 else 0))
+    if name == "r3_gr_matmul2_tc_multi":
+        nj, nv0, nv1, rows = int(args[0]), args[3], args[6], args[10]
+        return sum(512 * (int(rows[j]) + min(int(nv0[j]), int(rows[j])) + min(int(nv1[j]), int(rows[j])))
+                   for j in range(nj))
     if name == "r3_prf_ctr":
         return -(-int(args[2]) // 2)                       # AES blocks
     if name == "r3_prf_bits_packed":
@@ -715,6 +721,7 @@ def work_of(name, args) -> int:
 KERNEL_BOUND = {
     "r3_gr_matmul2_tc": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc16": ("hbm", "GB/s", 1e9),
+    "r3_gr_matmul2_tc_multi": ("hbm", "GB/s", 1e9),
     "r3_ew_flat": ("hbm", "GB/s", 1e9),
     "r3_u64_gemm_tc": ("tensor", "int8 TOP/s", 1e12),
     "r3_prf_ctr": ("aes", "G AES blocks/s", 1e9),

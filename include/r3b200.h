@@ -204,6 +204,15 @@ int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0,
                      const uint64_t* p1, int64_t rs1, int64_t nv1,
                      const uint64_t* M0, const uint64_t* M1, uint64_t* out,
                      int64_t rows, uint64_t mask, void* stream);
+/* Several r3_gr_matmul2_tc jobs sharing M0 / M1 in one launch (the line
+ * evaluations of every component a party reduces at one level,
+ * verify.py:239-240): job j is out_j[r] = P0_j[r] . M0 + P1_j[r] . M1 for
+ * r < rows[j], both operands present with >= 1 valid row; 1..8 jobs. */
+int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                           const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
+                           const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
+                           uint64_t* const* outs, const int64_t* rows, uint64_t mask,
+                           void* stream);
 /* One operand times q <= 4 public GR(2^64, 64) multiplication matrices in
  * one pass: outs[k][r] = p[r] . Ms[k] for r < rows (rows of 64 u64 at
  * stride rs words, 16-byte aligned).  The four level-2 tables of a

@@ -63,6 +63,9 @@ _SIGS = {
     "r3_gr_matmul": [LinOperand, u64p, C.c_int, LinOperand, u64p, i64, C.c_int, u64,
                      C.c_void_p],
     "r3_gr_matmul2_tc": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
+    "r3_gr_matmul2_tc_multi": [C.c_int, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64),
+                               C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64), u64p, u64p,
+                               C.POINTER(C.c_void_p), C.POINTER(i64), u64, C.c_void_p],
     "r3_gr_matmul2_tc16": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
     "r3_vfy_level_fold16_tc": [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64), i64,

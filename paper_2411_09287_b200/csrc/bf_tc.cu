@@ -51,22 +51,6 @@ struct BfArgs {
   int64_t N, nblk, kc;
 };
 
-__device__ __forceinline__ void bf_split16(const u64 (&v)[16], uint4 (&out)[8]) {
-  uint32_t w[32];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    w[2 * q] = uint32_t(v[q]);
-    w[2 * q + 1] = uint32_t(v[q] >> 32);
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int hiw = i >> 2, bi = i & 3;
-    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
-    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
-    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
-    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
-  }
-}
 
 __global__ void __launch_bounds__(BF_THREADS, 1)
 base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
@@ -200,7 +184,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         mbar_arrive(&raw_empty[st]);
       }
       uint4 pk[8];
-      bf_split16(v, pk);
+      split_limbs16(v, pk);
       if (g >= BF_STAGES) mbar_wait(&empty[st], uint32_t((g / BF_STAGES - 1) & 1));
       // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
       uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * BF_B_TILE;

@@ -63,22 +63,6 @@ __device__ __forceinline__ void l16_read_row(const uint8_t* row, int sw, u64 (&v
   }
 }
 
-__device__ __forceinline__ void l16_split16(const u64 (&v)[16], uint4 (&out)[8]) {
-  uint32_t w[32];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    w[2 * q] = uint32_t(v[q]);
-    w[2 * q + 1] = uint32_t(v[q] >> 32);
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int hiw = i >> 2, bi = i & 3;
-    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
-    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
-    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
-    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
-  }
-}
 
 __global__ void __launch_bounds__(L16_THREADS, 1)
 level_fold16_tc_kernel(const __grid_constant__ L16Args args) {
@@ -194,7 +178,7 @@ level_fold16_tc_kernel(const __grid_constant__ L16Args args) {
       fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
       mbar_arrive(&raw_empty[st]);
       uint4 pk[8];
-      l16_split16(v, pk);
+      split_limbs16(v, pk);
       if (kb >= L16_STAGES) mbar_wait(&empty[st], uint32_t((kb / L16_STAGES - 1) & 1));
       // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
       uint8_t* dst = isA ? sA + st * L16_A_TILE : sB + st * L16_B_TILE;

@@ -30,22 +30,6 @@ constexpr int MM_THREADS = 6 * 32;                         // producer, MMA, 4 e
 constexpr int MM_SMEM = MM_STAGES * (MM_A_TILE + MM_B_TILE) + 256;
 
 // 16 u64 -> 8 planes of 16 bytes (limb i of each value)
-__device__ __forceinline__ void split16(const u64 (&v)[16], uint4 (&out)[8]) {
-  uint32_t w[32];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    w[2 * q] = uint32_t(v[q]);
-    w[2 * q + 1] = uint32_t(v[q] >> 32);
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int hiw = i >> 2, bi = i & 3;
-    out[i].x = gather_byte(w[0 + hiw], w[2 + hiw], w[4 + hiw], w[6 + hiw], bi);
-    out[i].y = gather_byte(w[8 + hiw], w[10 + hiw], w[12 + hiw], w[14 + hiw], bi);
-    out[i].z = gather_byte(w[16 + hiw], w[18 + hiw], w[20 + hiw], w[22 + hiw], bi);
-    out[i].w = gather_byte(w[24 + hiw], w[26 + hiw], w[28 + hiw], w[30 + hiw], bi);
-  }
-}
 
 // A operand (rows x K, row-major u64, value = c0*P0 + c1*P1) -> tiles
 // [mb][kb][plane][128 x 32 core layout]
@@ -66,7 +50,7 @@ __global__ void limb_tiles_a_kernel(const u64* __restrict__ p0, u64 c0, const u6
       for (int q = 0; q < 16; ++q) v[q] += c1 * __ldg(s1 + q);
     }
     uint4 pk[8];
-    split16(v, pk);
+    split_limbs16(v, pk);
     const int64_t mb = row / MM_BM, kb = (kc * 16) / MM_BK;
     uint8_t* tile = dst + (mb * KB + kb) * MM_A_TILE;
     const uint32_t off = core_off(int(row % MM_BM), int((kc * 16) % MM_BK), MM_BM / 8);
@@ -93,7 +77,7 @@ __global__ void limb_tiles_b_kernel(const u64* __restrict__ p0, u64 c0, const u6
       v[q] = x;
     }
     uint4 pk[8];
-    split16(v, pk);
+    split_limbs16(v, pk);
     const int64_t nb = n / MM_BN, kb = (kc * 16) / MM_BK;
     uint8_t* tile = dst + (nb * KB + kb) * MM_B_TILE;
     // the 8 planes stacked as one 512-row K-major matrix (row 64 j + n), so a

@@ -73,10 +73,30 @@ __device__ __forceinline__ void conv_named_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(W_CONV * 32) : "memory");
 }
 
+// Jobs of one launch: every job is rows of P0 (and P1) times the same
+// public M0 (M1), so one CTA's B planes serve all of them (the line
+// evaluations of all components of a reduction level share M(1 - z), M(z));
+// tiles are numbered job after job (tile0 = prefix sums).
+constexpr int MM2_MAX_JOBS = 8;
+struct Mm2Jobs {
+  CUtensorMap tm[MM2_MAX_JOBS][2];
+  u64* out[MM2_MAX_JOBS];
+  int64_t rows[MM2_MAX_JOBS];
+  int64_t tile0[MM2_MAX_JOBS + 1];
+  int njobs, nops;
+};
+
+__device__ __forceinline__ int mm2_job(const Mm2Jobs& J, int64_t t) {
+  int j = 0;
+#pragma unroll 1
+  while (j + 1 < J.njobs && t >= J.tile0[j + 1]) ++j;
+  return j;
+}
+
 __global__ void __launch_bounds__(WS_THREADS, 1)
-gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-                     int nops, const u64* __restrict__ M0, const u64* __restrict__ M1, u64* __restrict__ out,
-                     int64_t rows, u64 mask) {
+gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ M0, const u64* __restrict__ M1,
+                     u64 mask) {
+  const int nops = J.nops;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;
@@ -124,7 +144,7 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t ntiles = J.tile0[J.njobs];
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int upt = 2 * nops;                        // units per tile: (operand, K-half)
   const int64_t nunits = my_tiles * upt;
@@ -136,12 +156,14 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
         const int st = int(g % DB_STAGES);
         if (g >= DB_STAGES) mbar_wait(&empty[st], uint32_t((g / DB_STAGES - 1) & 1));
         const int64_t t = blockIdx.x + (g / upt) * gridDim.x;
+        const int j = mm2_job(J, t);
+        const int64_t lt = t - J.tile0[j];
         const int op = int((g >> 1) % nops), h = int(g & 1);
-        const CUtensorMap* map = op ? &tm1 : &tm0;
+        const CUtensorMap* map = &J.tm[j][op];
         uint8_t* dst = sStage + st * RAW_BYTES;
         mbar_expect_tx(&raw_full[st], RAW_BYTES);
-        tma_load_2d(dst, map, h * TC_KH, int(t * TC_ROWS), &raw_full[st]);
-        tma_load_2d(dst + RAW_BYTES / 2, map, h * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
+        tma_load_2d(dst, map, h * TC_KH, int(lt * TC_ROWS), &raw_full[st]);
+        tma_load_2d(dst + RAW_BYTES / 2, map, h * TC_KH + 16, int(lt * TC_ROWS), &raw_full[st]);
       }
     }
     __syncwarp();
@@ -166,16 +188,10 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
       }
       conv_named_sync();    // every raw row of the stage is in registers before any limb write
       uint8_t* dst = stage + core_off(r, c * 16, TC_ROWS / 8);
+      uint4 pk[8];
+      split_limbs16(x, pk);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int hiw = i >> 2, bi = i & 3;
-        uint4 pk;
-        pk.x = gather_byte(x[0 + hiw], x[2 + hiw], x[4 + hiw], x[6 + hiw], bi);
-        pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
-        pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
-        pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
-        *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk;
-      }
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk[i];
       fence_async_smem();   // generic limb writes -> tensor-core (async proxy) reads
       mbar_arrive(&limb_full[st]);
     }
@@ -222,6 +238,10 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
     const int quad = warp & 3;
     const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int j = mm2_job(J, t);
+      const int64_t lt = t - J.tile0[j];
+      const int64_t rows = J.rows[j];
+      u64* __restrict__ out = J.out[j];
       for (int h = 0; h < 2; ++h) {
         mbar_wait(&tfull[h], ph[h]);
         ph[h] ^= 1;
@@ -238,7 +258,7 @@ gr_matmul2_db_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_const
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
-          const int64_t row = t * TC_ROWS + quad * 32 + lg * 16 + rq;
+          const int64_t row = lt * TC_ROWS + quad * 32 + lg * 16 + rq;
           const int col = DB_HALF * h + c0 + cq;
           if (row < rows)
             *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
@@ -367,16 +387,10 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
       }
       conv_named_sync();
       uint8_t* dst = stage + core_off(r, c * 16, TC_ROWS / 8);
+      uint4 pk[8];
+      split_limbs16(x, pk);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int hiw = i >> 2, bi = i & 3;
-        uint4 pk;
-        pk.x = gather_byte(x[0 + hiw], x[2 + hiw], x[4 + hiw], x[6 + hiw], bi);
-        pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
-        pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
-        pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
-        *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk;
-      }
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * LIMB_PLANE) = pk[i];
       fence_async_smem();
       mbar_arrive(&limb_full[st]);
     }
@@ -574,16 +588,10 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
       mbar_arrive(&raw_empty[st]);
       if (u >= T16_LIMB_STAGES) mbar_wait(&limb_empty[ls], uint32_t((u / T16_LIMB_STAGES - 1) & 1));
       uint8_t* dst = sLimb + ls * T16_LIMB + core_off(r, c * 16, TC_ROWS / 8);
+      uint4 pk[8];
+      split_limbs16(x, pk);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int hiw = i >> 2, bi = i & 3;
-        uint4 pk;
-        pk.x = gather_byte(x[0 + hiw], x[2 + hiw], x[4 + hiw], x[6 + hiw], bi);
-        pk.y = gather_byte(x[8 + hiw], x[10 + hiw], x[12 + hiw], x[14 + hiw], bi);
-        pk.z = gather_byte(x[16 + hiw], x[18 + hiw], x[20 + hiw], x[22 + hiw], bi);
-        pk.w = gather_byte(x[24 + hiw], x[26 + hiw], x[28 + hiw], x[30 + hiw], bi);
-        *reinterpret_cast<uint4*>(dst + i * T16_LIMB_PLANE) = pk;
-      }
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * T16_LIMB_PLANE) = pk[i];
       fence_async_smem();
       mbar_arrive(&limb_full[ls]);
     }
@@ -676,6 +684,14 @@ bool make_rows_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t rs
 
 using namespace r3;
 
+static int mm2_launch(const Mm2Jobs& J, const u64* M0, const u64* M1, uint64_t mask, cudaStream_t s) {
+  const int64_t tiles = J.tile0[J.njobs];
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
+  ensure_smem(gr_matmul2_db_kernel, DB_SMEM);
+  gr_matmul2_db_kernel<<<grid, WS_THREADS, DB_SMEM, s>>>(J, M0, M1, mask);
+  return check_launch("r3_gr_matmul2_tc");
+}
+
 extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, const uint64_t* p1, int64_t rs1,
                                 int64_t nv1, const uint64_t* M0, const uint64_t* M1, uint64_t* out, int64_t rows,
                                 uint64_t mask, void* stream) {
@@ -710,20 +726,55 @@ extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, co
     cudaMemsetAsync(out, 0, size_t(rows) * TC_D * 8, as_stream(stream));
     return check_launch("r3_gr_matmul2_tc(zero)");
   }
-  CUtensorMap tm[2];
+  Mm2Jobs J;
+  J.njobs = 1;
+  J.nops = nops;
   for (int q = 0; q < nops; ++q) {
-    if (!make_rows_tmap(&tm[q], Pk[q], nvk[q], rsk[q], TC_ROWS)) {
+    if (!make_rows_tmap(&J.tm[0][q], Pk[q], nvk[q], rsk[q], TC_ROWS)) {
       set_error("r3_gr_matmul2_tc: cuTensorMapEncodeTiled failed");
       return R3_ERR_CUDA;
     }
   }
-  if (nops == 1) tm[1] = tm[0];
-  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
-  ensure_smem(gr_matmul2_db_kernel, DB_SMEM);
-  gr_matmul2_db_kernel<<<grid, WS_THREADS, DB_SMEM, as_stream(stream)>>>(
-      tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
-  return check_launch("r3_gr_matmul2_tc");
+  if (nops == 1) J.tm[0][1] = J.tm[0][0];
+  J.out[0] = (u64*)out;
+  J.rows[0] = rows;
+  J.tile0[0] = 0;
+  J.tile0[1] = (rows + TC_ROWS - 1) / TC_ROWS;
+  return mm2_launch(J, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), mask, as_stream(stream));
+}
+
+extern "C" int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                                      const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
+                                      const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
+                                      uint64_t* const* outs, const int64_t* rows, uint64_t mask, void* stream) {
+  if (njobs < 1 || njobs > MM2_MAX_JOBS || !p0 || !p1 || !rs0 || !rs1 || !nv0 || !nv1 || !M0 || !M1 || !outs ||
+      !rows) {
+    set_error("r3_gr_matmul2_tc_multi: bad arguments (1..%d jobs)", MM2_MAX_JOBS);
+    return R3_ERR_ARG;
+  }
+  Mm2Jobs J;
+  J.njobs = njobs;
+  J.nops = 2;
+  J.tile0[0] = 0;
+  for (int j = 0; j < njobs; ++j) {
+    const int64_t r = rows[j];
+    const int64_t n0 = nv0[j] < r ? nv0[j] : r, n1 = nv1[j] < r ? nv1[j] : r;
+    if (r < 1 || r > (int64_t(1) << 31) - TC_ROWS || !p0[j] || !p1[j] || !outs[j] || n0 < 1 || n1 < 1 ||
+        ((rs0[j] | rs1[j]) & 1) || ((uintptr_t(p0[j]) | uintptr_t(p1[j])) & 15)) {
+      set_error("r3_gr_matmul2_tc_multi: job %d: bad operand (rows %lld, valid %lld/%lld, 16-byte aligned rows)",
+                j, (long long)r, (long long)n0, (long long)n1);
+      return R3_ERR_ARG;
+    }
+    if (!make_rows_tmap(&J.tm[j][0], p0[j], n0, rs0[j] > 0 ? rs0[j] : TC_D, TC_ROWS) ||
+        !make_rows_tmap(&J.tm[j][1], p1[j], n1, rs1[j] > 0 ? rs1[j] : TC_D, TC_ROWS)) {
+      set_error("r3_gr_matmul2_tc_multi: cuTensorMapEncodeTiled failed");
+      return R3_ERR_CUDA;
+    }
+    J.out[j] = (u64*)outs[j];
+    J.rows[j] = r;
+    J.tile0[j + 1] = J.tile0[j] + (r + TC_ROWS - 1) / TC_ROWS;
+  }
+  return mm2_launch(J, (const u64*)M0, (const u64*)M1, mask, as_stream(stream));
 }
 
 extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, const uint64_t* p1, int64_t rs1,

@@ -97,6 +97,40 @@ __device__ __forceinline__ uint32_t gather_byte(uint32_t x0, uint32_t x1, uint32
   return __byte_perm(lo, hi, 0x5410);
 }
 
+// 4 x 4 byte transpose in 8 PRMT: o_j = (byte j of a, b, c, d)
+__device__ __forceinline__ void bytes_t4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t& o0,
+                                         uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  o0 = __byte_perm(t0, t2, 0x5410);
+  o1 = __byte_perm(t0, t2, 0x7632);
+  o2 = __byte_perm(t1, t3, 0x5410);
+  o3 = __byte_perm(t1, t3, 0x7632);
+}
+
+// 16 u64 as 32 words (x[2q] low, x[2q+1] high half of word q) -> the 8
+// byte-limb planes of those 16 values (plane i = byte i of each, 16 bytes)
+__device__ __forceinline__ void split_limbs16(const uint32_t (&x)[32], uint4 (&out)[8]) {
+  uint32_t o[8][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    bytes_t4(x[8 * g + 0], x[8 * g + 2], x[8 * g + 4], x[8 * g + 6], o[0][g], o[1][g], o[2][g], o[3][g]);
+    bytes_t4(x[8 * g + 1], x[8 * g + 3], x[8 * g + 5], x[8 * g + 7], o[4][g], o[5][g], o[6][g], o[7][g]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) out[i] = make_uint4(o[i][0], o[i][1], o[i][2], o[i][3]);
+}
+
+__device__ __forceinline__ void split_limbs16(const u64 (&v)[16], uint4 (&out)[8]) {
+  uint32_t w[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    w[2 * q] = uint32_t(v[q]);
+    w[2 * q + 1] = uint32_t(v[q] >> 32);
+  }
+  split_limbs16(w, out);
+}
+
 // sum_s d[s] 2^(8 s) mod 2^64 for the 8 diagonal accumulators of one output,
 // in 32-bit halves: diagonals 0-3 straddle the word boundary (one carry
 // chain), diagonals 4-7 only reach the high word.

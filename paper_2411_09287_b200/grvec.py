@@ -486,6 +486,35 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
                      C_add=lin((1, tmp)), out=out)
 
 
+def rows_times2_batch(jobs: list, M0: torch.Tensor, M1: torch.Tensor, width: int) -> list:
+    """[rows_times(ev, M0, n0, P1=od, M1=M1, nvalid=(n0, n1)) for (ev, od,
+    n0, n1) in jobs]: for d = 64 every job with both operands present runs
+    in ONE tensor-core launch (r3_gr_matmul2_tc_multi, up to 8 jobs share
+    the B planes of M0 / M1); other shapes one rows_times each."""
+    d = M0.shape[0]
+    outs = [None] * len(jobs)
+    batch = []
+    for i, (ev, od, n0, n1) in enumerate(jobs):
+        if d == 64 and n0 >= 1 and n1 >= 1 and _tc_ok(ev) and _tc_ok(od):
+            batch.append(i)
+        else:
+            outs[i] = rows_times(ev, M0, n0, width, P1=od, M1=M1, nvalid=(n0, n1))
+    for s in range(0, len(batch), 8):
+        idx = batch[s:s + 8]
+        k = len(idx)
+        P = C.c_void_p * k
+        L = C.c_int64 * k
+        for i in idx:
+            outs[i] = empty((jobs[i][2], d))
+        rs = lambda t: t.stride(0) if t.shape[0] > 1 else d
+        call("r3_gr_matmul2_tc_multi", k, P(*[jobs[i][0].data_ptr() for i in idx]),
+             L(*[rs(jobs[i][0]) for i in idx]), L(*[jobs[i][2] for i in idx]),
+             P(*[jobs[i][1].data_ptr() for i in idx]), L(*[rs(jobs[i][1]) for i in idx]),
+             L(*[jobs[i][3] for i in idx]), ptr(M0), ptr(M1), P(*[outs[i].data_ptr() for i in idx]),
+             L(*[jobs[i][2] for i in idx]), ring_mask(width), stream())
+    return outs
+
+
 def rows_times_multi(P: torch.Tensor, Ms: list, rows: int, width: int, outs: list) -> list:
     """outs[k][r] = P[r] . Ms[k] for d = 64 and up to 4 matrices in one pass
     over P (r3_gr_matmul_q_tc); other degrees / layouts one rows_times each."""

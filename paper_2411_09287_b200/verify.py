@@ -865,11 +865,44 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     q = _quad(party, ze, gr)
     z_out = _recombine(party, z, h1, h2, q, gr)
     Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
+    if gr.d in (16, 64):
+        xo, yo, mx, my = _level_line_evals(party, X, Y, names, Ms, gr)
+        mk = lambda o, m, v: MVal(AShare(gr, role, **o, p0_halves=v.mask.p0_halves), m)
+        return mk(xo, mx, xs), mk(yo, my, ys), z_out
     out = lambda V, k: _line_eval(V[k], Ms, gr)
     mk = lambda V, v: MVal(AShare(gr, role, **{k: out(V, k) for k in names},
                                   p0_halves=v.mask.p0_halves),
                            _shared_m(party, lambda: out(V, "m")) if "m" in V else None)
     return mk(X, xs), mk(Y, ys), z_out
+
+
+def _level_line_evals(party, X: dict, Y: dict, names: list, Ms, gr: Ring):
+    """Every line evaluation f0 . M(1 - zeta) + f1 . M(zeta) (verify.py:239-240)
+    of one party's reduction level in one tensor-core launch (d = 64): its
+    mask components of x and y, plus the m components when this party is
+    the one that builds them (the _shared_m rule: in honest joint sessions
+    the first of P1 / P2 to arrive computes m's evaluations, the other
+    takes the same tensors)."""
+    jobs = [X[k] for k in names] + [Y[k] for k in names]
+    mx = my = None
+    key = None
+    build_m = "m" in X
+    if build_m and party.role != 0 and _joint_ok(party):
+        key = ("m", party.next_id("_shared_m"))
+        memo = party.sess.shared_m
+        if key in memo:
+            mx, my = memo.pop(key)
+            build_m = False
+    if build_m:
+        jobs += [X["m"], Y["m"]]
+    res = grvec.rows_times2_batch([(H.ev, H.od, H.n0, H.n1) for H in jobs], Ms[0], Ms[1], gr.ell)
+    n = len(names)
+    xo, yo = dict(zip(names, res[:n])), dict(zip(names, res[n:2 * n]))
+    if build_m:
+        mx, my = res[2 * n], res[2 * n + 1]
+        if key is not None:
+            party.sess.shared_m[key] = (mx, my)
+    return xo, yo, mx, my
 
 
 def _reduce_dimension_small(party, xs, ys, z, gr, zeta):
@@ -1188,6 +1221,14 @@ class _DenseBatch:
             return
         if comp is not None:
             self._write_level1(party, gr, ze, _line_tables(party, None, self.pw, comp.n, ze, gr))
+            return
+        if gr.d in (16, 64):   # every component in one launch
+            keys = [("x", k) for k in self.x] + [("y", k) for k in self.y]
+            hs = [_Halves(getattr(self, v)[k]) for v, k in keys]
+            res = grvec.rows_times2_batch([(H.ev, H.od, H.n0, H.n1) for H in hs], Ms[0], Ms[1], gr.ell)
+            nx = len(self.x)
+            self.x = dict(zip(self.x, res[:nx]))
+            self.y = dict(zip(self.y, res[nx:]))
             return
         self.x = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.x.items()}
         self.y = {k: _line_eval(_Halves(t), Ms, gr) for k, t in self.y.items()}

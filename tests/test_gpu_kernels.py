@@ -104,6 +104,30 @@ def test_gr_matmul2_tc_line_eval(cuda, d, rows):
         np.testing.assert_array_equal(host(outb), ogr.mul(Xb, z, 64, d) & np.uint64(1))
 
 
+def test_gr_matmul2_tc_multi_matches_single_launches(cuda):
+    """r3_gr_matmul2_tc_multi (several line evaluations sharing M(1 - z),
+    M(z) in one launch: ragged job sizes, odd lengths, a one-row job,
+    strided even/odd views) equals one r3_gr_matmul2_tc launch per job."""
+    from paper_2411_09287_b200 import grvec, host
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    mod = modulus_for_degree(64)
+    rng = np.random.default_rng(77)
+    z = _rand(rng, (1, 64))
+    one = np.zeros((1, 64), dtype=np.uint64)
+    one[0, 0] = 1
+    with np.errstate(over="ignore"):
+        Ma = grvec.gr_mulmat(grvec.dev(one - z), mod)
+    Mb = grvec.gr_mulmat(grvec.dev(z), mod)
+    jobs = []
+    for rows in (2, 3, 257, 4096, 70001, 129, 1000, 9):
+        Xd = grvec.dev(_rand(rng, (rows, 64)))
+        jobs.append((Xd[0::2], Xd[1::2], (rows + 1) // 2, rows // 2))
+    got = grvec.rows_times2_batch(jobs, Ma, Mb, 64)
+    for (ev, od, n0, n1), g in zip(jobs, got):
+        want = grvec.rows_times(ev, Ma, n0, 64, P1=od, M1=Mb, nvalid=(n0, n1))
+        np.testing.assert_array_equal(host(g), host(want))
+
+
 @pytest.mark.parametrize("rows,q", [(1, 4), (129, 4), (5000, 3), (70001, 4), (1 << 18, 2), (300, 1)])
 def test_gr_matmul_q_tc(cuda, rows, q):
     """r3_gr_matmul_q_tc: one operand times q public matrices in one pass
@@ -161,6 +185,35 @@ def test_level_fold_matches_oracle(cuda, d, N):
             g2 = host(grvec.reduce_poly(acc[1], mod, 64))
             np.testing.assert_array_equal(g1, w1 & np.uint64(2**64 - 1), err_msg=f"h1 role {role}")
             np.testing.assert_array_equal(g2, w2, err_msg=f"h2 role {role}")
+
+
+@pytest.mark.parametrize("N", [2 * 16384 * 148 + 4097, (1 << 21) + 1])
+def test_level_fold_tc_matches_cuda_core_at_scale(cuda, N):
+    """d = 64 tensor-core level fold (lf_tc.cu: o (x) o and t (x) t limb
+    products, multi-chunk items whose 2-stage raw / 3-stage limb rings wrap
+    many times, odd N) equals the CUDA-core fold (pinned to the oracle
+    above) at level-3 sizes.  The folds are sums over row pairs, so the
+    CUDA-core side runs over 8190-row slices (4095 pairs each: below the
+    tensor-core threshold) accumulating into one output."""
+    import torch
+    from paper_2411_09287_b200 import grvec, _lib
+    g = torch.Generator(device="cuda").manual_seed(N)
+    V = [torch.randint(-2**62, 2**62, (N, 64), dtype=torch.int64, device="cuda", generator=g) for _ in range(4)]
+    S = 8190
+
+    def fold(role, r0, r1, acc):
+        ops = [v[r0:r1] for v in V]
+        _lib.call("r3_vfy_level_fold", role, ops[0].data_ptr(), ops[1].data_ptr() if role else None,
+                  ops[2].data_ptr(), ops[3].data_ptr() if role else None, r1 - r0, 64,
+                  acc[0].data_ptr(), acc[1].data_ptr(), _lib.stream())
+
+    for role in (0, 1, 2):
+        tc = grvec.zeros((2, 127))
+        fold(role, 0, N, tc)
+        cc = grvec.zeros((2, 127))
+        for r0 in range(0, N, S):
+            fold(role, r0, min(N, r0 + S), cc)
+        assert torch.equal(tc, cc), f"role {role}"
 
 
 @pytest.mark.parametrize("M,K,N", [(128, 32, 64), (256, 96, 128), (384, 4096, 192)])
