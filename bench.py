@@ -687,9 +687,10 @@ def work_of(name, args) -> int:
         w = 512 if name == "r3_gr_matmul2_tc" else 128
         p1, nv0, nv1, rows = args[3], int(args[2]), int(args[5]), int(args[9])
         return w * (rows + min(nv0, rows) + (min(nv1, rows) if p1 else 0))
-    if name == "r3_gr_matmul2_tc_multi":
+    if name in ("r3_gr_matmul2_tc_multi", "r3_gr_matmul2_tc16_multi"):
+        w = 512 if name == "r3_gr_matmul2_tc_multi" else 128
         nj, nv0, nv1, rows = int(args[0]), args[3], args[6], args[10]
-        return sum(512 * (int(rows[j]) + min(int(nv0[j]), int(rows[j])) + min(int(nv1[j]), int(rows[j])))
+        return sum(w * (int(rows[j]) + min(int(nv0[j]), int(rows[j])) + min(int(nv1[j]), int(rows[j])))
                    for j in range(nj))
     if name == "r3_prf_ctr":
         return -(-int(args[2]) // 2)                       # AES blocks
@@ -722,6 +723,7 @@ KERNEL_BOUND = {
     "r3_gr_matmul2_tc": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc16": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc_multi": ("hbm", "GB/s", 1e9),
+    "r3_gr_matmul2_tc16_multi": ("hbm", "GB/s", 1e9),
     "r3_ew_flat": ("hbm", "GB/s", 1e9),
     "r3_u64_gemm_tc": ("tensor", "int8 TOP/s", 1e12),
     "r3_prf_ctr": ("aes", "G AES blocks/s", 1e9),

@@ -213,6 +213,12 @@ int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, const int64_t* 
                            const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
                            uint64_t* const* outs, const int64_t* rows, uint64_t mask,
                            void* stream);
+/* d = 16 form of r3_gr_matmul2_tc_multi (rows of 16 coefficients). */
+int r3_gr_matmul2_tc16_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                             const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
+                             const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
+                             uint64_t* const* outs, const int64_t* rows, uint64_t mask,
+                             void* stream);
 /* One operand times q <= 4 public GR(2^64, 64) multiplication matrices in
  * one pass: outs[k][r] = p[r] . Ms[k] for r < rows (rows of 64 u64 at
  * stride rs words, 16-byte aligned).  The four level-2 tables of a
@@ -250,6 +256,11 @@ int r3_gr_dotsum(r3_lin_operand F, r3_lin_operand G, int64_t rows, int d,
 int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms,
                       uint64_t* out, uint64_t mask, int accumulate,
                       void* stream);
+/* nrows reductions in one launch: row i of acc (2d - 1 words, consecutive)
+ * reduced mod f and masked into out[i*d .. i*d + d - 1] (the h(1) / h(2)
+ * folds of a level, verify.py:229-231). */
+int r3_gr_reduce_poly_rows(const uint64_t* acc, int nrows, int d, uint64_t lowterms,
+                           uint64_t* out, uint64_t mask, void* stream);
 
 /* ---- share-domain matmul on the tensor cores (ppml.py:412-427 algebra) ----
  * Operand preparation: value = c0*P0 + c1*P1 (P1 may be NULL) split into 8

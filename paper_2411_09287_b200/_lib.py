@@ -66,6 +66,9 @@ _SIGS = {
     "r3_gr_matmul2_tc_multi": [C.c_int, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64),
                                C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64), u64p, u64p,
                                C.POINTER(C.c_void_p), C.POINTER(i64), u64, C.c_void_p],
+    "r3_gr_matmul2_tc16_multi": [C.c_int, C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64),
+                                 C.POINTER(C.c_void_p), C.POINTER(i64), C.POINTER(i64), u64p, u64p,
+                                 C.POINTER(C.c_void_p), C.POINTER(i64), u64, C.c_void_p],
     "r3_gr_matmul2_tc16": [u64p, i64, i64, u64p, i64, i64, u64p, u64p, u64p, i64, u64, C.c_void_p],
     "r3_vfy_level_fold16_tc": [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64), i64,
@@ -78,6 +81,7 @@ _SIGS = {
                        i64, u64p, C.c_int, u64p, u64, C.c_void_p],
     "r3_gr_dotsum": [LinOperand, LinOperand, i64, C.c_int, u64p, C.c_void_p],
     "r3_gr_reduce_poly": [u64p, C.c_int, u64, u64p, u64, C.c_int, C.c_void_p],
+    "r3_gr_reduce_poly_rows": [u64p, C.c_int, C.c_int, u64, u64p, u64, C.c_void_p],
     "r3_vfy_powsum": [C.c_int, C.POINTER(C.c_void_p), i64, i64, u64p, C.c_int, u64p, u64,
                       C.c_void_p],
     "r3_vfy_l1_fold": [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p),

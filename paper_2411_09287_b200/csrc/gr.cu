@@ -954,6 +954,31 @@ extern "C" int r3_gr_reduce_poly(const uint64_t* acc, int d, uint64_t lowterms, 
   return check_launch("r3_gr_reduce_poly");
 }
 
+// nrows accumulators at acc + i (2d - 1), reduced into out + i d: one warp each
+template <int D>
+__global__ void reduce_poly_rows_kernel(const u64* __restrict__ acc, u64 lowterms, u64* __restrict__ out,
+                                        u64 mask) {
+  __shared__ u64 sp[2 * D], st[2 * D + 8], sadd[D];
+  const int lane = threadIdx.x;
+  const u64* a = acc + int64_t(blockIdx.x) * (2 * D - 1);
+  for (int i = lane; i < 2 * D; i += 32) sp[i] = i < 2 * D - 1 ? a[i] : 0;
+  for (int i = lane; i < D; i += 32) sadd[i] = 0;
+  __syncwarp();
+  reduce_poly_warp<D>(sp, st, lowterms, out + int64_t(blockIdx.x) * D, mask, lane, sadd);
+}
+
+extern "C" int r3_gr_reduce_poly_rows(const uint64_t* acc, int nrows, int d, uint64_t lowterms, uint64_t* out,
+                                      uint64_t mask, void* stream) {
+  if (!valid_d(d) || nrows < 0 || (nrows && (!acc || !out))) {
+    set_error("r3_gr_reduce_poly_rows: bad arguments (d %d, rows %d)", d, nrows);
+    return R3_ERR_ARG;
+  }
+  if (nrows == 0) return R3_OK;
+  cudaStream_t s = as_stream(stream);
+  R3_DISPATCH_D(d, (reduce_poly_rows_kernel<D><<<nrows, 32, 0, s>>>((const u64*)acc, lowterms, (u64*)out, mask)));
+  return check_launch("r3_gr_reduce_poly_rows");
+}
+
 static int finish_mask(u64* out, int64_t n, uint64_t mask, cudaStream_t s) {
   if (mask == ~0ull) return R3_OK;
   mask_rows_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n, mask);

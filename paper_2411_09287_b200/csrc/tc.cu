@@ -495,9 +495,9 @@ constexpr int T16_ACC = 4, T16_ACC_COLS = 128;            // TMEM accumulator bu
 constexpr int T16_THREADS = (T16_EPI + T16_CONV + 2) * 32;
 
 __global__ void __launch_bounds__(T16_THREADS, 1)
-gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-                       int nops, const u64* __restrict__ M0, const u64* __restrict__ M1, u64* __restrict__ out,
-                       int64_t rows, u64 mask) {
+gr_matmul2_tc16_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ M0, const u64* __restrict__ M1,
+                       u64 mask) {
+  const int nops = J.nops;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sRaw = smem;
@@ -544,7 +544,7 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t ntiles = J.tile0[J.njobs];
   const int64_t nunits = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
   if (warp == T16_EPI + T16_CONV) {
@@ -553,11 +553,13 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
       for (int64_t u = 0; u < nunits; ++u) {
         const int st = int(u % T16_RAW_STAGES);
         if (u >= T16_RAW_STAGES) mbar_wait(&raw_empty[st], uint32_t((u / T16_RAW_STAGES - 1) & 1));
-        const int y = int((blockIdx.x + u * gridDim.x) * TC_ROWS);
+        const int64_t t = blockIdx.x + u * gridDim.x;
+        const int j = mm2_job(J, t);
+        const int y = int((t - J.tile0[j]) * TC_ROWS);
         uint8_t* dst = sRaw + st * T16_RAW;
         mbar_expect_tx(&raw_full[st], uint32_t(nops * (T16_RAW / 2)));
-        tma_load_2d(dst, &tm0, 0, y, &raw_full[st]);
-        if (nops > 1) tma_load_2d(dst + T16_RAW / 2, &tm1, 0, y, &raw_full[st]);
+        tma_load_2d(dst, &J.tm[j][0], 0, y, &raw_full[st]);
+        if (nops > 1) tma_load_2d(dst + T16_RAW / 2, &J.tm[j][1], 0, y, &raw_full[st]);
       }
     }
     __syncwarp();
@@ -623,6 +625,11 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
     const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t u = 0; u < nunits; ++u) {
       const int b = int(u % T16_ACC);
+      const int64_t t = blockIdx.x + u * gridDim.x;
+      const int j = mm2_job(J, t);
+      const int64_t lt = t - J.tile0[j];
+      const int64_t rows = J.rows[j];
+      u64* __restrict__ out = J.out[j];
       mbar_wait(&tfull[b], uint32_t((u / T16_ACC) & 1));
       tc_fence_after();
 #pragma unroll 1
@@ -637,7 +644,7 @@ gr_matmul2_tc16_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_con
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
-        const int64_t row = (blockIdx.x + u * gridDim.x) * TC_ROWS + warp * 32 + lg * 16 + rq;
+        const int64_t row = lt * TC_ROWS + warp * 32 + lg * 16 + rq;
         if (row < rows)
           *reinterpret_cast<ulonglong2*>(out + row * T16_D + c0 + cq) = make_ulonglong2(acc[0], acc[1]);
         if (row + 8 < rows)
@@ -743,16 +750,15 @@ extern "C" int r3_gr_matmul2_tc(const uint64_t* p0, int64_t rs0, int64_t nv0, co
   return mm2_launch(J, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), mask, as_stream(stream));
 }
 
-extern "C" int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
-                                      const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
-                                      const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
-                                      uint64_t* const* outs, const int64_t* rows, uint64_t mask, void* stream) {
+// Jobs of a multi launch (both operands present, >= 1 valid row each).
+static int mm2_jobs(Mm2Jobs& J, const char* what, int d, int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                    const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1, const int64_t* nv1,
+                    const uint64_t* M0, const uint64_t* M1, uint64_t* const* outs, const int64_t* rows) {
   if (njobs < 1 || njobs > MM2_MAX_JOBS || !p0 || !p1 || !rs0 || !rs1 || !nv0 || !nv1 || !M0 || !M1 || !outs ||
       !rows) {
-    set_error("r3_gr_matmul2_tc_multi: bad arguments (1..%d jobs)", MM2_MAX_JOBS);
+    set_error("%s: bad arguments (1..%d jobs)", what, MM2_MAX_JOBS);
     return R3_ERR_ARG;
   }
-  Mm2Jobs J;
   J.njobs = njobs;
   J.nops = 2;
   J.tile0[0] = 0;
@@ -761,20 +767,37 @@ extern "C" int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, cons
     const int64_t n0 = nv0[j] < r ? nv0[j] : r, n1 = nv1[j] < r ? nv1[j] : r;
     if (r < 1 || r > (int64_t(1) << 31) - TC_ROWS || !p0[j] || !p1[j] || !outs[j] || n0 < 1 || n1 < 1 ||
         ((rs0[j] | rs1[j]) & 1) || ((uintptr_t(p0[j]) | uintptr_t(p1[j])) & 15)) {
-      set_error("r3_gr_matmul2_tc_multi: job %d: bad operand (rows %lld, valid %lld/%lld, 16-byte aligned rows)",
-                j, (long long)r, (long long)n0, (long long)n1);
+      set_error("%s: job %d: bad operand (rows %lld, valid %lld/%lld, 16-byte aligned rows)", what, j, (long long)r,
+                (long long)n0, (long long)n1);
       return R3_ERR_ARG;
     }
-    if (!make_rows_tmap(&J.tm[j][0], p0[j], n0, rs0[j] > 0 ? rs0[j] : TC_D, TC_ROWS) ||
-        !make_rows_tmap(&J.tm[j][1], p1[j], n1, rs1[j] > 0 ? rs1[j] : TC_D, TC_ROWS)) {
-      set_error("r3_gr_matmul2_tc_multi: cuTensorMapEncodeTiled failed");
+    if (!make_rows_tmap(&J.tm[j][0], p0[j], n0, rs0[j] > 0 ? rs0[j] : d, TC_ROWS, d) ||
+        !make_rows_tmap(&J.tm[j][1], p1[j], n1, rs1[j] > 0 ? rs1[j] : d, TC_ROWS, d)) {
+      set_error("%s: cuTensorMapEncodeTiled failed", what);
       return R3_ERR_CUDA;
     }
     J.out[j] = (u64*)outs[j];
     J.rows[j] = r;
     J.tile0[j + 1] = J.tile0[j] + (r + TC_ROWS - 1) / TC_ROWS;
   }
-  return mm2_launch(J, (const u64*)M0, (const u64*)M1, mask, as_stream(stream));
+  return R3_OK;
+}
+
+static int mm16_launch(const Mm2Jobs& J, const u64* M0, const u64* M1, uint64_t mask, cudaStream_t s) {
+  const int64_t tiles = J.tile0[J.njobs];
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
+  ensure_smem(gr_matmul2_tc16_kernel, T16_SMEM);
+  gr_matmul2_tc16_kernel<<<grid, T16_THREADS, T16_SMEM, s>>>(J, M0, M1, mask);
+  return check_launch("r3_gr_matmul2_tc16");
+}
+
+extern "C" int r3_gr_matmul2_tc_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                                      const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
+                                      const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
+                                      uint64_t* const* outs, const int64_t* rows, uint64_t mask, void* stream) {
+  Mm2Jobs J;
+  const int rc = mm2_jobs(J, "r3_gr_matmul2_tc_multi", TC_D, njobs, p0, rs0, nv0, p1, rs1, nv1, M0, M1, outs, rows);
+  return rc != R3_OK ? rc : mm2_launch(J, (const u64*)M0, (const u64*)M1, mask, as_stream(stream));
 }
 
 extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, const uint64_t* p1, int64_t rs1,
@@ -809,20 +832,31 @@ extern "C" int r3_gr_matmul2_tc16(const uint64_t* p0, int64_t rs0, int64_t nv0, 
     cudaMemsetAsync(out, 0, size_t(rows) * T16_D * 8, as_stream(stream));
     return check_launch("r3_gr_matmul2_tc16(zero)");
   }
-  CUtensorMap tm[2];
+  Mm2Jobs J;
+  J.njobs = 1;
+  J.nops = nops;
   for (int q = 0; q < nops; ++q) {
-    if (!make_rows_tmap(&tm[q], Pk[q], nvk[q], rsk[q], TC_ROWS, T16_D)) {
+    if (!make_rows_tmap(&J.tm[0][q], Pk[q], nvk[q], rsk[q], TC_ROWS, T16_D)) {
       set_error("r3_gr_matmul2_tc16: cuTensorMapEncodeTiled failed");
       return R3_ERR_CUDA;
     }
   }
-  if (nops == 1) tm[1] = tm[0];
-  ensure_smem(gr_matmul2_tc16_kernel, T16_SMEM);
-  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
-  gr_matmul2_tc16_kernel<<<grid, T16_THREADS, T16_SMEM, as_stream(stream)>>>(
-      tm[0], tm[1], nops, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), (u64*)out, rows, mask);
-  return check_launch("r3_gr_matmul2_tc16");
+  if (nops == 1) J.tm[0][1] = J.tm[0][0];
+  J.out[0] = (u64*)out;
+  J.rows[0] = rows;
+  J.tile0[0] = 0;
+  J.tile0[1] = (rows + TC_ROWS - 1) / TC_ROWS;
+  return mm16_launch(J, (const u64*)Mk[0], (const u64*)(nops > 1 ? Mk[1] : Mk[0]), mask, as_stream(stream));
+}
+
+extern "C" int r3_gr_matmul2_tc16_multi(int njobs, const uint64_t* const* p0, const int64_t* rs0,
+                                        const int64_t* nv0, const uint64_t* const* p1, const int64_t* rs1,
+                                        const int64_t* nv1, const uint64_t* M0, const uint64_t* M1,
+                                        uint64_t* const* outs, const int64_t* rows, uint64_t mask, void* stream) {
+  Mm2Jobs J;
+  const int rc = mm2_jobs(J, "r3_gr_matmul2_tc16_multi", T16_D, njobs, p0, rs0, nv0, p1, rs1, nv1, M0, M1, outs,
+                          rows);
+  return rc != R3_OK ? rc : mm16_launch(J, (const u64*)M0, (const u64*)M1, mask, as_stream(stream));
 }
 
 extern "C" int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows, const uint64_t* const* Ms,

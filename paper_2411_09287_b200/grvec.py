@@ -362,6 +362,16 @@ def reduce_poly(acc: torch.Tensor, mod: GrModulus, width: int, out: torch.Tensor
     return out
 
 
+def reduce_poly_rows(acc: torch.Tensor, mod: GrModulus, width: int) -> torch.Tensor:
+    """Every (2d - 1)-word row of the contiguous acc reduced: (rows, d), one
+    launch (r3_gr_reduce_poly_rows)."""
+    d = mod.degree
+    rows = acc.numel() // (2 * d - 1)
+    out = empty((rows, d))
+    call("r3_gr_reduce_poly_rows", ptr(acc), rows, d, mod.lowterms_mask, ptr(out), ring_mask(width), stream())
+    return out
+
+
 def gr_dot(a, b, width: int, mod: GrModulus) -> torch.Tensor:
     """Sum of pairwise products, shape (1, d)."""
     d = mod.degree
@@ -488,14 +498,15 @@ def rows_times(P0: torch.Tensor, M0: torch.Tensor, rows: int, width: int, *,
 
 def rows_times2_batch(jobs: list, M0: torch.Tensor, M1: torch.Tensor, width: int) -> list:
     """[rows_times(ev, M0, n0, P1=od, M1=M1, nvalid=(n0, n1)) for (ev, od,
-    n0, n1) in jobs]: for d = 64 every job with both operands present runs
-    in ONE tensor-core launch (r3_gr_matmul2_tc_multi, up to 8 jobs share
-    the B planes of M0 / M1); other shapes one rows_times each."""
+    n0, n1) in jobs]: for d = 64 / 16 every job with both operands present
+    runs in ONE tensor-core launch (r3_gr_matmul2_tc_multi / _tc16_multi,
+    up to 8 jobs share the B planes of M0 / M1); other shapes one
+    rows_times each."""
     d = M0.shape[0]
     outs = [None] * len(jobs)
     batch = []
     for i, (ev, od, n0, n1) in enumerate(jobs):
-        if d == 64 and n0 >= 1 and n1 >= 1 and _tc_ok(ev) and _tc_ok(od):
+        if d in (16, 64) and n0 >= 1 and n1 >= 1 and _tc_ok(ev) and _tc_ok(od):
             batch.append(i)
         else:
             outs[i] = rows_times(ev, M0, n0, width, P1=od, M1=M1, nvalid=(n0, n1))
@@ -507,7 +518,8 @@ def rows_times2_batch(jobs: list, M0: torch.Tensor, M1: torch.Tensor, width: int
         for i in idx:
             outs[i] = empty((jobs[i][2], d))
         rs = lambda t: t.stride(0) if t.shape[0] > 1 else d
-        call("r3_gr_matmul2_tc_multi", k, P(*[jobs[i][0].data_ptr() for i in idx]),
+        call("r3_gr_matmul2_tc_multi" if d == 64 else "r3_gr_matmul2_tc16_multi", k,
+             P(*[jobs[i][0].data_ptr() for i in idx]),
              L(*[rs(jobs[i][0]) for i in idx]), L(*[jobs[i][2] for i in idx]),
              P(*[jobs[i][1].data_ptr() for i in idx]), L(*[rs(jobs[i][1]) for i in idx]),
              L(*[jobs[i][3] for i in idx]), ptr(M0), ptr(M1), P(*[outs[i].data_ptr() for i in idx]),

@@ -770,7 +770,8 @@ def _level_folds_joint16(party, xt: dict, yt: dict, gr: Ring):
 
     def folds(slots):
         N = slots[0]["x"][0].shape[0]
-        accs = {r: grvec.zeros((2, 2 * gr.d - 1)) for r in range(3)}
+        acc_all = grvec.zeros((3, 2, 2 * gr.d - 1))
+        accs = {r: acc_all[r] for r in range(3)}
         P = C.c_void_p
         xa, ya = slots[0]["x"][0], slots[0]["y"][0]
         # P0's single term: one y half, 1/8 of the MMA used -- still faster
@@ -792,8 +793,8 @@ def _level_folds_joint16(party, xt: dict, yt: dict, gr: Ring):
         a1 = (P * 3)(None, accs[1][0].data_ptr(), accs[2][0].data_ptr())
         a2 = (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr())
         call("r3_vfy_level_fold16_tc", 4, party_ids, xs, y0, y1, c0, c1, N, a1, a2, stream())
-        return {r: (grvec.reduce_poly(accs[r][0], gr.mod, gr.ell), grvec.reduce_poly(accs[r][1], gr.mod, gr.ell))
-                for r in range(3)}
+        red = grvec.reduce_poly_rows(acc_all, gr.mod, gr.ell)   # (6, d): one launch
+        return {r: (red[2 * r:2 * r + 1], red[2 * r + 1:2 * r + 2]) for r in range(3)}
 
     return party.sess.joint(("fold16", party.next_id("_joint.fold16")), role, mine, folds)
 
@@ -822,7 +823,8 @@ def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring, party=None):
     acc = grvec.zeros((2, 2 * gr.d - 1))
     call("r3_vfy_level_fold", role, ptr(xa), ptr(xb), ptr(ya), ptr(yb), N, gr.d,
          ptr(acc[0]), ptr(acc[1]), stream())
-    return (grvec.reduce_poly(acc[0], gr.mod, gr.ell), grvec.reduce_poly(acc[1], gr.mod, gr.ell))
+    red = grvec.reduce_poly_rows(acc, gr.mod, gr.ell)
+    return red[0:1], red[1:2]
 
 
 def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:

@@ -104,23 +104,25 @@ def test_gr_matmul2_tc_line_eval(cuda, d, rows):
         np.testing.assert_array_equal(host(outb), ogr.mul(Xb, z, 64, d) & np.uint64(1))
 
 
-def test_gr_matmul2_tc_multi_matches_single_launches(cuda):
-    """r3_gr_matmul2_tc_multi (several line evaluations sharing M(1 - z),
-    M(z) in one launch: ragged job sizes, odd lengths, a one-row job,
-    strided even/odd views) equals one r3_gr_matmul2_tc launch per job."""
+@pytest.mark.parametrize("d", [64, 16])
+def test_gr_matmul2_tc_multi_matches_single_launches(cuda, d):
+    """r3_gr_matmul2_tc_multi / _tc16_multi (several line evaluations
+    sharing M(1 - z), M(z) in one launch: ragged job sizes, odd lengths, a
+    one-row job, strided even/odd views) equals one single-job launch per
+    job."""
     from paper_2411_09287_b200 import grvec, host
     from paper_2411_09287_b200.rings import modulus_for_degree
-    mod = modulus_for_degree(64)
-    rng = np.random.default_rng(77)
-    z = _rand(rng, (1, 64))
-    one = np.zeros((1, 64), dtype=np.uint64)
+    mod = modulus_for_degree(d)
+    rng = np.random.default_rng(77 + d)
+    z = _rand(rng, (1, d))
+    one = np.zeros((1, d), dtype=np.uint64)
     one[0, 0] = 1
     with np.errstate(over="ignore"):
         Ma = grvec.gr_mulmat(grvec.dev(one - z), mod)
     Mb = grvec.gr_mulmat(grvec.dev(z), mod)
     jobs = []
-    for rows in (2, 3, 257, 4096, 70001, 129, 1000, 9):
-        Xd = grvec.dev(_rand(rng, (rows, 64)))
+    for rows in (2, 3, 257, 4096, 70001, 129, 1000, 9, 33):
+        Xd = grvec.dev(_rand(rng, (rows, d)))
         jobs.append((Xd[0::2], Xd[1::2], (rows + 1) // 2, rows // 2))
     got = grvec.rows_times2_batch(jobs, Ma, Mb, 64)
     for (ev, od, n0, n1), g in zip(jobs, got):

@@ -50,7 +50,7 @@ def test_deferred_digest_mismatch_aborts(cuda):
     with pytest.raises(AbortError):
         sess.run(_mul_open_program())
     assert Tamper.done
-    assert sess._deferred is None and sess._deferred_what == []
+    assert sess._deferred is None and sess._deferred_what == [] and sess._deferred_small == []
     ok = Session(seed=5).run(_mul_open_program())
     assert [int(v) for v in ok[0].cpu()] == [12, 30]
 

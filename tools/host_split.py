@@ -57,6 +57,9 @@ for mod in list(sys.modules.values()):
 b = runtime._Baton
 b.yield_to_scheduler = timed("coop.yield(parked)", b.yield_to_scheduler)
 transport.CoopRouter.send = timed("router.send", transport.CoopRouter.send)
+Session._settle_deferred = timed("settle (device drain)", Session._settle_deferred)
+import torch as _t  # noqa: E402
+_t.Tensor.item = timed("tensor.item (sync)", _t.Tensor.item)
 
 t0 = time.perf_counter()
 Session(seed=9).run(prog, *args)
