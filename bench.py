@@ -678,6 +678,19 @@ class CallProfiler:
         return {"bound": kind, "achieved": self.work[name] / secs / scale, "unit": unit}
 
 
+def table_roofline(tab: dict, peaks: dict) -> dict:
+    """Roofline of the largest-time kernel with a known bound in a kernel
+    table (CallProfiler.table): achieved rate against the peak of its bound,
+    and its share of the leg's wall time."""
+    for t in tab.get("top", []):
+        if "bound" in t and t["bound"] in peaks and t.get("achieved"):
+            peak, src = peaks[t["bound"]]
+            return {"bound": t["bound"], "kernel": t["entry_point"], "achieved": t["achieved"], "peak": peak,
+                    "unit": t["unit"], "frac": t["achieved"] / peak, "share_of_wall": t["share_of_wall"],
+                    "launches": t["launches"], "peak_source": src}
+    return {"bound": None, "why": "no bounded kernel among the top entries"}
+
+
 def work_of(name, args) -> int:
     """Algorithmic work of one call: bytes moved for the HBM-bound tensor-core
     line evaluations (r3_gr_matmul2_tc reads nops rows of 512 B and writes one
@@ -981,6 +994,25 @@ def run_b200(args):
                                  "peak_source": "measured in-run: r3_prf_ctr bulk keystream rate (2^26 blocks)",
                                  "work": "AES blocks of keystream the protocol consumes per lane (every "
                                          "distinct pairwise stream up to its final offset) x lanes / exec time"}
+    # C4 / C5: roofline of each leg's dominant bounded kernel (its kernel
+    # table, CUDA events around every call of one extra session)
+    peaks = None
+    for key in ("mlp", "lenet"):
+        r = side.get(key)
+        if not r:
+            continue
+        if peaks is None:
+            peaks = {"hbm": (hbm_peak()[0] / 1e9, "MEASURED_PEAKS.json hbm_gbs (burst copy)"),
+                     "aes": (prf_peak_blocks(torch, _lib) / 1e9, "measured in-run: r3_prf_ctr bulk rate"),
+                     "tensor": (INT8_DENSE_NOMINAL / 1e12, "nominal dense int8 (4.5 POPS)"),
+                     "int-alu": (imad_peak_macs(torch, _lib) / 1e12, "measured in-run: r3_imad_peak")}
+        rl = {}
+        for leg in ("exec", "verified"):
+            tab = r.get(leg + "_kernels")
+            if tab:
+                rl[leg] = table_roofline(tab, peaks)
+        if rl:
+            r["roofline"] = rl
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
