@@ -169,6 +169,7 @@ def stream() -> int:
 # ---------------------------------------------------------------------------
 
 _cuda_ok = None
+_devices: dict = {}
 
 
 def device() -> torch.device:
@@ -177,7 +178,11 @@ def device() -> torch.device:
         _cuda_ok = torch.cuda.is_available()
     if not _cuda_ok:
         raise RuntimeError("ring3pc-b200 requires a CUDA device (no CPU fallback)")
-    return torch.device("cuda", torch._C._cuda_getDevice())
+    i = torch._C._cuda_getDevice()
+    d = _devices.get(i)
+    if d is None:
+        d = _devices[i] = torch.device("cuda", i)
+    return d
 
 
 def as_i64(v: int) -> int:

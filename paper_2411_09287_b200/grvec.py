@@ -605,8 +605,15 @@ def ew_fields(op: int, a: list, b, mask: int) -> list:
     if not ok:
         return [ew(op, a[c], bl[c] if bl is not None else b, mask) for c in range(k)]
     n = a[0].numel()
-    outs = [torch.empty(shape, dtype=torch.int64, device=a[0].device) for _ in range(k)]
-    arr = _PTRS12(*[o.data_ptr() for o in outs], *([None] * (4 - k)),
+    # one allocation for the k outputs (value semantics: the views are never
+    # written after this call)
+    # rows padded to an even word count keep every output 16-byte aligned
+    npad = n + (n & 1)
+    block = torch.empty((k, npad), dtype=torch.int64, device=a[0].device)
+    outs = [block[c, :n].view(shape) for c in range(k)]
+    base_out = block.data_ptr()
+    step = npad * 8
+    arr = _PTRS12(*[base_out + c * step for c in range(k)], *([None] * (4 - k)),
                   *[t.data_ptr() for t in a], *([None] * (4 - k)),
                   *([u.data_ptr() for u in bl] if bl is not None else [None] * k), *([None] * (4 - k)))
     base = C.addressof(arr)
@@ -622,14 +629,18 @@ def gr_lincomb(terms: list, coeffs: list, width: int, mod: GrModulus) -> list:
     d = mod.degree
     nterms, k = len(terms), len(terms[0])
     shape = terms[0][0].shape
-    flat = [t.reshape(-1, d).contiguous() for row in terms for t in row]
-    cs = [c.reshape(-1)[:d].contiguous() if isinstance(c, torch.Tensor) else to_device(c).reshape(-1)[:d]
-          for c in coeffs]
-    rows = flat[0].shape[0]
-    outs = [torch.empty(shape, dtype=torch.int64, device=flat[0].device) for _ in range(k)]
+    # the kernel reads rows of d words: any contiguous tensor is its own
+    # (rows, d) view, so only non-contiguous operands are copied
+    flat = [t if t.is_contiguous() else t.contiguous() for row in terms for t in row]
+    cs = [(c if c.is_contiguous() else c.contiguous()) if isinstance(c, torch.Tensor)
+          else to_device(c).reshape(-1)[:d] for c in coeffs]
+    rows = flat[0].numel() // d
+    block = torch.empty((k,) + tuple(shape), dtype=torch.int64, device=flat[0].device)
+    outs = list(block.unbind(0)) if k > 1 else [block[0]]
+    step = rows * d * 8
     pa = (C.c_void_p * (nterms * k))(*[t.data_ptr() for t in flat])
     pc = (C.c_void_p * nterms)(*[c.data_ptr() for c in cs])
-    po = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    po = (C.c_void_p * k)(*[block.data_ptr() + i * step for i in range(k)])
     call("r3_gr_lincomb", k, nterms, C.addressof(pa), C.addressof(pc), C.addressof(po), rows, d,
          mod.lowterms_mask, ring_mask(width), stream())
     return outs
