@@ -380,6 +380,39 @@ int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int d, uint64_t* const* out, uint64_t mask,
                         void* stream);
 
+/* ---- packed GF(2^d) verification of boolean multiplication logs ----
+ * Over the boolean ring the verification ring is GR(2, d) = GF(2^d) (d <= 32);
+ * the reference multiplies its (n, d) 0/1 words on bit-packed words
+ * (grvec.py:96-115).  Level vectors here are packed from the start: one
+ * uint32 per element, bit k = coefficient of x^k.  f_low = the modulus f
+ * without x^d (rings.py:180-188).  r, ze: (1, d) 0/1 words in device memory
+ * (the opened challenge r and the opened even point ze = 2 zeta).  Party leg
+ * terms are nterms component-index pairs (tx[t], ty[t]); their +-1
+ * coefficients are 1 mod 2.  Folds come back unpacked, (rows, d) 0/1 words.
+ * scratch: 8 uint32 of device memory per call in flight.
+ *
+ * Level 0 straight from the base log (verify.py:168-179 fused with the first
+ * reduction's inner products, verify.py:229-231): h1 = sum over odd i of
+ * r^i t_i, h2 = sum over even i (char 2: f2 = 2 f1 - f0 = f0), t_i = the xor
+ * of the leg bit products x_tx[i] y_ty[i]; zsum_c = sum_i r^i z_c[i].
+ * folds: (2 + nz) rows h1, h2, zsum_0, zsum_1. */
+int r3_gfv_base_fold(int ncomp, const uint64_t* const* x, const uint64_t* const* y,
+                     int nterms, const int* tx, const int* ty, int nz,
+                     const uint64_t* const* z, int64_t N, const uint64_t* r,
+                     int d, uint32_t f_low, uint64_t* folds, uint32_t* scratch,
+                     void* stream);
+/* One line evaluation out_j = f0_j + (f1_j - f0_j) ze (verify.py:239-240,
+ * odd n_in padded with a zero row, verify.py:220-222) of every component,
+ * from the base bits and the powers r^i (src_base: x'_i = r^i x_i,
+ * y'_i = y_i) or from packed uint32 rows (16-byte aligned), fused with the
+ * h(1)/h(2) folds of the output level (folds != NULL: 2 rows).  Outputs:
+ * ceil(n_in / 2) packed uint32 rows, or (rows, d) 0/1 words if unpacked. */
+int r3_gfv_line(int src_base, int ncomp, const void* const* x, const void* const* y,
+                int64_t n_in, const uint64_t* r, const uint64_t* ze, int d,
+                uint32_t f_low, int unpacked, void* const* ox, void* const* oy,
+                int nterms, const int* tx, const int* ty, uint64_t* folds,
+                uint32_t* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1007,9 +1007,72 @@ def batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None
     ys = _concat_all(log.muls, lambda b: b.y)
     zs = _concat_all(log.muls, lambda b: b.z)
     comp = _compressed_from_log(xs, ys, party.role, 1)
+    if _gf2_packed_ok(gr, R):
+        return _verify_muls_gf2(party, comp, zs, gr, ctx, R)
     zc = zs
     (xv, yv), z = _compress_reduce_first(party, comp, zc, comp.N, 1, gr, ctx, R)
     return _verify_tail(party, xv, yv, z, gr, ctx, R, start=_levels_done(R, gr))
+
+
+def _gf2_packed_ok(gr: Ring, R: int) -> bool:
+    return gr.ell == 1 and 2 <= gr.d <= 32 and R >= 1
+
+
+def _verify_muls_gf2(party, comp: _Compressed, zs: MVal, gr: Ring, chal: Challenges, R: int) -> bool:
+    """Pi_tran + R x Pi_rd + Pi_vdot on a boolean multiplication log with the
+    level vectors packed as GF(2^d) words (csrc/gf2.cu): level 0's folds
+    and z power sums straight from the base bits (r3_gfv_base_fold), then
+    every line evaluation fused with the next level's folds (r3_gfv_line);
+    the last level is written in the reference's (n, d) layout for the
+    check.  Every fold, message and verdict equals the reference's
+    (characteristic 2: the same values as the (n, d) word arithmetic of
+    verify.py:168-263)."""
+    role = party.role
+    names = list(comp.x)
+    idx = {k: i for i, k in enumerate(names)}
+    terms = [(idx[a], idx[b]) for _, a, b in _role_terms(role)]
+    nc, nt = len(names), len(terms)
+    tx = (C.c_int * nt)(*[t[0] for t in terms])
+    ty = (C.c_int * nt)(*[t[1] for t in terms])
+    zc = _components(zs, role)
+    znames = list(zc)
+    zc = {k: t.reshape(-1).contiguous() for k, t in zc.items()}
+    d, f_low = gr.d, gr.mod.lowterms_mask
+    P = C.c_void_p
+    scratch = empty((4,))
+    r = _open_challenge(party, chal.r, "vfy.r")
+    folds = empty((2 + len(znames), d))
+    call("r3_gfv_base_fold", nc, (P * nc)(*[ptr(comp.x[k]) for k in names]),
+         (P * nc)(*[ptr(comp.y[k]) for k in names]), nt, tx, ty, len(znames),
+         (P * 2)(*[ptr(zc[k]) for k in znames]), comp.N, ptr(r), d, f_low, ptr(folds), ptr(scratch), stream())
+    z = _mval_from({k: folds[2 + i:3 + i] for i, k in enumerate(znames)}, gr, role)
+    h1f, h2f = folds[0:1], folds[1:2]
+    n = comp.N
+    src = ([comp.x[k] for k in names], [comp.y[k] for k in names])
+    for k in range(R):
+        rows = (n + 1) // 2
+        h1 = _gr_dot_folded(party, gr, rows, h1f)
+        h2 = _gr_dot_folded(party, gr, rows, h2f)
+        ze = _open_challenge(party, chal.zetas[k].scale_pub(2), "vfy.zeta")
+        z = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
+        last = k == R - 1
+        if last:
+            outs = [empty((rows, d)) for _ in range(2 * nc)]
+            nxt = None
+        else:
+            outs = [torch.empty(rows + 4, dtype=torch.int32, device=r.device) for _ in range(2 * nc)]
+            nxt = empty((2, d))
+        call("r3_gfv_line", 1 if k == 0 else 0, nc, (P * nc)(*[ptr(t) for t in src[0]]),
+             (P * nc)(*[ptr(t) for t in src[1]]), n, ptr(r), ptr(ze), d, f_low, 1 if last else 0,
+             (P * nc)(*[ptr(t) for t in outs[:nc]]), (P * nc)(*[ptr(t) for t in outs[nc:]]), nt, tx, ty,
+             ptr(nxt), ptr(scratch), stream())
+        src = (outs[:nc], outs[nc:])
+        if nxt is not None:
+            h1f, h2f = nxt[0:1], nxt[1:2]
+        n = rows
+    xs = _mval_from(dict(zip(names, src[0])), gr, role)
+    ys = _mval_from(dict(zip(names, src[1])), gr, role)
+    return check_inner_product(party, xs, ys, z, gr, chal.alpha)
 
 
 def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:

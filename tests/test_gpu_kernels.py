@@ -480,3 +480,88 @@ def test_ew3_matches_two_subtractions(cuda):
         for w in (64, 1, 37):
             np.testing.assert_array_equal(host(grvec.sub3(a, b, c, w)),
                                           host(grvec.sub(grvec.sub(a, b, w), c, w)))
+
+
+@pytest.mark.parametrize("d,N", [(16, 1), (16, 7), (16, 1000), (8, 4099), (32, 2051), (16, 100003)])
+def test_gfv_packed_boolean_levels_match_oracle(cuda, d, N):
+    """The packed GF(2^d) boolean verification kernels (csrc/gf2.cu) against
+    the oracle's GR(2, d) arithmetic on (n, d) 0/1 words with the general
+    formulas (f2 = 2 f1 - f0, line f0 + (f1 - f0) ze): level-0 folds and z
+    power sums from the base bits, the first line evaluation from the base
+    bits fused with the level-1 folds, then a packed line evaluation written
+    unpacked (verify.py:168-241)."""
+    import ctypes as C
+    import torch
+    from oracle import gr as ogr
+    from paper_2411_09287_b200 import _lib, grvec, host
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    rng = np.random.default_rng(N + d)
+    mod = modulus_for_degree(d)
+    nc, terms = 2, [(1, 1), (1, 0), (0, 1)]
+    X = [rng.integers(0, 2, N, dtype=np.uint64) for _ in range(nc)]
+    Y = [rng.integers(0, 2, N, dtype=np.uint64) for _ in range(nc)]
+    Z = [rng.integers(0, 2, N, dtype=np.uint64) for _ in range(2)]
+    r = rng.integers(0, 2, (1, d), dtype=np.uint64)
+    zes = [rng.integers(0, 2, (1, d), dtype=np.uint64) for _ in range(2)]
+    pw = ogr.powers(r, N, 1, d)
+    xl = [ogr.mul(ogr.embed(x, d), pw, 1, d) for x in X]
+    yl = [ogr.embed(y, d) for y in Y]
+
+    def folds(xv, yv):
+        n = xv[0].shape[0]
+        pad = lambda a: np.vstack([a, np.zeros((1, d), np.uint64)]) if n % 2 else a
+        h1 = np.zeros((1, d), np.uint64)
+        h2 = np.zeros((1, d), np.uint64)
+        for tx, ty in terms:
+            fx, fy = pad(xv[tx]), pad(yv[ty])
+            f2x = (2 * fx[1::2] - fx[0::2]) & np.uint64(1)
+            f2y = (2 * fy[1::2] - fy[0::2]) & np.uint64(1)
+            h1 = (h1 + ogr.dot(fx[1::2], fy[1::2], 1, d)) & np.uint64(1)
+            h2 = (h2 + ogr.dot(f2x, f2y, 1, d)) & np.uint64(1)
+        return np.vstack([h1, h2])
+
+    def line(v, ze):
+        v = np.vstack([v, np.zeros((1, d), np.uint64)]) if v.shape[0] % 2 else v
+        f0, f1 = v[0::2], v[1::2]
+        with np.errstate(over="ignore"):
+            return (f0 + ogr.mul(f1 - f0, ze, 1, d)) & np.uint64(1)
+
+    P = C.c_void_p
+    dev = lambda a: grvec.dev(np.ascontiguousarray(a))
+    Xd, Yd, Zd = [dev(x) for x in X], [dev(y) for y in Y], [dev(z) for z in Z]
+    rd, zed = dev(r), [dev(z) for z in zes]
+    tx = (C.c_int * 3)(*[t[0] for t in terms])
+    ty = (C.c_int * 3)(*[t[1] for t in terms])
+    scratch = grvec.zeros((4,))
+    f_low = mod.lowterms_mask
+    out0 = grvec.empty((4, d))
+    _lib.call("r3_gfv_base_fold", nc, (P * nc)(*[t.data_ptr() for t in Xd]), (P * nc)(*[t.data_ptr() for t in Yd]),
+              3, tx, ty, 2, (P * 2)(*[t.data_ptr() for t in Zd]), N, rd.data_ptr(), d, f_low, out0.data_ptr(),
+              scratch.data_ptr(), _lib.stream())
+    want0 = folds(xl, yl)
+    zs = [(ogr.dot(ogr.embed(z, d), pw, 1, d)) & np.uint64(1) for z in Z]
+    np.testing.assert_array_equal(host(out0), np.vstack([want0] + zs))
+    # first line evaluation from the base bits + level-1 folds
+    n1 = (N + 1) // 2
+    o1 = [torch.empty(n1 + 4, dtype=torch.int32, device="cuda") for _ in range(2 * nc)]
+    f1 = grvec.empty((2, d))
+    _lib.call("r3_gfv_line", 1, nc, (P * nc)(*[t.data_ptr() for t in Xd]), (P * nc)(*[t.data_ptr() for t in Yd]),
+              N, rd.data_ptr(), zed[0].data_ptr(), d, f_low, 0, (P * nc)(*[t.data_ptr() for t in o1[:nc]]),
+              (P * nc)(*[t.data_ptr() for t in o1[nc:]]), 3, tx, ty, f1.data_ptr(), scratch.data_ptr(), _lib.stream())
+    x1 = [line(v, zes[0]) for v in xl]
+    y1 = [line(v, zes[0]) for v in yl]
+    pack = lambda a: (a.astype(np.uint64) << np.arange(d, dtype=np.uint64)).sum(axis=1).astype(np.uint64)
+    for c in range(nc):
+        np.testing.assert_array_equal(o1[c][:n1].cpu().numpy().view(np.uint32).astype(np.uint64), pack(x1[c]))
+        np.testing.assert_array_equal(o1[nc + c][:n1].cpu().numpy().view(np.uint32).astype(np.uint64), pack(y1[c]))
+    np.testing.assert_array_equal(host(f1), folds(x1, y1))
+    # packed line evaluation, unpacked output, no fold
+    n2 = (n1 + 1) // 2
+    o2 = [grvec.empty((n2, d)) for _ in range(2 * nc)]
+    _lib.call("r3_gfv_line", 0, nc, (P * nc)(*[t.data_ptr() for t in o1[:nc]]),
+              (P * nc)(*[t.data_ptr() for t in o1[nc:]]), n1, None, zed[1].data_ptr(), d, f_low, 1,
+              (P * nc)(*[t.data_ptr() for t in o2[:nc]]), (P * nc)(*[t.data_ptr() for t in o2[nc:]]), 0, None, None,
+              None, None, _lib.stream())
+    for c in range(nc):
+        np.testing.assert_array_equal(host(o2[c]), line(x1[c], zes[1]))
+        np.testing.assert_array_equal(host(o2[nc + c]), line(y1[c], zes[1]))
