@@ -350,6 +350,16 @@ int r3_vfy_base_fold_q4(int np, const int* nterms, const int64_t* coef,
                         const int* nz, const uint64_t* const* zc, const int64_t* zs,
                         int64_t N, const uint64_t* pw4, int d, uint64_t* const* acc,
                         uint64_t* const* zraw, void* stream);
+/* Base fold over blocks of eight against pw8[j] = r^(8j) (d = 64, N >= 8 *
+ * 4096, tensor cores): acc'[a*8+b] = sum_j s^{ab}_j r^(8j) (64 x d) and
+ * zraw[c*8+a] = sum_j z_c[8j+a] r^(8j) -- every accumulator the first THREE
+ * reductions need (verify.py:215-241 at k = 0, 1, 2); same operand
+ * conventions as r3_vfy_base_fold_q4. */
+int r3_vfy_base_fold_q8(int np, const int* nterms, const int64_t* coef,
+                        const uint64_t* const* xc, const uint64_t* const* yc,
+                        const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                        int64_t N, const uint64_t* pw8, int d, uint64_t* const* acc,
+                        uint64_t* const* zraw, void* stream);
 /* h1/h2 level-1 folds from the 16 accumulators; masks the nz z sums. */
 int r3_vfy_base_fold_finish(int d, int nz, const uint64_t* acc, uint64_t* h1,
                             uint64_t* h2, uint64_t* zsum, uint64_t mask, void* stream);
@@ -369,12 +379,14 @@ int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                    int64_t ls, const uint64_t* pw, int d, uint64_t* acc,
                    void* stream);
 /* out_c[j] = sum_{a<B} X_c[Bj+a] * T_a[(Bj+a)/tq] with tables T_a at
- * tabs + a*tab_stride (words): level-B vectors from the base log. */
+ * tabs + a*tab_stride (words), B <= 8 (B > 4: multiplication logs, n = 1,
+ * tq = B): level-log2(B) vectors from the base log. */
 int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N,
                   int64_t n, int64_t ks, int64_t ls, const uint64_t* tabs,
                   int64_t tab_stride, int64_t tq, int d, uint64_t* const* out,
                   uint64_t mask, void* stream);
-/* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B public GR constants). */
+/* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B <= 8 public GR constants; B > 4
+ * for n = 1 only). */
 int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int64_t n, int64_t ks, int64_t ls, const uint64_t* g,
                         int d, uint64_t* const* out, uint64_t mask,

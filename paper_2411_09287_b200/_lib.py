@@ -95,6 +95,8 @@ _SIGS = {
                                C.c_void_p, C.c_void_p, u64, C.c_void_p],
     "r3_vfy_base_fold_q4": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
+    "r3_vfy_base_fold_q8": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                            C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
     "r3_vfy_base_fold_finish": [C.c_int, C.c_int, u64p, u64p, u64p, u64p, u64, C.c_void_p],
     "r3_vfy_l2_fold": [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i64,
                        i64, i64, i64, u64p, C.c_int, u64p, C.c_void_p],
@@ -258,6 +260,20 @@ def to_device(x) -> torch.Tensor:
             arr = arr.astype(np.uint64)
     arr = np.ascontiguousarray(arr)
     return torch.from_numpy(arr.view(np.int64)).to(device())
+
+
+_consts: dict = {}
+
+
+def const(key, make) -> torch.Tensor:
+    """A constant device tensor built once per process and device by make():
+    a host array -> device copy from pageable memory synchronises the
+    stream, which the protocol driver must not do per call."""
+    k = (key, torch._C._cuda_getDevice())
+    t = _consts.get(k)
+    if t is None:
+        t = _consts[k] = make()
+    return t
 
 
 def to_host(t) -> np.ndarray:

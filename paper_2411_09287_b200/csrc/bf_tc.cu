@@ -40,8 +40,8 @@ struct BfParty {
   u64 coef[3];
   int nterms, nz;
   int64_t zs;
-  u64* acc;    // 16 x 64
-  u64* zraw;   // (4 nz) x 64
+  u64* acc;    // B^2 x 64
+  u64* zraw;   // (B nz) x 64
 };
 
 struct BfArgs {
@@ -52,6 +52,11 @@ struct BfArgs {
 };
 
 
+// B = 4: the three parties' features share the 128 MMA rows (party p:
+// 32 p + q).  B = 8: 64 s products + 8 nz z values per party, so a work item
+// is (K chunk, party) and the np items of one chunk are adjacent in the
+// grid (co-resident: the table rows come from HBM once, L2 for the others).
+template <int B>
 __global__ void __launch_bounds__(BF_THREADS, 1)
 base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -71,9 +76,10 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 
   // persistent: CTA b takes K-chunks (items) b, b + grid, ... of kc blocks;
   // unit g enumerates (item, K-step) in that order
-  const int64_t nitems = (args.nblk + args.kc - 1) / args.kc;
+  const int64_t nchunks = (args.nblk + args.kc - 1) / args.kc;
+  const int64_t nitems = B == 4 ? nchunks : nchunks * args.np;
   auto item_range = [&](int64_t it, int64_t& j0, int64_t& j1) {
-    j0 = it * args.kc;
+    j0 = (B == 4 ? it : it / args.np) * args.kc;
     j1 = min(args.nblk, j0 + args.kc);
   };
 
@@ -122,10 +128,10 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     const bool isA = lt < 256;
     const int k = lt & 31;
     const int c = isA ? (lt >> 5) : ((lt - 256) >> 5);
-    const int p = c >> 1, h = c & 1;
-    const bool live = isA && p < args.np;
     int64_t g = -1;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int p = B == 4 ? c >> 1 : int(it % args.np), h = B == 4 ? c & 1 : (c < 4 ? 0 : (c == 4 ? 1 : 2));
+    const bool live = isA && p < args.np && h < 2;
     int64_t j0, j1;
     item_range(it, j0, j1);
     const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
@@ -138,7 +144,39 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = 0;
       if (isA) {
-        if (live && ok) {
+        if (live && ok && B == 8) {
+          const BfParty& P = args.p[p];
+          const int64_t i0 = 8 * j;
+          if (h == 0) {          // s products of rows a = 2c, 2c + 1: v[(a - 2c) 8 + b]
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              if (t >= P.nterms) break;
+              u64 xv[2], yv[8];
+#pragma unroll
+              for (int a = 0; a < 2; ++a) {
+                const int64_t i = i0 + 2 * c + a;
+                xv[a] = i < args.N ? __ldg(P.x[t] + i) : 0ull;
+              }
+#pragma unroll
+              for (int b = 0; b < 8; ++b) yv[b] = i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
+#pragma unroll
+              for (int a = 0; a < 2; ++a) {
+                const u64 cx = P.coef[t] * xv[a];
+#pragma unroll
+                for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[b];
+              }
+            }
+          } else {               // z values: v[cz 8 + a]
+#pragma unroll
+            for (int cz = 0; cz < 2; ++cz) {
+              if (cz < P.nz) {
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+                  v[cz * 8 + a] = i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
+              }
+            }
+          }
+        } else if (live && ok) {
           const BfParty& P = args.p[p];
           const int64_t i0 = 4 * j;
           if (h == 0) {
@@ -243,10 +281,17 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       ph ^= 1;
       tc_fence_after();
       const int f = warp * 32 + lane;
-      const int p = f >> 5, q = f & 31;
-      const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
       u64* dst = nullptr;
-      if (live) dst = q < 16 ? args.p[p].acc + q * 64 : args.p[p].zraw + (q - 16) * 64;
+      if (B == 4) {
+        const int p = f >> 5, q = f & 31;
+        const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
+        if (live) dst = q < 16 ? args.p[p].acc + q * 64 : args.p[p].zraw + (q - 16) * 64;
+      } else {
+        const BfParty& P = args.p[it % args.np];
+        if (f < 64) dst = P.acc + f * 64;
+        else if (f < 64 + 8 * P.nz) dst = P.zraw + (f - 64) * 64;
+      }
+      const bool live = dst != nullptr;
       const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
 #pragma unroll 1
       for (int c0 = 0; c0 < 64; c0 += 8) {
@@ -278,13 +323,14 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 
 using namespace r3;
 
-// d = 64 form of r3_vfy_base_fold_q4 (same contract); -1 if not applicable.
-int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
-                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
-                    int64_t N, const uint64_t* pw4, uint64_t* const* acc, uint64_t* const* zraw,
-                    cudaStream_t s) {
-  const int64_t nblk = (N + 3) / 4;
-  if (nblk < 4096 || (uintptr_t(pw4) & 15)) return -1;
+namespace {
+
+template <int B>
+int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                        const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                        int64_t N, const uint64_t* pw, uint64_t* const* acc, uint64_t* const* zraw,
+                        cudaStream_t s, const char* what) {
+  const int64_t nblk = (N + B - 1) / B;
   BfArgs args{};
   args.np = np;
   args.N = N;
@@ -303,20 +349,59 @@ int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64
     P.acc = reinterpret_cast<u64*>(acc[q]);
     P.zraw = reinterpret_cast<u64*>(zraw[q]);
   }
-  if (!make_rows_tmap(&args.pw4, pw4, nblk, 64, BF_BK, 64)) {
-    set_error("r3_vfy_base_fold_q4(tc): cuTensorMapEncodeTiled failed");
+  if (!make_rows_tmap(&args.pw4, pw, nblk, 64, BF_BK, 64)) {
+    set_error("%s: cuTensorMapEncodeTiled failed", what);
     return R3_ERR_CUDA;
   }
-  // K-chunks of <= BF_MAX_K blocks, a whole number of chunks per CTA of a
+  // K-chunks of <= BF_MAX_K blocks, a whole number of items per CTA of a
   // persistent grid (no partial second wave)
-  int64_t items = (nblk + BF_MAX_K - 1) / BF_MAX_K;
+  const int per = B == 4 ? 1 : np;          // items per K-chunk
+  int64_t chunks = (nblk + BF_MAX_K - 1) / BF_MAX_K;
+  int64_t items = chunks * per;
   items = (items + num_sms() - 1) / num_sms() * num_sms();
-  int64_t kc = (nblk + items - 1) / items;
+  chunks = (items + per - 1) / per;
+  int64_t kc = (nblk + chunks - 1) / chunks;
   kc = (kc + BF_BK - 1) / BF_BK * BF_BK;
-  items = (nblk + kc - 1) / kc;
+  items = (nblk + kc - 1) / kc * per;
   args.kc = kc;
-  const unsigned grid = unsigned(items < num_sms() ? items : num_sms());
-  ensure_smem(base_fold_tc_kernel, BF_SMEM);
-  base_fold_tc_kernel<<<grid, BF_THREADS, BF_SMEM, s>>>(args);
-  return check_launch("r3_vfy_base_fold_q4(tc)");
+  const unsigned grid = unsigned(items < num_sms() ? items : num_sms() / per * per);
+  ensure_smem(base_fold_tc_kernel<B>, BF_SMEM);
+  base_fold_tc_kernel<B><<<grid, BF_THREADS, BF_SMEM, s>>>(args);
+  return check_launch(what);
+}
+
+}  // namespace
+
+// d = 64 form of r3_vfy_base_fold_q4 (same contract); -1 if not applicable.
+int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                    int64_t N, const uint64_t* pw4, uint64_t* const* acc, uint64_t* const* zraw,
+                    cudaStream_t s) {
+  const int64_t nblk = (N + 3) / 4;
+  if (nblk < 4096 || (uintptr_t(pw4) & 15)) return -1;
+  return base_fold_tc_launch<4>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw4, acc, zraw, s,
+                                "r3_vfy_base_fold_q4(tc)");
+}
+
+extern "C" int r3_vfy_base_fold_q8(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                                   const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                                   const int64_t* zs, int64_t N, const uint64_t* pw8, int d,
+                                   uint64_t* const* acc, uint64_t* const* zraw, void* stream) {
+  if (np < 1 || np > 3 || d != 64 || N < 8 * 4096 || (uintptr_t(pw8) & 15) || !nterms || !nz) {
+    set_error("r3_vfy_base_fold_q8: bad arguments (np %d, d %d, N %lld)", np, d, (long long)N);
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  for (int q = 0; q < np; ++q) {
+    if (nterms[q] < 1 || nterms[q] > 3 || nz[q] < 0 || nz[q] > 2 || zs[q] < 1) {
+      set_error("r3_vfy_base_fold_q8: bad terms / z count for party %d", q);
+      return R3_ERR_ARG;
+    }
+    if (cudaMemsetAsync(acc[q], 0, size_t(64) * 64 * 8, s) != cudaSuccess ||
+        (nz[q] > 0 && cudaMemsetAsync(zraw[q], 0, size_t(nz[q]) * 8 * 64 * 8, s) != cudaSuccess)) {
+      set_error("r3_vfy_base_fold_q8: memset failed");
+      return R3_ERR_CUDA;
+    }
+  }
+  return base_fold_tc_launch<8>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw8, acc, zraw, s, "r3_vfy_base_fold_q8");
 }

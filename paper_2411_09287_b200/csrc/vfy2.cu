@@ -109,24 +109,25 @@ l2_fold_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t
 template <int D>
 __host__ __device__ constexpr int lb_cpt() { return D == 16 ? 4 : 2; }
 
-template <int D, bool ONE, bool TAB>
-__global__ void __launch_bounds__(256, 4)
+template <int D, bool ONE, bool TAB, int BM>
+__global__ void __launch_bounds__(256, BM == 8 ? 2 : 4)
 line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
   // Lane (row j, coefficients k..k+CPT-1); the 4 lanes of an aligned quad
-  // share j (H is a multiple of 4), lane b of a quad loads the scalar of
-  // element B j + b for every component, and the quad exchanges them by
-  // shuffles: one load per component per lane, all issued before any store.
-  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT;
+  // share j (H is a multiple of 4), lane b of a quad loads the scalars of
+  // elements B j + b (+ 4h for blocks of BM = 8) for every component, and the
+  // quad exchanges them by shuffles: BM / 4 loads per component per lane, all
+  // issued before any store.
+  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT, NH = BM / 4;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
   const int lane = threadIdx.x & 31, bl = lane & 3, quad0 = lane & ~3;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int k = CPT * int((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) % H);   // invariant: H | stride
-  ulonglong2 w[4][V];
+  ulonglong2 w[BM][V];
   if (!TAB) {   // public constants g (B x D): per lane, loaded once
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < BM; ++a)
 #pragma unroll
       for (int q = 0; q < V; ++q)
         w[a][q] = a < B ? __ldg(reinterpret_cast<const ulonglong2*>(tabs + a * D + k) + q) : make_ulonglong2(0ull, 0ull);
@@ -135,15 +136,18 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
     const int64_t e = e0 + lane;
     const bool live = e < total;
     const int64_t j = e / H;
-    const int64_t i = B * j + bl;
-    const bool ok = live && bl < B && i < N;
-    const int64_t off = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : 0;
-    u64 xs[8];
+    u64 xs[8][NH];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) xs[c] = (c < ncomp && ok) ? __ldg(xc.p[c] + off) : 0ull;
+    for (int h = 0; h < NH; ++h) {
+      const int64_t i = B * j + bl + 4 * h;
+      const bool ok = live && bl + 4 * h < B && i < N;
+      const int64_t off = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : 0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) xs[c][h] = (c < ncomp && ok) ? __ldg(xc.p[c] + off) : 0ull;
+    }
     if (TAB) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
+      for (int a = 0; a < BM; ++a) {
         const int64_t ia = B * j + a;
         const bool oka = live && a < B && ia < N;
         const int64_t row = ONE ? j : qdiv(ia, tq);
@@ -160,8 +164,8 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
 #pragma unroll
         for (int q = 0; q < V; ++q) v[q] = make_ulonglong2(0ull, 0ull);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const u64 xv = __shfl_sync(0xffffffffu, xs[c], quad0 + a);
+        for (int a = 0; a < BM; ++a) {
+          const u64 xv = __shfl_sync(0xffffffffu, xs[c][a >> 2], quad0 + (a & 3));
 #pragma unroll
           for (int q = 0; q < V; ++q) {
             v[q].x += xv * w[a][q].x;
@@ -459,7 +463,7 @@ extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* c
 extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N, int64_t n, int64_t ks,
                              int64_t ls, const uint64_t* tabs, int64_t tab_stride, int64_t tq, int d,
                              uint64_t* const* out, uint64_t mask, void* stream) {
-  if (B < 1 || B > 4 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1) {
+  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1 || (B > 4 && (n != 1 || tq != B))) {
     set_error("r3_vfy_line_b: bad arguments");
     return R3_ERR_ARG;
   }
@@ -472,11 +476,14 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
   }
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
-  if (n == 1 && tq == B) {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, true, true><<<grid_for(total, 256), 256, 0, s>>>(
+  if (n == 1 && tq == B && B > 4) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, true, 8><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  } else if (n == 1 && tq == B) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, true, 4><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
   } else {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, false, true><<<grid_for(total, 256), 256, 0, s>>>(
+    R3_DISPATCH_D2(d, (line_b_kernel<D, false, true, 4><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
   }
   return check_launch("r3_vfy_line_b");
@@ -485,7 +492,7 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
 extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
                                    int64_t ls, const uint64_t* g, int d, uint64_t* const* out, uint64_t mask,
                                    void* stream) {
-  if (B < 1 || B > 4 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1) {
+  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || (B > 4 && n != 1)) {
     set_error("r3_vfy_line_b_const: bad arguments");
     return R3_ERR_ARG;
   }
@@ -498,11 +505,14 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   }
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
-  if (n == 1) {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, true, false><<<grid_for(total, 256), 256, 0, s>>>(
+  if (n == 1 && B > 4) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, false, 8><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
+  } else if (n == 1) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, false, 4><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
   } else {
-    R3_DISPATCH_D2(d, (line_b_kernel<D, false, false><<<grid_for(total, 256), 256, 0, s>>>(
+    R3_DISPATCH_D2(d, (line_b_kernel<D, false, false, 4><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
   }
   return check_launch("r3_vfy_line_b_const");

@@ -478,6 +478,10 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     base_acc = q4 = pw = None
     base_ok = (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
                and len(names) <= 2)
+    if base_ok and R >= 3 and gr.d == 64 and comp.N >= _Q8_MIN_N:
+        # three reductions from one pass over r^(8j): the dense tail starts
+        # at level 3 (N/8 rows)
+        return _reduce_three_from_base(party, comp, [zc[k] for k in names], names, z_stride, r, gr, chal)
     if base_ok and gr.d == 64:
         # one pass over the table r^(4j) on the tensor cores: z power sum,
         # level-2 accumulators and the level-1 folds derived from them; the
@@ -494,7 +498,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
         zsum = _powsum([zc[k] for k in names], z_stride, z_lanes, pw, gr)
     z = _mval_from({k: zsum[i] for i, k in enumerate(names)}, gr, party.role)
     if R == 0:
-        return _materialise(comp, pw, gr, party.role), z
+        return _materialise(comp, pw, gr, party.role), z, 0
     if base_acc is None:
         h1f, h2f = _l1_folds(party, comp, pw, gr)
     h1 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h1f)
@@ -502,7 +506,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
     z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
     if R >= 2 and gr.d >= 8:
-        return _reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc, q4)
+        return (*_reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc, q4), 2)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
     tq = 2 if comp.n == 1 else comp.n
     half = (comp.N + 1) // 2
@@ -515,7 +519,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
          comp.ls, ptr(one_m), ptr(ze), gr.d, _ptrs([yo[k] for k in yk]), gr.mask, stream())
     xs1 = _mval_from(xo, gr, party.role)
     ys1 = _mval_from(yo, gr, party.role)
-    return (xs1, ys1), z_out
+    return (xs1, ys1), z_out, 1
 
 
 def _l2_weights(party, ze1: torch.Tensor, gr: Ring):
@@ -597,6 +601,213 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     else:
         res = level2_vectors({role: mine})[role]
     return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z2
+
+
+_Q8_MIN_N = 8 * 4096
+
+
+def _powers8(party, r: torch.Tensor, n8: int, gr: Ring):
+    """(r^(8j) for j < n8, r^0..r^7): every eighth power and the in-block
+    offsets (pw[8j + a] = pw8[j] r^a)."""
+    key = ("pow8", gr.ell, gr.d, _opened_key(party, r), n8)
+
+    def build():
+        rpow = grvec.gr_powers(r, 9, gr.ell, gr.mod)
+        return grvec.gr_powers(rpow[8:9], n8, gr.ell, gr.mod), rpow[:8].contiguous()
+    return _public(party, key, build)
+
+
+def _base_fold_q8(party, comp: _Compressed, zcomps: list, z_stride: int, q8, gr: Ring):
+    """(zsum (nz, 1, d), acc (64, d)) with acc[a*8+b] = sum_j s^{ab}_j r^(8j+a)
+    and zsum_c = sum_i z_c[i] r^i, from ONE pass over the r^(8j) table on the
+    tensor cores (r3_vfy_base_fold_q8; the raw sums over r^(8j) are taken
+    times r^a here).  Honest joint sessions fold all three parties in one
+    launch (the adjacent party items share the table rows in L2)."""
+    pw8, rpow = q8
+    mine = {"terms": _role_terms(party.role), "x": comp.x, "y": comp.y, "z": zcomps}
+    d = gr.d
+    r_acc = rpow.repeat_interleave(8, dim=0)          # row a*8 + b -> r^a
+
+    def folds(slots):
+        roles = sorted(slots)
+        np_ = len(roles)
+        nterms = (C.c_int * np_)(*[len(slots[r]["terms"]) for r in roles])
+        nz = (C.c_int * np_)(*[len(slots[r]["z"]) for r in roles])
+        coef = (C.c_int64 * (3 * np_))()
+        xs, ys, zp = (C.c_void_p * (3 * np_))(), (C.c_void_p * (3 * np_))(), (C.c_void_p * (2 * np_))()
+        raw = {}
+        for q, r in enumerate(roles):
+            sl = slots[r]
+            for t, (cf, xk, yk) in enumerate(sl["terms"]):
+                coef[3 * q + t], xs[3 * q + t], ys[3 * q + t] = cf, ptr(sl["x"][xk]), ptr(sl["y"][yk])
+            for c, zt in enumerate(sl["z"]):
+                zp[2 * q + c] = ptr(zt)
+            raw[r] = (empty((64, d)), empty((max(1, len(sl["z"])) * 8, d)))
+        zs = (C.c_int64 * np_)(*([z_stride] * np_))
+        arrs = [(C.c_void_p * np_)(*[ptr(raw[r][i]) for r in roles]) for i in range(2)]
+        call("r3_vfy_base_fold_q8", np_, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+             C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zs), comp.N, ptr(pw8), d,
+             C.addressof(arrs[0]), C.addressof(arrs[1]), stream())
+        out = {}
+        for r in roles:
+            acc_raw, z_raw = raw[r]
+            nzr = len(slots[r]["z"])
+            acc = grvec.gr_mul(acc_raw, r_acc, gr.ell, gr.mod)
+            zsum = empty((nzr, 1, d))
+            if nzr:
+                zc = grvec.gr_mul(z_raw[:8 * nzr], rpow.repeat(nzr, 1), gr.ell, gr.mod)
+                for c in range(nzr):
+                    zsum[c] = grvec.sum_axis0(zc[8 * c:8 * c + 8], gr.ell, keepdims=True)
+            out[r] = (zsum, acc)
+        return out
+
+    if _joint_ok(party):
+        return party.sess.joint(("bfold8", party.next_id("_joint.bfold8")), party.role, mine, folds)
+    return folds({party.role: mine})[party.role]
+
+
+def _block_fold_weights(party, k: int, ws: list, gr: Ring):
+    """Public weights (W1, W2), each (64, d), of level k < 3's folds over the
+    64 block accumulators: h = sum_q acc[q] (x) W[q] (verify.py:229-231 with
+    the level-k vectors expanded into the base blocks of eight).  A level-k
+    row spans 2^k base elements a with line weight V_a = prod_{l<k}
+    ws[l][bit l of a]; the pair (f0, f1) of rows spans 2^(k+1), bit k of a
+    tells f0 from f1.  W1 keeps a, b both in f1; W2 weighs alpha_a alpha_b
+    (alpha = -1 on f0, 2 on f1: f2 = 2 f1 - f0)."""
+    key = ("bw8", gr.ell, gr.d, k, tuple(_opened_key(party, w[1]) for w in ws))
+
+    def build():
+        d = gr.d
+        nv = 1 << k
+        if k == 0:
+            vals = grvec.gr_const(1, gr.mod, gr.ell)
+        else:
+            vals = None
+            for lvl in range(k):      # V[u] for u < 2^k: bit l of u picks ws[l][.]
+                w = torch.cat([ws[lvl][0], ws[lvl][1]])
+                if vals is None:
+                    vals = w
+                else:
+                    n = vals.shape[0]
+                    vals = grvec.gr_mul(vals.repeat(2, 1), w.repeat_interleave(n, dim=0), gr.ell, gr.mod)
+        prod = grvec.gr_mul(vals.repeat_interleave(nv, dim=0), vals.repeat(nv, 1), gr.ell, gr.mod)  # [u*nv + v]
+        idx, c1, c2 = _block_fold_index(k, prod.device)
+        rows = prod[idx]
+        m = _lib_i64(gr.mask)
+        W1 = (rows * c1) & m
+        W2 = (rows * c2) & m
+        return W1.contiguous(), W2.contiguous()
+    return _public(party, key, build)
+
+
+_BF_INDEX: dict = {}
+
+
+def _block_fold_index(k: int, dev):
+    """Device constants of _block_fold_weights for level k: the product row
+    of each accumulator and its integer coefficients in W1 / W2.  Built once
+    per process and device (a host list -> device copy synchronises the
+    stream, which the protocol driver must not do per session)."""
+    key = (k, dev)
+    hit = _BF_INDEX.get(key)
+    if hit is None:
+        nv = 1 << k
+        idx, c1, c2 = [], [], []
+        alpha = (-1, 2)
+        for a in range(8):
+            for b in range(8):
+                same = (a >> (k + 1)) == (b >> (k + 1))
+                ba, bb = (a >> k) & 1, (b >> k) & 1
+                idx.append((a & (nv - 1)) * nv + (b & (nv - 1)))
+                c1.append(1 if same and ba and bb else 0)
+                c2.append(alpha[ba] * alpha[bb] if same else 0)
+        hit = _BF_INDEX[key] = (torch.tensor(idx, device=dev), torch.tensor(c1, device=dev)[:, None],
+                                torch.tensor(c2, device=dev)[:, None])
+    return hit
+
+
+def _lib_i64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >> 63 else v
+
+
+def _reduce_three_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
+                            r: torch.Tensor, gr: Ring, chal: Challenges):
+    """Pi_tran and the first THREE Pi_rd (verify.py:168-179 + 215-241 at
+    k = 0, 1, 2) from the base log: the 64 accumulators of blocks of eight
+    (r3_vfy_base_fold_q8) give every level's h(1)/h(2) folds through public
+    weights, and the level-3 vectors for the dense tail are written straight
+    from the base shares with the public tables V_a[j] = r^(8j) (r^a kappa_a)
+    (r3_gr_matmul_q_tc, then r3_vfy_line_b with blocks of eight).  Returns
+    ((xs, ys), z, 3)."""
+    role = party.role
+    n8 = (comp.N + 7) // 8
+    q8 = _powers8(party, r, n8, gr)
+    zsum, acc = _base_fold_q8(party, comp, zlist, z_stride, q8, gr)
+    z = _mval_from({k: zsum[i] for i, k in enumerate(znames)}, gr, role)
+    ws = []
+    n = comp.N
+    for k in range(3):
+        W1, W2 = _block_fold_weights(party, k, ws, gr)
+        fold = lambda W: _dotsum_terms([([(1, acc, 64)], [(1, W, 64)])], 64, gr)
+        rows = (n + 1) // 2
+        h1 = _gr_dot_folded(party, gr, rows, fold(W1))
+        h2 = _gr_dot_folded(party, gr, rows, fold(W2))
+        ze = _open_challenge(party, chal.zetas[k].scale_pub(2), "vfy.zeta")
+        q = _quad(party, ze, gr)
+        z = _recombine(party, z, h1, h2, q, gr)
+        ws.append((q.one_m, ze))
+        n = rows
+    tabs, kappa = _l3_tables(party, q8, ws, gr)
+    geo = (comp.N, comp.n, comp.ks, comp.ls)
+
+    def level3_vectors(slots):
+        out = {}
+        for side in ("x", "y"):
+            # m is the same public value at P1 and P2 (honest joint session)
+            srcs = [(rr, k, t) for rr, sl in sorted(slots.items()) for k, t in sl[side].items()
+                    if not (rr == 2 and k == "m" and 1 in slots and "m" in slots[1][side])]
+            dst = [empty((n8, gr.d)) for _ in srcs]
+            for c0 in range(0, len(srcs), 8):
+                part, pdst = srcs[c0:c0 + 8], dst[c0:c0 + 8]
+                if side == "x":
+                    call("r3_vfy_line_b", 8, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
+                         n8 * gr.d, 8, gr.d, _ptrs(pdst), gr.mask, stream())
+                else:
+                    call("r3_vfy_line_b_const", 8, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(kappa),
+                         gr.d, _ptrs(pdst), gr.mask, stream())
+            for (rr, k, _), o in zip(srcs, dst):
+                out.setdefault(rr, {"x": {}, "y": {}})[side][k] = o
+            if 2 in slots and "m" in slots[2][side] and "m" not in out.get(2, {}).get(side, {}):
+                out.setdefault(2, {"x": {}, "y": {}})[side]["m"] = out[1][side]["m"]
+        return out
+
+    mine = {"x": comp.x, "y": comp.y}
+    if _joint_ok(party):
+        res = party.sess.joint(("l3vec", party.next_id("_joint.l3vec")), role, mine, level3_vectors)
+    else:
+        res = level3_vectors({role: mine})[role]
+    return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z, 3
+
+
+def _l3_tables(party, q8, ws: list, gr: Ring):
+    """kappa_a = w1_{a&1} w2_{(a>>1)&1} w3_{a>>2} (the level-3 line weight of
+    base element 8j + a) and the tables V_a[j] = pw8[j] (r^a kappa_a), a < 8."""
+    pw8, rpow = q8
+    key = ("l3t", gr.ell, gr.d, id(pw8), pw8.shape[0], tuple(_opened_key(party, w[1]) for w in ws))
+
+    def build():
+        kap = torch.cat([ws[0][a & 1] for a in range(8)])
+        kap = grvec.gr_mul(kap, torch.cat([ws[1][(a >> 1) & 1] for a in range(8)]), gr.ell, gr.mod)
+        kappa = grvec.gr_mul(kap, torch.cat([ws[2][a >> 2] for a in range(8)]), gr.ell, gr.mod)
+        rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
+        rows = pw8.shape[0]
+        tabs = grvec.empty((8, rows, gr.d))
+        for h in (0, 4):
+            grvec.rows_times_multi(pw8, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(h, h + 4)], rows,
+                                   gr.ell, [tabs[a] for a in range(h, h + 4)])
+        return tabs, kappa
+    return _public(party, key, build)
 
 
 def _joint_ok(party) -> bool:
@@ -940,19 +1151,15 @@ def check_inner_product(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, alpha: MVa
     delta = _gr_dot(party, pairs_x, pairs_y, gr)
     opened = rec(party, delta, "vfy.delta", style="aux")
     party.round_barrier()
-    return int(grvec.count_nonequal(opened).item()) == 0
+    bad = grvec.count_nonequal(opened)
+    if getattr(party, "_deferred_verdicts", None) is not None:
+        return bad            # verify_session reads every log's count at its end
+    return int(bad.item()) == 0
 
 
 # ---------------------------------------------------------------------------
 # drivers
 # ---------------------------------------------------------------------------
-
-def _levels_done(R: int, gr: Ring) -> int:
-    """Reductions performed by _compress_reduce_first before the dense tail."""
-    if R >= 2 and gr.d >= 8:
-        return 2
-    return min(R, 1)
-
 
 def _cat_mvals(vals: list, dim: int = 0) -> MVal:
     """One torch.cat per field for the whole list (MVal.concat / _map
@@ -1009,9 +1216,8 @@ def batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None
     comp = _compressed_from_log(xs, ys, party.role, 1)
     if _gf2_packed_ok(gr, R):
         return _verify_muls_gf2(party, comp, zs, gr, ctx, R)
-    zc = zs
-    (xv, yv), z = _compress_reduce_first(party, comp, zc, comp.N, 1, gr, ctx, R)
-    return _verify_tail(party, xv, yv, z, gr, ctx, R, start=_levels_done(R, gr))
+    (xv, yv), z, done = _compress_reduce_first(party, comp, zs, comp.N, 1, gr, ctx, R)
+    return _verify_tail(party, xv, yv, z, gr, ctx, R, start=done)
 
 
 def _gf2_packed_ok(gr: Ring, R: int) -> bool:
@@ -1096,8 +1302,8 @@ def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     cat1 = lambda pick: _concat_lanes([pick(b) for b in log.dots])
     xs, ys, zs = cat1(lambda b: b.xs), cat1(lambda b: b.ys), _concat_all(log.dots, lambda b: b.z)
     comp = _compressed_from_log(xs, ys, party.role, n)
-    (xv, yv), z = _compress_reduce_first(party, comp, zs, comp.N // n, 1, gr, ctx, R)
-    return _verify_tail(party, xv, yv, z, gr, ctx, R, start=_levels_done(R, gr))
+    (xv, yv), z, done = _compress_reduce_first(party, comp, zs, comp.N // n, 1, gr, ctx, R)
+    return _verify_tail(party, xv, yv, z, gr, ctx, R, start=done)
 
 
 # ---------------------------------------------------------------------------
@@ -1407,14 +1613,21 @@ def verify_session(party, d: int, R: int | str = "auto", profile: str = "lan") -
         raise ConfigError("verification runs in the postprocessing phase")
     party.freeze_logs()
     _require_kept_logs(party)
-    results: dict[str, bool] = {}
-    for kind, base_ell in (("arith", party.ell), ("bool", 1)):
-        log = party.logs[kind]
-        if log.muls:
-            r_eff = pick_r(log.mul_count(), base_ell, d, profile) if R == "auto" else int(R)
-            results[f"mul.{kind}"] = batch_verify_muls(party, base_ell, d, r_eff)
-        if log.dots:
-            n_total = sum(b.lanes * b.n for b in log.dots)
-            r_eff = pick_r(n_total, base_ell, d, profile) if R == "auto" else int(R)
-            results[f"dot.{kind}"] = batch_verify_dots(party, base_ell, d, r_eff)
-    return results
+    results: dict = {}
+    # the logs' zero tests are read once at the end (one device -> host
+    # synchronisation per session instead of one per log, so the host
+    # enqueues the next log's verification while the GPU finishes this one)
+    party._deferred_verdicts = True
+    try:
+        for kind, base_ell in (("arith", party.ell), ("bool", 1)):
+            log = party.logs[kind]
+            if log.muls:
+                r_eff = pick_r(log.mul_count(), base_ell, d, profile) if R == "auto" else int(R)
+                results[f"mul.{kind}"] = batch_verify_muls(party, base_ell, d, r_eff)
+            if log.dots:
+                n_total = sum(b.lanes * b.n for b in log.dots)
+                r_eff = pick_r(n_total, base_ell, d, profile) if R == "auto" else int(R)
+                results[f"dot.{kind}"] = batch_verify_dots(party, base_ell, d, r_eff)
+    finally:
+        party._deferred_verdicts = None
+    return {k: v if isinstance(v, bool) else int(v.item()) == 0 for k, v in results.items()}

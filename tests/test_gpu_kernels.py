@@ -383,7 +383,8 @@ def test_level_fold16_tc_matches_cuda_core(cuda, N):
 
 @pytest.mark.parametrize("N", [(1 << 16) + 37, 1 << 20])
 @pytest.mark.parametrize("joint", [True, False])
-def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
+@pytest.mark.parametrize("B", [4, 8])
+def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B):
     """r3_vfy_base_fold_q4 on the tensor cores (bf_tc.cu, d = 64) -- the
     headline's base fold -- against its definition
         acc'[a*4+b] = sum_j s^{ab}_j pw4[j],  zraw[c*4+a] = sum_j z_c[4j+a] pw4[j]
@@ -392,12 +393,15 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
     persistent grid runs >= 4 (2^16 + 37) and 56 (2^20) 32-block K-steps, so
     the 3-stage TMA / mbarrier ring wraps many times; N = 2^16 + 37 also has
     a ragged last block.  joint=True is the honest-session form (all three
-    parties' features in one pass), joint=False one launch per party."""
+    parties' features in one pass), joint=False one launch per party.
+    B = 8 is r3_vfy_base_fold_q8 (blocks of eight against r^(8j): the 64
+    accumulators of the first three reductions; one work item per party and
+    K-chunk)."""
     import ctypes as C
     from paper_2411_09287_b200 import grvec, host, _lib
     d = 64
     rng = np.random.default_rng(N + 3)
-    nblk = (N + 3) // 4
+    nblk = (N + B - 1) // B
     pw4 = _rand(rng, (nblk, d))
     roles = {0: [(1, 0, 0)], 1: [(-1, 0, 1), (-1, 1, 0)], 2: [(1, 0, 0), (-1, 0, 1), (-1, 1, 0)]}
     data, want = {}, {}
@@ -406,14 +410,14 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
         ys = [_rand(rng, (N,)) for _ in range(2)]
         zs = [_rand(rng, (N,)) for _ in range(1 if role == 0 else 2)]
         data[role] = (terms, xs, ys, zs)
-        pad = lambda a: np.concatenate([a, np.zeros((-N) % 4, np.uint64)]).reshape(nblk, 4)
+        pad = lambda a: np.concatenate([a, np.zeros((-N) % B, np.uint64)]).reshape(nblk, B)
         X, Y, Z = [pad(a) for a in xs], [pad(a) for a in ys], [pad(a) for a in zs]
         with np.errstate(over="ignore"):
-            S = np.zeros((nblk, 16), np.uint64)
+            S = np.zeros((nblk, B * B), np.uint64)
             for cf, xi, yi in terms:
-                S += np.uint64(cf % 2**64) * (X[xi][:, :, None] * Y[yi][:, None, :]).reshape(nblk, 16)
+                S += np.uint64(cf % 2**64) * (X[xi][:, :, None] * Y[yi][:, None, :]).reshape(nblk, B * B)
             acc = S.T @ pw4
-            zr = np.concatenate([z.T @ pw4 for z in Z]) if Z else np.zeros((4, d), np.uint64)
+            zr = np.concatenate([z.T @ pw4 for z in Z]) if Z else np.zeros((B, d), np.uint64)
         want[role] = (acc, zr)
     D = grvec.dev
     dev = {r: ([D(a) for a in v[1]], [D(a) for a in v[2]], [D(a) for a in v[3]]) for r, v in data.items()}
@@ -433,12 +437,12 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint):
             for c, zt in enumerate(dev[r][2]):
                 zp[2 * q + c] = zt.data_ptr()
             # garbage-filled outputs: the entry point must initialise them
-            outs[r] = (grvec.dev(np.full((16, d), 0xDEADBEEF, np.uint64)),
-                       grvec.dev(np.full((4 * len(dev[r][2]), d), 0xDEADBEEF, np.uint64)))
+            outs[r] = (grvec.dev(np.full((B * B, d), 0xDEADBEEF, np.uint64)),
+                       grvec.dev(np.full((B * len(dev[r][2]), d), 0xDEADBEEF, np.uint64)))
         zstr = (C.c_int64 * n)(*([1] * n))
         acc = (P * n)(*[outs[r][0].data_ptr() for r in rs])
         zr = (P * n)(*[outs[r][1].data_ptr() for r in rs])
-        _lib.call("r3_vfy_base_fold_q4", n, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+        _lib.call(f"r3_vfy_base_fold_q{B}", n, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
                   C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zstr), N, dpw4.data_ptr(), d,
                   C.addressof(acc), C.addressof(zr), _lib.stream())
         return outs
