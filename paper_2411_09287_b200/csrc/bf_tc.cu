@@ -48,6 +48,7 @@ struct BfArgs {
   CUtensorMap pw4;
   BfParty p[3];
   int np;
+  int vec;     // every base-log pointer 16-byte aligned: 128-bit loads
   int64_t N, nblk, kc;
 };
 
@@ -148,31 +149,58 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           const BfParty& P = args.p[p];
           const int64_t i0 = 8 * j;
           if (h == 0) {          // s products of rows a = 2c, 2c + 1: v[(a - 2c) 8 + b]
+            // every term's loads are issued before any product (one memory
+            // round trip per K-step); 128-bit loads when the block is whole
+            u64 xv[3][2], yv[3][8];
+            const bool whole = args.vec && i0 + 8 <= args.N;
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
-              if (t >= P.nterms) break;
-              u64 xv[2], yv[8];
+              const bool tl = t < P.nterms;
+              if (whole) {
+                const ulonglong2 xx = tl ? __ldg(reinterpret_cast<const ulonglong2*>(P.x[t] + i0 + 2 * c))
+                                         : make_ulonglong2(0ull, 0ull);
+                xv[t][0] = xx.x, xv[t][1] = xx.y;
 #pragma unroll
-              for (int a = 0; a < 2; ++a) {
-                const int64_t i = i0 + 2 * c + a;
-                xv[a] = i < args.N ? __ldg(P.x[t] + i) : 0ull;
+                for (int q = 0; q < 4; ++q) {
+                  const ulonglong2 yy = tl ? __ldg(reinterpret_cast<const ulonglong2*>(P.y[t] + i0) + q)
+                                           : make_ulonglong2(0ull, 0ull);
+                  yv[t][2 * q] = yy.x, yv[t][2 * q + 1] = yy.y;
+                }
+              } else {
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                  const int64_t i = i0 + 2 * c + a;
+                  xv[t][a] = tl && i < args.N ? __ldg(P.x[t] + i) : 0ull;
+                }
+#pragma unroll
+                for (int b = 0; b < 8; ++b) yv[t][b] = tl && i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
               }
+            }
 #pragma unroll
-              for (int b = 0; b < 8; ++b) yv[b] = i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
+            for (int t = 0; t < 3; ++t) {
 #pragma unroll
               for (int a = 0; a < 2; ++a) {
-                const u64 cx = P.coef[t] * xv[a];
+                const u64 cx = P.coef[t] * xv[t][a];
 #pragma unroll
-                for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[b];
+                for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[t][b];
               }
             }
           } else {               // z values: v[cz 8 + a]
+            const bool whole = args.vec && P.zs == 1 && i0 + 8 <= args.N;
 #pragma unroll
             for (int cz = 0; cz < 2; ++cz) {
-              if (cz < P.nz) {
+              const bool zl = cz < P.nz;
+              if (whole) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const ulonglong2 zz = zl ? __ldg(reinterpret_cast<const ulonglong2*>(P.z[cz] + i0) + q)
+                                           : make_ulonglong2(0ull, 0ull);
+                  v[cz * 8 + 2 * q] = zz.x, v[cz * 8 + 2 * q + 1] = zz.y;
+                }
+              } else {
 #pragma unroll
                 for (int a = 0; a < 8; ++a)
-                  v[cz * 8 + a] = i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
+                  v[cz * 8 + a] = zl && i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
               }
             }
           }
@@ -349,6 +377,13 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
     P.acc = reinterpret_cast<u64*>(acc[q]);
     P.zraw = reinterpret_cast<u64*>(zraw[q]);
   }
+  uintptr_t align = 0;
+  for (int q = 0; q < np; ++q) {
+    for (int t = 0; t < args.p[q].nterms; ++t)
+      align |= reinterpret_cast<uintptr_t>(args.p[q].x[t]) | reinterpret_cast<uintptr_t>(args.p[q].y[t]);
+    for (int c = 0; c < args.p[q].nz; ++c) align |= reinterpret_cast<uintptr_t>(args.p[q].z[c]);
+  }
+  args.vec = (align & 15) == 0;
   if (!make_rows_tmap(&args.pw4, pw, nblk, 64, BF_BK, 64)) {
     set_error("%s: cuTensorMapEncodeTiled failed", what);
     return R3_ERR_CUDA;

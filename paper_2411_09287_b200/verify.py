@@ -182,11 +182,35 @@ _cache_lock = threading.Lock()
 
 
 def _public(party, key, build):
-    cache = party.sess.public_cache
+    sess = party.sess
+    cache = sess.public_cache
     with _cache_lock:
         if key not in cache:
             cache[key] = build()
+            group = party._vgroup
+            if group is not None:
+                sess.public_groups.setdefault(group, []).append(key)
         return cache[key]
+
+
+def _verification_group(party, name: str, run):
+    """Run one log's verification; the public tables it builds (powers,
+    line / level tables) are dropped as soon as all three parties have
+    finished that log, so the logs of a session verify one after the other
+    at the largest one's peak instead of the sum."""
+    group = (name, party.next_id("_vgroup"))
+    party._vgroup = group
+    try:
+        return run()
+    finally:
+        party._vgroup = None
+        sess = party.sess
+        with _cache_lock:
+            done = sess.public_groups_done[group] = sess.public_groups_done.get(group, 0) + 1
+            if done == 3:
+                del sess.public_groups_done[group]
+                for key in sess.public_groups.pop(group, ()):
+                    sess.public_cache.pop(key, None)
 
 
 def _shared_m(party, build):
@@ -1201,6 +1225,10 @@ def _require_kept_logs(party) -> None:
 
 def batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None = None) -> bool:
     """Verify every logged multiplication of the given base ring."""
+    return _verification_group(party, "mul", lambda: _batch_verify_muls(party, base_ell, d, R, kind_key))
+
+
+def _batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | None) -> bool:
     _require_kept_logs(party)
     kind = "bool" if base_ell == 1 else "arith"
     log = party.logs[kind]
@@ -1283,6 +1311,10 @@ def _verify_muls_gf2(party, comp: _Compressed, zs: MVal, gr: Ring, chal: Challen
 
 def batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     """Verify every logged inner-product gate of the given base ring."""
+    return _verification_group(party, "dot", lambda: _batch_verify_dots(party, base_ell, d, R))
+
+
+def _batch_verify_dots(party, base_ell: int, d: int, R: int) -> bool:
     _require_kept_logs(party)
     kind = "bool" if base_ell == 1 else "arith"
     log = party.logs[kind]

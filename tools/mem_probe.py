@@ -56,9 +56,9 @@ def main():
         Session(seed=1).run(prog, torch.from_numpy(xv), True)
     else:
         model = ppml.lenet28_model(np.random.default_rng(0)) if what == "lenet" else ppml.secureml_model(np.random.default_rng(0))
-        imgs = np.random.default_rng(1).normal(0, 1, (n,) + model.input_shape)
+        imgs = np.random.default_rng(1).normal(0, 1, (n, int(np.prod(model.input_shape))))
         torch.cuda.reset_peak_memory_stats()
-        Session(seed=1).run(lambda p: ppml.infer_batch(p, model, imgs if p.role == 0 else None, ppml.InferConfig(d=16), batch=n))
+        Session(seed=1).run(lambda p: ppml.infer_batch(p, model, imgs, ppml.InferConfig(d=16)))
     snap["peak_gib"] = torch.cuda.max_memory_allocated() / 2 ** 30
     print(what, n, snap)
 
