@@ -5,7 +5,9 @@ Workload (BASELINE.json configs[1]): the reference's `mulv` program
 batched Pi_mul, prepare_verification, online mul_finish, then the GR(2^64, d)
 batch verification Pi_mulv -- run end to end through the drop-in API
 (`Session(seed).run(program)`), all three parties simulated on each GPU.
-A "step" is one complete verified session over N multiplications.
+A "step" is one complete verified session over N multiplications; the
+default N = 2^25 per GPU is config 2's sweep end, 2^28, at 8 GPUs (weak
+scaling), and the side key `mulv_sweep` covers 2^20 .. 2^26 on one GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--log2n L] [--d D]
                     [--R R|auto] [--impl b200|reference]
@@ -41,7 +43,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--log2n", type=int, default=24)
+    # 2^25 multiplications per GPU: config 2's sweep end (2^28) at 8 GPUs,
+    # weak scaling (every N runs the same per-GPU batch)
+    ap.add_argument("--log2n", type=int, default=25)
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--R", default="auto")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -56,8 +60,10 @@ def parse():
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--relu-sweep-log2n", type=int, default=20)
-    ap.add_argument("--mulv-sweep", default="20,22,26",
+    ap.add_argument("--mulv-sweep", default="20,22,24,26",
                     help="comma list of log2 batch sizes for the config-2 sweep on one GPU ('' = off)")
+    ap.add_argument("--mulv-variants", default="24:16:auto,24:64:7",
+                    help="extra config-2 points log2n:d:R (R an integer or auto = pick_r); '' = off")
     ap.add_argument("--matmul-n", type=int, default=4096)
     ap.add_argument("--matmul-verified-rows", type=int, default=256,
                     help="rows of X per verified C3 session (0 = skip the verified C3 leg)")
@@ -319,22 +325,26 @@ def relu_rates(N_total: int, d: int, steps: int, rank: int, world: int, prof: bo
     return out
 
 
-def mulv_sweep(sizes, d: int, steps: int = 3) -> dict:
+def mulv_sweep(sizes, d: int, steps: int = 3, variants=()) -> dict:
     """Config 2's sweep on one GPU: verified mults/s per batch size (same
     program as the headline, R = pick_r), median of `steps` sessions after
     one warm-up, with the peak device memory; a size that does not fit in
-    HBM is reported as such (2^28 is meant for 8 GPUs: 2^25 per rank)."""
+    HBM is reported as such (2^28 is meant for 8 GPUs: 2^25 per rank).
+    `variants`: extra (log2n, d, R) points -- SURVEY 8(d) C2 also names
+    d = 16 and the fixed R = 7 beside d = 64 with pick_r."""
     import torch
     from paper_2411_09287_b200 import verify
     from paper_2411_09287_b200.runtime import Session
     out = {"unit": UNIT, "d": d, "timing": f"median of {steps} sessions after 1 warm-up, wall clock incl. host",
            "points": []}
-    for lg in sizes:
+    todo = [(lg, d, None) for lg in sizes] + list(variants)
+    for lg, dd, r_fixed in todo:
         N = 1 << lg
-        R = verify.pick_r(N, 64, d)
-        prog, _ = make_programs(N, d, R)
+        R = verify.pick_r(N, 64, dd) if r_fixed is None else r_fixed
+        prog, _ = make_programs(N, dd, R)
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
+        point = {"log2n": lg, "d": dd, "R": R, "R_rule": "pick_r(lan)" if r_fixed is None else "fixed"}
         try:
             Session(seed=1).run(prog)
             times = []
@@ -346,12 +356,13 @@ def mulv_sweep(sizes, d: int, steps: int = 3) -> dict:
                 times.append(time.perf_counter() - t0)
             assert all(ok), "honest mulv rejected"
         except torch.OutOfMemoryError:
-            out["points"].append({"log2n": lg, "R": R, "fits": False})
+            point["fits"] = False
+            out["points"].append(point)
             torch.cuda.empty_cache()
             continue
         dt = statistics.median(times)
-        out["points"].append({"log2n": lg, "R": R, "value": N / dt, "ms": dt * 1e3,
-                              "peak_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
+        point.update({"value": N / dt, "ms": dt * 1e3, "peak_gib": torch.cuda.max_memory_allocated() / 2 ** 30})
+        out["points"].append(point)
     torch.cuda.empty_cache()
     return out
 
@@ -844,6 +855,7 @@ def run_b200(args):
     timer = KernelTimer(args.profile_kernel)
     launches0 = _lib.load().r3_launch_count()
     _lib.CALL_HOOK = timer.hook
+    _lib.CALL_HOOK_ONLY = timer.names
     barrier()
     with Clocks(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -856,6 +868,7 @@ def run_b200(args):
         barrier()
         wall = time.perf_counter() - wall0
     _lib.CALL_HOOK = None
+    _lib.CALL_HOOK_ONLY = None
     launches = _lib.load().r3_launch_count() - launches0
     assert all(res)
     secs = pdist.max_over_ranks(t0.elapsed_time(t1) / 1e3)
@@ -950,13 +963,20 @@ def run_b200(args):
         torch.cuda.synchronize()
         _lib.CALL_HOOK = None
         step_kernels = cp.table(time.perf_counter() - tp)
-        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a_ev.record()
-        ok = Session(seed=pdist.session_seed(rank, (1 << 20) + 1), joint=False).run(mulv)
-        b_ev.record()
-        torch.cuda.synchronize()
-        assert all(ok)
-        pp = a_ev.elapsed_time(b_ev) / 1e3
+        # one warm-up session (first-use allocations of the per-party
+        # launches), then the median of three
+        Session(seed=pdist.session_seed(rank, (1 << 20) + 1), joint=False).run(mulv)
+        pps = []
+        for j in range(3):
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a_ev.record()
+            ok = Session(seed=pdist.session_seed(rank, (1 << 20) + 2 + j), joint=False).run(mulv)
+            b_ev.record()
+            torch.cuda.synchronize()
+            assert all(ok)
+            pps.append(a_ev.elapsed_time(b_ev) / 1e3)
+        pp = statistics.median(pps)
         per_party = {"value": N / pp, "unit": UNIT, "ms_per_step": pp * 1e3,
                      "what": "one session with joint kernels off (Session(joint=False)): each simulated "
                              "party launches its own kernels; the headline's joint launches batch the "
@@ -978,7 +998,9 @@ def run_b200(args):
         side["lenet"] = ppml_rates("lenet", args.lenet_batch, args.lenet_verified_batch, rank, world,
                                    args.lenet_batch)
     if world == 1 and args.mulv_sweep:
-        side["mulv_sweep"] = mulv_sweep([int(v) for v in args.mulv_sweep.split(",")], d)
+        variants = [tuple(None if x == "auto" else int(x) for x in v.split(":"))
+                    for v in args.mulv_variants.split(",") if v]
+        side["mulv_sweep"] = mulv_sweep([int(v) for v in args.mulv_sweep.split(",")], d, variants=variants)
 
     if rank != 0:
         pdist.finalize()
@@ -1020,7 +1042,9 @@ def run_b200(args):
         "data": "synthetic: PRF-generated (AES-128-CTR) random shares, distinct seed per rank and step",
         "config": {"workload": "mulv: batched 3PC Pi_mul + GR(2^64,d) batch verification "
                                "(tests/test_acceptance.py:124-136), 3 parties per GPU",
-                   "N_per_gpu": N, "ell": 64, "d": d, "R": R, "engine": args.engine,
+                   "N_per_gpu": N, "sweep_point": "2^28 over 8 GPUs = 2^25 per GPU (config 2's sweep "
+                                                  "end, weak scaling); 2^20..2^26 on one GPU in mulv_sweep",
+                   "ell": 64, "d": d, "R": R, "engine": args.engine,
                    "l2": f"inputs larger than L2 ({N * 8 * 12 / 2**20:.0f} MiB of shares per step)",
                    "parallelism": f"weak dp{world}: element batch sharded, one 3-party session per rank "
                                   f"shard, NCCL gather of opened outputs"},

@@ -149,6 +149,9 @@ def exported_symbols() -> list[str]:
 # optional instrumentation: callable(name, args, run) -> rc (bench.py times
 # one entry point with CUDA events around its launches)
 CALL_HOOK = None
+# optional set of entry-point names: only those calls go through CALL_HOOK
+# (a timer of one kernel leaves every other call unwrapped)
+CALL_HOOK_ONLY = None
 
 
 _fns: dict = {}
@@ -158,7 +161,7 @@ def call(name: str, *args) -> None:
     fn = _fns.get(name)
     if fn is None:
         fn = _fns[name] = getattr(load(), name)
-    if CALL_HOOK is None:
+    if CALL_HOOK is None or (CALL_HOOK_ONLY is not None and name not in CALL_HOOK_ONLY):
         rc = fn(*args)
     else:
         rc = CALL_HOOK(name, args, lambda: fn(*args))
