@@ -28,10 +28,23 @@ constexpr int BF_RAW = 4 * BF_BOX;              // one K-step of table rows: 16 
 constexpr int BF_STAGES = 3;
 constexpr int BF_CONV = 12 * 32;                // 256 A tasks + 128 B tasks per K-step
 constexpr int BF_THREADS = 4 * 32 + BF_CONV + 2 * 32;
-constexpr int BF_OFF_LIMB = BF_STAGES * BF_RAW;
-constexpr int BF_OFF_BAR = BF_OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
-constexpr int BF_SMEM = BF_OFF_BAR + 256 + 1024;
 constexpr int64_t BF_MAX_K = 16384;
+constexpr int BF_LOG_SLOT = 8 * 8 * BF_BK;      // one base-log array over a K-step (B = 8): 2 KB
+constexpr int BF_MAX_SLOTS = 6;                 // distinct x / y / z arrays of a party
+
+// Shared-memory layout.  B = 4: three raw stages of table rows.  B = 8: two
+// raw stages, each the table rows plus the party's base-log arrays of the
+// K-step (bulk async copies, so the converters never wait on global loads).
+template <int B>
+struct BfLayout {
+  static constexpr int RS = B == 8 ? 2 : 3;
+  static constexpr int RAWST = BF_RAW + (B == 8 ? BF_MAX_SLOTS * BF_LOG_SLOT : 0);
+  static constexpr int OFF_LIMB = RS * RAWST;
+  static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+static_assert(BfLayout<8>::SMEM <= 232448, "base fold q8 shared memory");
+static_assert(BfLayout<4>::SMEM <= 232448, "base fold q4 shared memory");
 
 struct BfParty {
   const u64* x[3];
@@ -42,6 +55,11 @@ struct BfParty {
   int64_t zs;
   u64* acc;    // B^2 x 64
   u64* zraw;   // (B nz) x 64
+  // B = 8: the distinct base-log arrays (bulk-copied per K-step) and each
+  // term's / z component's slot among them
+  const u64* slot[BF_MAX_SLOTS];
+  int nslot;
+  int sx[3], sy[3], sz[2];
 };
 
 struct BfArgs {
@@ -60,17 +78,19 @@ struct BfArgs {
 template <int B>
 __global__ void __launch_bounds__(BF_THREADS, 1)
 base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
+  using L = BfLayout<B>;
+  constexpr int RS = L::RS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sRaw = smem;
-  uint8_t* sA = smem + BF_OFF_LIMB;
+  uint8_t* sA = smem + L::OFF_LIMB;
   uint8_t* sB = sA + BF_STAGES * BF_A_TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + BF_OFF_BAR);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* raw_full = bars;
-  uint64_t* raw_empty = bars + BF_STAGES;
-  uint64_t* full = bars + 2 * BF_STAGES;
-  uint64_t* empty = bars + 3 * BF_STAGES;
-  uint64_t* tfull = bars + 4 * BF_STAGES;
+  uint64_t* raw_empty = bars + RS;
+  uint64_t* full = bars + 2 * RS;
+  uint64_t* empty = bars + 2 * RS + BF_STAGES;
+  uint64_t* tfull = bars + 2 * RS + 2 * BF_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,9 +105,11 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < BF_STAGES; ++s) {
+    for (int s = 0; s < RS; ++s) {
       mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], 128);
+      mbar_init(&raw_empty[s], B == 8 ? BF_CONV : 128);   // B = 8: A threads read the log stage too
+    }
+    for (int s = 0; s < BF_STAGES; ++s) {
       mbar_init(&full[s], BF_CONV);
       mbar_init(&empty[s], 1);
     }
@@ -112,13 +134,21 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         int64_t j0, j1;
         item_range(it, j0, j1);
         const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
+        const BfParty& P = args.p[B == 4 ? 0 : int(it % args.np)];
         for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
-          const int st = int(g % BF_STAGES);
-          if (g >= BF_STAGES) mbar_wait(&raw_empty[st], uint32_t((g / BF_STAGES - 1) & 1));
+          const int rs = int(g % RS);
+          if (g >= RS) mbar_wait(&raw_empty[rs], uint32_t((g / RS - 1) & 1));
           const int y = int(j0 + kb * BF_BK);
-          mbar_expect_tx(&raw_full[st], uint32_t(BF_RAW));
+          // B = 8: the K-step's 256 elements of every base-log array, unless
+          // the step crosses the end of the log (converters load those)
+          const bool whole = B == 8 && args.vec && (j0 + (kb + 1) * BF_BK) * 8 <= args.N;
+          uint8_t* dst = sRaw + rs * L::RAWST;
+          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? P.nslot * BF_LOG_SLOT : 0)));
           for (int c = 0; c < 4; ++c)
-            tma_load_2d(sRaw + st * BF_RAW + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[st]);
+            tma_load_2d(dst + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[rs]);
+          if (whole)
+            for (int q = 0; q < P.nslot; ++q)
+              bulk_copy_g2s(dst + BF_RAW + q * BF_LOG_SLOT, P.slot[q] + int64_t(y) * 8, BF_LOG_SLOT, &raw_full[rs]);
         }
       }
     }
@@ -139,72 +169,94 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     for (int64_t kb = 0; kb < nkb; ++kb) {
       ++g;
       const int st = int(g % BF_STAGES);
+      const int rs = int(g % RS);
       const int64_t j = j0 + kb * BF_BK + k;
       const bool ok = j < j1;
       u64 v[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = 0;
-      if (isA) {
-        if (live && ok && B == 8) {
+      bool staged = false;
+      if (B == 8 && isA) {
+        // the K-step's base-log arrays arrive with the table rows
+        mbar_wait(&raw_full[rs], uint32_t((g / RS) & 1));
+        staged = args.vec && (j0 + (kb + 1) * BF_BK) * 8 <= args.N;
+        if (live && staged) {
           const BfParty& P = args.p[p];
-          const int64_t i0 = 8 * j;
-          if (h == 0) {          // s products of rows a = 2c, 2c + 1: v[(a - 2c) 8 + b]
-            // every term's loads are issued before any product (one memory
-            // round trip per K-step); 128-bit loads when the block is whole
-            u64 xv[3][2], yv[3][8];
-            const bool whole = args.vec && i0 + 8 <= args.N;
+          const uint8_t* lg = sRaw + rs * L::RAWST + BF_RAW;
+          if (h == 0) {
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
-              const bool tl = t < P.nterms;
-              if (whole) {
-                const ulonglong2 xx = tl ? __ldg(reinterpret_cast<const ulonglong2*>(P.x[t] + i0 + 2 * c))
-                                         : make_ulonglong2(0ull, 0ull);
-                xv[t][0] = xx.x, xv[t][1] = xx.y;
+              if (t < P.nterms) {
+                const ulonglong2 xx =
+                    *reinterpret_cast<const ulonglong2*>(lg + P.sx[t] * BF_LOG_SLOT + (k * 8 + 2 * c) * 8);
+                const u64* yr = reinterpret_cast<const u64*>(lg + P.sy[t] * BF_LOG_SLOT + k * 64);
+                u64 yv[8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const ulonglong2 yy = tl ? __ldg(reinterpret_cast<const ulonglong2*>(P.y[t] + i0) + q)
-                                           : make_ulonglong2(0ull, 0ull);
-                  yv[t][2 * q] = yy.x, yv[t][2 * q + 1] = yy.y;
+                  const ulonglong2 yy = reinterpret_cast<const ulonglong2*>(yr)[q];
+                  yv[2 * q] = yy.x, yv[2 * q + 1] = yy.y;
                 }
-              } else {
+                const u64 c0 = P.coef[t] * xx.x, c1 = P.coef[t] * xx.y;
 #pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                  const int64_t i = i0 + 2 * c + a;
-                  xv[t][a] = tl && i < args.N ? __ldg(P.x[t] + i) : 0ull;
+                for (int b = 0; b < 8; ++b) {
+                  v[b] += c0 * yv[b];
+                  v[8 + b] += c1 * yv[b];
                 }
-#pragma unroll
-                for (int b = 0; b < 8; ++b) yv[t][b] = tl && i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
               }
             }
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-#pragma unroll
-              for (int a = 0; a < 2; ++a) {
-                const u64 cx = P.coef[t] * xv[t][a];
-#pragma unroll
-                for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[t][b];
-              }
-            }
-          } else {               // z values: v[cz 8 + a]
-            const bool whole = args.vec && P.zs == 1 && i0 + 8 <= args.N;
+          } else {
 #pragma unroll
             for (int cz = 0; cz < 2; ++cz) {
-              const bool zl = cz < P.nz;
-              if (whole) {
+              if (cz < P.nz) {
+                const u64* zr = reinterpret_cast<const u64*>(lg + P.sz[cz] * BF_LOG_SLOT + k * 64);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const ulonglong2 zz = zl ? __ldg(reinterpret_cast<const ulonglong2*>(P.z[cz] + i0) + q)
-                                           : make_ulonglong2(0ull, 0ull);
+                  const ulonglong2 zz = reinterpret_cast<const ulonglong2*>(zr)[q];
                   v[cz * 8 + 2 * q] = zz.x, v[cz * 8 + 2 * q + 1] = zz.y;
                 }
-              } else {
-#pragma unroll
-                for (int a = 0; a < 8; ++a)
-                  v[cz * 8 + a] = zl && i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
               }
             }
           }
-        } else if (live && ok) {
+        }
+        fence_async_smem();   // generic-proxy reads before the next bulk write (WAR)
+        mbar_arrive(&raw_empty[rs]);
+      }
+      if (isA) {
+        if (live && ok && B == 8 && !staged) {
+          const BfParty& P = args.p[p];
+          const int64_t i0 = 8 * j;
+          if (h == 0) {          // s products of rows a = 2c, 2c + 1: v[(a - 2c) 8 + b]
+            // (the K-step crossing the end of the log: plain loads)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              if (t < P.nterms) {
+                u64 xv[2], yv[8];
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                  const int64_t i = i0 + 2 * c + a;
+                  xv[a] = i < args.N ? __ldg(P.x[t] + i) : 0ull;
+                }
+#pragma unroll
+                for (int b = 0; b < 8; ++b) yv[b] = i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                  const u64 cx = P.coef[t] * xv[a];
+#pragma unroll
+                  for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[b];
+                }
+              }
+            }
+          } else {               // z values: v[cz 8 + a]
+#pragma unroll
+            for (int cz = 0; cz < 2; ++cz) {
+              if (cz < P.nz) {
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+                  v[cz * 8 + a] = i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
+              }
+            }
+          }
+        } else if (B == 4 && live && ok) {
           const BfParty& P = args.p[p];
           const int64_t i0 = 4 * j;
           if (h == 0) {
@@ -237,8 +289,8 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           }
         }
       } else {
-        mbar_wait(&raw_full[st], uint32_t((g / BF_STAGES) & 1));
-        const uint8_t* row = sRaw + st * BF_RAW + c * BF_BOX + k * 128;
+        mbar_wait(&raw_full[rs], uint32_t((g / RS) & 1));
+        const uint8_t* row = sRaw + rs * L::RAWST + c * BF_BOX + k * 128;
         const int sw = k & 7;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -247,7 +299,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           v[2 * q + 1] = x.y;
         }
         fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
-        mbar_arrive(&raw_empty[st]);
+        mbar_arrive(&raw_empty[rs]);
       }
       uint4 pk[8];
       split_limbs16(v, pk);
@@ -384,6 +436,21 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
     for (int c = 0; c < args.p[q].nz; ++c) align |= reinterpret_cast<uintptr_t>(args.p[q].z[c]);
   }
   args.vec = (align & 15) == 0;
+  if (B == 8) {
+    // distinct base-log arrays per party (bulk-copied once per K-step)
+    for (int q = 0; q < np; ++q) {
+      BfParty& P = args.p[q];
+      auto slot_of = [&](const u64* a) {
+        for (int s2 = 0; s2 < P.nslot; ++s2)
+          if (P.slot[s2] == a) return s2;
+        P.slot[P.nslot] = a;
+        return P.nslot++;
+      };
+      for (int t = 0; t < P.nterms; ++t) P.sx[t] = slot_of(P.x[t]), P.sy[t] = slot_of(P.y[t]);
+      for (int c = 0; c < P.nz; ++c) P.sz[c] = P.zs == 1 ? slot_of(P.z[c]) : 0;
+      if (P.nz && P.zs != 1) args.vec = 0;
+    }
+  }
   if (!make_rows_tmap(&args.pw4, pw, nblk, 64, BF_BK, 64)) {
     set_error("%s: cuTensorMapEncodeTiled failed", what);
     return R3_ERR_CUDA;
@@ -400,8 +467,8 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
   items = (nblk + kc - 1) / kc * per;
   args.kc = kc;
   const unsigned grid = unsigned(items < num_sms() ? items : num_sms() / per * per);
-  ensure_smem(base_fold_tc_kernel<B>, BF_SMEM);
-  base_fold_tc_kernel<B><<<grid, BF_THREADS, BF_SMEM, s>>>(args);
+  ensure_smem(base_fold_tc_kernel<B>, BfLayout<B>::SMEM);
+  base_fold_tc_kernel<B><<<grid, BF_THREADS, BfLayout<B>::SMEM, s>>>(args);
   return check_launch(what);
 }
 

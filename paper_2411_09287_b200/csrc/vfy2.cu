@@ -430,6 +430,73 @@ using namespace r3;
     default: set_error("unsupported degree %d", d); return R3_ERR_ARG; \
   }
 
+// The 16 level-2 accumulators of a dot log (n % 4 == 0): blocks of four never
+// straddle a lane and every element of lane l carries pw[l], so
+//   acc[a*4+b] = sum_l S^{ab}_l pw[l],  S^{ab}_l = sum_{blocks j of lane l} s^{ab}_j
+// -- 16 scalar sums per lane, then 16 D MACs per lane (instead of 16 D per
+// block).  Phase 1: one thread per lane (coalesced across lanes); phase 2:
+// thread (q, k) of the block sums its lanes' S^q times pw[l][k].
+template <int D>
+__global__ void __launch_bounds__(256)
+l2_fold_lanes_kernel(int nterms, Comps8 xc, Comps8 yc, int64_t c0, int64_t c1, int64_t c2, int64_t L, int64_t n,
+                     int64_t ks, int64_t ls, const u64* __restrict__ pw, u64* __restrict__ acc_out) {
+  constexpr int NQ = (16 * D + 255) / 256;
+  __shared__ u64 sS[16][256];
+  const int64_t coefs[3] = {c0, c1, c2};
+  u64 acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0;
+  for (int64_t l0 = int64_t(blockIdx.x) * 256; l0 < L; l0 += int64_t(gridDim.x) * 256) {
+    const int64_t l = l0 + threadIdx.x;
+    u64 S[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) S[q] = 0;
+    if (l < L) {
+      for (int64_t k = 0; k < n; k += 4) {
+        const int64_t o = k * ks + l * ls;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          if (t < nterms) {
+            u64 xv[4], yv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              xv[a] = __ldg(xc.p[t] + o + a * ks);
+              yv[a] = __ldg(yc.p[t] + o + a * ks);
+            }
+            const u64 cf = u64(coefs[t]);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const u64 cx = cf * xv[a];
+#pragma unroll
+              for (int b = 0; b < 4; ++b) S[a * 4 + b] += cx * yv[b];
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sS[q][threadIdx.x] = S[q];
+    __syncthreads();
+    const int nl = int(L - l0 < 256 ? L - l0 : 256);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      if (e < 16 * D) {
+        const int qq = e / D, kk = e % D;
+        u64 a = 0;
+        for (int r = 0; r < nl; ++r) a += sS[qq][r] * __ldg(pw + (l0 + r) * D + kk);
+        acc[q] += a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    if (e < 16 * D) atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + e), (unsigned long long)acc[q]);
+  }
+}
+
 extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                               const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks, int64_t ls,
                               const uint64_t* pw, int d, uint64_t* acc, void* stream) {
@@ -451,6 +518,13 @@ extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* c
     cf[t] = coef[t];
   }
   const int64_t nblk = (N + 3) / 4;
+  if (n >= 4 && n % 4 == 0 && N % n == 0) {
+    // dot log: per-lane scalar sums, one power row per lane
+    const int64_t L = N / n;
+    R3_DISPATCH_D2(d, (l2_fold_lanes_kernel<D><<<grid_for(L, 256, 4), 256, 0, s>>>(
+                          nterms, xp, yp, cf[0], cf[1], cf[2], L, n, ks, ls, (const u64*)pw, (u64*)acc)));
+    return check_launch("r3_vfy_l2_fold");
+  }
   R3_DISPATCH_D2(d, ({
                    constexpr int RP = 256 / D;
                    unsigned grid = grid_for((nblk + RP - 1) / RP, 1, 4);

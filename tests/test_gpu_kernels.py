@@ -569,3 +569,49 @@ def test_gfv_packed_boolean_levels_match_oracle(cuda, d, N):
     for c in range(nc):
         np.testing.assert_array_equal(host(o2[c]), line(x1[c], zes[1]))
         np.testing.assert_array_equal(host(o2[nc + c]), line(y1[c], zes[1]))
+
+
+@pytest.mark.parametrize("d,n,L", [(16, 64, 4099), (64, 8, 700), (16, 4, 33)])
+def test_dot_log_folds_per_lane_match_definitions(cuda, d, n, L):
+    """r3_vfy_l1_fold / r3_vfy_l2_fold on a dot log ((n, L) layout, element i
+    at (i % n, i // n), power pw[i // n]) -- the per-lane scalar-sum form --
+    against the level-1 folds and 16 level-2 accumulators written out from
+    their definitions (verify.py:182-212 consolidation + 215-241)."""
+    import ctypes as C
+    from paper_2411_09287_b200 import grvec, host, _lib
+    rng = np.random.default_rng(n * L + d)
+    N = n * L
+    pw = _rand(rng, (L, d))
+    P = np.repeat(pw, n, axis=0)                      # power of element i
+    for role, terms in ((0, [(1, 0, 0)]), (2, [(1, 0, 0), (-1, 0, 1), (-1, 1, 0)])):
+        cx = [_rand(rng, (n, L)) for _ in range(2)]
+        cy = [_rand(rng, (n, L)) for _ in range(2)]
+        flat = lambda a: a.T.reshape(-1)              # consolidated order i = l n + k
+        X, Y = [flat(a) for a in cx], [flat(a) for a in cy]
+        with np.errstate(over="ignore"):
+            acc = np.zeros((16, d), np.uint64)
+            for a in range(4):
+                for b in range(4):
+                    sab = np.zeros(N // 4, np.uint64)
+                    for cf, xi, yi in terms:
+                        sab += np.uint64(cf % 2**64) * X[xi][a::4] * Y[yi][b::4]
+                    acc[a * 4 + b] = (sab[:, None] * P[a::4]).sum(axis=0)
+            h1 = np.zeros(d, np.uint64)
+            h2 = np.zeros(d, np.uint64)
+            for cf, xi, yi in terms:
+                c = np.uint64(cf % 2**64)
+                xe, xo, ye, yo = X[xi][0::2], X[xi][1::2], Y[yi][0::2], Y[yi][1::2]
+                h1 += ((c * xo * yo)[:, None] * P[1::2]).sum(axis=0)
+                h2 += ((c * (np.uint64(2) * xo - xe) * (np.uint64(2) * yo - ye))[:, None] * P[0::2]).sum(axis=0)
+        dx, dy, dpw = [grvec.dev(a) for a in cx], [grvec.dev(a) for a in cy], grvec.dev(pw)
+        coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+        xs = (C.c_void_p * len(terms))(*[dx[t[1]].data_ptr() for t in terms])
+        ys = (C.c_void_p * len(terms))(*[dy[t[2]].data_ptr() for t in terms])
+        g_acc, g_h1, g_h2 = grvec.empty((16, d)), grvec.empty((1, d)), grvec.empty((1, d))
+        _lib.call("r3_vfy_l2_fold", len(terms), coef, xs, ys, N, n, L, 1, dpw.data_ptr(), d, g_acc.data_ptr(),
+                  _lib.stream())
+        _lib.call("r3_vfy_l1_fold", len(terms), coef, xs, ys, N, n, L, 1, dpw.data_ptr(), d, g_h1.data_ptr(),
+                  g_h2.data_ptr(), (1 << 64) - 1, _lib.stream())
+        np.testing.assert_array_equal(host(g_acc), acc, err_msg=f"acc role {role}")
+        np.testing.assert_array_equal(host(g_h1)[0], h1, err_msg=f"h1 role {role}")
+        np.testing.assert_array_equal(host(g_h2)[0], h2, err_msg=f"h2 role {role}")
