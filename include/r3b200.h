@@ -380,13 +380,13 @@ int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                    void* stream);
 /* out_c[j] = sum_{a<B} X_c[Bj+a] * T_a[(Bj+a)/tq] with tables T_a at
  * tabs + a*tab_stride (words), B <= 8 (B > 4: multiplication logs, n = 1,
- * tq = B): level-log2(B) vectors from the base log. */
+ * tq = B, ncomp <= 4): level-log2(B) vectors from the base log. */
 int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N,
                   int64_t n, int64_t ks, int64_t ls, const uint64_t* tabs,
                   int64_t tab_stride, int64_t tq, int d, uint64_t* const* out,
                   uint64_t mask, void* stream);
 /* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B <= 8 public GR constants; B > 4
- * for n = 1 only). */
+ * for n = 1 and ncomp <= 4 only). */
 int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int64_t n, int64_t ks, int64_t ls, const uint64_t* g,
                         int d, uint64_t* const* out, uint64_t mask,

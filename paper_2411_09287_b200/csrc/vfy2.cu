@@ -110,7 +110,7 @@ template <int D>
 __host__ __device__ constexpr int lb_cpt() { return D == 16 ? 4 : 2; }
 
 template <int D, bool ONE, bool TAB, int BM>
-__global__ void __launch_bounds__(256, BM == 8 ? 2 : 4)
+__global__ void __launch_bounds__(256, BM == 8 ? 3 : 4)
 line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
   // Lane (row j, coefficients k..k+CPT-1); the 4 lanes of an aligned quad
@@ -118,7 +118,8 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
   // elements B j + b (+ 4h for blocks of BM = 8) for every component, and the
   // quad exchanges them by shuffles: BM / 4 loads per component per lane, all
   // issued before any store.
-  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT, NH = BM / 4;
+  // blocks of eight: at most 4 components per launch (registers for 4 waves)
+  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT, NH = BM / 4, MC = BM == 8 ? 4 : 8;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
   const int lane = threadIdx.x & 31, bl = lane & 3, quad0 = lane & ~3;
@@ -136,14 +137,14 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
     const int64_t e = e0 + lane;
     const bool live = e < total;
     const int64_t j = e / H;
-    u64 xs[8][NH];
+    u64 xs[MC][NH];
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
       const int64_t i = B * j + bl + 4 * h;
       const bool ok = live && bl + 4 * h < B && i < N;
       const int64_t off = ok ? (ONE ? i * ls : elem_off(i, n, ks, ls)) : 0;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) xs[c][h] = (c < ncomp && ok) ? __ldg(xc.p[c] + off) : 0ull;
+      for (int c = 0; c < MC; ++c) xs[c][h] = (c < ncomp && ok) ? __ldg(xc.p[c] + off) : 0ull;
     }
     if (TAB) {
 #pragma unroll
@@ -158,7 +159,7 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
       }
     }
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < MC; ++c) {
       if (c < ncomp) {
         ulonglong2 v[V];
 #pragma unroll
@@ -537,7 +538,8 @@ extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* c
 extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N, int64_t n, int64_t ks,
                              int64_t ls, const uint64_t* tabs, int64_t tab_stride, int64_t tq, int d,
                              uint64_t* const* out, uint64_t mask, void* stream) {
-  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1 || (B > 4 && (n != 1 || tq != B))) {
+  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1 ||
+      (B > 4 && (n != 1 || tq != B || ncomp > 4))) {
     set_error("r3_vfy_line_b: bad arguments");
     return R3_ERR_ARG;
   }
@@ -566,7 +568,7 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
 extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
                                    int64_t ls, const uint64_t* g, int d, uint64_t* const* out, uint64_t mask,
                                    void* stream) {
-  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || (B > 4 && n != 1)) {
+  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || (B > 4 && (n != 1 || ncomp > 4))) {
     set_error("r3_vfy_line_b_const: bad arguments");
     return R3_ERR_ARG;
   }

@@ -792,8 +792,8 @@ def _reduce_three_from_base(party, comp: _Compressed, zlist: list, znames: list,
             srcs = [(rr, k, t) for rr, sl in sorted(slots.items()) for k, t in sl[side].items()
                     if not (rr == 2 and k == "m" and 1 in slots and "m" in slots[1][side])]
             dst = [empty((n8, gr.d)) for _ in srcs]
-            for c0 in range(0, len(srcs), 8):
-                part, pdst = srcs[c0:c0 + 8], dst[c0:c0 + 8]
+            for c0 in range(0, len(srcs), 4):          # blocks of eight: <= 4 components per launch
+                part, pdst = srcs[c0:c0 + 4], dst[c0:c0 + 4]
                 if side == "x":
                     call("r3_vfy_line_b", 8, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
                          n8 * gr.d, 8, gr.d, _ptrs(pdst), gr.mask, stream())
