@@ -360,6 +360,14 @@ int r3_vfy_base_fold_q8(int np, const int* nterms, const int64_t* coef,
                         const int* nz, const uint64_t* const* zc, const int64_t* zs,
                         int64_t N, const uint64_t* pw8, int d, uint64_t* const* acc,
                         uint64_t* const* zraw, void* stream);
+/* The same over blocks of sixteen against pw16[j] = r^(16j) (N >= 16 * 4096):
+ * acc'[a*16+b] (256 x d) and zraw[c*16+a] -- the accumulators of the first
+ * FOUR reductions. */
+int r3_vfy_base_fold_q16(int np, const int* nterms, const int64_t* coef,
+                         const uint64_t* const* xc, const uint64_t* const* yc,
+                         const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                         int64_t N, const uint64_t* pw16, int d, uint64_t* const* acc,
+                         uint64_t* const* zraw, void* stream);
 /* h1/h2 level-1 folds from the 16 accumulators; masks the nz z sums. */
 int r3_vfy_base_fold_finish(int d, int nz, const uint64_t* acc, uint64_t* h1,
                             uint64_t* h2, uint64_t* zsum, uint64_t mask, void* stream);
@@ -379,13 +387,13 @@ int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                    int64_t ls, const uint64_t* pw, int d, uint64_t* acc,
                    void* stream);
 /* out_c[j] = sum_{a<B} X_c[Bj+a] * T_a[(Bj+a)/tq] with tables T_a at
- * tabs + a*tab_stride (words), B <= 8 (B > 4: multiplication logs, n = 1,
+ * tabs + a*tab_stride (words), B <= 16 (B > 4: multiplication logs, n = 1,
  * tq = B, ncomp <= 4): level-log2(B) vectors from the base log. */
 int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N,
                   int64_t n, int64_t ks, int64_t ls, const uint64_t* tabs,
                   int64_t tab_stride, int64_t tq, int d, uint64_t* const* out,
                   uint64_t mask, void* stream);
-/* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B <= 8 public GR constants; B > 4
+/* out_c[j] = sum_{b<B} Y_c[Bj+b] * g_b (B <= 16 public GR constants; B > 4
  * for n = 1 and ncomp <= 4 only). */
 int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int64_t n, int64_t ks, int64_t ls, const uint64_t* g,

@@ -97,6 +97,8 @@ _SIGS = {
                             C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
     "r3_vfy_base_fold_q8": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
+    "r3_vfy_base_fold_q16": [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_void_p, C.c_void_p, i64, u64p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p],
     "r3_vfy_base_fold_finish": [C.c_int, C.c_int, u64p, u64p, u64p, u64p, u64, C.c_void_p],
     "r3_vfy_l2_fold": [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i64,
                        i64, i64, i64, u64p, C.c_int, u64p, C.c_void_p],

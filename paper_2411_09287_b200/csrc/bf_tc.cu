@@ -29,20 +29,31 @@ constexpr int BF_STAGES = 3;
 constexpr int BF_CONV = 12 * 32;                // 256 A tasks + 128 B tasks per K-step
 constexpr int BF_THREADS = 4 * 32 + BF_CONV + 2 * 32;
 constexpr int64_t BF_MAX_K = 16384;
-constexpr int BF_LOG_SLOT = 8 * 8 * BF_BK;      // one base-log array over a K-step (B = 8): 2 KB
 constexpr int BF_MAX_SLOTS = 6;                 // distinct x / y / z arrays of a party
 
-// Shared-memory layout.  B = 4: three raw stages of table rows.  B = 8: two
-// raw stages, each the table rows plus the party's base-log arrays of the
-// K-step (bulk async copies, so the converters never wait on global loads).
+// Shared-memory layout.  B = 4: three raw stages of table rows.  B = 8, 16
+// ("wide"): two raw stages, each the table rows plus the base-log arrays the
+// work item reads in the K-step, all by TMA (so the converters never wait on
+// global loads): B = 8 all of the party's arrays (x / y / z, <= 6 x 2 KB),
+// B = 16 either its x / y arrays or its z arrays (<= 4 x 4 KB).  A log
+// array is viewed as rows of 16 words (128 B) with the 128-byte swizzle,
+// which makes the converters' per-block reads bank-conflict free.
+// G = work items (feature groups of <= 128 MMA rows) per party and chunk:
+// B = 16 has 256 s products + 16 nz z values per party -> s rows a < 8,
+// s rows a >= 8, z values.
 template <int B>
 struct BfLayout {
-  static constexpr int RS = B == 8 ? 2 : 3;
-  static constexpr int RAWST = BF_RAW + (B == 8 ? BF_MAX_SLOTS * BF_LOG_SLOT : 0);
+  static constexpr bool WIDE = B >= 8;
+  static constexpr int RS = WIDE ? 2 : 3;
+  static constexpr int SLOT = BF_BK * B * 8;    // one array over a K-step (TMA box, 128B swizzle)
+  static constexpr int NSLOT = B == 8 ? 6 : 4;
+  static constexpr int G = B == 16 ? 3 : 1;
+  static constexpr int RAWST = (BF_RAW + (WIDE ? NSLOT * SLOT : 0) + 1023) / 1024 * 1024;
   static constexpr int OFF_LIMB = RS * RAWST;
   static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
+static_assert(BfLayout<16>::SMEM <= 232448, "base fold q16 shared memory");
 static_assert(BfLayout<8>::SMEM <= 232448, "base fold q8 shared memory");
 static_assert(BfLayout<4>::SMEM <= 232448, "base fold q4 shared memory");
 
@@ -55,15 +66,16 @@ struct BfParty {
   int64_t zs;
   u64* acc;    // B^2 x 64
   u64* zraw;   // (B nz) x 64
-  // B = 8: the distinct base-log arrays (bulk-copied per K-step) and each
-  // term's / z component's slot among them
+  // wide B: the distinct x / y arrays (slot[0, nxy)) and z arrays
+  // (slot[nxy, nxy + nz)), bulk-copied per K-step, and each term's slots
   const u64* slot[BF_MAX_SLOTS];
-  int nslot;
-  int sx[3], sy[3], sz[2];
+  int nxy;
+  int sx[3], sy[3];
 };
 
 struct BfArgs {
   CUtensorMap pw4;
+  CUtensorMap lmap[3][BF_MAX_SLOTS];   // wide B: the parties' base-log arrays as 16-word rows
   BfParty p[3];
   int np;
   int vec;     // every base-log pointer 16-byte aligned: 128-bit loads
@@ -97,17 +109,21 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 
   // persistent: CTA b takes K-chunks (items) b, b + grid, ... of kc blocks;
   // unit g enumerates (item, K-step) in that order
+  constexpr int G = L::G;
   const int64_t nchunks = (args.nblk + args.kc - 1) / args.kc;
-  const int64_t nitems = B == 4 ? nchunks : nchunks * args.np;
+  const int64_t nitems = B == 4 ? nchunks : nchunks * args.np * G;
   auto item_range = [&](int64_t it, int64_t& j0, int64_t& j1) {
-    j0 = (B == 4 ? it : it / args.np) * args.kc;
+    j0 = (B == 4 ? it : it / (args.np * G)) * args.kc;
     j1 = min(args.nblk, j0 + args.kc);
   };
+  // wide B: item -> (party, feature group)
+  auto item_party = [&](int64_t it) { return B == 4 ? 0 : int((it / G) % args.np); };
+  auto item_group = [&](int64_t it) { return B == 4 ? 0 : int(it % G); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) {
       mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], B == 8 ? BF_CONV : 128);   // B = 8: A threads read the log stage too
+      mbar_init(&raw_empty[s], L::WIDE ? BF_CONV : 128);   // wide B: A threads read the log stage too
     }
     for (int s = 0; s < BF_STAGES; ++s) {
       mbar_init(&full[s], BF_CONV);
@@ -127,28 +143,35 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 4 + 12) {
-    // ---------------- TMA producer: table rows j of the K-step
+    // ---------------- TMA producer: table rows j of the K-step; wide B:
+    // also the base-log rows of the arrays the item reads
     if (lane == 0) {
       int64_t g = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         int64_t j0, j1;
         item_range(it, j0, j1);
         const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
-        const BfParty& P = args.p[B == 4 ? 0 : int(it % args.np)];
+        const int pi = item_party(it);
+        const BfParty& P = args.p[pi];
+        const int grp = item_group(it);
+        // the arrays this item reads: B = 8 all, B = 16 x / y (s groups) or z
+        const int s0 = B == 16 && grp == 2 ? P.nxy : 0;
+        const int s1 = B == 16 && grp < 2 ? P.nxy : P.nxy + P.nz;
         for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
           const int rs = int(g % RS);
           if (g >= RS) mbar_wait(&raw_empty[rs], uint32_t((g / RS - 1) & 1));
           const int y = int(j0 + kb * BF_BK);
-          // B = 8: the K-step's 256 elements of every base-log array, unless
-          // the step crosses the end of the log (converters load those)
-          const bool whole = B == 8 && args.vec && (j0 + (kb + 1) * BF_BK) * 8 <= args.N;
+          // wide B: the K-step's 32 B elements of the arrays, unless the step
+          // crosses the end of the log (the converters load those)
+          const bool whole = L::WIDE && args.vec && (j0 + (kb + 1) * BF_BK) * B <= args.N;
           uint8_t* dst = sRaw + rs * L::RAWST;
-          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? P.nslot * BF_LOG_SLOT : 0)));
+          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? (s1 - s0) * L::SLOT : 0)));
           for (int c = 0; c < 4; ++c)
             tma_load_2d(dst + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[rs]);
           if (whole)
-            for (int q = 0; q < P.nslot; ++q)
-              bulk_copy_g2s(dst + BF_RAW + q * BF_LOG_SLOT, P.slot[q] + int64_t(y) * 8, BF_LOG_SLOT, &raw_full[rs]);
+            for (int q = s0; q < s1; ++q)
+              tma_load_2d(dst + BF_RAW + (q - s0) * L::SLOT, &args.lmap[pi][q], 0, int(int64_t(y) * B / 16),
+                          &raw_full[rs]);
         }
       }
     }
@@ -161,8 +184,17 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     const int c = isA ? (lt >> 5) : ((lt - 256) >> 5);
     int64_t g = -1;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int p = B == 4 ? c >> 1 : int(it % args.np), h = B == 4 ? c & 1 : (c < 4 ? 0 : (c == 4 ? 1 : 2));
+    // h: 0 = s products, 1 = z values, 2 = zero rows.  B = 8: chunk c < 4
+    // holds s rows a = 2c, 2c + 1, chunk 4 the z values.  B = 16: s groups
+    // hold row a = 8 grp + c per chunk, the z group z_c in chunk c < nz.
+    const int grp = item_group(it);
+    const int p = B == 4 ? c >> 1 : item_party(it);
+    const int h = B == 4 ? (c & 1)
+                  : B == 8 ? (c < 4 ? 0 : (c == 4 ? 1 : 2))
+                           : (grp < 2 ? 0 : (c < 2 ? 1 : 2));
     const bool live = isA && p < args.np && h < 2;
+    constexpr int NA = B == 8 ? 2 : 1;               // s rows per chunk (wide B)
+    const int a0 = B == 8 ? 2 * c : 8 * grp + c;     // first s row of the chunk
     int64_t j0, j1;
     item_range(it, j0, j1);
     const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
@@ -176,43 +208,53 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = 0;
       bool staged = false;
-      if (B == 8 && isA) {
+      if (L::WIDE && isA) {
         // the K-step's base-log arrays arrive with the table rows
         mbar_wait(&raw_full[rs], uint32_t((g / RS) & 1));
-        staged = args.vec && (j0 + (kb + 1) * BF_BK) * 8 <= args.N;
+        staged = args.vec && (j0 + (kb + 1) * BF_BK) * B <= args.N;
         if (live && staged) {
           const BfParty& P = args.p[p];
           const uint8_t* lg = sRaw + rs * L::RAWST + BF_RAW;
-          if (h == 0) {
+          // block k's 16-byte chunk ch of a slot: row k (B = 16) or k / 2
+          // (B = 8, second half of the row for odd k), 128-byte swizzle
+          const int rrow = B == 16 ? k : (k >> 1);
+          const int cb = B == 16 ? 0 : (k & 1) * 4;
+          auto chunk = [&](int slot, int ch) {
+            return lg + slot * L::SLOT + rrow * 128 + (((cb + ch) ^ (rrow & 7)) << 4);
+          };
+          if (h == 0) {          // v[(a - a0) B + b] = sum_t c_t x_t[B j + a] y_t[B j + b]
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
               if (t < P.nterms) {
-                const ulonglong2 xx =
-                    *reinterpret_cast<const ulonglong2*>(lg + P.sx[t] * BF_LOG_SLOT + (k * 8 + 2 * c) * 8);
-                const u64* yr = reinterpret_cast<const u64*>(lg + P.sy[t] * BF_LOG_SLOT + k * 64);
-                u64 yv[8];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const ulonglong2 yy = reinterpret_cast<const ulonglong2*>(yr)[q];
-                  yv[2 * q] = yy.x, yv[2 * q + 1] = yy.y;
+                u64 cx[NA];
+                if constexpr (NA == 2) {
+                  const ulonglong2 xx = *reinterpret_cast<const ulonglong2*>(chunk(P.sx[t], a0 >> 1));
+                  cx[0] = P.coef[t] * xx.x;
+                  cx[NA - 1] = P.coef[t] * xx.y;
+                } else {
+                  cx[0] = P.coef[t] * *reinterpret_cast<const u64*>(chunk(P.sx[t], a0 >> 1) + (a0 & 1) * 8);
                 }
-                const u64 c0 = P.coef[t] * xx.x, c1 = P.coef[t] * xx.y;
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                  v[b] += c0 * yv[b];
-                  v[8 + b] += c1 * yv[b];
+                for (int q = 0; q < B / 2; ++q) {
+                  const ulonglong2 yy = *reinterpret_cast<const ulonglong2*>(chunk(P.sy[t], q));
+#pragma unroll
+                  for (int a = 0; a < NA; ++a) {
+                    v[a * B + 2 * q] += cx[a] * yy.x;
+                    v[a * B + 2 * q + 1] += cx[a] * yy.y;
+                  }
                 }
               }
             }
-          } else {
+          } else {               // z values: B = 8 v[cz 8 + a] (chunk 4), B = 16 v[a] (chunk cz)
+            const int zbase = B == 8 ? P.nxy : 0;   // z arrays follow the x / y arrays in the stage
 #pragma unroll
-            for (int cz = 0; cz < 2; ++cz) {
-              if (cz < P.nz) {
-                const u64* zr = reinterpret_cast<const u64*>(lg + P.sz[cz] * BF_LOG_SLOT + k * 64);
+            for (int cz = 0; cz < (B == 8 ? 2 : 1); ++cz) {
+              const int zc = B == 8 ? cz : c;
+              if (zc < P.nz) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const ulonglong2 zz = reinterpret_cast<const ulonglong2*>(zr)[q];
-                  v[cz * 8 + 2 * q] = zz.x, v[cz * 8 + 2 * q + 1] = zz.y;
+                for (int q = 0; q < B / 2; ++q) {
+                  const ulonglong2 zz = *reinterpret_cast<const ulonglong2*>(chunk(zbase + zc, q));
+                  v[cz * B + 2 * q] = zz.x, v[cz * B + 2 * q + 1] = zz.y;
                 }
               }
             }
@@ -222,37 +264,38 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         mbar_arrive(&raw_empty[rs]);
       }
       if (isA) {
-        if (live && ok && B == 8 && !staged) {
+        if (live && ok && L::WIDE && !staged) {
+          // the K-step crossing the end of the log: plain loads
           const BfParty& P = args.p[p];
-          const int64_t i0 = 8 * j;
-          if (h == 0) {          // s products of rows a = 2c, 2c + 1: v[(a - 2c) 8 + b]
-            // (the K-step crossing the end of the log: plain loads)
+          const int64_t i0 = int64_t(B) * j;
+          if (h == 0) {
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
               if (t < P.nterms) {
-                u64 xv[2], yv[8];
+                u64 xv[NA], yv[B];
 #pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                  const int64_t i = i0 + 2 * c + a;
+                for (int a = 0; a < NA; ++a) {
+                  const int64_t i = i0 + a0 + a;
                   xv[a] = i < args.N ? __ldg(P.x[t] + i) : 0ull;
                 }
 #pragma unroll
-                for (int b = 0; b < 8; ++b) yv[b] = i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
+                for (int b = 0; b < B; ++b) yv[b] = i0 + b < args.N ? __ldg(P.y[t] + i0 + b) : 0ull;
 #pragma unroll
-                for (int a = 0; a < 2; ++a) {
+                for (int a = 0; a < NA; ++a) {
                   const u64 cx = P.coef[t] * xv[a];
 #pragma unroll
-                  for (int b = 0; b < 8; ++b) v[a * 8 + b] += cx * yv[b];
+                  for (int b = 0; b < B; ++b) v[a * B + b] += cx * yv[b];
                 }
               }
             }
-          } else {               // z values: v[cz 8 + a]
+          } else {
 #pragma unroll
-            for (int cz = 0; cz < 2; ++cz) {
-              if (cz < P.nz) {
+            for (int cz = 0; cz < (B == 8 ? 2 : 1); ++cz) {
+              const int zc = B == 8 ? cz : c;
+              if (zc < P.nz) {
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
-                  v[cz * 8 + a] = i0 + a < args.N ? __ldg(P.z[cz] + (i0 + a) * P.zs) : 0ull;
+                for (int a = 0; a < B; ++a)
+                  v[cz * B + a] = i0 + a < args.N ? __ldg(P.z[zc] + (i0 + a) * P.zs) : 0ull;
               }
             }
           }
@@ -366,10 +409,15 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         const int p = f >> 5, q = f & 31;
         const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
         if (live) dst = q < 16 ? args.p[p].acc + q * 64 : args.p[p].zraw + (q - 16) * 64;
-      } else {
-        const BfParty& P = args.p[it % args.np];
+      } else if (B == 8) {
+        const BfParty& P = args.p[item_party(it)];
         if (f < 64) dst = P.acc + f * 64;
         else if (f < 64 + 8 * P.nz) dst = P.zraw + (f - 64) * 64;
+      } else {
+        const BfParty& P = args.p[item_party(it)];
+        const int grp = item_group(it);
+        if (grp < 2) dst = P.acc + (128 * grp + f) * 64;
+        else if (f < 16 * P.nz) dst = P.zraw + f * 64;
       }
       const bool live = dst != nullptr;
       const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
@@ -436,20 +484,28 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
     for (int c = 0; c < args.p[q].nz; ++c) align |= reinterpret_cast<uintptr_t>(args.p[q].z[c]);
   }
   args.vec = (align & 15) == 0;
-  if (B == 8) {
-    // distinct base-log arrays per party (bulk-copied once per K-step)
+  if (BfLayout<B>::WIDE) {
+    // distinct x / y arrays per party, then its z arrays (bulk-copied per K-step)
     for (int q = 0; q < np; ++q) {
       BfParty& P = args.p[q];
       auto slot_of = [&](const u64* a) {
-        for (int s2 = 0; s2 < P.nslot; ++s2)
+        for (int s2 = 0; s2 < P.nxy; ++s2)
           if (P.slot[s2] == a) return s2;
-        P.slot[P.nslot] = a;
-        return P.nslot++;
+        P.slot[P.nxy] = a;
+        return P.nxy++;
       };
       for (int t = 0; t < P.nterms; ++t) P.sx[t] = slot_of(P.x[t]), P.sy[t] = slot_of(P.y[t]);
-      for (int c = 0; c < P.nz; ++c) P.sz[c] = P.zs == 1 ? slot_of(P.z[c]) : 0;
+      if (P.nxy > 4) args.vec = 0;             // (<= 4 distinct x / y arrays in every leg form)
+      for (int c = 0; c < P.nz; ++c) P.slot[P.nxy + c] = P.z[c];
       if (P.nz && P.zs != 1) args.vec = 0;
     }
+    // each array as floor(N / 16) rows of 16 words; a K-step's box: 32 blocks
+    for (int q = 0; q < np && args.vec; ++q)
+      for (int s2 = 0; s2 < args.p[q].nxy + args.p[q].nz; ++s2)
+        if (!make_rows_tmap(&args.lmap[q][s2], args.p[q].slot[s2], N / 16, 16, BF_BK * B / 16, 16)) {
+          set_error("%s: cuTensorMapEncodeTiled (log) failed", what);
+          return R3_ERR_CUDA;
+        }
   }
   if (!make_rows_tmap(&args.pw4, pw, nblk, 64, BF_BK, 64)) {
     set_error("%s: cuTensorMapEncodeTiled failed", what);
@@ -457,7 +513,7 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
   }
   // K-chunks of <= BF_MAX_K blocks, a whole number of items per CTA of a
   // persistent grid (no partial second wave)
-  const int per = B == 4 ? 1 : np;          // items per K-chunk
+  const int per = B == 4 ? 1 : np * BfLayout<B>::G;   // items per K-chunk
   int64_t chunks = (nblk + BF_MAX_K - 1) / BF_MAX_K;
   int64_t items = chunks * per;
   items = (items + num_sms() - 1) / num_sms() * num_sms();
@@ -485,25 +541,46 @@ int base_fold_q4_tc(int np, const int* nterms, const int64_t* coef, const uint64
                                 "r3_vfy_base_fold_q4(tc)");
 }
 
-extern "C" int r3_vfy_base_fold_q8(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
-                                   const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
-                                   const int64_t* zs, int64_t N, const uint64_t* pw8, int d,
-                                   uint64_t* const* acc, uint64_t* const* zraw, void* stream) {
-  if (np < 1 || np > 3 || d != 64 || N < 8 * 4096 || (uintptr_t(pw8) & 15) || !nterms || !nz) {
-    set_error("r3_vfy_base_fold_q8: bad arguments (np %d, d %d, N %lld)", np, d, (long long)N);
+namespace {
+
+template <int B>
+int base_fold_wide(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                   const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
+                   int64_t N, const uint64_t* pw, int d, uint64_t* const* acc, uint64_t* const* zraw,
+                   void* stream, const char* what) {
+  if (np < 1 || np > 3 || d != 64 || N < int64_t(B) * 4096 || (uintptr_t(pw) & 15) || !nterms || !nz) {
+    set_error("%s: bad arguments (np %d, d %d, N %lld)", what, np, d, (long long)N);
     return R3_ERR_ARG;
   }
   cudaStream_t s = as_stream(stream);
   for (int q = 0; q < np; ++q) {
     if (nterms[q] < 1 || nterms[q] > 3 || nz[q] < 0 || nz[q] > 2 || zs[q] < 1) {
-      set_error("r3_vfy_base_fold_q8: bad terms / z count for party %d", q);
+      set_error("%s: bad terms / z count for party %d", what, q);
       return R3_ERR_ARG;
     }
-    if (cudaMemsetAsync(acc[q], 0, size_t(64) * 64 * 8, s) != cudaSuccess ||
-        (nz[q] > 0 && cudaMemsetAsync(zraw[q], 0, size_t(nz[q]) * 8 * 64 * 8, s) != cudaSuccess)) {
-      set_error("r3_vfy_base_fold_q8: memset failed");
+    if (cudaMemsetAsync(acc[q], 0, size_t(B) * B * 64 * 8, s) != cudaSuccess ||
+        (nz[q] > 0 && cudaMemsetAsync(zraw[q], 0, size_t(nz[q]) * B * 64 * 8, s) != cudaSuccess)) {
+      set_error("%s: memset failed", what);
       return R3_ERR_CUDA;
     }
   }
-  return base_fold_tc_launch<8>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw8, acc, zraw, s, "r3_vfy_base_fold_q8");
+  return base_fold_tc_launch<B>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, acc, zraw, s, what);
+}
+
+}  // namespace
+
+extern "C" int r3_vfy_base_fold_q8(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                                   const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                                   const int64_t* zs, int64_t N, const uint64_t* pw8, int d,
+                                   uint64_t* const* acc, uint64_t* const* zraw, void* stream) {
+  return base_fold_wide<8>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw8, d, acc, zraw, stream,
+                           "r3_vfy_base_fold_q8");
+}
+
+extern "C" int r3_vfy_base_fold_q16(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
+                                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc,
+                                    const int64_t* zs, int64_t N, const uint64_t* pw16, int d,
+                                    uint64_t* const* acc, uint64_t* const* zraw, void* stream) {
+  return base_fold_wide<16>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw16, d, acc, zraw, stream,
+                            "r3_vfy_base_fold_q16");
 }

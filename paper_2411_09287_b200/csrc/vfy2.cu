@@ -110,7 +110,7 @@ template <int D>
 __host__ __device__ constexpr int lb_cpt() { return D == 16 ? 4 : 2; }
 
 template <int D, bool ONE, bool TAB, int BM>
-__global__ void __launch_bounds__(256, BM == 8 ? 3 : 4)
+__global__ void __launch_bounds__(256, BM == 16 ? 2 : (BM == 8 ? 3 : 4))
 line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int64_t ls,
               const u64* __restrict__ tabs, int64_t tab_stride, int64_t tq, Outs8 out, u64 mask) {
   // Lane (row j, coefficients k..k+CPT-1); the 4 lanes of an aligned quad
@@ -119,7 +119,7 @@ line_b_kernel(int B, int ncomp, Comps8 xc, int64_t N, int64_t n, int64_t ks, int
   // quad exchanges them by shuffles: BM / 4 loads per component per lane, all
   // issued before any store.
   // blocks of eight: at most 4 components per launch (registers for 4 waves)
-  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT, NH = BM / 4, MC = BM == 8 ? 4 : 8;
+  constexpr int CPT = lb_cpt<D>(), V = CPT / 2, H = D / CPT, NH = BM / 4, MC = BM >= 8 ? 4 : 8;
   const int64_t nblk = (N + B - 1) / B;
   const int64_t total = nblk * H;
   const int lane = threadIdx.x & 31, bl = lane & 3, quad0 = lane & ~3;
@@ -538,7 +538,7 @@ extern "C" int r3_vfy_l2_fold(int nterms, const int64_t* coef, const uint64_t* c
 extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_t N, int64_t n, int64_t ks,
                              int64_t ls, const uint64_t* tabs, int64_t tab_stride, int64_t tq, int d,
                              uint64_t* const* out, uint64_t mask, void* stream) {
-  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1 ||
+  if (B < 1 || B > 16 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || tq < 1 ||
       (B > 4 && (n != 1 || tq != B || ncomp > 4))) {
     set_error("r3_vfy_line_b: bad arguments");
     return R3_ERR_ARG;
@@ -552,7 +552,10 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
   }
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
-  if (n == 1 && tq == B && B > 4) {
+  if (n == 1 && tq == B && B > 8) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, true, 16><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
+  } else if (n == 1 && tq == B && B > 4) {
     R3_DISPATCH_D2(d, (line_b_kernel<D, true, true, 8><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, xp, N, n, ks, ls, (const u64*)tabs, tab_stride, tq, op, mask)));
   } else if (n == 1 && tq == B) {
@@ -568,7 +571,7 @@ extern "C" int r3_vfy_line_b(int B, int ncomp, const uint64_t* const* xc, int64_
 extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N, int64_t n, int64_t ks,
                                    int64_t ls, const uint64_t* g, int d, uint64_t* const* out, uint64_t mask,
                                    void* stream) {
-  if (B < 1 || B > 8 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || (B > 4 && (n != 1 || ncomp > 4))) {
+  if (B < 1 || B > 16 || ncomp < 1 || ncomp > 8 || N < 0 || n < 1 || (B > 4 && (n != 1 || ncomp > 4))) {
     set_error("r3_vfy_line_b_const: bad arguments");
     return R3_ERR_ARG;
   }
@@ -581,7 +584,10 @@ extern "C" int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, 
   }
   const int64_t total = (N + B - 1) / B * (d / (d == 16 ? 4 : 2));
   cudaStream_t s = as_stream(stream);
-  if (n == 1 && B > 4) {
+  if (n == 1 && B > 8) {
+    R3_DISPATCH_D2(d, (line_b_kernel<D, true, false, 16><<<grid_for(total, 256), 256, 0, s>>>(
+                          B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
+  } else if (n == 1 && B > 4) {
     R3_DISPATCH_D2(d, (line_b_kernel<D, true, false, 8><<<grid_for(total, 256), 256, 0, s>>>(
                           B, ncomp, yp, N, n, ks, ls, (const u64*)g, 0, B, op, mask)));
   } else if (n == 1) {

@@ -28,6 +28,7 @@ B200 structure (SURVEY.md findings 4-5):
 from __future__ import annotations
 
 import math
+import os
 import threading
 from dataclasses import dataclass
 
@@ -502,10 +503,11 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     base_acc = q4 = pw = None
     base_ok = (R >= 2 and gr.d >= 8 and comp.n == 1 and comp.ls == 1 and z_lanes == comp.N
                and len(names) <= 2)
-    if base_ok and R >= 3 and gr.d == 64 and comp.N >= _Q8_MIN_N:
-        # three reductions from one pass over r^(8j): the dense tail starts
-        # at level 3 (N/8 rows)
-        return _reduce_three_from_base(party, comp, [zc[k] for k in names], names, z_stride, r, gr, chal)
+    B = _base_block(comp, R, gr) if base_ok else 0
+    if B:
+        # log2 B reductions from one pass over r^(Bj): the dense tail starts
+        # at level log2 B (N / B rows)
+        return _reduce_from_base(party, comp, [zc[k] for k in names], names, z_stride, r, B, gr, chal)
     if base_ok and gr.d == 64:
         # one pass over the table r^(4j) on the tensor cores: z power sum,
         # level-2 accumulators and the level-1 folds derived from them; the
@@ -627,30 +629,48 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z2
 
 
-_Q8_MIN_N = 8 * 4096
+# diagnostics: R3_BASE_BLOCK=0 / 8 caps the base reduction's block size
+_BASE_BLOCK_CAP = int(os.environ.get("R3_BASE_BLOCK", "16"))
 
 
-def _powers8(party, r: torch.Tensor, n8: int, gr: Ring):
-    """(r^(8j) for j < n8, r^0..r^7): every eighth power and the in-block
-    offsets (pw[8j + a] = pw8[j] r^a)."""
-    key = ("pow8", gr.ell, gr.d, _opened_key(party, r), n8)
+def _base_block(comp: _Compressed, R: int, gr: Ring) -> int:
+    """Block size of the multi-level base reduction of a d = 64
+    multiplication log: 16 (four reductions from the base log, dense tail
+    from N/16 rows) or 8 (three, N/8), each on the tensor cores once the log
+    has >= 4096 blocks; 0 = the two-level form."""
+    if gr.d != 64:
+        return 0
+    cap = _BASE_BLOCK_CAP
+    if cap < 16 and R >= 3 and comp.N >= 8 * 4096:
+        return 8 if cap >= 8 else 0
+    if R >= 4 and comp.N >= 16 * 4096:
+        return 16
+    if R >= 3 and comp.N >= 8 * 4096:
+        return 8
+    return 0
+
+
+def _powers_b(party, r: torch.Tensor, nb: int, B: int, gr: Ring):
+    """(r^(Bj) for j < nb, r^0..r^(B-1)): every B-th power and the in-block
+    offsets (pw[Bj + a] = pwB[j] r^a)."""
+    key = ("powb", B, gr.ell, gr.d, _opened_key(party, r), nb)
 
     def build():
-        rpow = grvec.gr_powers(r, 9, gr.ell, gr.mod)
-        return grvec.gr_powers(rpow[8:9], n8, gr.ell, gr.mod), rpow[:8].contiguous()
+        rpow = grvec.gr_powers(r, B + 1, gr.ell, gr.mod)
+        return grvec.gr_powers(rpow[B:B + 1], nb, gr.ell, gr.mod), rpow[:B].contiguous()
     return _public(party, key, build)
 
 
-def _base_fold_q8(party, comp: _Compressed, zcomps: list, z_stride: int, q8, gr: Ring):
-    """(zsum (nz, 1, d), acc (64, d)) with acc[a*8+b] = sum_j s^{ab}_j r^(8j+a)
-    and zsum_c = sum_i z_c[i] r^i, from ONE pass over the r^(8j) table on the
-    tensor cores (r3_vfy_base_fold_q8; the raw sums over r^(8j) are taken
-    times r^a here).  Honest joint sessions fold all three parties in one
-    launch (the adjacent party items share the table rows in L2)."""
-    pw8, rpow = q8
+def _base_fold_b(party, comp: _Compressed, zcomps: list, z_stride: int, qb, B: int, gr: Ring):
+    """(zsum (nz, 1, d), acc (B^2, d)) with acc[a*B+b] = sum_j s^{ab}_j r^(Bj+a)
+    and zsum_c = sum_i z_c[i] r^i, from ONE pass over the r^(Bj) table on the
+    tensor cores (r3_vfy_base_fold_q8 / _q16; the raw sums over r^(Bj) are
+    taken times r^a here).  Honest joint sessions fold all three parties in
+    one launch (the adjacent items of a K chunk share its table rows in L2)."""
+    pwb, rpow = qb
     mine = {"terms": _role_terms(party.role), "x": comp.x, "y": comp.y, "z": zcomps}
     d = gr.d
-    r_acc = rpow.repeat_interleave(8, dim=0)          # row a*8 + b -> r^a
+    r_acc = rpow.repeat_interleave(B, dim=0)          # row a*B + b -> r^a
 
     def folds(slots):
         roles = sorted(slots)
@@ -666,11 +686,11 @@ def _base_fold_q8(party, comp: _Compressed, zcomps: list, z_stride: int, q8, gr:
                 coef[3 * q + t], xs[3 * q + t], ys[3 * q + t] = cf, ptr(sl["x"][xk]), ptr(sl["y"][yk])
             for c, zt in enumerate(sl["z"]):
                 zp[2 * q + c] = ptr(zt)
-            raw[r] = (empty((64, d)), empty((max(1, len(sl["z"])) * 8, d)))
+            raw[r] = (empty((B * B, d)), empty((max(1, len(sl["z"])) * B, d)))
         zs = (C.c_int64 * np_)(*([z_stride] * np_))
         arrs = [(C.c_void_p * np_)(*[ptr(raw[r][i]) for r in roles]) for i in range(2)]
-        call("r3_vfy_base_fold_q8", np_, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
-             C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zs), comp.N, ptr(pw8), d,
+        call(f"r3_vfy_base_fold_q{B}", np_, C.addressof(nterms), C.addressof(coef), C.addressof(xs),
+             C.addressof(ys), C.addressof(nz), C.addressof(zp), C.addressof(zs), comp.N, ptr(pwb), d,
              C.addressof(arrs[0]), C.addressof(arrs[1]), stream())
         out = {}
         for r in roles:
@@ -679,29 +699,28 @@ def _base_fold_q8(party, comp: _Compressed, zcomps: list, z_stride: int, q8, gr:
             acc = grvec.gr_mul(acc_raw, r_acc, gr.ell, gr.mod)
             zsum = empty((nzr, 1, d))
             if nzr:
-                zc = grvec.gr_mul(z_raw[:8 * nzr], rpow.repeat(nzr, 1), gr.ell, gr.mod)
+                zc = grvec.gr_mul(z_raw[:B * nzr], rpow.repeat(nzr, 1), gr.ell, gr.mod)
                 for c in range(nzr):
-                    zsum[c] = grvec.sum_axis0(zc[8 * c:8 * c + 8], gr.ell, keepdims=True)
+                    zsum[c] = grvec.sum_axis0(zc[B * c:B * c + B], gr.ell, keepdims=True)
             out[r] = (zsum, acc)
         return out
 
     if _joint_ok(party):
-        return party.sess.joint(("bfold8", party.next_id("_joint.bfold8")), party.role, mine, folds)
+        return party.sess.joint(("bfoldb", party.next_id("_joint.bfoldb")), party.role, mine, folds)
     return folds({party.role: mine})[party.role]
 
 
-def _block_fold_weights(party, k: int, ws: list, gr: Ring):
-    """Public weights (W1, W2), each (64, d), of level k < 3's folds over the
-    64 block accumulators: h = sum_q acc[q] (x) W[q] (verify.py:229-231 with
-    the level-k vectors expanded into the base blocks of eight).  A level-k
-    row spans 2^k base elements a with line weight V_a = prod_{l<k}
-    ws[l][bit l of a]; the pair (f0, f1) of rows spans 2^(k+1), bit k of a
-    tells f0 from f1.  W1 keeps a, b both in f1; W2 weighs alpha_a alpha_b
-    (alpha = -1 on f0, 2 on f1: f2 = 2 f1 - f0)."""
-    key = ("bw8", gr.ell, gr.d, k, tuple(_opened_key(party, w[1]) for w in ws))
+def _block_fold_weights(party, k: int, ws: list, B: int, gr: Ring):
+    """Public weights (W1, W2), each (B^2, d), of level k's folds
+    (k < log2 B) over the B^2 block accumulators: h = sum_q acc[q] (x) W[q]
+    (verify.py:229-231 with the level-k vectors expanded into the base blocks
+    of B).  A level-k row spans 2^k base elements a with line weight V_a =
+    prod_{l<k} ws[l][bit l of a]; the pair (f0, f1) of rows spans 2^(k+1),
+    bit k of a tells f0 from f1.  W1 keeps a, b both in f1; W2 weighs
+    alpha_a alpha_b (alpha = -1 on f0, 2 on f1: f2 = 2 f1 - f0)."""
+    key = ("bwb", B, gr.ell, gr.d, k, tuple(_opened_key(party, w[1]) for w in ws))
 
     def build():
-        d = gr.d
         nv = 1 << k
         if k == 0:
             vals = grvec.gr_const(1, gr.mod, gr.ell)
@@ -715,7 +734,7 @@ def _block_fold_weights(party, k: int, ws: list, gr: Ring):
                     n = vals.shape[0]
                     vals = grvec.gr_mul(vals.repeat(2, 1), w.repeat_interleave(n, dim=0), gr.ell, gr.mod)
         prod = grvec.gr_mul(vals.repeat_interleave(nv, dim=0), vals.repeat(nv, 1), gr.ell, gr.mod)  # [u*nv + v]
-        idx, c1, c2 = _block_fold_index(k, prod.device)
+        idx, c1, c2 = _block_fold_index(k, B, prod.device)
         rows = prod[idx]
         m = _lib_i64(gr.mask)
         W1 = (rows * c1) & m
@@ -727,19 +746,20 @@ def _block_fold_weights(party, k: int, ws: list, gr: Ring):
 _BF_INDEX: dict = {}
 
 
-def _block_fold_index(k: int, dev):
-    """Device constants of _block_fold_weights for level k: the product row
-    of each accumulator and its integer coefficients in W1 / W2.  Built once
-    per process and device (a host list -> device copy synchronises the
-    stream, which the protocol driver must not do per session)."""
-    key = (k, dev)
+def _block_fold_index(k: int, B: int, dev):
+    """Device constants of _block_fold_weights for level k and block size B:
+    the product row of each accumulator and its integer coefficients in W1 /
+    W2.  Built once per process and device (a host list -> device copy
+    synchronises the stream, which the protocol driver must not do per
+    session)."""
+    key = (k, B, dev)
     hit = _BF_INDEX.get(key)
     if hit is None:
         nv = 1 << k
         idx, c1, c2 = [], [], []
         alpha = (-1, 2)
-        for a in range(8):
-            for b in range(8):
+        for a in range(B):
+            for b in range(B):
                 same = (a >> (k + 1)) == (b >> (k + 1))
                 ba, bb = (a >> k) & 1, (b >> k) & 1
                 idx.append((a & (nv - 1)) * nv + (b & (nv - 1)))
@@ -755,25 +775,26 @@ def _lib_i64(v: int) -> int:
     return v - (1 << 64) if v >> 63 else v
 
 
-def _reduce_three_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
-                            r: torch.Tensor, gr: Ring, chal: Challenges):
-    """Pi_tran and the first THREE Pi_rd (verify.py:168-179 + 215-241 at
-    k = 0, 1, 2) from the base log: the 64 accumulators of blocks of eight
-    (r3_vfy_base_fold_q8) give every level's h(1)/h(2) folds through public
-    weights, and the level-3 vectors for the dense tail are written straight
-    from the base shares with the public tables V_a[j] = r^(8j) (r^a kappa_a)
-    (r3_gr_matmul_q_tc, then r3_vfy_line_b with blocks of eight).  Returns
-    ((xs, ys), z, 3)."""
+def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
+                      r: torch.Tensor, B: int, gr: Ring, chal: Challenges):
+    """Pi_tran and the first L = log2 B Pi_rd (verify.py:168-179 + 215-241
+    at k < L) from the base log: the B^2 accumulators of blocks of B
+    (r3_vfy_base_fold_q8 / _q16) give every level's h(1)/h(2) folds through
+    public weights, and the level-L vectors for the dense tail are written
+    straight from the base shares with the public tables V_a[j] = r^(Bj)
+    (r^a kappa_a) (r3_gr_matmul_q_tc, then r3_vfy_line_b with blocks of B).
+    Returns ((xs, ys), z, L)."""
     role = party.role
-    n8 = (comp.N + 7) // 8
-    q8 = _powers8(party, r, n8, gr)
-    zsum, acc = _base_fold_q8(party, comp, zlist, z_stride, q8, gr)
+    levels = B.bit_length() - 1
+    nb = (comp.N + B - 1) // B
+    qb = _powers_b(party, r, nb, B, gr)
+    zsum, acc = _base_fold_b(party, comp, zlist, z_stride, qb, B, gr)
     z = _mval_from({k: zsum[i] for i, k in enumerate(znames)}, gr, role)
     ws = []
     n = comp.N
-    for k in range(3):
-        W1, W2 = _block_fold_weights(party, k, ws, gr)
-        fold = lambda W: _dotsum_terms([([(1, acc, 64)], [(1, W, 64)])], 64, gr)
+    for k in range(levels):
+        W1, W2 = _block_fold_weights(party, k, ws, B, gr)
+        fold = lambda W: _dotsum_terms([([(1, acc, B * B)], [(1, W, B * B)])], B * B, gr)
         rows = (n + 1) // 2
         h1 = _gr_dot_folded(party, gr, rows, fold(W1))
         h2 = _gr_dot_folded(party, gr, rows, fold(W2))
@@ -782,23 +803,23 @@ def _reduce_three_from_base(party, comp: _Compressed, zlist: list, znames: list,
         z = _recombine(party, z, h1, h2, q, gr)
         ws.append((q.one_m, ze))
         n = rows
-    tabs, kappa = _l3_tables(party, q8, ws, gr)
+    tabs, kappa = _base_tables(party, qb, ws, B, gr)
     geo = (comp.N, comp.n, comp.ks, comp.ls)
 
-    def level3_vectors(slots):
+    def level_vectors(slots):
         out = {}
         for side in ("x", "y"):
             # m is the same public value at P1 and P2 (honest joint session)
             srcs = [(rr, k, t) for rr, sl in sorted(slots.items()) for k, t in sl[side].items()
                     if not (rr == 2 and k == "m" and 1 in slots and "m" in slots[1][side])]
-            dst = [empty((n8, gr.d)) for _ in srcs]
-            for c0 in range(0, len(srcs), 4):          # blocks of eight: <= 4 components per launch
+            dst = [empty((nb, gr.d)) for _ in srcs]
+            for c0 in range(0, len(srcs), 4):          # wide blocks: <= 4 components per launch
                 part, pdst = srcs[c0:c0 + 4], dst[c0:c0 + 4]
                 if side == "x":
-                    call("r3_vfy_line_b", 8, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
-                         n8 * gr.d, 8, gr.d, _ptrs(pdst), gr.mask, stream())
+                    call("r3_vfy_line_b", B, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
+                         nb * gr.d, B, gr.d, _ptrs(pdst), gr.mask, stream())
                 else:
-                    call("r3_vfy_line_b_const", 8, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(kappa),
+                    call("r3_vfy_line_b_const", B, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(kappa),
                          gr.d, _ptrs(pdst), gr.mask, stream())
             for (rr, k, _), o in zip(srcs, dst):
                 out.setdefault(rr, {"x": {}, "y": {}})[side][k] = o
@@ -808,29 +829,31 @@ def _reduce_three_from_base(party, comp: _Compressed, zlist: list, znames: list,
 
     mine = {"x": comp.x, "y": comp.y}
     if _joint_ok(party):
-        res = party.sess.joint(("l3vec", party.next_id("_joint.l3vec")), role, mine, level3_vectors)
+        res = party.sess.joint(("lbvec", party.next_id("_joint.lbvec")), role, mine, level_vectors)
     else:
-        res = level3_vectors({role: mine})[role]
-    return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z, 3
+        res = level_vectors({role: mine})[role]
+    return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z, levels
 
 
-def _l3_tables(party, q8, ws: list, gr: Ring):
-    """kappa_a = w1_{a&1} w2_{(a>>1)&1} w3_{a>>2} (the level-3 line weight of
-    base element 8j + a) and the tables V_a[j] = pw8[j] (r^a kappa_a), a < 8."""
-    pw8, rpow = q8
-    key = ("l3t", gr.ell, gr.d, id(pw8), pw8.shape[0], tuple(_opened_key(party, w[1]) for w in ws))
+def _base_tables(party, qb, ws: list, B: int, gr: Ring):
+    """kappa_a = prod_{l < log2 B} w_(l+1)[bit l of a] (the level line weight
+    of base element Bj + a) and the tables V_a[j] = pwB[j] (r^a kappa_a),
+    a < B, built four at a time from one pass over pwB."""
+    pwb, rpow = qb
+    key = ("lbt", B, gr.ell, gr.d, id(pwb), pwb.shape[0], tuple(_opened_key(party, w[1]) for w in ws))
 
     def build():
-        kap = torch.cat([ws[0][a & 1] for a in range(8)])
-        kap = grvec.gr_mul(kap, torch.cat([ws[1][(a >> 1) & 1] for a in range(8)]), gr.ell, gr.mod)
-        kappa = grvec.gr_mul(kap, torch.cat([ws[2][a >> 2] for a in range(8)]), gr.ell, gr.mod)
+        kappa = None
+        for lvl, w in enumerate(ws):
+            f = torch.cat([w[(a >> lvl) & 1] for a in range(B)])
+            kappa = f if kappa is None else grvec.gr_mul(kappa, f, gr.ell, gr.mod)
         rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
-        rows = pw8.shape[0]
-        tabs = grvec.empty((8, rows, gr.d))
-        for h in (0, 4):
-            grvec.rows_times_multi(pw8, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(h, h + 4)], rows,
+        rows = pwb.shape[0]
+        tabs = grvec.empty((B, rows, gr.d))
+        for h in range(0, B, 4):
+            grvec.rows_times_multi(pwb, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(h, h + 4)], rows,
                                    gr.ell, [tabs[a] for a in range(h, h + 4)])
-        return tabs, kappa
+        return tabs, kappa.contiguous()
     return _public(party, key, build)
 
 

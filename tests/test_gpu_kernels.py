@@ -383,7 +383,7 @@ def test_level_fold16_tc_matches_cuda_core(cuda, N):
 
 @pytest.mark.parametrize("N", [(1 << 16) + 37, 1 << 20])
 @pytest.mark.parametrize("joint", [True, False])
-@pytest.mark.parametrize("B", [4, 8])
+@pytest.mark.parametrize("B", [4, 8, 16])
 def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B):
     """r3_vfy_base_fold_q4 on the tensor cores (bf_tc.cu, d = 64) -- the
     headline's base fold -- against its definition
@@ -396,7 +396,8 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B):
     parties' features in one pass), joint=False one launch per party.
     B = 8 is r3_vfy_base_fold_q8 (blocks of eight against r^(8j): the 64
     accumulators of the first three reductions; one work item per party and
-    K-chunk)."""
+    K-chunk), B = 16 r3_vfy_base_fold_q16 (256 accumulators, three feature
+    groups per party and K-chunk)."""
     import ctypes as C
     from paper_2411_09287_b200 import grvec, host, _lib
     d = 64

@@ -85,3 +85,56 @@ def test_session_rerun_after_discarded_logs(cuda):
     sess.run(unverified)
     assert all(p.logs[k].discard for p in sess.parties for k in p.logs)
     assert all(Session(seed=9).run(verified))
+
+
+@pytest.mark.parametrize("N,R", [((1 << 16) + 5, 5), ((1 << 15) + 3, 3)])
+def test_base_reduction_block_sizes_give_identical_transcripts(cuda, N, R, monkeypatch):
+    """The d = 64 verification of one multiplication log through the
+    two-level base reduction (blocks of four, B = 0), three levels from
+    the base (B = 8) and four (B = 16, where the log is large enough): every
+    message payload (per sender, in order), the verdict and the opened
+    product are identical -- the block size only changes how the same
+    values are computed (verify.py:168-241).  A tampered leg is still
+    rejected under the widest form (per-party launches: adversary sessions
+    do not batch the parties)."""
+    import hashlib
+    from paper_2411_09287_b200 import gates, host, verify
+    from paper_2411_09287_b200.runtime import Session
+    from paper_2411_09287_b200.sharing import Ring, reconstruct_clear, shc_random
+    from paper_2411_09287_b200.transport import Phase
+
+    def prog(party):
+        ring = Ring(64)
+        party.enter_phase(Phase.PRE)
+        x = shc_random(party, N, ring)
+        y = shc_random(party, N, ring)
+        g = gates.mul_prepare(party, x.mask, y.mask, N)
+        verify.prepare_verification(party, d=64, r_max=R)
+        party.round_barrier()
+        party.enter_phase(Phase.ONLINE)
+        z = gates.mul_finish(party, g, x, y)
+        party.round_barrier()
+        party.enter_phase(Phase.POST)
+        return z, verify.batch_verify_muls(party, 64, d=64, R=R)
+
+    orig = verify._base_block
+    runs = {}
+    for B in (0, 8, 16):
+        monkeypatch.setattr(verify, "_base_block",
+                            lambda comp, R_, gr, B=B: min(B, orig(comp, R_, gr)) if B else 0)
+        sess = Session(seed=11)
+        log = []
+        sess.message_hook = lambda frm, to, ph, label, arr, cls, ring: log.append(
+            (frm, label, hashlib.sha256(host(arr).tobytes()).hexdigest()))
+        res = sess.run(prog)
+        z = host(reconstruct_clear([r[0] for r in res]))
+        runs[B] = (sorted(log), [r[1] for r in res], z)
+    for B in (8, 16):
+        assert runs[B][1] == runs[0][1] == [True, True, True]
+        np.testing.assert_array_equal(runs[B][2], runs[0][2])
+        assert runs[B][0] == runs[0][0], f"B = {B}: message payloads differ from the two-level form"
+    monkeypatch.setattr(verify, "_base_block", orig)
+    from paper_2411_09287_b200.transport import AdversaryConfig, Injection
+    adv = AdversaryConfig(corrupted=1, injections=[Injection("dot.mz", delta=1, gate=0, lane=7)])
+    res = Session(seed=11, adversary=adv).run(prog)
+    assert not any(r[1] for r in res), "a tampered leg passed verification"
