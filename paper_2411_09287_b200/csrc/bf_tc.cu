@@ -93,7 +93,9 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   using L = BfLayout<B>;
   constexpr int RS = L::RS;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sA = smem + L::OFF_LIMB;
   uint8_t* sB = sA + BF_STAGES * BF_A_TILE;

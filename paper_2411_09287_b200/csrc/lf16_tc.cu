@@ -67,7 +67,9 @@ __device__ __forceinline__ void l16_read_row(const uint8_t* row, int sw, u64 (&v
 __global__ void __launch_bounds__(L16_THREADS, 1)
 level_fold16_tc_kernel(const __grid_constant__ L16Args args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sA = smem + L16_OFF_LIMB;
   uint8_t* sB = sA + L16_STAGES * L16_A_TILE;

@@ -114,7 +114,9 @@ __device__ __forceinline__ void lf_accum(const uint8_t* ro, const uint8_t* re, b
 __global__ void __launch_bounds__(LF_THREADS, 1)
 level_fold_tc_kernel(const __grid_constant__ LfArgs args, u64* __restrict__ acc1, u64* __restrict__ acc2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sLimb = smem + LF_OFF_LIMB;             // stage: A_o, A_t, B_o, B_t
   u64* red = reinterpret_cast<u64*>(smem);         // epilogue only (raw stages are idle by then)

@@ -98,7 +98,9 @@ gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ 
                      u64 mask) {
   const int nops = J.nops;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sStage = smem;
   uint8_t* sB = smem + DB_OFF_B;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DB_OFF_BAR);
@@ -300,7 +302,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ MqArgs args, int64_t rows,
                    u64 mask) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sStage = smem;
   uint8_t* sB = smem + MQ_OFF_B;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MQ_OFF_BAR);
@@ -499,7 +503,9 @@ gr_matmul2_tc16_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict_
                        u64 mask) {
   const int nops = J.nops;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by offsetting the shared array itself (keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sLimb = smem + T16_OFF_LIMB;
   uint8_t* sB = smem + T16_OFF_B;
