@@ -35,19 +35,20 @@ constexpr int BF_MAX_SLOTS = 6;                 // distinct x / y / z arrays of 
 // ("wide"): two raw stages, each the table rows plus the base-log arrays the
 // work item reads in the K-step, all by TMA (so the converters never wait on
 // global loads): B = 8 all of the party's arrays (x / y / z, <= 6 x 2 KB),
-// B = 16 either its x / y arrays or its z arrays (<= 4 x 4 KB).  A log
+// B = 16 either a party's x / y arrays (<= 4 x 4 KB) or, for the one z
+// item of a chunk, every party's distinct z arrays (<= 6 x 4 KB).  A log
 // array is viewed as rows of 16 words (128 B) with the 128-byte swizzle,
 // which makes the converters' per-block reads bank-conflict free.
-// G = work items (feature groups of <= 128 MMA rows) per party and chunk:
-// B = 16 has 256 s products + 16 nz z values per party -> s rows a < 8,
-// s rows a >= 8, z values.
+// Work items per K chunk: B = 8 one per party (64 + 8 nz features fill the
+// 128 MMA rows); B = 16 two per party (256 s products: rows a < 8 and
+// a >= 8) plus ONE z item for all parties (16 features per distinct z
+// array).
 template <int B>
 struct BfLayout {
   static constexpr bool WIDE = B >= 8;
   static constexpr int RS = WIDE ? 2 : 3;
   static constexpr int SLOT = BF_BK * B * 8;    // one array over a K-step (TMA box, 128B swizzle)
-  static constexpr int NSLOT = B == 8 ? 6 : 4;
-  static constexpr int G = B == 16 ? 3 : 1;
+  static constexpr int NSLOT = 6;               // B = 16: <= 4 x / y arrays, or the z item's <= 6
   static constexpr int RAWST = (BF_RAW + (WIDE ? NSLOT * SLOT : 0) + 1023) / 1024 * 1024;
   static constexpr int OFF_LIMB = RS * RAWST;
   static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
@@ -76,6 +77,14 @@ struct BfParty {
 struct BfArgs {
   CUtensorMap pw4;
   CUtensorMap lmap[3][BF_MAX_SLOTS];   // wide B: the parties' base-log arrays as 16-word rows
+  // B = 16: ONE z item per K chunk for every party -- the distinct z arrays
+  // (the honest m is shared by P1 and P2), their maps and where each one's
+  // sums go (party, component)
+  CUtensorMap zmap[BF_MAX_SLOTS];
+  const u64* zslot[BF_MAX_SLOTS];
+  int nzs;
+  int zdst_n[BF_MAX_SLOTS], zdst_p[BF_MAX_SLOTS][2], zdst_c[BF_MAX_SLOTS][2];
+  int per;     // work items per K chunk
   BfParty p[3];
   int np;
   int vec;     // every base-log pointer 16-byte aligned: 128-bit loads
@@ -111,16 +120,24 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 
   // persistent: CTA b takes K-chunks (items) b, b + grid, ... of kc blocks;
   // unit g enumerates (item, K-step) in that order
-  constexpr int G = L::G;
   const int64_t nchunks = (args.nblk + args.kc - 1) / args.kc;
-  const int64_t nitems = B == 4 ? nchunks : nchunks * args.np * G;
+  const int per = B == 4 ? 1 : args.per;
+  const int64_t nitems = nchunks * per;
   auto item_range = [&](int64_t it, int64_t& j0, int64_t& j1) {
-    j0 = (B == 4 ? it : it / (args.np * G)) * args.kc;
+    j0 = (it / per) * args.kc;
     j1 = min(args.nblk, j0 + args.kc);
   };
-  // wide B: item -> (party, feature group)
-  auto item_party = [&](int64_t it) { return B == 4 ? 0 : int((it / G) % args.np); };
-  auto item_group = [&](int64_t it) { return B == 4 ? 0 : int(it % G); };
+  // wide B: item -> (party, feature group).  B = 8: one item per party.
+  // B = 16: items 2q, 2q + 1 of a chunk are party q's s rows a < 8 / a >= 8,
+  // the last one the shared z item (party 0 stands in; group 2)
+  auto item_party = [&](int64_t it) {
+    const int r = int(it % per);
+    return B == 4 ? 0 : (B == 8 ? r : (r < 2 * args.np ? r >> 1 : 0));
+  };
+  auto item_group = [&](int64_t it) {
+    const int r = int(it % per);
+    return B == 16 ? (r < 2 * args.np ? (r & 1) : 2) : 0;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) {
@@ -156,9 +173,10 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         const int pi = item_party(it);
         const BfParty& P = args.p[pi];
         const int grp = item_group(it);
-        // the arrays this item reads: B = 8 all, B = 16 x / y (s groups) or z
-        const int s0 = B == 16 && grp == 2 ? P.nxy : 0;
-        const int s1 = B == 16 && grp < 2 ? P.nxy : P.nxy + P.nz;
+        // the arrays this item reads: B = 8 all of the party's, B = 16 its x /
+        // y arrays (s groups) or every party's distinct z arrays (z item)
+        const bool zitem = B == 16 && grp == 2;
+        const int nsl = zitem ? args.nzs : (B == 16 ? P.nxy : P.nxy + P.nz);
         for (int64_t kb = 0; kb < nkb; ++kb, ++g) {
           const int rs = int(g % RS);
           if (g >= RS) mbar_wait(&raw_empty[rs], uint32_t((g / RS - 1) & 1));
@@ -167,13 +185,13 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           // crosses the end of the log (the converters load those)
           const bool whole = L::WIDE && args.vec && (j0 + (kb + 1) * BF_BK) * B <= args.N;
           uint8_t* dst = sRaw + rs * L::RAWST;
-          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? (s1 - s0) * L::SLOT : 0)));
+          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? nsl * L::SLOT : 0)));
           for (int c = 0; c < 4; ++c)
             tma_load_2d(dst + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[rs]);
           if (whole)
-            for (int q = s0; q < s1; ++q)
-              tma_load_2d(dst + BF_RAW + (q - s0) * L::SLOT, &args.lmap[pi][q], 0, int(int64_t(y) * B / 16),
-                          &raw_full[rs]);
+            for (int q = 0; q < nsl; ++q)
+              tma_load_2d(dst + BF_RAW + q * L::SLOT, zitem ? &args.zmap[q] : &args.lmap[pi][q], 0,
+                          int(int64_t(y) * B / 16), &raw_full[rs]);
         }
       }
     }
@@ -193,7 +211,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     const int p = B == 4 ? c >> 1 : item_party(it);
     const int h = B == 4 ? (c & 1)
                   : B == 8 ? (c < 4 ? 0 : (c == 4 ? 1 : 2))
-                           : (grp < 2 ? 0 : (c < 2 ? 1 : 2));
+                           : (grp < 2 ? 0 : (c < args.nzs ? 1 : 2));
     const bool live = isA && p < args.np && h < 2;
     constexpr int NA = B == 8 ? 2 : 1;               // s rows per chunk (wide B)
     const int a0 = B == 8 ? 2 * c : 8 * grp + c;     // first s row of the chunk
@@ -247,12 +265,12 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
                 }
               }
             }
-          } else {               // z values: B = 8 v[cz 8 + a] (chunk 4), B = 16 v[a] (chunk cz)
-            const int zbase = B == 8 ? P.nxy : 0;   // z arrays follow the x / y arrays in the stage
+          } else {               // z values: B = 8 v[cz 8 + a] (chunk 4), B = 16 v[a] (z slot c)
+            const int zbase = B == 8 ? P.nxy : 0;   // B = 8: z arrays follow the party's x / y arrays
 #pragma unroll
             for (int cz = 0; cz < (B == 8 ? 2 : 1); ++cz) {
               const int zc = B == 8 ? cz : c;
-              if (zc < P.nz) {
+              if (zc < (B == 8 ? P.nz : args.nzs)) {
 #pragma unroll
                 for (int q = 0; q < B / 2; ++q) {
                   const ulonglong2 zz = *reinterpret_cast<const ulonglong2*>(chunk(zbase + zc, q));
@@ -294,10 +312,12 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 #pragma unroll
             for (int cz = 0; cz < (B == 8 ? 2 : 1); ++cz) {
               const int zc = B == 8 ? cz : c;
-              if (zc < P.nz) {
+              if (zc < (B == 8 ? P.nz : args.nzs)) {
+                const u64* zp = B == 8 ? P.z[zc] : args.zslot[zc];
+                const int64_t zst = B == 8 ? P.zs : 1;
 #pragma unroll
                 for (int a = 0; a < B; ++a)
-                  v[cz * B + a] = i0 + a < args.N ? __ldg(P.z[zc] + (i0 + a) * P.zs) : 0ull;
+                  v[cz * B + a] = i0 + a < args.N ? __ldg(zp + (i0 + a) * zst) : 0ull;
               }
             }
           }
@@ -407,6 +427,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       tc_fence_after();
       const int f = warp * 32 + lane;
       u64* dst = nullptr;
+      u64* dst2 = nullptr;
       if (B == 4) {
         const int p = f >> 5, q = f & 31;
         const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
@@ -416,10 +437,15 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         if (f < 64) dst = P.acc + f * 64;
         else if (f < 64 + 8 * P.nz) dst = P.zraw + (f - 64) * 64;
       } else {
-        const BfParty& P = args.p[item_party(it)];
         const int grp = item_group(it);
-        if (grp < 2) dst = P.acc + (128 * grp + f) * 64;
-        else if (f < 16 * P.nz) dst = P.zraw + f * 64;
+        if (grp < 2) {
+          dst = args.p[item_party(it)].acc + (128 * grp + f) * 64;
+        } else if ((f >> 4) < args.nzs) {
+          // z slot f / 16 feeds one or two (party, component) sums
+          const int zs = f >> 4, a = f & 15;
+          dst = args.p[args.zdst_p[zs][0]].zraw + (16 * args.zdst_c[zs][0] + a) * 64;
+          if (args.zdst_n[zs] > 1) dst2 = args.p[args.zdst_p[zs][1]].zraw + (16 * args.zdst_c[zs][1] + a) * 64;
+        }
       }
       const bool live = dst != nullptr;
       const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
@@ -436,6 +462,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
 #pragma unroll
             for (int s = 0; s < 8; ++s) P += u64(v[s][e]) << (8 * s);
             atomicAdd(reinterpret_cast<unsigned long long*>(dst + c0 + e), (unsigned long long)P);
+            if (dst2) atomicAdd(reinterpret_cast<unsigned long long*>(dst2 + c0 + e), (unsigned long long)P);
           }
         }
       }
@@ -501,9 +528,38 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
       for (int c = 0; c < P.nz; ++c) P.slot[P.nxy + c] = P.z[c];
       if (P.nz && P.zs != 1) args.vec = 0;
     }
+    if (B == 16) {
+      // the shared z item: distinct z arrays of all parties and their sums
+      for (int q = 0; q < np; ++q) {
+        const BfParty& P = args.p[q];
+        for (int c = 0; c < P.nz; ++c) {
+          int zs = 0;
+          while (zs < args.nzs && args.zslot[zs] != P.z[c]) ++zs;
+          if (zs == args.nzs) {
+            if (args.nzs == BF_MAX_SLOTS || P.zs != 1) {
+              set_error("%s: more than 6 distinct z arrays (or strided z)", what);
+              return R3_ERR_ARG;
+            }
+            args.zslot[args.nzs] = P.z[c];
+            args.zdst_n[args.nzs++] = 0;
+          }
+          if (args.zdst_n[zs] == 2) {
+            set_error("%s: a z array shared by more than two parties", what);
+            return R3_ERR_ARG;
+          }
+          args.zdst_p[zs][args.zdst_n[zs]] = q;
+          args.zdst_c[zs][args.zdst_n[zs]++] = c;
+        }
+      }
+      for (int zs = 0; zs < args.nzs && args.vec; ++zs)
+        if (!make_rows_tmap(&args.zmap[zs], args.zslot[zs], N / 16, 16, BF_BK * B / 16, 16)) {
+          set_error("%s: cuTensorMapEncodeTiled (z) failed", what);
+          return R3_ERR_CUDA;
+        }
+    }
     // each array as floor(N / 16) rows of 16 words; a K-step's box: 32 blocks
     for (int q = 0; q < np && args.vec; ++q)
-      for (int s2 = 0; s2 < args.p[q].nxy + args.p[q].nz; ++s2)
+      for (int s2 = 0; s2 < args.p[q].nxy + (B == 8 ? args.p[q].nz : 0); ++s2)
         if (!make_rows_tmap(&args.lmap[q][s2], args.p[q].slot[s2], N / 16, 16, BF_BK * B / 16, 16)) {
           set_error("%s: cuTensorMapEncodeTiled (log) failed", what);
           return R3_ERR_CUDA;
@@ -515,7 +571,8 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
   }
   // K-chunks of <= BF_MAX_K blocks, a whole number of items per CTA of a
   // persistent grid (no partial second wave)
-  const int per = B == 4 ? 1 : np * BfLayout<B>::G;   // items per K-chunk
+  const int per = B == 4 ? 1 : (B == 8 ? np : 2 * np + (args.nzs > 0 ? 1 : 0));   // items per K-chunk
+  args.per = per;
   int64_t chunks = (nblk + BF_MAX_K - 1) / BF_MAX_K;
   int64_t items = chunks * per;
   items = (items + num_sms() - 1) / num_sms() * num_sms();
