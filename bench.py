@@ -729,6 +729,16 @@ def work_of(name, args) -> int:
     if name == "r3_u64_gemm_tc":
         npairs, K, M, N = int(args[0]), args[3], int(args[4]), int(args[5])
         return 2 * 36 * M * N * sum(int(K[p]) for p in range(npairs))
+    if name in ("r3_vfy_base_fold_q8", "r3_vfy_base_fold_q16"):
+        # useful accumulator updates as int8 limb ops: per block of B, every
+        # party's B^2 s products and B z values per z array times one table
+        # row of 64 coefficients (36 limb products x 2)
+        import ctypes as C
+        B = 8 if name.endswith("q8") else 16
+        np_, N = int(args[0]), int(args[8])
+        nz = (C.c_int * np_).from_address(int(args[5]))
+        feats = np_ * B * B + B * sum(int(v) for v in nz)
+        return 72 * 64 * feats * ((N + B - 1) // B)
     if name == "r3_vfy_level_fold":
         # per pair: h(1) and h(2), one outer product each for P0, two for P1/P2
         role, N, d = args[0], args[5], args[6]
@@ -750,6 +760,8 @@ KERNEL_BOUND = {
     "r3_gr_matmul2_tc16_multi": ("hbm", "GB/s", 1e9),
     "r3_ew_flat": ("hbm", "GB/s", 1e9),
     "r3_u64_gemm_tc": ("tensor", "int8 TOP/s", 1e12),
+    "r3_vfy_base_fold_q8": ("tensor", "int8 TOP/s", 1e12),
+    "r3_vfy_base_fold_q16": ("tensor", "int8 TOP/s", 1e12),
     "r3_prf_ctr": ("aes", "G AES blocks/s", 1e9),
     "r3_prf_bits_packed": ("aes", "G AES blocks/s", 1e9),
     "r3_ripple_msb": ("aes", "G AES blocks/s", 1e9),
@@ -1066,6 +1078,12 @@ def run_b200(args):
     if step_kernels is not None:
         line["step_kernels"] = step_kernels
         line["per_party_rate"] = per_party
+        # the step's largest-time bounded kernel (the base fold is tensor /
+        # converter bound, so its fraction is of nominal dense int8)
+        top = step_kernels["top"][0]["entry_point"] if step_kernels.get("top") else None
+        tpeaks = {"hbm": (hbm_peak()[0] / 1e9, "MEASURED_PEAKS.json hbm_gbs (burst copy)"),
+                  "tensor": (INT8_DENSE_NOMINAL / 1e12, "nominal dense int8 (4.5 POPS)")}
+        line["roofline_step_top"] = dict(table_roofline(step_kernels, tpeaks), top_entry_point=top)
     line.update(side)
     if world == 1 and not args.no_cpu_baseline:
         # same-run CPU baselines (rank 0, N = 1): the unmodified reference on
