@@ -106,9 +106,15 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._pump, daemon=True).start()
+            # nvidia-smi takes a while to start: the timed region (a fraction
+            # of a second) must not begin before the sampler is running
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
@@ -119,6 +125,8 @@ class Clocks:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            if not self.lines:                 # region shorter than one interval
+                time.sleep(0.06)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
