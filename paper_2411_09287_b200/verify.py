@@ -276,6 +276,98 @@ def _recombine(party, z: MVal, h1: MVal, h2: MVal, q: _Quad, gr: Ring) -> MVal:
     return MVal(mask, outs[-1] if with_m else None)
 
 
+def _reduction_round(party, gr: Ring, rows: int, h1f: torch.Tensor, h2f: torch.Tensor, z: MVal, zeta: MVal):
+    """The protocol steps of one reduction (verify.py:229-236) after the
+    party's local folds: h(1), h(2) as Pi_dot gates of single GR elements
+    (Gamma dealt by P0, legs exchanged), the opened even point ze = 2 zeta,
+    its Lagrange weights and z' = (z - h1) l0 + h1 l1 + h2 l2.  Returns
+    (z', ze, quad).  Honest joint sessions run the three parties' steps in
+    one rendezvous (_round_joint: the same draws, messages and values, a
+    handful of launches for all parties instead of about fifteen per party);
+    every other session runs them gate by gate as the reference does."""
+    if _joint_ok(party):
+        key = ("round", party.next_id("_joint.round"))
+        z2, ze, q = party.sess.joint(key, party.role, (h1f, h2f, z, zeta),
+                                     lambda slots: _round_joint(party.sess, gr, rows, slots))
+        party.round_barrier()
+        return z2, ze, q
+    h1 = _gr_dot_folded(party, gr, rows, h1f)
+    h2 = _gr_dot_folded(party, gr, rows, h2f)
+    ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
+    q = _quad(party, ze, gr)
+    return _recombine(party, z, h1, h2, q, gr), ze, q
+
+
+def _round_joint(sess, gr: Ring, rows: int, slots: dict) -> dict:
+    """_reduction_round for all three simulated parties at once (run by the
+    last party to arrive; honest joint coop session).  Per party the PRF
+    streams advance exactly as in gate-by-gate execution (gates.py:52-74 via
+    prepare_gate: output-mask shares, then P0's Gamma share s1, per gate)
+    and every party sends its messages with the reference's labels, classes
+    and per-sender order: P0 the two Gamma shares then the r1 / r2 legs of
+    the opening; P1 its two legs, then m and the r1 digest; P2 its two legs,
+    then the m and r2 digests.  Every send precedes its receive, so no party
+    blocks inside the rendezvous."""
+    P = sess.parties
+    ell, d = gr.ell, gr.d
+    (f01, f02, z0, zt0), (f11, f12, z1, zt1), (f21, f22, z2, zt2) = (slots[r] for r in range(3))
+    if z0.mask.s1 is not None or z0.mask.total is None:
+        raise HarnessError("joint reduction round: P0's running z must hold only its mask sum")
+    gids = [[p.next_id("vfy.dot") for _ in range(2)] for p in P]
+    # draws per stream in gate order (sha_random's mask share, then P0's
+    # Gamma share s1 on the 01 stream); pairwise streams give both holders
+    # the same words, so P0's tensors stand for P1's / P2's
+    d01 = P[0].prg("01", "sha").draw_gr(4, ell, gr.mod)          # om1.s1, g1.s1, om2.s1, g2.s1
+    d02 = P[0].prg("02", "sha").draw_gr(2, ell, gr.mod)          # om1.s2, om2.s2
+    P[1].prg("01", "sha").draw_gr(4, ell, gr.mod)
+    P[2].prg("02", "sha").draw_gr(2, ell, gr.mod)
+    om_s1, g_s1, om_s2 = d01[0::2], d01[1::2], d02
+    om_tot = grvec.add(om_s1, om_s2, ell)
+    F0, F1, F2 = torch.cat([f01, f02]), torch.cat([f11, f12]), torch.cat([f21, f22])
+    g_s2 = grvec.sub(grvec.add(F0, om_tot, ell), g_s1, ell)      # P0 -> P2: Gamma - s1
+    leg1 = grvec.add(F1, g_s1, ell)
+    leg2 = grvec.add(F2, g_s2, ell)
+    m = grvec.add(leg1, leg2, ell)
+    for g in range(2):
+        gid = gids[0][g]
+        P[0].send(2, f"sha.vfy.dot.gamma.{gid}", g_s2[g:g + 1], gr, cls=OFFLINE, site="vfy.dot.gamma", gate=gid)
+        P[2].recv(0, f"sha.vfy.dot.gamma.{gids[2][g]}", gr, 1)
+        l1, l2 = f"vfy.dot.mz.{gids[1][g]}", f"vfy.dot.mz.{gids[2][g]}"
+        P[1].send(2, f"{l1}.leg1", leg1[g:g + 1], gr, cls=PAYLOAD, site="vfy.dot.mz", gate=gids[1][g])
+        P[2].send(1, f"{l2}.leg2", leg2[g:g + 1], gr, cls=PAYLOAD, site="vfy.dot.mz", gate=gids[2][g])
+        P[1].recv(2, f"{l1}.leg2", gr, 1)
+        P[2].recv(1, f"{l2}.leg1", gr, 1)
+    # open ze = 2 zeta (sharing.rec, style "challenge"): P0's halves stand
+    # for P1's s1 / P2's s2, P1's m for P2's
+    two = lambda a: grvec.ew(grvec.MUL, a, 2, gr.mask)
+    S1, S2, M = two(zt0.mask.s1), two(zt0.mask.s2), two(zt1.m)
+    ze = grvec.sub3(M, S1, S2, ell)
+    tags = [f"vfy.zeta#{p.next_id('rec')}" for p in P]
+    L = lambda r, leg: f"rec.{tags[r]}.{leg}"
+    P[0].send(2, L(0, "r1"), S1, gr, cls=AUX)
+    P[0].send(1, L(0, "r2"), S2, gr, cls=AUX)
+    P[1].send(0, L(1, "m"), M, gr, cls=PAYLOAD)
+    P[1].send_digest(2, L(1, "r1"), S1, gr)
+    P[2].send_digest(0, L(2, "m"), M, gr)
+    P[2].send_digest(1, L(2, "r2"), S2, gr)
+    m0 = P[0].recv(1, L(0, "m"), gr, 1)
+    P[0].check_digest(2, L(0, "m"), m0, gr, f"rec {tags[0]} m")
+    s2_1 = P[1].recv(0, L(1, "r2"), gr, 1)
+    P[1].check_digest(2, L(1, "r2"), s2_1, gr, f"rec {tags[1]} r2")
+    s1_2 = P[2].recv(0, L(2, "r1"), gr, 1)
+    P[2].check_digest(1, L(2, "r1"), s1_2, gr, f"rec {tags[2]} r1")
+    q = _quad(P[0], ze, gr)
+    # z' for every party's fields in one launch: P0 total, P1 s1, P2 s2, m
+    w = list(q.w)
+    terms = [[z0.mask.total, z1.mask.s1, z2.mask.s2, z1.m],
+             [om_tot[0:1], om_s1[0:1], om_s2[0:1], m[0:1]],
+             [om_tot[1:2], om_s1[1:2], om_s2[1:2], m[1:2]]]
+    o_tot, o_s1, o_s2, o_m = grvec.gr_lincomb(terms, w, ell, gr.mod)
+    return {0: (MVal(AShare(gr, 0, total=o_tot, p0_halves=False), None), ze, q),
+            1: (MVal(AShare(gr, 1, s1=o_s1, p0_halves=z1.mask.p0_halves), o_m), ze, q),
+            2: (MVal(AShare(gr, 2, s2=o_s2, p0_halves=z2.mask.p0_halves), o_m), ze, q)}
+
+
 def _powers(party, r: torch.Tensor, n: int, gr: Ring) -> torch.Tensor:
     key = ("pow", gr.ell, gr.d, _opened_key(party, r), n)
     return _public(party, key, lambda: grvec.gr_powers(r, n, gr.ell, gr.mod))
@@ -527,10 +619,7 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
         return _materialise(comp, pw, gr, party.role), z, 0
     if base_acc is None:
         h1f, h2f = _l1_folds(party, comp, pw, gr)
-    h1 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h1f)
-    h2 = _gr_dot_folded(party, gr, (comp.N + 1) // 2, h2f)
-    ze = _open_challenge(party, chal.zetas[0].scale_pub(2), "vfy.zeta")
-    z_out = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
+    z_out, ze, _ = _reduction_round(party, gr, (comp.N + 1) // 2, h1f, h2f, z, chal.zetas[0])
     if R >= 2 and gr.d >= 8:
         return (*_reduce_second_from_base(party, comp, pw, ze, z_out, gr, chal, base_acc, q4), 2)
     A, B, one_m = _line_tables(party, r, pw, comp.n, ze, gr)
@@ -586,10 +675,7 @@ def _reduce_second_from_base(party, comp: _Compressed, pw: torch.Tensor, ze1: to
     fold = lambda W: _dotsum_terms([([(1, acc, 16)], [(1, W, 16)])], 16, gr)
     n1 = (comp.N + 1) // 2
     rows = (n1 + 1) // 2
-    h1 = _gr_dot_folded(party, gr, rows, fold(W1))
-    h2 = _gr_dot_folded(party, gr, rows, fold(W2))
-    ze2 = _open_challenge(party, chal.zetas[1].scale_pub(2), "vfy.zeta")
-    z2 = _recombine(party, z1, h1, h2, _quad(party, ze2, gr), gr)
+    z2, ze2, _ = _reduction_round(party, gr, rows, fold(W1), fold(W2), z1, chal.zetas[1])
     if q4 is not None:
         tabs, kappa, tq, stride = _l2_tables_q4(party, q4, w1, ze2, gr)
     else:
@@ -796,11 +882,7 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
         W1, W2 = _block_fold_weights(party, k, ws, B, gr)
         fold = lambda W: _dotsum_terms([([(1, acc, B * B)], [(1, W, B * B)])], B * B, gr)
         rows = (n + 1) // 2
-        h1 = _gr_dot_folded(party, gr, rows, fold(W1))
-        h2 = _gr_dot_folded(party, gr, rows, fold(W2))
-        ze = _open_challenge(party, chal.zetas[k].scale_pub(2), "vfy.zeta")
-        q = _quad(party, ze, gr)
-        z = _recombine(party, z, h1, h2, q, gr)
+        z, ze, q = _reduction_round(party, gr, rows, fold(W1), fold(W2), z, chal.zetas[k])
         ws.append((q.one_m, ze))
         n = rows
     tabs, kappa = _base_tables(party, qb, ws, B, gr)
@@ -1119,11 +1201,7 @@ def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     else:
         fold1 = _level_folds(role, X, Y, "f1", rows, gr)
         fold2 = _level_folds(role, X, Y, "f2", rows, gr)
-    h1 = _gr_dot_folded(party, gr, rows, fold1)
-    h2 = _gr_dot_folded(party, gr, rows, fold2)
-    ze = _open_challenge(party, zeta.scale_pub(2), "vfy.zeta")
-    q = _quad(party, ze, gr)
-    z_out = _recombine(party, z, h1, h2, q, gr)
+    z_out, ze, q = _reduction_round(party, gr, rows, fold1, fold2, z, zeta)
     Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
     if gr.d in (16, 64):
         xo, yo, mx, my = _level_line_evals(party, X, Y, names, Ms, gr)
@@ -1308,10 +1386,7 @@ def _verify_muls_gf2(party, comp: _Compressed, zs: MVal, gr: Ring, chal: Challen
     src = ([comp.x[k] for k in names], [comp.y[k] for k in names])
     for k in range(R):
         rows = (n + 1) // 2
-        h1 = _gr_dot_folded(party, gr, rows, h1f)
-        h2 = _gr_dot_folded(party, gr, rows, h2f)
-        ze = _open_challenge(party, chal.zetas[k].scale_pub(2), "vfy.zeta")
-        z = _recombine(party, z, h1, h2, _quad(party, ze, gr), gr)
+        z, ze, _ = _reduction_round(party, gr, rows, h1f, h2f, z, chal.zetas[k])
         last = k == R - 1
         if last:
             outs = [empty((rows, d)) for _ in range(2 * nc)]
@@ -1637,11 +1712,7 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
         for f1, f2 in folds[1:]:
             fold1, fold2 = grvec.add(fold1, f1, gr.ell), grvec.add(fold2, f2, gr.ell)
         rows = sum(pt.length() for pt in parts) // 2
-        h1 = _gr_dot_folded(party, gr, rows, fold1)
-        h2 = _gr_dot_folded(party, gr, rows, fold2)
-        ze = _open_challenge(party, ctx.zetas[k].scale_pub(2), "vfy.zeta")
-        q = _quad(party, ze, gr)
-        z = _recombine(party, z, h1, h2, q, gr)
+        z, ze, q = _reduction_round(party, gr, rows, fold1, fold2, z, ctx.zetas[k])
         Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
         for pt in parts:
             if isinstance(pt, _DenseBatch):
