@@ -1108,35 +1108,39 @@ def _level_folds_joint16(party, xt: dict, yt: dict, gr: Ring):
     names = ("total",) if role == 0 else ("m", "s1" if role == 1 else "s2")
     mine = {"x": [xt[k].contiguous() for k in names], "y": [yt[k].contiguous() for k in names]}
 
-    def folds(slots):
-        N = slots[0]["x"][0].shape[0]
-        acc_all = grvec.zeros((3, 2, 2 * gr.d - 1))
-        accs = {r: acc_all[r] for r in range(3)}
-        P = C.c_void_p
-        xa, ya = slots[0]["x"][0], slots[0]["y"][0]
-        # P0's single term: one y half, 1/8 of the MMA used -- still faster
-        # than its CUDA-core fold
-        call("r3_vfy_level_fold16_tc", 1, (C.c_int * 1)(0), (P * 1)(xa.data_ptr()), (P * 1)(ya.data_ptr()),
-             (P * 1)(None), (C.c_int64 * 1)(1), (C.c_int64 * 1)(0), N,
-             (P * 3)(accs[0][0].data_ptr(), None, None), (P * 3)(accs[0][1].data_ptr(), None, None), stream())
-        (m1x, s1x), (m1y, s1y) = slots[1]["x"], slots[1]["y"]
-        (m2x, s2x), (m2y, s2y) = slots[2]["x"], slots[2]["y"]
-        # P1: -(m_x s_y1) - (s_x1 m_y);  P2: m_x (m_y - s_y2) - s_x2 m_y
-        terms = [(1, m1x, s1y, None, -1, 0), (1, s1x, m1y, None, -1, 0),
-                 (2, m2x, m2y, s2y, 1, -1), (2, s2x, m2y, None, -1, 0)]
-        party_ids = (C.c_int * 4)(*[t[0] for t in terms])
-        xs = (P * 4)(*[t[1].data_ptr() for t in terms])
-        y0 = (P * 4)(*[t[2].data_ptr() for t in terms])
-        y1 = (P * 4)(*[None if t[3] is None else t[3].data_ptr() for t in terms])
-        c0 = (C.c_int64 * 4)(*[t[4] for t in terms])
-        c1 = (C.c_int64 * 4)(*[t[5] for t in terms])
-        a1 = (P * 3)(None, accs[1][0].data_ptr(), accs[2][0].data_ptr())
-        a2 = (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr())
-        call("r3_vfy_level_fold16_tc", 4, party_ids, xs, y0, y1, c0, c1, N, a1, a2, stream())
-        red = grvec.reduce_poly_rows(acc_all, gr.mod, gr.ell)   # (6, d): one launch
-        return {r: (red[2 * r:2 * r + 1], red[2 * r + 1:2 * r + 2]) for r in range(3)}
+    return party.sess.joint(("fold16", party.next_id("_joint.fold16")), role, mine,
+                            lambda slots: _folds16_all(slots, gr))
 
-    return party.sess.joint(("fold16", party.next_id("_joint.fold16")), role, mine, folds)
+
+def _folds16_all(slots: dict, gr: Ring) -> dict:
+    """The d = 16 tensor-core folds of all three parties (slots[r]["x"] /
+    ["y"]: P0 [total], P1 / P2 [m, s1 / s2]): {r: (fold h1, fold h2)}."""
+    N = slots[0]["x"][0].shape[0]
+    acc_all = grvec.zeros((3, 2, 2 * gr.d - 1))
+    accs = {r: acc_all[r] for r in range(3)}
+    P = C.c_void_p
+    xa, ya = slots[0]["x"][0], slots[0]["y"][0]
+    # P0's single term: one y half, 1/8 of the MMA used -- still faster
+    # than its CUDA-core fold
+    call("r3_vfy_level_fold16_tc", 1, (C.c_int * 1)(0), (P * 1)(xa.data_ptr()), (P * 1)(ya.data_ptr()),
+         (P * 1)(None), (C.c_int64 * 1)(1), (C.c_int64 * 1)(0), N,
+         (P * 3)(accs[0][0].data_ptr(), None, None), (P * 3)(accs[0][1].data_ptr(), None, None), stream())
+    (m1x, s1x), (m1y, s1y) = slots[1]["x"], slots[1]["y"]
+    (m2x, s2x), (m2y, s2y) = slots[2]["x"], slots[2]["y"]
+    # P1: -(m_x s_y1) - (s_x1 m_y);  P2: m_x (m_y - s_y2) - s_x2 m_y
+    terms = [(1, m1x, s1y, None, -1, 0), (1, s1x, m1y, None, -1, 0),
+             (2, m2x, m2y, s2y, 1, -1), (2, s2x, m2y, None, -1, 0)]
+    party_ids = (C.c_int * 4)(*[t[0] for t in terms])
+    xs = (P * 4)(*[t[1].data_ptr() for t in terms])
+    y0 = (P * 4)(*[t[2].data_ptr() for t in terms])
+    y1 = (P * 4)(*[None if t[3] is None else t[3].data_ptr() for t in terms])
+    c0 = (C.c_int64 * 4)(*[t[4] for t in terms])
+    c1 = (C.c_int64 * 4)(*[t[5] for t in terms])
+    a1 = (P * 3)(None, accs[1][0].data_ptr(), accs[2][0].data_ptr())
+    a2 = (P * 3)(None, accs[1][1].data_ptr(), accs[2][1].data_ptr())
+    call("r3_vfy_level_fold16_tc", 4, party_ids, xs, y0, y1, c0, c1, N, a1, a2, stream())
+    red = grvec.reduce_poly_rows(acc_all, gr.mod, gr.ell)   # (6, d): one launch
+    return {r: (red[2 * r:2 * r + 1], red[2 * r + 1:2 * r + 2]) for r in range(3)}
 
 
 def _level_folds_fused(role: int, xt: dict, yt: dict, gr: Ring, party=None):
@@ -1178,9 +1182,77 @@ def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:
     return grvec.gr_matmul(_lin(H.d10()), M_z, H.n0, gr.d, gr.ell, C_add=_lin(H.f0()))
 
 
+def _rdim_joint_ok(party, xs: MVal, gr: Ring) -> bool:
+    if gr.d not in (16, 64) or not _joint_ok(party):
+        return False
+    if party.role == 0:
+        return xs.mask.total is not None and xs.mask.s1 is None
+    return xs.m is not None
+
+
+def _reduce_dimension_joint(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
+    """reduce_dimension of all three simulated parties in ONE rendezvous
+    (honest joint sessions, d = 64 / 16): every party's folds, the reduction
+    round (_round_joint) and every line evaluation of the level (one
+    multi-job tensor-core launch; m's evaluations once for P1 and P2).
+    Local work and messages are the reference's; the round barrier follows
+    the rendezvous as it follows the opening in reduce_dimension."""
+    key = ("rdim", party.next_id("_joint.rdim"))
+    out = party.sess.joint(key, party.role, (xs, ys, z, zeta), lambda slots: _rdim_compute(party.sess, gr, slots))
+    party.round_barrier()
+    return out
+
+
+def _rdim_compute(sess, gr: Ring, slots: dict) -> dict:
+    (x0, y0, z0, t0), (x1, y1, z1, t1), (x2, y2, z2, t2) = (slots[r] for r in range(3))
+    comps = {0: (("total", x0.mask.total, y0.mask.total),),
+             1: (("m", x1.m, y1.m), ("s1", x1.mask.s1, y1.mask.s1)),
+             2: (("m", x2.m, y2.m), ("s2", x2.mask.s2, y2.mask.s2))}
+    n = x0.mask.total.shape[0]
+    rows = (n + 1) // 2
+    d = gr.d
+    if d == 16 and n >= _JOINT16_MIN_ROWS:
+        folds = _folds16_all({r: {"x": [c[1].contiguous() for c in comps[r]],
+                                  "y": [c[2].contiguous() for c in comps[r]]} for r in range(3)}, gr)
+    else:
+        # one r3_vfy_level_fold per party into one accumulator block, one reduction
+        acc = grvec.zeros((3, 2, 2 * d - 1))
+        for r in range(3):
+            c = comps[r]
+            xa, ya = c[0][1].contiguous(), c[0][2].contiguous()
+            xb = c[1][1].contiguous() if len(c) > 1 else None
+            yb = c[1][2].contiguous() if len(c) > 1 else None
+            call("r3_vfy_level_fold", r, ptr(xa), ptr(xb), ptr(ya), ptr(yb), n, d,
+                 ptr(acc[r, 0]), ptr(acc[r, 1]), stream())
+        red = grvec.reduce_poly_rows(acc, gr.mod, gr.ell)
+        folds = {r: (red[2 * r:2 * r + 1], red[2 * r + 1:2 * r + 2]) for r in range(3)}
+    rnd = _round_joint(sess, gr, rows, {r: (folds[r][0], folds[r][1], slots[r][2], slots[r][3]) for r in range(3)})
+    q = rnd[0][2]
+    # every component's line evaluation in one launch: P0 total, P1 s1,
+    # P2 s2 (x and y), m once
+    srcs = [(0, "total", "x", x0.mask.total), (0, "total", "y", y0.mask.total),
+            (1, "s1", "x", x1.mask.s1), (1, "s1", "y", y1.mask.s1),
+            (2, "s2", "x", x2.mask.s2), (2, "s2", "y", y2.mask.s2),
+            (1, "m", "x", x1.m), (1, "m", "y", y1.m)]
+    hs = [_Halves(t) for *_, t in srcs]
+    res = grvec.rows_times2_batch([(H.ev, H.od, H.n0, H.n1) for H in hs], q.M_one_m, q.M_ze, gr.ell)
+    o = {(r, k, side): v for (r, k, side, _), v in zip(srcs, res)}
+    mx, my = o[(1, "m", "x")], o[(1, "m", "y")]
+    out = {}
+    for r, (xs, ys) in ((0, (x0, y0)), (1, (x1, y1)), (2, (x2, y2))):
+        k = ("total", "s1", "s2")[r]
+        m_x, m_y = (None, None) if r == 0 else (mx, my)
+        xo = MVal(AShare(gr, r, **{k: o[(r, k, "x")]}, p0_halves=xs.mask.p0_halves), m_x)
+        yo = MVal(AShare(gr, r, **{k: o[(r, k, "y")]}, p0_halves=ys.mask.p0_halves), m_y)
+        out[r] = (xo, yo, rnd[r][0])
+    return out
+
+
 def reduce_dimension(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
     """Halve the triple (verify.py:215-241): pad odd lengths with a zero lane,
     h(1), h(2) by inner products, h(0) = z - h(1), evaluate at 2*zeta."""
+    if _rdim_joint_ok(party, xs, gr):
+        return _reduce_dimension_joint(party, xs, ys, z, gr, zeta)
     role = party.role
     names = [k for k in ("s1", "s2", "total") if getattr(xs.mask, k) is not None]
     X = {k: _Halves(getattr(xs.mask, k)) for k in names}
