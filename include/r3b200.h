@@ -400,6 +400,19 @@ int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int d, uint64_t* const* out, uint64_t mask,
                         void* stream);
 
+/* The local arithmetic of one verification reduction round for all three
+ * simulated parties (gates.py:52-177 for the h(1) / h(2) vfy.dot gates of
+ * single GR elements, sharing.py:364-420 for the opened even point 2 zeta):
+ * F0/F1/F2 the parties' two folds (2 x d each, contiguous rows), d01 the
+ * 01-stream draws (om1.s1, g1.s1, om2.s1, g2.s1), d02 the 02-stream draws
+ * (om1.s2, om2.s2), zs1 / zs2 / zm zeta's shares; out (14 x d): om_tot[2],
+ * Gamma - s1 [2], leg1[2], leg2[2], m[2], 2 zeta.s1, 2 zeta.s2, 2 zeta.m,
+ * ze = 2 zeta. */
+int r3_vfy_round(int d, const uint64_t* F0, const uint64_t* F1, const uint64_t* F2,
+                 const uint64_t* d01, const uint64_t* d02, const uint64_t* zs1,
+                 const uint64_t* zs2, const uint64_t* zm, uint64_t* out, uint64_t mask,
+                 void* stream);
+
 /* ---- packed GF(2^d) verification of boolean multiplication logs ----
  * Over the boolean ring the verification ring is GR(2, d) = GF(2^d) (d <= 32);
  * the reference multiplies its (n, d) 0/1 words on bit-packed words

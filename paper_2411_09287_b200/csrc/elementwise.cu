@@ -456,3 +456,53 @@ extern "C" int r3_mul_leg(int role, int64_t n, int64_t lanes, const uint64_t* mx
                                             (const u64*)g, (u64*)out, mask);
   return check_launch("r3_mul_leg");
 }
+
+// ---------------------------------------------------------------------------
+// The local arithmetic of one verification reduction round for all three
+// simulated parties (verify._round_joint; gates.py:52-177 for the two vfy.dot
+// gates of single GR elements, sharing.py:364-420 for the opened even point):
+//   om_tot[g] = om_s1[g] + om_s2[g]                 (P0's output-mask sum)
+//   g_s2[g]   = F0[g] + om_tot[g] - g_s1[g]         (P0 -> P2: Gamma - s1)
+//   leg1[g]   = F1[g] + g_s1[g],  leg2[g] = F2[g] + g_s2[g],  m[g] = leg1 + leg2
+//   S1 = 2 zeta.s1, S2 = 2 zeta.s2, M = 2 zeta.m, ze = M - S1 - S2
+// for the gates g = 0, 1; d01 rows = (om1.s1, g1.s1, om2.s1, g2.s1), d02 rows =
+// (om1.s2, om2.s2).  out rows: om_tot[2], g_s2[2], leg1[2], leg2[2], m[2], S1,
+// S2, M, ze (14 rows of d words).  One thread per coefficient.
+__global__ void vfy_round_kernel(int d, const u64* __restrict__ F0, const u64* __restrict__ F1,
+                                 const u64* __restrict__ F2, const u64* __restrict__ d01,
+                                 const u64* __restrict__ d02, const u64* __restrict__ zs1,
+                                 const u64* __restrict__ zs2, const u64* __restrict__ zm, u64* __restrict__ out,
+                                 u64 mask) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d) return;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const u64 os1 = d01[(2 * g) * d + k], gs1 = d01[(2 * g + 1) * d + k], os2 = d02[g * d + k];
+    const u64 tot = os1 + os2;
+    const u64 gs2 = F0[g * d + k] + tot - gs1;
+    const u64 l1 = F1[g * d + k] + gs1, l2 = F2[g * d + k] + gs2;
+    out[(0 + g) * d + k] = tot & mask;
+    out[(2 + g) * d + k] = gs2 & mask;
+    out[(4 + g) * d + k] = l1 & mask;
+    out[(6 + g) * d + k] = l2 & mask;
+    out[(8 + g) * d + k] = (l1 + l2) & mask;
+  }
+  const u64 s1 = 2 * zs1[k], s2 = 2 * zs2[k], m = 2 * zm[k];
+  out[10 * d + k] = s1 & mask;
+  out[11 * d + k] = s2 & mask;
+  out[12 * d + k] = m & mask;
+  out[13 * d + k] = (m - s1 - s2) & mask;
+}
+
+extern "C" int r3_vfy_round(int d, const uint64_t* F0, const uint64_t* F1, const uint64_t* F2, const uint64_t* d01,
+                            const uint64_t* d02, const uint64_t* zs1, const uint64_t* zs2, const uint64_t* zm,
+                            uint64_t* out, uint64_t mask, void* stream) {
+  if (d < 1 || d > 1024 || !F0 || !F1 || !F2 || !d01 || !d02 || !zs1 || !zs2 || !zm || !out) {
+    set_error("r3_vfy_round: bad arguments");
+    return R3_ERR_ARG;
+  }
+  vfy_round_kernel<<<(d + 127) / 128, 128, 0, as_stream(stream)>>>(
+      d, (const u64*)F0, (const u64*)F1, (const u64*)F2, (const u64*)d01, (const u64*)d02, (const u64*)zs1,
+      (const u64*)zs2, (const u64*)zm, (u64*)out, mask);
+  return check_launch("r3_vfy_round");
+}

@@ -321,13 +321,17 @@ def _round_joint(sess, gr: Ring, rows: int, slots: dict) -> dict:
     d02 = P[0].prg("02", "sha").draw_gr(2, ell, gr.mod)          # om1.s2, om2.s2
     P[1].prg("01", "sha").draw_gr(4, ell, gr.mod)
     P[2].prg("02", "sha").draw_gr(2, ell, gr.mod)
-    om_s1, g_s1, om_s2 = d01[0::2], d01[1::2], d02
-    om_tot = grvec.add(om_s1, om_s2, ell)
-    F0, F1, F2 = torch.cat([f01, f02]), torch.cat([f11, f12]), torch.cat([f21, f22])
-    g_s2 = grvec.sub(grvec.add(F0, om_tot, ell), g_s1, ell)      # P0 -> P2: Gamma - s1
-    leg1 = grvec.add(F1, g_s1, ell)
-    leg2 = grvec.add(F2, g_s2, ell)
-    m = grvec.add(leg1, leg2, ell)
+    om_s1, om_s2 = d01[0::2], d02
+    # every party's local arithmetic of the round in one launch (r3_vfy_round)
+    cat2 = lambda a, b: torch.cat([a, b]) if a.is_contiguous() and b.is_contiguous() else \
+        torch.cat([a.contiguous(), b.contiguous()])
+    F0, F1, F2 = cat2(f01, f02), cat2(f11, f12), cat2(f21, f22)
+    blk = empty((14, d))
+    call("r3_vfy_round", d, ptr(F0), ptr(F1), ptr(F2), ptr(d01.contiguous()), ptr(d02.contiguous()),
+         ptr(zt0.mask.s1.contiguous()), ptr(zt0.mask.s2.contiguous()), ptr(zt1.m.contiguous()), ptr(blk),
+         gr.mask, stream())
+    om_tot, g_s2, leg1, leg2, m = blk[0:2], blk[2:4], blk[4:6], blk[6:8], blk[8:10]
+    S1, S2, M, ze = blk[10:11], blk[11:12], blk[12:13], blk[13:14]
     for g in range(2):
         gid = gids[0][g]
         P[0].send(2, f"sha.vfy.dot.gamma.{gid}", g_s2[g:g + 1], gr, cls=OFFLINE, site="vfy.dot.gamma", gate=gid)
@@ -339,9 +343,6 @@ def _round_joint(sess, gr: Ring, rows: int, slots: dict) -> dict:
         P[2].recv(1, f"{l2}.leg1", gr, 1)
     # open ze = 2 zeta (sharing.rec, style "challenge"): P0's halves stand
     # for P1's s1 / P2's s2, P1's m for P2's
-    two = lambda a: grvec.ew(grvec.MUL, a, 2, gr.mask)
-    S1, S2, M = two(zt0.mask.s1), two(zt0.mask.s2), two(zt1.m)
-    ze = grvec.sub3(M, S1, S2, ell)
     tags = [f"vfy.zeta#{p.next_id('rec')}" for p in P]
     L = lambda r, leg: f"rec.{tags[r]}.{leg}"
     P[0].send(2, L(0, "r1"), S1, gr, cls=AUX)

@@ -68,7 +68,10 @@ def main():
             tl.parked = parked() + time.perf_counter() - t0
     runtime._Baton.yield_to_scheduler = y
     for mod, names in ((verify, ["_gr_dot_folded", "_open_challenge", "_recombine", "_quad", "_level_folds_fused",
-                                 "_level_line_evals", "reduce_dimension", "check_inner_product", "_dotsum_terms"]),
+                                 "_level_line_evals", "reduce_dimension", "check_inner_product", "_dotsum_terms",
+                                 "_round_joint", "_rdim_compute", "_folds16_all", "_reduction_round"]),
+                       (runtime.Party, ["send", "recv", "send_digest", "check_digest", "round_barrier"]),
+                       (runtime.Session, ["joint", "defer_check"]),
                        (gates, ["prepare_gate", "dot_finish"]),
                        (sharing, ["sha_random", "sha_input"]),
                        (_lib, ["call", "empty", "zeros"]),
