@@ -1186,9 +1186,99 @@ def _line_eval(H: _Halves, Ms, gr: Ring) -> torch.Tensor:
 def _rdim_joint_ok(party, xs: MVal, gr: Ring) -> bool:
     if gr.d not in (16, 64) or not _joint_ok(party):
         return False
+    return _rdim_shapes_ok(party, xs)
+
+
+def _rdim_shapes_ok(party, xs: MVal) -> bool:
+    """The honest tail shapes every party can decide alone: P0 holds only
+    the mask sums of its vectors, P1 / P2 their half and m."""
     if party.role == 0:
         return xs.mask.total is not None and xs.mask.s1 is None
     return xs.m is not None
+
+
+def _check_joint(sess, gr: Ring, slots: dict):
+    """check_inner_product (Pi_vdot, verify.py:244-263) for all three parties
+    in one rendezvous (honest joint sessions): the x' = alpha x gate
+    (vfy.amul, n lanes), the vfy.dot gate of the n + 1 pairs
+    ((x', alpha), (y, -z)) and the opening of delta (style "aux"), with every
+    party's draws, messages (labels, classes, per-sender order) and values
+    as in gate-by-gate execution.  Returns the zero test's device count."""
+    P = sess.parties
+    ell, d, mod = gr.ell, gr.d, gr.mod
+    (x0, y0, z0, a0), (x1, y1, z1, a1), (x2, y2, z2, a2) = (slots[r] for r in range(3))
+    n = x0.mask.total.shape[0]
+    X0, X1s, X1m, X2s, X2m = x0.mask.total, x1.mask.s1, x1.m, x2.mask.s2, x1.m
+    As1, As2, At, Am = a0.mask.s1, a0.mask.s2, a0.mask.total, a1.m
+    # -- gate vfy.amul (lanes n): draws in stream order per party
+    gid1 = [p.next_id("vfy.amul") for p in P]
+    d01 = P[0].prg("01", "sha").draw_gr(2 * n, ell, mod)     # om.s1 (n), g.s1 (n)
+    d02 = P[0].prg("02", "sha").draw_gr(n, ell, mod)         # om.s2
+    P[1].prg("01", "sha").draw_gr(2 * n, ell, mod)
+    P[2].prg("02", "sha").draw_gr(n, ell, mod)
+    om_s1, g_s1, om_s2 = d01[:n], d01[n:], d02
+    om_tot = grvec.add(om_s1, om_s2, ell)
+    g_s2 = grvec.sub(grvec.add(grvec.gr_mul(X0, At, ell, mod), om_tot, ell), g_s1, ell)   # Gamma - s1
+    # P1: -(x.m alpha.s1) - (alpha.m x.s1) + Gamma.s1; P2: x.m (alpha.m - alpha.s2) - alpha.m x.s2 + Gamma.s2
+    leg1 = grvec.sub3(g_s1, grvec.gr_mul(X1m, As1, ell, mod), grvec.gr_mul(X1s, Am, ell, mod), ell)
+    leg2 = grvec.sub(grvec.add(grvec.gr_mul(X2m, grvec.sub(Am, As2, ell), ell, mod), g_s2, ell),
+                     grvec.gr_mul(X2s, Am, ell, mod), ell)
+    mx = grvec.add(leg1, leg2, ell)
+    P[0].send(2, f"sha.vfy.amul.gamma.{gid1[0]}", g_s2, gr, cls=OFFLINE, site="vfy.amul.gamma", gate=gid1[0])
+    P[2].recv(0, f"sha.vfy.amul.gamma.{gid1[2]}", gr, n)
+    P[1].send(2, f"vfy.amul.mz.{gid1[1]}.leg1", leg1, gr, cls=PAYLOAD, site="vfy.amul.mz", gate=gid1[1])
+    P[2].send(1, f"vfy.amul.mz.{gid1[2]}.leg2", leg2, gr, cls=AUX, site="vfy.amul.mz", gate=gid1[2])
+    P[1].recv(2, f"vfy.amul.mz.{gid1[1]}.leg2", gr, n)
+    P[2].recv(1, f"vfy.amul.mz.{gid1[2]}.leg1", gr, n)
+    # -- gate vfy.dot over the n + 1 pairs (x', alpha) . (y, -z)
+    cat = lambda a, b: torch.cat([a, b])
+    pxt, pyt = cat(om_tot, At), cat(y0.mask.total, grvec.vneg(z0.mask.total, ell))
+    px1, py1 = cat(om_s1, As1), cat(y1.mask.s1, grvec.vneg(z1.mask.s1, ell))
+    px2, py2 = cat(om_s2, As2), cat(y2.mask.s2, grvec.vneg(z2.mask.s2, ell))
+    pxm, pym = cat(mx, Am), cat(y1.m, grvec.vneg(z1.m, ell))
+    rows = n + 1
+    acc = grvec.zeros((3, 2 * d - 1))
+    L = grvec.lin
+    grvec.dotsum_add(acc[0], L((1, pxt)), L((1, pyt)), rows, d)                     # P0 cross
+    grvec.dotsum_add(acc[1], L((-1, pxm)), L((1, py1)), rows, d)                    # P1 legs
+    grvec.dotsum_add(acc[1], L((-1, pym)), L((1, px1)), rows, d)
+    grvec.dotsum_add(acc[2], L((1, pxm)), L((1, pym), (-1, py2)), rows, d)          # P2 legs
+    grvec.dotsum_add(acc[2], L((-1, px2)), L((1, pym)), rows, d)
+    red = grvec.reduce_poly_rows(acc, mod, ell)
+    gid2 = [p.next_id("vfy.dot") for p in P]
+    e01 = P[0].prg("01", "sha").draw_gr(2, ell, mod)          # om2.s1, g2.s1
+    e02 = P[0].prg("02", "sha").draw_gr(1, ell, mod)          # om2.s2
+    P[1].prg("01", "sha").draw_gr(2, ell, mod)
+    P[2].prg("02", "sha").draw_gr(1, ell, mod)
+    om2_s1, g2_s1, om2_s2 = e01[0:1], e01[1:2], e02
+    om2_tot = grvec.add(om2_s1, om2_s2, ell)
+    g2_s2 = grvec.sub(grvec.add(red[0:1], om2_tot, ell), g2_s1, ell)
+    l1 = grvec.add(red[1:2], g2_s1, ell)
+    l2 = grvec.add(red[2:3], g2_s2, ell)
+    dm = grvec.add(l1, l2, ell)
+    P[0].send(2, f"sha.vfy.dot.gamma.{gid2[0]}", g2_s2, gr, cls=OFFLINE, site="vfy.dot.gamma", gate=gid2[0])
+    P[2].recv(0, f"sha.vfy.dot.gamma.{gid2[2]}", gr, 1)
+    P[1].send(2, f"vfy.dot.mz.{gid2[1]}.leg1", l1, gr, cls=PAYLOAD, site="vfy.dot.mz", gate=gid2[1])
+    P[2].send(1, f"vfy.dot.mz.{gid2[2]}.leg2", l2, gr, cls=PAYLOAD, site="vfy.dot.mz", gate=gid2[2])
+    P[1].recv(2, f"vfy.dot.mz.{gid2[1]}.leg2", gr, 1)
+    P[2].recv(1, f"vfy.dot.mz.{gid2[2]}.leg1", gr, 1)
+    # -- open delta (sharing.rec, style "aux": every leg auxiliary)
+    tags = [f"vfy.delta#{p.next_id('rec')}" for p in P]
+    T = lambda r, leg: f"rec.{tags[r]}.{leg}"
+    P[0].send(2, T(0, "r1"), om2_s1, gr, cls=AUX)
+    P[0].send(1, T(0, "r2"), om2_s2, gr, cls=AUX)
+    P[1].send(0, T(1, "m"), dm, gr, cls=AUX)
+    P[1].send_digest(2, T(1, "r1"), om2_s1, gr)
+    P[2].send_digest(0, T(2, "m"), dm, gr)
+    P[2].send_digest(1, T(2, "r2"), om2_s2, gr)
+    m0 = P[0].recv(1, T(0, "m"), gr, 1)
+    P[0].check_digest(2, T(0, "m"), m0, gr, f"rec {tags[0]} m")
+    s2_1 = P[1].recv(0, T(1, "r2"), gr, 1)
+    P[1].check_digest(2, T(1, "r2"), s2_1, gr, f"rec {tags[1]} r2")
+    s1_2 = P[2].recv(0, T(2, "r1"), gr, 1)
+    P[2].check_digest(1, T(2, "r1"), s1_2, gr, f"rec {tags[2]} r1")
+    bad = grvec.count_nonequal(grvec.sub3(dm, om2_s1, om2_s2, ell))
+    return {0: bad, 1: bad, 2: bad}
 
 
 def _reduce_dimension_joint(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, zeta: MVal):
@@ -1337,6 +1427,14 @@ def _reduce_dimension_small(party, xs, ys, z, gr, zeta):
 def check_inner_product(party, xs: MVal, ys: MVal, z: MVal, gr: Ring, alpha: MVal) -> bool:
     """Pi_vdot (verify.py:244-263): x' = alpha * x, fold (alpha, -z) in as
     the last pair, open the combination, accept iff it is zero."""
+    if gr.mod is not None and _joint_ok(party) and _rdim_shapes_ok(party, xs):
+        key = ("check", party.next_id("_joint.check"))
+        bad = party.sess.joint(key, party.role, (xs, ys, z, alpha),
+                               lambda slots: _check_joint(party.sess, gr, slots))
+        party.round_barrier()
+        if getattr(party, "_deferred_verdicts", None) is not None:
+            return bad
+        return int(bad.item()) == 0
     n = xs.lanes
     bcast = lambda a: a.expand((n,) + tuple(a.shape[1:]))
     alpha_n = MVal(alpha.mask._map(bcast), None if alpha.m is None else bcast(alpha.m), alpha.sealed)

@@ -18,7 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2411_09287_b200 import _lib, gates, grvec, runtime, sharing, verify  # noqa: E402
+from paper_2411_09287_b200 import _lib, gates, grvec, nonlinear, runtime, sharing, verify  # noqa: E402
 from paper_2411_09287_b200.runtime import Session  # noqa: E402
 
 tl = threading.local()
@@ -69,7 +69,11 @@ def main():
     runtime._Baton.yield_to_scheduler = y
     for mod, names in ((verify, ["_gr_dot_folded", "_open_challenge", "_recombine", "_quad", "_level_folds_fused",
                                  "_level_line_evals", "reduce_dimension", "check_inner_product", "_dotsum_terms",
-                                 "_round_joint", "_rdim_compute", "_folds16_all", "_reduction_round"]),
+                                 "_round_joint", "_rdim_compute", "_folds16_all", "_reduction_round",
+                                 "verify_session", "batch_verify_muls", "batch_verify_dots", "_compress_reduce_first",
+                                 "_reduce_second_from_base", "_verify_muls_gf2", "_verify_tail", "prepare_verification",
+                                 "_base_fold", "_powers", "_l2_tables"]),
+                       (nonlinear, ["relu_prepare", "relu_online"]),
                        (runtime.Party, ["send", "recv", "send_digest", "check_digest", "round_barrier"]),
                        (runtime.Session, ["joint", "defer_check"]),
                        (gates, ["prepare_gate", "dot_finish"]),
@@ -91,7 +95,7 @@ def main():
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / reps
     print(f"{kind} 2^{lg}: {1e3 * wall:.1f} ms per session (instrumented)")
-    for k, v in own.most_common(30):
+    for k, v in own.most_common(45):
         print(f"  {1e3 * v / reps:8.2f} ms  {cnt[k] / reps:7.0f} calls  {1e6 * v / max(1, cnt[k]):6.1f} us/call  {k}")
 
 
