@@ -51,7 +51,7 @@ def main():
     if kind.startswith("relu"):
         xh = torch.from_numpy(np.trunc(np.random.default_rng(1).normal(0, 4, N) * 2 ** 16).astype(np.int64)).pin_memory()
         prog = bench.make_relu_program(N, 16)
-        args = (xh, True)
+        args = (xh, kind != "relu_x")          # relu_x: execution only (PRE + ONLINE)
     else:
         prog, _ = bench.make_programs(N, 64, verify.pick_r(N, 64, 64))
         args = ()
@@ -73,7 +73,10 @@ def main():
                                  "verify_session", "batch_verify_muls", "batch_verify_dots", "_compress_reduce_first",
                                  "_reduce_second_from_base", "_verify_muls_gf2", "_verify_tail", "prepare_verification",
                                  "_base_fold", "_powers", "_l2_tables"]),
-                       (nonlinear, ["relu_prepare", "relu_online"]),
+                       (nonlinear, ["relu_prepare", "relu_online", "edabits_prepare", "dabit_prepare", "_xor_arith",
+                                    "a2b", "_ripple_msb_fused", "b2a", "_bit_share", "drelu_online"]),
+                       (gates, ["dot_prepare", "mul_prepare", "mul_finish"]),
+                       (sharing, ["shc_input_mask", "shc_input_online", "rec"]),
                        (runtime.Party, ["send", "recv", "send_digest", "check_digest", "round_barrier"]),
                        (runtime.Session, ["joint", "defer_check"]),
                        (gates, ["prepare_gate", "dot_finish"]),
