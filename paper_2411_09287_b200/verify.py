@@ -1707,11 +1707,44 @@ class _FCBatch:
         self.K //= 2
 
     def materialise(self, gr: Ring):
-        """The batch's level vectors in the reference layout (lane-major)."""
+        """The batch's level vectors in the reference layout (lane-major):
+        x[(l, i)] = r^(P+l) X[m(l), i], y[(l, i)] = W[i, n(l)].  For d = 16 /
+        64 the lane power is split, r^(P+l) = r^c(n) (r^P r^a(m)): the M K
+        products X'' = r^(P+a(m)) X are formed once, then X'' times every
+        n's multiplication matrix M(r^c(n)) is ONE byte-limb u64 GEMM on the
+        tensor cores (X'' [M K x d] . [M(r^c(0)) | ... ] [d x N d], instead of
+        M N K elementwise GR products), gathered into lane order."""
         K, d = self.K, gr.d
-        p_rep = self.pw_lanes.repeat_interleave(K, dim=0)
-        xo = {k: grvec.gr_mul(t[self.lane_m].reshape(-1, d), p_rep, gr.ell, gr.mod) for k, t in self.X.items()}
         yo = {k: t[self.lane_n].reshape(-1, d).contiguous() for k, t in self.Wt.items()}
+        if d not in (16, 64):
+            p_rep = self.pw_lanes.repeat_interleave(K, dim=0)
+            xo = {k: grvec.gr_mul(t[self.lane_m].reshape(-1, d), p_rep, gr.ell, gr.mod) for k, t in self.X.items()}
+            return xo, yo
+        M, N = self.M, self.N
+        R = M * K
+        rpa = grvec.gr_mul(self.RM, self.rP, gr.ell, gr.mod).repeat_interleave(K, dim=0)    # (M K, d)
+        # B = [M(r^c(0)) | ... | M(r^c(N-1))] as K-major byte-limb tiles, built
+        # once per batch (the lane powers do not change across levels)
+        Kp, Np = max(32, d), -(-(N * d) // 64) * 64
+        bt = getattr(self, "_rn_tiles", None)
+        if bt is None:
+            # all N multiplication matrices in one product: row k of M(x) is
+            # x t^k, so M(r^c(n))[k] = r^c(n) (x) t^k for the d monomials t^k
+            eye = torch.eye(d, dtype=torch.int64, device=self.RN.device)
+            mats = grvec.gr_mul(self.RN.repeat_interleave(d, dim=0), eye.repeat(N, 1), gr.ell, gr.mod)
+            Bm = grvec.zeros((Kp, Np))
+            Bm[:d, :N * d] = mats.view(N, d, d).permute(1, 0, 2).reshape(d, N * d)
+            bt = self._rn_tiles = grvec.limb_tiles_b(Bm)
+        Rp = -(-R // 128) * 128
+        dev = rpa.device
+        idx = ((self.lane_m[:, None] * K + torch.arange(K, device=dev)[None, :]) * (Np // d)
+               + self.lane_n[:, None]).reshape(-1)
+        xo = {}
+        for k, t in self.X.items():
+            A = grvec.zeros((Rp, Kp))
+            A[:R, :d] = grvec.gr_mul(t.reshape(-1, d).contiguous(), rpa, gr.ell, gr.mod)   # r^(P+a(m)) X
+            out = grvec.u64_gemm([(grvec.limb_tiles_a(A), bt, Kp)], Rp, Np, gr.ell)       # every n in one GEMM
+            xo[k] = out.view(-1, d)[idx]
         return xo, yo
 
     def to_dense(self, gr: Ring) -> "_DenseBatch":

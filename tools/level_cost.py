@@ -72,7 +72,8 @@ def main():
                                  "_round_joint", "_rdim_compute", "_folds16_all", "_reduction_round",
                                  "verify_session", "batch_verify_muls", "batch_verify_dots", "_compress_reduce_first",
                                  "_reduce_second_from_base", "_verify_muls_gf2", "_verify_tail", "prepare_verification",
-                                 "_base_fold", "_powers", "_l2_tables"]),
+                                 "_base_fold", "_powers", "_l2_tables", "_reduce_from_base", "_powers_b",
+                                 "_base_fold_b", "_block_fold_weights", "_base_tables", "_open_challenge"]),
                        (nonlinear, ["relu_prepare", "relu_online", "edabits_prepare", "dabit_prepare", "_xor_arith",
                                     "a2b", "_ripple_msb_fused", "b2a", "_bit_share", "drelu_online"]),
                        (gates, ["dot_prepare", "mul_prepare", "mul_finish"]),
