@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--engine", default="coop", choices=["coop", "threads"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to test the N > 1 path on fewer GPUs than ranks")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-profile", action="store_true",
