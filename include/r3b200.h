@@ -400,6 +400,17 @@ int r3_vfy_line_b_const(int B, int ncomp, const uint64_t* const* yc, int64_t N,
                         int d, uint64_t* const* out, uint64_t mask,
                         void* stream);
 
+/* r3_vfy_level_fold of all three simulated parties in ONE launch (d = 64,
+ * tensor cores; honest sessions where P1 and P2 hold the same m): vectors
+ * tx / ty (P0's sums), mx / my (m), s1x / s1y (P1), s2x / s2y (P2), each N
+ * rows of 64 words; acc1[r] / acc2[r] (127 words each, zeroed here) receive
+ * party r's unreduced h(1) / h(2) folds.  The items of a K chunk are
+ * adjacent, so m is read from HBM about once for both of its parties. */
+int r3_vfy_level_fold_joint(const uint64_t* tx, const uint64_t* ty, const uint64_t* mx,
+                            const uint64_t* my, const uint64_t* s1x, const uint64_t* s1y,
+                            const uint64_t* s2x, const uint64_t* s2y, int64_t N,
+                            uint64_t* const* acc1, uint64_t* const* acc2, void* stream);
+
 /* The local arithmetic of one verification reduction round for all three
  * simulated parties (gates.py:52-177 for the h(1) / h(2) vfy.dot gates of
  * single GR elements, sharing.py:364-420 for the opened even point 2 zeta):

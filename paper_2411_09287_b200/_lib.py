@@ -110,6 +110,8 @@ _SIGS = {
                          C.c_int, C.POINTER(C.c_void_p), u64, C.c_void_p],
     "r3_vfy_l1_line_y": [C.c_int, C.POINTER(C.c_void_p), i64, i64, i64, i64, u64p, u64p,
                          C.c_int, C.POINTER(C.c_void_p), u64, C.c_void_p],
+    "r3_vfy_level_fold_joint": [u64p, u64p, u64p, u64p, u64p, u64p, u64p, u64p, i64, C.c_void_p, C.c_void_p,
+                                C.c_void_p],
     "r3_vfy_round": [C.c_int, u64p, u64p, u64p, u64p, u64p, u64p, u64p, u64p, u64p, u64, C.c_void_p],
     "r3_gfv_base_fold": [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int),
                          C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p), i64, u64p, C.c_int, C.c_uint32,

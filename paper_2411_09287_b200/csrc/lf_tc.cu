@@ -57,15 +57,23 @@ struct LfVec {
   CUtensorMap lo, hi;
 };
 
-// One leg term: x (x) (c0 y0 + c1 y1) (y1 < 0: none).
+// One leg term: x (x) (c0 y0 + c1 y1) (y1 < 0: none), added to party
+// `out`'s two folds.
 struct LfTerm {
   int x, y0, y1;
   u64 c0, c1;
+  int out;
 };
 
+// Up to the three simulated parties' terms in one launch (honest joint
+// sessions: P0 1, P1 2, P2 2 terms over 7 distinct vectors, m shared by P1
+// and P2); the items of a chunk are adjacent, so a vector read by several
+// terms comes from HBM about once.
 struct LfArgs {
-  LfVec v[4];
-  LfTerm t[2];
+  LfVec v[8];
+  LfTerm t[5];
+  u64* acc1[3];
+  u64* acc2[3];
   int nterms;
   int64_t rows, npairs, kc, nchunks;
 };
@@ -112,7 +120,7 @@ __device__ __forceinline__ void lf_accum(const uint8_t* ro, const uint8_t* re, b
 }
 
 __global__ void __launch_bounds__(LF_THREADS, 1)
-level_fold_tc_kernel(const __grid_constant__ LfArgs args, u64* __restrict__ acc1, u64* __restrict__ acc2) {
+level_fold_tc_kernel(const __grid_constant__ LfArgs args) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned by offsetting the shared array itself (keeps the shared
   // address space visible to the compiler: LDS / STS instead of generic LD / ST)
@@ -288,8 +296,8 @@ level_fold_tc_kernel(const __grid_constant__ LfArgs args, u64* __restrict__ acc1
       lf_named_sync(1, 128);
       const int t = threadIdx.x;
       if (t < 127) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(acc1 + t), (unsigned long long)red[t]);
-        atomicAdd(reinterpret_cast<unsigned long long*>(acc2 + t), (unsigned long long)red[128 + t]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(args.acc1[T.out] + t), (unsigned long long)red[t]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(args.acc2[T.out] + t), (unsigned long long)red[128 + t]);
       }
     }
   }
@@ -313,6 +321,8 @@ static bool lf_vec(LfVec& V, const uint64_t* a, int64_t rows) {
   return ok;
 }
 
+int lf_launch(LfArgs& args, int64_t N, cudaStream_t s);
+
 // Called by r3_vfy_level_fold for d == 64 (same contract).
 int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64_t* ya, const uint64_t* yb,
                   int64_t N, uint64_t* acc1, uint64_t* acc2, cudaStream_t s) {
@@ -327,17 +337,62 @@ int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64
     return R3_ERR_CUDA;
   }
   if (role == 0) {  // P0: s_x (x) s_y
-    args.t[0] = LfTerm{0, 2, -1, 1, 0};
+    args.t[0] = LfTerm{0, 2, -1, 1, 0, 0};
     args.nterms = 1;
   } else if (role == 1) {  // -(m_x s_y) - (s_x m_y)
-    args.t[0] = LfTerm{0, 3, -1, M1, 0};
-    args.t[1] = LfTerm{1, 2, -1, M1, 0};
+    args.t[0] = LfTerm{0, 3, -1, M1, 0, 0};
+    args.t[1] = LfTerm{1, 2, -1, M1, 0, 0};
     args.nterms = 2;
   } else {  // m_x (m_y - s_y) - s_x m_y
-    args.t[0] = LfTerm{0, 2, 3, 1, M1};
-    args.t[1] = LfTerm{1, 2, -1, M1, 0};
+    args.t[0] = LfTerm{0, 2, 3, 1, M1, 0};
+    args.t[1] = LfTerm{1, 2, -1, M1, 0, 0};
     args.nterms = 2;
   }
+  args.acc1[0] = reinterpret_cast<u64*>(acc1);
+  args.acc2[0] = reinterpret_cast<u64*>(acc2);
+  return lf_launch(args, N, s);
+}
+
+// All three parties in one launch: P0 total (x, y), P1 (m, s1), P2 (s2; m
+// shared with P1) -- vectors 0 tx, 1 ty, 2 mx, 3 my, 4 s1x, 5 s1y, 6 s2x, 7
+// s2y; acc1 / acc2 of party r at acc1[r] / acc2[r].
+extern "C" int r3_vfy_level_fold_joint(const uint64_t* tx, const uint64_t* ty, const uint64_t* mx,
+                                       const uint64_t* my, const uint64_t* s1x, const uint64_t* s1y,
+                                       const uint64_t* s2x, const uint64_t* s2y, int64_t N, uint64_t* const* acc1,
+                                       uint64_t* const* acc2, void* stream) {
+  if (N <= 1 || !tx || !ty || !mx || !my || !s1x || !s1y || !s2x || !s2y || !acc1 || !acc2) {
+    set_error("r3_vfy_level_fold_joint: bad arguments (N %lld)", (long long)N);
+    return R3_ERR_ARG;
+  }
+  LfArgs args{};
+  const u64 M1 = ~0ull;
+  const uint64_t* vs[8] = {tx, ty, mx, my, s1x, s1y, s2x, s2y};
+  for (int i = 0; i < 8; ++i) {
+    if (!lf_vec(args.v[i], vs[i], N)) {
+      set_error("r3_vfy_level_fold_joint: cuTensorMapEncodeTiled failed");
+      return R3_ERR_CUDA;
+    }
+  }
+  cudaStream_t s = as_stream(stream);
+  for (int r = 0; r < 3; ++r) {
+    args.acc1[r] = reinterpret_cast<u64*>(acc1[r]);
+    args.acc2[r] = reinterpret_cast<u64*>(acc2[r]);
+    if (cudaMemsetAsync(acc1[r], 0, 127 * 8, s) != cudaSuccess || cudaMemsetAsync(acc2[r], 0, 127 * 8, s) != cudaSuccess) {
+      set_error("r3_vfy_level_fold_joint: memset failed");
+      return R3_ERR_CUDA;
+    }
+  }
+  // P1's terms next to P2's (m_x / m_y shared), P0's first
+  args.t[0] = LfTerm{0, 1, -1, 1, 0, 0};        // P0: s_x (x) s_y
+  args.t[1] = LfTerm{2, 5, -1, M1, 0, 1};       // P1: -(m_x s1_y)
+  args.t[2] = LfTerm{2, 3, 7, 1, M1, 2};        // P2: m_x (m_y - s2_y)
+  args.t[3] = LfTerm{4, 3, -1, M1, 0, 1};       // P1: -(s1_x m_y)
+  args.t[4] = LfTerm{6, 3, -1, M1, 0, 2};       // P2: -(s2_x m_y)
+  args.nterms = 5;
+  return lf_launch(args, N, s);
+}
+
+int lf_launch(LfArgs& args, int64_t N, cudaStream_t s) {
   args.rows = N;
   args.npairs = (N + 1) / 2;
   int64_t nchunks = (args.npairs + LF_MAX_K - 1) / LF_MAX_K;
@@ -354,6 +409,6 @@ int level_fold_tc(int role, const uint64_t* xa, const uint64_t* xb, const uint64
   args.nchunks = nchunks;
   ensure_smem(level_fold_tc_kernel, LF_SMEM);
   const unsigned grid = unsigned(nchunks * per_chunk_items);
-  level_fold_tc_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(args, (u64*)acc1, (u64*)acc2);
+  level_fold_tc_kernel<<<grid, LF_THREADS, LF_SMEM, s>>>(args);
   return check_launch("r3_vfy_level_fold(tc)");
 }

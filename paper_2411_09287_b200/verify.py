@@ -1305,6 +1305,17 @@ def _rdim_compute(sess, gr: Ring, slots: dict) -> dict:
     if d == 16 and n >= _JOINT16_MIN_ROWS:
         folds = _folds16_all({r: {"x": [c[1].contiguous() for c in comps[r]],
                                   "y": [c[2].contiguous() for c in comps[r]]} for r in range(3)}, gr)
+    elif d == 64 and (n + 1) // 2 >= 4096:           # the tensor-core size range of r3_vfy_level_fold
+        # every party's terms in one tensor-core launch (m read once for P1
+        # and P2), one reduction
+        acc = empty((3, 2, 2 * d - 1))
+        cc = lambda t: t.contiguous()
+        Pp = C.c_void_p * 3
+        call("r3_vfy_level_fold_joint", ptr(cc(x0.mask.total)), ptr(cc(y0.mask.total)), ptr(cc(x1.m)), ptr(cc(y1.m)),
+             ptr(cc(x1.mask.s1)), ptr(cc(y1.mask.s1)), ptr(cc(x2.mask.s2)), ptr(cc(y2.mask.s2)), n,
+             Pp(*[ptr(acc[r, 0]) for r in range(3)]), Pp(*[ptr(acc[r, 1]) for r in range(3)]), stream())
+        red = grvec.reduce_poly_rows(acc, gr.mod, gr.ell)
+        folds = {r: (red[2 * r:2 * r + 1], red[2 * r + 1:2 * r + 2]) for r in range(3)}
     else:
         # one r3_vfy_level_fold per party into one accumulator block, one reduction
         acc = grvec.zeros((3, 2, 2 * d - 1))

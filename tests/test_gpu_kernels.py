@@ -616,3 +616,27 @@ def test_dot_log_folds_per_lane_match_definitions(cuda, d, n, L):
         np.testing.assert_array_equal(host(g_acc), acc, err_msg=f"acc role {role}")
         np.testing.assert_array_equal(host(g_h1)[0], h1, err_msg=f"h1 role {role}")
         np.testing.assert_array_equal(host(g_h2)[0], h2, err_msg=f"h2 role {role}")
+
+
+@pytest.mark.parametrize("N", [8193, 1 << 16])
+def test_level_fold_joint_matches_per_party(cuda, N):
+    """r3_vfy_level_fold_joint (the three parties' d = 64 dense folds in one
+    tensor-core launch, m shared by P1 and P2) against three per-party
+    r3_vfy_level_fold launches (pinned to the oracle above)."""
+    import ctypes as C
+    from paper_2411_09287_b200 import grvec, host, _lib
+    rng = np.random.default_rng(N)
+    V = {k: grvec.dev(_rand(rng, (N, 64))) for k in ("tx", "ty", "mx", "my", "s1x", "s1y", "s2x", "s2y")}
+    want = grvec.zeros((3, 2, 127))
+    args = {0: (V["tx"], None, V["ty"], None), 1: (V["mx"], V["s1x"], V["my"], V["s1y"]),
+            2: (V["mx"], V["s2x"], V["my"], V["s2y"])}
+    for r, (xa, xb, ya, yb) in args.items():
+        p = lambda t: None if t is None else t.data_ptr()
+        _lib.call("r3_vfy_level_fold", r, p(xa), p(xb), p(ya), p(yb), N, 64, want[r, 0].data_ptr(),
+                  want[r, 1].data_ptr(), _lib.stream())
+    got = grvec.dev(np.full((3, 2, 127), 0xABCD, np.uint64))
+    P3 = C.c_void_p * 3
+    _lib.call("r3_vfy_level_fold_joint", *[V[k].data_ptr() for k in ("tx", "ty", "mx", "my", "s1x", "s1y", "s2x", "s2y")],
+              N, P3(*[got[r, 0].data_ptr() for r in range(3)]), P3(*[got[r, 1].data_ptr() for r in range(3)]),
+              _lib.stream())
+    np.testing.assert_array_equal(host(got), host(want))
