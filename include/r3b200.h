@@ -350,7 +350,7 @@ int r3_vfy_base_fold_q4(int np, const int* nterms, const int64_t* coef,
                         const int* nz, const uint64_t* const* zc, const int64_t* zs,
                         int64_t N, const uint64_t* pw4, int d, uint64_t* const* acc,
                         uint64_t* const* zraw, void* stream);
-/* Base fold over blocks of eight against pw8[j] = r^(8j) (d = 64, N >= 8 *
+/* Base fold over blocks of eight against pw8[j] = r^(8j) (d = 64 or 16, N >= 8 *
  * 4096, tensor cores): acc'[a*8+b] = sum_j s^{ab}_j r^(8j) (64 x d) and
  * zraw[c*8+a] = sum_j z_c[8j+a] r^(8j) -- every accumulator the first THREE
  * reductions need (verify.py:215-241 at k = 0, 1, 2); same operand

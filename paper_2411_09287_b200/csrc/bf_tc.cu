@@ -43,15 +43,21 @@ constexpr int BF_MAX_SLOTS = 6;                 // distinct x / y / z arrays of 
 // 128 MMA rows); B = 16 two per party (256 s products: rows a < 8 and
 // a >= 8) plus ONE z item for all parties (16 features per distinct z
 // array).
-template <int B>
+// D = extension degree (table row width): 64 or 16.  The table rows of a
+// K-step are D / 16 TMA boxes; the B operand is D columns per limb plane.
+template <int B, int D = 64>
 struct BfLayout {
   static constexpr bool WIDE = B >= 8;
   static constexpr int RS = WIDE ? 2 : 3;
+  static constexpr int NBOX = D / 16;
+  static constexpr int RAW = NBOX * BF_BOX;     // one K-step of table rows
+  static constexpr int B_PLANE = D * BF_BK;
+  static constexpr int B_TILE = 8 * B_PLANE;
   static constexpr int SLOT = BF_BK * B * 8;    // one array over a K-step (TMA box, 128B swizzle)
   static constexpr int NSLOT = 6;               // B = 16: <= 4 x / y arrays, or the z item's <= 6
-  static constexpr int RAWST = (BF_RAW + (WIDE ? NSLOT * SLOT : 0) + 1023) / 1024 * 1024;
+  static constexpr int RAWST = (RAW + (WIDE ? NSLOT * SLOT : 0) + 1023) / 1024 * 1024;
   static constexpr int OFF_LIMB = RS * RAWST;
-  static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + BF_B_TILE);
+  static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + B_TILE);
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 static_assert(BfLayout<16>::SMEM <= 232448, "base fold q16 shared memory");
@@ -96,10 +102,10 @@ struct BfArgs {
 // 32 p + q).  B = 8: 64 s products + 8 nz z values per party, so a work item
 // is (K chunk, party) and the np items of one chunk are adjacent in the
 // grid (co-resident: the table rows come from HBM once, L2 for the others).
-template <int B>
+template <int B, int D>
 __global__ void __launch_bounds__(BF_THREADS, 1)
 base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
-  using L = BfLayout<B>;
+  using L = BfLayout<B, D>;
   constexpr int RS = L::RS;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned by offsetting the shared array itself (keeps the shared
@@ -107,7 +113,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sA = smem + L::OFF_LIMB;
-  uint8_t* sB = sA + BF_STAGES * BF_A_TILE;
+  uint8_t* sB = sA + BF_STAGES * BF_A_TILE;   // B tiles: L::B_TILE each
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = bars + RS;
@@ -185,12 +191,12 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
           // crosses the end of the log (the converters load those)
           const bool whole = L::WIDE && args.vec && (j0 + (kb + 1) * BF_BK) * B <= args.N;
           uint8_t* dst = sRaw + rs * L::RAWST;
-          mbar_expect_tx(&raw_full[rs], uint32_t(BF_RAW + (whole ? nsl * L::SLOT : 0)));
-          for (int c = 0; c < 4; ++c)
+          mbar_expect_tx(&raw_full[rs], uint32_t(L::RAW + (whole ? nsl * L::SLOT : 0)));
+          for (int c = 0; c < L::NBOX; ++c)
             tma_load_2d(dst + c * BF_BOX, &args.pw4, c * 16, y, &raw_full[rs]);
           if (whole)
             for (int q = 0; q < nsl; ++q)
-              tma_load_2d(dst + BF_RAW + q * L::SLOT, zitem ? &args.zmap[q] : &args.lmap[pi][q], 0,
+              tma_load_2d(dst + L::RAW + q * L::SLOT, zitem ? &args.zmap[q] : &args.lmap[pi][q], 0,
                           int(int64_t(y) * B / 16), &raw_full[rs]);
         }
       }
@@ -234,7 +240,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         staged = args.vec && (j0 + (kb + 1) * BF_BK) * B <= args.N;
         if (live && staged) {
           const BfParty& P = args.p[p];
-          const uint8_t* lg = sRaw + rs * L::RAWST + BF_RAW;
+          const uint8_t* lg = sRaw + rs * L::RAWST + L::RAW;
           // block k's 16-byte chunk ch of a slot: row k (B = 16) or k / 2
           // (B = 8, second half of the row for odd k), 128-byte swizzle
           const int rrow = B == 16 ? k : (k >> 1);
@@ -355,13 +361,15 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
         }
       } else {
         mbar_wait(&raw_full[rs], uint32_t((g / RS) & 1));
-        const uint8_t* row = sRaw + rs * L::RAWST + c * BF_BOX + k * 128;
-        const int sw = k & 7;
+        if (c < L::NBOX) {   // D = 16: one 16-coefficient chunk; the other B threads only keep the barriers
+          const uint8_t* row = sRaw + rs * L::RAWST + c * BF_BOX + k * 128;
+          const int sw = k & 7;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(row + ((q ^ sw) << 4));
-          v[2 * q] = x.x;
-          v[2 * q + 1] = x.y;
+          for (int q = 0; q < 8; ++q) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(row + ((q ^ sw) << 4));
+            v[2 * q] = x.x;
+            v[2 * q + 1] = x.y;
+          }
         }
         fence_async_smem();   // generic-proxy reads before the next TMA write (WAR)
         mbar_arrive(&raw_empty[rs]);
@@ -370,11 +378,13 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       split_limbs16(v, pk);
       if (g >= BF_STAGES) mbar_wait(&empty[st], uint32_t((g / BF_STAGES - 1) & 1));
       // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
-      uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * BF_B_TILE;
-      const int plane = isA ? BF_A_PLANE : BF_B_PLANE;
+      uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * L::B_TILE;
+      const int plane = isA ? BF_A_PLANE : L::B_PLANE;
       const uint32_t off = uint32_t(c * 512 + k * 16);
+      if (isA || c < L::NBOX) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * plane + off) = pk[i];
+        for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + i * plane + off) = pk[i];
+      }
       fence_async_smem();
       mbar_arrive(&full[st]);
     }
@@ -399,15 +409,15 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(sA + st * BF_A_TILE);
-        const uint32_t b0 = smem_u32(sB + st * BF_B_TILE);
+        const uint32_t b0 = smem_u32(sB + st * L::B_TILE);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const uint64_t ad = umma_desc(a0 + i * BF_A_PLANE, 128, 512);
 #pragma unroll
-          for (int n0 = 0; n0 < 64 * (8 - i); n0 += 256) {
-            const int nn = 64 * (8 - i) - n0 < 256 ? 64 * (8 - i) - n0 : 256;
+          for (int n0 = 0; n0 < D * (8 - i); n0 += 256) {
+            const int nn = D * (8 - i) - n0 < 256 ? D * (8 - i) - n0 : 256;
             const uint64_t bd = umma_desc(b0 + uint32_t(n0 / 16) * 512, 128, 512);
-            mma_u8(tmem + uint32_t(i * 64 + n0), ad, bd, IDESC_M128 | (uint32_t(nn >> 3) << 17),
+            mma_u8(tmem + uint32_t(i * D + n0), ad, bd, IDESC_M128 | (uint32_t(nn >> 3) << 17),
                    (kb == 0 && i == 0) ? 0u : 1u);
           }
         }
@@ -431,29 +441,29 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       if (B == 4) {
         const int p = f >> 5, q = f & 31;
         const bool live = p < args.np && (q < 16 || q < 16 + 4 * args.p[p < 3 ? p : 0].nz);
-        if (live) dst = q < 16 ? args.p[p].acc + q * 64 : args.p[p].zraw + (q - 16) * 64;
+        if (live) dst = q < 16 ? args.p[p].acc + q * D : args.p[p].zraw + (q - 16) * D;
       } else if (B == 8) {
         const BfParty& P = args.p[item_party(it)];
-        if (f < 64) dst = P.acc + f * 64;
-        else if (f < 64 + 8 * P.nz) dst = P.zraw + (f - 64) * 64;
+        if (f < 64) dst = P.acc + f * D;
+        else if (f < 64 + 8 * P.nz) dst = P.zraw + (f - 64) * D;
       } else {
         const int grp = item_group(it);
         if (grp < 2) {
-          dst = args.p[item_party(it)].acc + (128 * grp + f) * 64;
+          dst = args.p[item_party(it)].acc + (128 * grp + f) * D;
         } else if ((f >> 4) < args.nzs) {
           // z slot f / 16 feeds one or two (party, component) sums
           const int zs = f >> 4, a = f & 15;
-          dst = args.p[args.zdst_p[zs][0]].zraw + (16 * args.zdst_c[zs][0] + a) * 64;
-          if (args.zdst_n[zs] > 1) dst2 = args.p[args.zdst_p[zs][1]].zraw + (16 * args.zdst_c[zs][1] + a) * 64;
+          dst = args.p[args.zdst_p[zs][0]].zraw + (16 * args.zdst_c[zs][0] + a) * D;
+          if (args.zdst_n[zs] > 1) dst2 = args.p[args.zdst_p[zs][1]].zraw + (16 * args.zdst_c[zs][1] + a) * D;
         }
       }
       const bool live = dst != nullptr;
       const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 8) {
+      for (int c0 = 0; c0 < D; c0 += 8) {
         uint32_t v[8][8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * 64 + c0), v[s]);
+        for (int s = 0; s < 8; ++s) tmem_ld8(lane_base + uint32_t(s * D + c0), v[s]);
         tmem_wait_ld();
         if (live) {
 #pragma unroll
@@ -482,7 +492,7 @@ using namespace r3;
 
 namespace {
 
-template <int B>
+template <int B, int D = 64>
 int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const uint64_t* const* xc,
                         const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
                         int64_t N, const uint64_t* pw, uint64_t* const* acc, uint64_t* const* zraw,
@@ -565,7 +575,7 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
           return R3_ERR_CUDA;
         }
   }
-  if (!make_rows_tmap(&args.pw4, pw, nblk, 64, BF_BK, 64)) {
+  if (!make_rows_tmap(&args.pw4, pw, nblk, D, BF_BK, D)) {
     set_error("%s: cuTensorMapEncodeTiled failed", what);
     return R3_ERR_CUDA;
   }
@@ -582,8 +592,8 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
   items = (nblk + kc - 1) / kc * per;
   args.kc = kc;
   const unsigned grid = unsigned(items < num_sms() ? items : num_sms() / per * per);
-  ensure_smem(base_fold_tc_kernel<B>, BfLayout<B>::SMEM);
-  base_fold_tc_kernel<B><<<grid, BF_THREADS, BfLayout<B>::SMEM, s>>>(args);
+  ensure_smem(base_fold_tc_kernel<B, D>, BfLayout<B, D>::SMEM);
+  base_fold_tc_kernel<B, D><<<grid, BF_THREADS, BfLayout<B, D>::SMEM, s>>>(args);
   return check_launch(what);
 }
 
@@ -607,7 +617,7 @@ int base_fold_wide(int np, const int* nterms, const int64_t* coef, const uint64_
                    const uint64_t* const* yc, const int* nz, const uint64_t* const* zc, const int64_t* zs,
                    int64_t N, const uint64_t* pw, int d, uint64_t* const* acc, uint64_t* const* zraw,
                    void* stream, const char* what) {
-  if (np < 1 || np > 3 || d != 64 || N < int64_t(B) * 4096 || (uintptr_t(pw) & 15) || !nterms || !nz) {
+  if (np < 1 || np > 3 || (d != 64 && d != 16) || N < int64_t(B) * 4096 || (uintptr_t(pw) & 15) || !nterms || !nz) {
     set_error("%s: bad arguments (np %d, d %d, N %lld)", what, np, d, (long long)N);
     return R3_ERR_ARG;
   }
@@ -617,13 +627,14 @@ int base_fold_wide(int np, const int* nterms, const int64_t* coef, const uint64_
       set_error("%s: bad terms / z count for party %d", what, q);
       return R3_ERR_ARG;
     }
-    if (cudaMemsetAsync(acc[q], 0, size_t(B) * B * 64 * 8, s) != cudaSuccess ||
-        (nz[q] > 0 && cudaMemsetAsync(zraw[q], 0, size_t(nz[q]) * B * 64 * 8, s) != cudaSuccess)) {
+    if (cudaMemsetAsync(acc[q], 0, size_t(B) * B * d * 8, s) != cudaSuccess ||
+        (nz[q] > 0 && cudaMemsetAsync(zraw[q], 0, size_t(nz[q]) * B * d * 8, s) != cudaSuccess)) {
       set_error("%s: memset failed", what);
       return R3_ERR_CUDA;
     }
   }
-  return base_fold_tc_launch<B>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, acc, zraw, s, what);
+  return d == 64 ? base_fold_tc_launch<B, 64>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, acc, zraw, s, what)
+                 : base_fold_tc_launch<B, 16>(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, acc, zraw, s, what);
 }
 
 }  // namespace

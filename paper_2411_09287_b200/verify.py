@@ -721,11 +721,11 @@ _BASE_BLOCK_CAP = int(os.environ.get("R3_BASE_BLOCK", "16"))
 
 
 def _base_block(comp: _Compressed, R: int, gr: Ring) -> int:
-    """Block size of the multi-level base reduction of a d = 64
+    """Block size of the multi-level base reduction of a d = 64 / 16
     multiplication log: 16 (four reductions from the base log, dense tail
     from N/16 rows) or 8 (three, N/8), each on the tensor cores once the log
     has >= 4096 blocks; 0 = the two-level form."""
-    if gr.d != 64:
+    if gr.d not in (16, 64):
         return 0
     cap = _BASE_BLOCK_CAP
     if cap < 16 and R >= 3 and comp.N >= 8 * 4096:

@@ -383,8 +383,8 @@ def test_level_fold16_tc_matches_cuda_core(cuda, N):
 
 @pytest.mark.parametrize("N", [(1 << 16) + 37, 1 << 20])
 @pytest.mark.parametrize("joint", [True, False])
-@pytest.mark.parametrize("B", [4, 8, 16])
-def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B):
+@pytest.mark.parametrize("B,d", [(4, 64), (8, 64), (16, 64), (8, 16), (16, 16)])
+def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B, d):
     """r3_vfy_base_fold_q4 on the tensor cores (bf_tc.cu, d = 64) -- the
     headline's base fold -- against its definition
         acc'[a*4+b] = sum_j s^{ab}_j pw4[j],  zraw[c*4+a] = sum_j z_c[4j+a] pw4[j]
@@ -397,10 +397,10 @@ def test_base_fold_q4_tensor_core_matches_definitions(cuda, N, joint, B):
     B = 8 is r3_vfy_base_fold_q8 (blocks of eight against r^(8j): the 64
     accumulators of the first three reductions; one work item per party and
     K-chunk), B = 16 r3_vfy_base_fold_q16 (256 accumulators, three feature
-    groups per party and K-chunk)."""
+    groups per party and K-chunk); d = 16 runs the same kernels with
+    16-coefficient table rows (B operand of 16 columns per limb plane)."""
     import ctypes as C
     from paper_2411_09287_b200 import grvec, host, _lib
-    d = 64
     rng = np.random.default_rng(N + 3)
     nblk = (N + B - 1) // B
     pw4 = _rand(rng, (nblk, d))

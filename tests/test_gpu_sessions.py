@@ -87,8 +87,8 @@ def test_session_rerun_after_discarded_logs(cuda):
     assert all(Session(seed=9).run(verified))
 
 
-@pytest.mark.parametrize("N,R", [((1 << 16) + 5, 5), ((1 << 15) + 3, 3)])
-def test_base_reduction_block_sizes_give_identical_transcripts(cuda, N, R, monkeypatch):
+@pytest.mark.parametrize("N,R,d", [((1 << 16) + 5, 5, 64), ((1 << 15) + 3, 3, 64), ((1 << 16) + 5, 5, 16)])
+def test_base_reduction_block_sizes_give_identical_transcripts(cuda, N, R, d, monkeypatch):
     """The d = 64 verification of one multiplication log through the
     two-level base reduction (blocks of four, B = 0), three levels from
     the base (B = 8) and four (B = 16, where the log is large enough): every
@@ -109,13 +109,13 @@ def test_base_reduction_block_sizes_give_identical_transcripts(cuda, N, R, monke
         x = shc_random(party, N, ring)
         y = shc_random(party, N, ring)
         g = gates.mul_prepare(party, x.mask, y.mask, N)
-        verify.prepare_verification(party, d=64, r_max=R)
+        verify.prepare_verification(party, d=d, r_max=R)
         party.round_barrier()
         party.enter_phase(Phase.ONLINE)
         z = gates.mul_finish(party, g, x, y)
         party.round_barrier()
         party.enter_phase(Phase.POST)
-        return z, verify.batch_verify_muls(party, 64, d=64, R=R)
+        return z, verify.batch_verify_muls(party, 64, d=d, R=R)
 
     orig = verify._base_block
     runs = {}
