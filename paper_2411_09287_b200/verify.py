@@ -1907,7 +1907,10 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
         zg = _sum_lanes(MVal(zl.mask._map(lambda a: grvec.gr_mul(a, p, gr.ell, gr.mod)),
                              None if zl.m is None else grvec.gr_mul(zl.m, p, gr.ell, gr.mod)), gr)
         z_acc = zg if z_acc is None else z_acc + zg
-        split = _FCBatch.split(b) if isinstance(b, MatmulBatchRec) else None
+        # an odd dot dimension (conv 5x5 over one channel: K = 25) gains
+        # nothing from the factorised form; its base-form dense batch never
+        # lifts levels 0 and 1 (a quarter of the lifted level-0 bytes)
+        split = _FCBatch.split(b) if isinstance(b, MatmulBatchRec) and b.K % 2 == 0 else None
         if split is not None:
             parts.append(_FCBatch(b, role, gr, pos, pw, split))
         else:
