@@ -228,6 +228,14 @@ int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows,
                       const uint64_t* const* Ms, uint64_t* const* outs, int q,
                       uint64_t mask, void* stream);
 
+/* out[j] = sum_{a < 16} p[16 j + a] K[a] (K: 16 x 64 words, p: rows x 16
+ * words, 16-byte aligned) as a K = 16 byte-limb GEMM on the tensor cores:
+ * the level-4 y-side rows kappa_a y_(16j + a) of a multiplication log with
+ * blocks of sixteen (verify.py:237-240 applied four times from the base
+ * log; the arithmetic of r3_vfy_line_b_const with B = 16, d = 64). */
+int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
+                        uint64_t* out, uint64_t mask, void* stream);
+
 /* Dense-level leg folds for d = 16 of up to four leg terms (several
  * simulated parties) in one tensor-core pass: term k (x, y' = c0 y0 + c1 y1,
  * (N, 16) row-major, y1 may be null) adds its h(1) = sum o_x (x) o_y' and

@@ -37,7 +37,10 @@ constexpr int TC_KH = 32;           // K per unit (one MMA K-step of kind::i8)
 // accumulator.  Each A plane is read by the tensor core once per unit and
 // output half instead of once per (i, j) limb product.
 // ---------------------------------------------------------------------------
-constexpr int W_EPI = 4, W_CONV = 8;
+// eight epilogue warps: two per TMEM lane quadrant, each recombining half
+// of a piece's columns (four warps left the tensor pipe ~34 % active in the
+// table build: the epilogue, not the MMA, paced the TMEM double buffer)
+constexpr int W_EPI = 8, W_CONV = 8;
 constexpr int WS_THREADS = (W_EPI + W_CONV + 2) * 32;
 constexpr int RAW_BYTES = TC_ROWS * TC_KH * 8;           // 32 KB
 constexpr int LIMB_PLANE = TC_ROWS * TC_KH;              // 4 KB
@@ -237,7 +240,7 @@ gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ 
     // (16-lane x 8-column loads: 4 threads per row, so every store writes
     // 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes)
     uint32_t ph[2] = {0, 0};
-    const int quad = warp & 3;
+    const int quad = warp & 3, grp = warp >> 2;
     const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int j = mm2_job(J, t);
@@ -249,7 +252,7 @@ gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ 
         ph[h] ^= 1;
         tc_fence_after();
 #pragma unroll 1
-        for (int it = 0; it < 2 * (DB_HALF / 8); ++it) {
+        for (int it = grp * (DB_HALF / 8); it < (grp + 1) * (DB_HALF / 8); ++it) {
           const int lg = it & 1, c0 = 8 * (it >> 1);
           const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * h + c0);
           uint32_t v[8][4];
@@ -296,6 +299,8 @@ struct MqArgs {
   const u64* M[MQ_MAX];
   u64* out[MQ_MAX];
   int q;
+  int k16;   // 1: P rows hold 16 words and each M is 16 x 64 (K = 16: one
+             // K-unit per tile, the unit's upper 16 K columns meet zero rows of B)
 };
 
 __global__ void __launch_bounds__(WS_THREADS, 1)
@@ -317,13 +322,14 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Q = args.q;
 
+  const int kmax = args.k16 ? 16 : TC_D;
   for (int q = 0; q < Q; ++q) {
     const u64* M = args.M[q];
     uint8_t* dst = sB + q * BALL_BYTES;
     for (int e = tid; e < TC_D * TC_D; e += WS_THREADS) {
       const int k = e / TC_D, n = e % TC_D;
       const int h = n / DB_HALF, c = n % DB_HALF;
-      const u64 v = M[e];
+      const u64 v = k < kmax ? M[e] : 0ull;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         dst[core_off(256 * h + DB_HALF * j + c, k, BALL_ROWS / 8)] = uint8_t(v >> (8 * j));
@@ -352,7 +358,8 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t nunits = my_tiles * 2;
+  const int upt = args.k16 ? 1 : 2;                  // K-units per tile
+  const int64_t nunits = my_tiles * upt;
   const int pieces = 2 * Q;
 
   if (warp == W_EPI + W_CONV) {
@@ -361,12 +368,12 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
       for (int64_t g = 0; g < nunits; ++g) {
         const int st = int(g % MQ_STAGES);
         if (g >= MQ_STAGES) mbar_wait(&empty[st], uint32_t((g / MQ_STAGES - 1) & 1));
-        const int64_t t = blockIdx.x + (g >> 1) * gridDim.x;
-        const int kh = int(g & 1);
+        const int64_t t = blockIdx.x + (g / upt) * gridDim.x;
+        const int kh = int(g % upt);
         uint8_t* dst = sStage + st * RAW_BYTES;
-        mbar_expect_tx(&raw_full[st], RAW_BYTES);
+        mbar_expect_tx(&raw_full[st], upt == 2 ? RAW_BYTES : RAW_BYTES / 2);
         tma_load_2d(dst, &tm, kh * TC_KH, int(t * TC_ROWS), &raw_full[st]);
-        tma_load_2d(dst + RAW_BYTES / 2, &tm, kh * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
+        if (upt == 2) tma_load_2d(dst + RAW_BYTES / 2, &tm, kh * TC_KH + 16, int(t * TC_ROWS), &raw_full[st]);
       }
     }
     __syncwarp();
@@ -402,7 +409,7 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
     // ------------------------------ MMA issuer: pieces p = (q, h), buffer p & 1
     uint32_t tph[2] = {0, 0};
     int64_t use = 0;                                  // pieces issued so far (buffer uses)
-    for (int64_t g0 = 0; g0 < nunits; g0 += 2) {
+    for (int64_t g0 = 0; g0 < nunits; g0 += upt) {
       for (int p = 0; p < pieces; ++p, ++use) {
         const int b = int(use & 1);
         if (use >= 2) {
@@ -410,7 +417,7 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
           tph[b] ^= 1;
         }
         const int q = p >> 1, h = p & 1;
-        for (int kh = 0; kh < 2; ++kh) {
+        for (int kh = 0; kh < upt; ++kh) {
           const int64_t g = g0 + kh;
           const int st = int(g % MQ_STAGES);
           if (p == 0) mbar_wait(&limb_full[st], uint32_t((g / MQ_STAGES) & 1));
@@ -426,7 +433,7 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
                      (kh == 0 && i == 0) ? 0u : 1u);
             }
             if (p == pieces - 1) mma_commit(&empty[st]);
-            if (kh == 1) mma_commit(&tfull[b]);
+            if (kh == upt - 1) mma_commit(&tfull[b]);
           }
           __syncwarp();
         }
@@ -436,7 +443,7 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
     // ------------------------------ epilogue
     uint32_t ph[2] = {0, 0};
     int64_t use = 0;
-    const int quad = warp & 3;
+    const int quad = warp & 3, grp = warp >> 2;
     const int rq = lane >> 2, cq = 2 * (lane & 3);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int p = 0; p < pieces; ++p, ++use) {
@@ -446,7 +453,7 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
         tc_fence_after();
         u64* out = args.out[q];
 #pragma unroll 1
-        for (int it = 0; it < 2 * (DB_HALF / 8); ++it) {
+        for (int it = grp * (DB_HALF / 8); it < (grp + 1) * (DB_HALF / 8); ++it) {
           const int lg = it & 1, c0 = 8 * (it >> 1);
           const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * b + c0);
           uint32_t v[8][4];
@@ -865,6 +872,20 @@ extern "C" int r3_gr_matmul2_tc16_multi(int njobs, const uint64_t* const* p0, co
   return rc != R3_OK ? rc : mm16_launch(J, (const u64*)M0, (const u64*)M1, mask, as_stream(stream));
 }
 
+static int mq_launch(const MqArgs& a, const void* p, int64_t rs, int width, int64_t rows, u64 mask, void* stream,
+                     const char* who) {
+  CUtensorMap tm;
+  if (!make_rows_tmap(&tm, p, rows, rs, TC_ROWS, width)) {
+    set_error("%s: cuTensorMapEncodeTiled failed", who);
+    return R3_ERR_CUDA;
+  }
+  ensure_smem(gr_matmul_q_kernel, MQ_SMEM);
+  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
+  gr_matmul_q_kernel<<<grid, WS_THREADS, MQ_SMEM, as_stream(stream)>>>(tm, a, rows, mask);
+  return check_launch(who);
+}
+
 extern "C" int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows, const uint64_t* const* Ms,
                                  uint64_t* const* outs, int q, uint64_t mask, void* stream) {
   if (!p || !Ms || !outs || q < 1 || q > MQ_MAX || rows < 0 || (rs & 1) || (uintptr_t(p) & 15)) {
@@ -886,14 +907,29 @@ extern "C" int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows, co
     a.M[i] = reinterpret_cast<const u64*>(Ms[i]);
     a.out[i] = reinterpret_cast<u64*>(outs[i]);
   }
-  CUtensorMap tm;
-  if (!make_rows_tmap(&tm, p, rows, rs > 0 ? rs : TC_D, TC_ROWS)) {
-    set_error("r3_gr_matmul_q_tc: cuTensorMapEncodeTiled failed");
-    return R3_ERR_CUDA;
+  return mq_launch(a, p, rs > 0 ? rs : TC_D, TC_D, rows, mask, stream, "r3_gr_matmul_q_tc");
+}
+
+// out[j] = sum_{a < 16} p[16 j + a] K[a] for a 16 x 64 matrix K: the
+// level-4 rows of the y side of a multiplication log with blocks of 16,
+// kappa_a times base elements (r3_vfy_line_b_const's arithmetic as a K = 16
+// byte-limb GEMM, so the step is bound by the row bytes, not by the CUDA
+// cores' 1024 multiply-adds per row and component).  p: rows x 16 words.
+extern "C" int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K, uint64_t* out,
+                                   uint64_t mask, void* stream) {
+  if (!p || !K || !out || rows < 0 || (uintptr_t(p) & 15)) {
+    set_error("r3_gr_matmul_k16_tc: bad arguments (16-byte aligned rows)");
+    return R3_ERR_ARG;
   }
-  ensure_smem(gr_matmul_q_kernel, MQ_SMEM);
-  const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
-  gr_matmul_q_kernel<<<grid, WS_THREADS, MQ_SMEM, as_stream(stream)>>>(tm, a, rows, mask);
-  return check_launch("r3_gr_matmul_q_tc");
+  if (rows == 0) return R3_OK;
+  if (rows > (int64_t(1) << 31) - TC_ROWS) {
+    set_error("r3_gr_matmul_k16_tc: rows %lld exceed the TMA coordinate range", (long long)rows);
+    return R3_ERR_ARG;
+  }
+  MqArgs a{};
+  a.q = 1;
+  a.k16 = 1;
+  a.M[0] = reinterpret_cast<const u64*>(K);
+  a.out[0] = reinterpret_cast<u64*>(out);
+  return mq_launch(a, p, 16, 16, rows, mask, stream, "r3_gr_matmul_k16_tc");
 }

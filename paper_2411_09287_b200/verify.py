@@ -862,6 +862,9 @@ def _lib_i64(v: int) -> int:
     return v - (1 << 64) if v >> 63 else v
 
 
+_K16_OFF = os.environ.get("R3_K16_TC", "1") == "0"     # diagnostics: y-side level-4 rows on the CUDA cores
+
+
 def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
                       r: torch.Tensor, B: int, gr: Ring, chal: Challenges):
     """Pi_tran and the first L = log2 B Pi_rd (verify.py:168-179 + 215-241
@@ -891,6 +894,9 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
 
     def level_vectors(slots):
         out = {}
+        k16 = (B == 16 and gr.d == 64 and comp.n == 1 and comp.N % 16 == 0 and not _K16_OFF
+               and all(t.is_contiguous() and t.data_ptr() % 16 == 0
+                       for sl in slots.values() for t in sl["y"].values()))
         for side in ("x", "y"):
             # m is the same public value at P1 and P2 (honest joint session)
             srcs = [(rr, k, t) for rr, sl in sorted(slots.items()) for k, t in sl[side].items()
@@ -901,6 +907,10 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
                 if side == "x":
                     call("r3_vfy_line_b", B, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
                          nb * gr.d, B, gr.d, _ptrs(pdst), gr.mask, stream())
+                elif k16:
+                    # kappa_a y_(16j + a) as a K = 16 byte-limb GEMM per component
+                    for (_, _, t), o in zip(part, pdst):
+                        call("r3_gr_matmul_k16_tc", ptr(t), nb, ptr(kappa), ptr(o), gr.mask, stream())
                 else:
                     call("r3_vfy_line_b_const", B, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(kappa),
                          gr.d, _ptrs(pdst), gr.mask, stream())

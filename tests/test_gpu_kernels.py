@@ -152,6 +152,36 @@ def test_gr_matmul_q_tc(cuda, rows, q):
     np.testing.assert_array_equal(host(outs63[-1]), ogr.mul(X[0::2], zs[-1], 64, d) & np.uint64((1 << 63) - 1))
 
 
+@pytest.mark.parametrize("rows", [1, 129, 5000, 1 << 17])
+def test_gr_matmul_k16_tc(cuda, rows):
+    """r3_gr_matmul_k16_tc (y-side level-4 rows, K = 16 byte-limb GEMM)
+    against its definition sum_a y[16j + a] K[a] (numpy, wrapping u64) and
+    against r3_vfy_line_b_const with blocks of sixteen."""
+    from paper_2411_09287_b200 import _lib, grvec, host
+    from paper_2411_09287_b200._lib import call, ptr, stream
+    import ctypes as C
+    rng = np.random.default_rng(rows)
+    Y = _rand(rng, (rows * 16,))
+    K = _rand(rng, (16, 64))
+    yd, kd = grvec.dev(Y), grvec.dev(K)
+    out = grvec.empty((rows, 64))
+    call("r3_gr_matmul_k16_tc", ptr(yd), rows, ptr(kd), ptr(out), (1 << 64) - 1, stream())
+    want = np.zeros((rows, 64), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for a in range(16):
+            want += Y[a::16][:, None] * K[a][None, :]
+    np.testing.assert_array_equal(host(out), want)
+    ref = grvec.empty((rows, 64))
+    P = C.c_void_p * 1
+    call("r3_vfy_line_b_const", 16, 1, P(ptr(yd)), rows * 16, 1, 0, 1, ptr(kd), 64, P(ptr(ref)),
+         (1 << 64) - 1, stream())
+    np.testing.assert_array_equal(host(ref), want)
+    out63 = grvec.empty((rows, 64))
+    call("r3_gr_matmul_k16_tc", ptr(yd), rows, ptr(kd), ptr(out63), (1 << 63) - 1, stream())
+    np.testing.assert_array_equal(host(out63), want & np.uint64((1 << 63) - 1))
+    assert _lib is not None
+
+
 @pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
 def test_level_fold_matches_oracle(cuda, d, N):
     """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
