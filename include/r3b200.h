@@ -236,6 +236,21 @@ int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows,
 int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
                         uint64_t* out, uint64_t mask, void* stream);
 
+/* Dot logs (n, L) with n % 16 == 0 at d = 16 (the edaBits inner products,
+ * verify.py:182-241): the first four reductions from the base log.
+ * r3_vfy_lane16_fold: acc[a*16 + b] = sum_l pw[l] sum_{blocks j of lane l}
+ * sum_t coef[t] x_t[16j + a] y_t[16j + b] (256 x d words, zeroed here);
+ * element i of lane l at i*L + l.  r3_vfy_lane16_line: the level-4 rows
+ * (row l*(n/16) + j) sum_a kappa[a] x[16j + a], times pw[l] in GR(2^64, d)
+ * when pow_side (f = t^d + sum of the lowterms monomials). */
+int r3_vfy_lane16_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                       const uint64_t* const* yc, int64_t L, int64_t n,
+                       const uint64_t* pw, int d, uint64_t* acc, void* stream);
+int r3_vfy_lane16_line(int pow_side, int ncomp, const uint64_t* const* xc, int64_t L,
+                       int64_t n, const uint64_t* pw, const uint64_t* kappa,
+                       uint64_t lowterms, int d, uint64_t* const* out, uint64_t mask,
+                       void* stream);
+
 /* Dense-level leg folds for d = 16 of up to four leg terms (several
  * simulated parties) in one tensor-core pass: term k (x, y' = c0 y0 + c1 y1,
  * (N, 16) row-major, y1 may be null) adds its h(1) = sum o_x (x) o_y' and

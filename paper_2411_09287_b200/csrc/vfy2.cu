@@ -715,3 +715,210 @@ extern "C" int r3_vfy_base_fold_multi(int np, const int* nterms, const int64_t* 
   return base_fold_launch(np, nterms, coef, xc, yc, nz, zc, zs, N, pw, d, acc, h1, h2, zsum, mask,
                           as_stream(stream));
 }
+
+// ---------------------------------------------------------------------------
+// Dot logs with n % 16 == 0, d = 16 (the edaBits inner products of length
+// ell: verify.py:182-241 on the consolidated lane-major vector).  Blocks of
+// sixteen consecutive elements lie inside one lane and share its power
+// r^(P+l), so the folds of the first FOUR reductions come from 256 per-lane
+// scalar sums
+//   acc[a*16+b] = sum_l S^{ab}_l pw[l],  S^{ab}_l = sum_{blocks j of lane l} sum_t c_t x_t[16j+a] y_t[16j+b]
+// (public level weights, verify._block_fold_weights), and the level-4 rows
+// are written straight from the base shares (r3_vfy_lane16_line):
+//   x: pw[l] (x) sum_a kappa_a x[16j+a],   y: sum_a kappa_a y[16j+a]
+// -- the dense tail starts at N/16 rows instead of N/4.
+// ---------------------------------------------------------------------------
+constexpr int L16_TILE = 16;     // lanes per tile
+constexpr int L16_PAD = L16_TILE + 1;
+
+// Leg terms grouped by their x component: sum_t c_t x_t y_t =
+// sum_g x_g (sum_k c_gk y_gk) (P2's three terms are two products).
+struct L16Groups {
+  const u64* x[3];
+  const u64* y[3][2];
+  int64_t c[3][2];
+  int ny[3];
+  int ng;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+lane16_fold_kernel(const __grid_constant__ L16Groups G, int64_t L, int64_t n, const u64* __restrict__ pw,
+                   u64* __restrict__ acc_out) {
+  // thread (a, b): S^{ab} of the tile's lanes in registers, then its D
+  // accumulator words; one block of 16 elements per group staged at a time
+  // (x, and the group's combined y)
+  __shared__ u64 sX[3][16][L16_PAD], sY[3][16][L16_PAD];
+  __shared__ u64 sP[L16_TILE][D];
+  const int tid = threadIdx.x, a = tid >> 4, b = tid & 15;
+  const int ng = G.ng;
+  u64 acc[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) acc[c] = 0;
+  const int64_t ntiles = (L + L16_TILE - 1) / L16_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t l0 = tile * L16_TILE;
+    u64 S[L16_TILE];
+#pragma unroll
+    for (int q = 0; q < L16_TILE; ++q) S[q] = 0;
+    for (int64_t j = 0; j < n; j += 16) {
+      for (int e = tid; e < ng * 16 * L16_TILE; e += 256) {
+        const int ln = e % L16_TILE, r = (e / L16_TILE) % 16, g = e / (16 * L16_TILE);
+        const int64_t l = l0 + ln;
+        u64 xv = 0, yv = 0;
+        if (l < L) {
+          const int64_t off = (j + r) * L + l;
+          xv = __ldg(G.x[g] + off);
+          yv = u64(G.c[g][0]) * __ldg(G.y[g][0] + off);
+          if (G.ny[g] > 1) yv += u64(G.c[g][1]) * __ldg(G.y[g][1] + off);
+        }
+        sX[g][r][ln] = xv;
+        sY[g][r][ln] = yv;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        if (g < ng) {
+#pragma unroll
+          for (int q = 0; q < L16_TILE; ++q) S[q] += sX[g][a][q] * sY[g][b][q];
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < L16_TILE * D; e += 256) {
+      const int64_t l = l0 + e / D;
+      sP[e / D][e % D] = l < L ? __ldg(pw + l * D + e % D) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < L16_TILE; ++q) {
+#pragma unroll
+      for (int c = 0; c < D; c += 2) {
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2*>(&sP[q][c]);
+        acc[c] += S[q] * pv.x;
+        acc[c + 1] += S[q] * pv.y;
+      }
+    }
+    __syncthreads();
+  }
+  u64* dst = acc_out + (a * 16 + b) * D;
+#pragma unroll
+  for (int c = 0; c < D; ++c) atomicAdd(reinterpret_cast<unsigned long long*>(dst + c), (unsigned long long)acc[c]);
+}
+
+// Level-4 rows of one component: row l (n/16) + j of the consolidated
+// order holds base elements 16j..16j+15 of lane l.  One thread per row
+// (lanes fastest: coalesced base loads); POW multiplies by pw[l] in
+// GR(2^64, D) (schoolbook product reduced by t^D = -sum_{k in lowterms} t^k).
+template <int D, bool POW>
+__global__ void __launch_bounds__(256)
+lane16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t L, int64_t n, const u64* __restrict__ pw,
+                   const u64* __restrict__ kappa, u64 lowterms, const __grid_constant__ Outs8 out, u64 mask) {
+  __shared__ u64 sK[16][D];
+  for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) sK[e / D][e % D] = kappa[e];
+  __syncthreads();
+  const int64_t nb = n / 16, rows = L * nb;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t l = i % L, j = i / L;
+    u64 p[D];
+    if (POW) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) p[c] = __ldg(pw + l * D + c);
+    }
+    for (int cp = 0; cp < ncomp; ++cp) {
+      u64 u[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[c] = 0;
+#pragma unroll
+      for (int a = 0; a < 16; ++a) {
+        const u64 v = __ldg(xc.p[cp] + (16 * j + a) * L + l);
+#pragma unroll
+        for (int c = 0; c < D; ++c) u[c] += v * sK[a][c];
+      }
+      u64* o = out.p[cp] + (l * nb + j) * D;
+      if (POW) {
+        u64 pr[2 * D - 1];
+#pragma unroll
+        for (int k = 0; k < 2 * D - 1; ++k) pr[k] = 0;
+#pragma unroll
+        for (int x = 0; x < D; ++x) {
+#pragma unroll
+          for (int y = 0; y < D; ++y) pr[x + y] += p[x] * u[y];
+        }
+#pragma unroll
+        for (int k = 2 * D - 2; k >= D; --k) {
+          const u64 top = pr[k];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if ((lowterms >> q) & 1ull) pr[k - D + q] -= top;
+        }
+#pragma unroll
+        for (int c = 0; c < D; c += 2)
+          *reinterpret_cast<ulonglong2*>(o + c) = make_ulonglong2(pr[c] & mask, pr[c + 1] & mask);
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c += 2)
+          *reinterpret_cast<ulonglong2*>(o + c) = make_ulonglong2(u[c] & mask, u[c + 1] & mask);
+      }
+    }
+  }
+}
+
+extern "C" int r3_vfy_lane16_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
+                                  const uint64_t* const* yc, int64_t L, int64_t n, const uint64_t* pw, int d,
+                                  uint64_t* acc, void* stream) {
+  if (nterms < 1 || nterms > 3 || L < 0 || n < 16 || n % 16 || d != 16 || !pw || !acc) {
+    set_error("r3_vfy_lane16_fold: bad arguments (1 <= nterms <= 3, n %% 16 == 0, d = 16)");
+    return R3_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(acc, 0, size_t(256) * d * 8, s) != cudaSuccess) {
+    set_error("r3_vfy_lane16_fold: memset failed");
+    return R3_ERR_CUDA;
+  }
+  if (L == 0) return R3_OK;
+  L16Groups G{};
+  for (int t = 0; t < nterms; ++t) {
+    int g = 0;
+    while (g < G.ng && G.x[g] != reinterpret_cast<const u64*>(xc[t])) ++g;
+    if (g == G.ng) {
+      G.x[g] = reinterpret_cast<const u64*>(xc[t]);
+      ++G.ng;
+    }
+    G.y[g][G.ny[g]] = reinterpret_cast<const u64*>(yc[t]);
+    G.c[g][G.ny[g]] = coef[t];
+    if (++G.ny[g] > 2) {
+      set_error("r3_vfy_lane16_fold: more than two terms share an x component");
+      return R3_ERR_ARG;
+    }
+  }
+  const int64_t tiles = (L + L16_TILE - 1) / L16_TILE;
+  const unsigned grid = unsigned(tiles < int64_t(num_sms()) * 2 ? tiles : int64_t(num_sms()) * 2);
+  lane16_fold_kernel<16><<<grid, 256, 0, s>>>(G, L, n, (const u64*)pw, (u64*)acc);
+  return check_launch("r3_vfy_lane16_fold");
+}
+
+extern "C" int r3_vfy_lane16_line(int pow_side, int ncomp, const uint64_t* const* xc, int64_t L, int64_t n,
+                                  const uint64_t* pw, const uint64_t* kappa, uint64_t lowterms, int d,
+                                  uint64_t* const* out, uint64_t mask, void* stream) {
+  if (ncomp < 1 || ncomp > 8 || L < 0 || n < 16 || n % 16 || d != 16 || !kappa || (pow_side && !pw)) {
+    set_error("r3_vfy_lane16_line: bad arguments (1 <= ncomp <= 8, n %% 16 == 0, d = 16)");
+    return R3_ERR_ARG;
+  }
+  if (L == 0) return R3_OK;
+  Comps8 xp{};
+  Outs8 op{};
+  for (int c = 0; c < ncomp; ++c) {
+    xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for(L * (n / 16), 256, 4);
+  if (pow_side)
+    lane16_line_kernel<16, true><<<grid, 256, 0, s>>>(ncomp, xp, L, n, (const u64*)pw, (const u64*)kappa, lowterms,
+                                                      op, mask);
+  else
+    lane16_line_kernel<16, false><<<grid, 256, 0, s>>>(ncomp, xp, L, n, nullptr, (const u64*)kappa, lowterms, op,
+                                                       mask);
+  return check_launch("r3_vfy_lane16_line");
+}

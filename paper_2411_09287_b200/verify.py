@@ -618,6 +618,8 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     z = _mval_from({k: zsum[i] for i, k in enumerate(names)}, gr, party.role)
     if R == 0:
         return _materialise(comp, pw, gr, party.role), z, 0
+    if _lanes16_ok(comp, R, gr):
+        return _reduce_lanes16(party, comp, pw, z, gr, chal)
     if base_acc is None:
         h1f, h2f = _l1_folds(party, comp, pw, gr)
     z_out, ze, _ = _reduction_round(party, gr, (comp.N + 1) // 2, h1f, h2f, z, chal.zetas[0])
@@ -636,6 +638,67 @@ def _compress_reduce_first(party, comp: _Compressed, zs: MVal, z_lanes: int, z_s
     xs1 = _mval_from(xo, gr, party.role)
     ys1 = _mval_from(yo, gr, party.role)
     return (xs1, ys1), z_out, 1
+
+
+_LANES16_OFF = os.environ.get("R3_LANES16", "1") == "0"      # diagnostics: dot logs on the two-level form
+
+
+def _lanes16_ok(comp: _Compressed, R: int, gr: Ring) -> bool:
+    """Dot log (n, L) with n % 16 == 0 at d = 16 and at least four reductions."""
+    return (not _LANES16_OFF and gr.d == 16 and R >= 4 and comp.n >= 16 and comp.n % 16 == 0
+            and comp.ls == 1 and comp.ks * comp.n == comp.N)
+
+
+def _lane_kappa(party, ws: list, gr: Ring) -> torch.Tensor:
+    """kappa_a = prod_{l < 4} ws[l][bit l of a], a < 16: the line weight of
+    base element 16j + a in its level-4 row."""
+    key = ("lk16", gr.ell, gr.d, tuple(_opened_key(party, w[1]) for w in ws))
+
+    def build():
+        kappa = None
+        for lvl, w in enumerate(ws):
+            f = torch.cat([w[(a >> lvl) & 1] for a in range(16)])
+            kappa = f if kappa is None else grvec.gr_mul(kappa, f, gr.ell, gr.mod)
+        return kappa.contiguous()
+    return _public(party, key, build)
+
+
+def _reduce_lanes16(party, comp: _Compressed, pw: torch.Tensor, z: MVal, gr: Ring, chal: Challenges):
+    """The first four Pi_rd of a dot log whose lanes hold a multiple of 16
+    elements (verify.py:215-241 at k < 4; the edaBits inner products of
+    length ell): blocks of 16 consecutive elements never straddle a lane and
+    share its power r^(P+l), so every fold of those levels is a public-weight
+    combination of 256 per-lane scalar sums times pw[l] (r3_vfy_lane16_fold,
+    weights verify._block_fold_weights), and the level-4 rows come straight
+    from the base shares (r3_vfy_lane16_line): the dense tail starts at N/16
+    rows.  Returns ((xs, ys), z, 4)."""
+    role, d = party.role, gr.d
+    terms = _role_terms(role)
+    coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+    L = comp.N // comp.n
+    acc = empty((256, d))
+    call("r3_vfy_lane16_fold", len(terms), coef, _ptrs([comp.x[t[1]] for t in terms]),
+         _ptrs([comp.y[t[2]] for t in terms]), L, comp.n, ptr(pw), d, ptr(acc), stream())
+    ws = []
+    n = comp.N
+    for k in range(4):
+        W1, W2 = _block_fold_weights(party, k, ws, 16, gr)
+        fold = lambda W: _dotsum_terms([([(1, acc, 256)], [(1, W, 256)])], 256, gr)
+        rows = (n + 1) // 2
+        z, ze, q = _reduction_round(party, gr, rows, fold(W1), fold(W2), z, chal.zetas[k])
+        ws.append((q.one_m, ze))
+        n = rows
+    kappa = _lane_kappa(party, ws, gr)
+    rows4 = comp.N // 16
+    out = {}
+    for side, src, pow_side in (("x", comp.x, 1), ("y", comp.y, 0)):
+        keys = list(src)
+        dst = {k: empty((rows4, d)) for k in keys}
+        call("r3_vfy_lane16_line", pow_side, len(keys), _ptrs([src[k] for k in keys]), L, comp.n,
+             ptr(pw) if pow_side else None, ptr(kappa), gr.mod.lowterms_mask, d, _ptrs([dst[k] for k in keys]),
+             gr.mask, stream())
+        out[side] = _mval_from(dst, gr, role)
+    return (out["x"], out["y"]), z, 4
 
 
 def _l2_weights(party, ze1: torch.Tensor, gr: Ring):

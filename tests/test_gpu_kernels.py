@@ -182,6 +182,58 @@ def test_gr_matmul_k16_tc(cuda, rows):
     assert _lib is not None
 
 
+@pytest.mark.parametrize("L,n,nterms", [(1, 16, 1), (45, 64, 2), (1000, 32, 3), (4099, 64, 2)])
+def test_lane16_fold_and_line_match_definitions(cuda, L, n, nterms):
+    """r3_vfy_lane16_fold / _line (dot logs with n % 16 == 0, d = 16) against
+    their definitions: acc[a*16+b] = sum_l pw[l] sum_j sum_t c_t x_t[16j+a][l]
+    y_t[16j+b][l]; level-4 rows sum_a kappa_a x[16j+a][l] (times pw[l] in GR
+    on the x side, the oracle's GR product)."""
+    from oracle import gr as ogr
+    from paper_2411_09287_b200 import grvec, host
+    from paper_2411_09287_b200._lib import call, ptr, stream
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    import ctypes as C
+    d = 16
+    mod = modulus_for_degree(d)
+    rng = np.random.default_rng(L * 7 + n)
+    xs = [_rand(rng, (n, L)) for _ in range(nterms)]
+    ys = [_rand(rng, (n, L)) for _ in range(nterms)]
+    coef = [1, -1, 2][:nterms]
+    pw = _rand(rng, (L, d))
+    xd, yd, pwd = [grvec.dev(x) for x in xs], [grvec.dev(y) for y in ys], grvec.dev(pw)
+    acc = grvec.empty((256, d))
+    P = lambda ts: (C.c_void_p * len(ts))(*[ptr(t) for t in ts])
+    call("r3_vfy_lane16_fold", nterms, (C.c_int64 * nterms)(*coef), P(xd), P(yd), L, n, ptr(pwd), d,
+         ptr(acc), stream())
+    want = np.zeros((256, d), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        S = np.zeros((256, L), dtype=np.uint64)
+        for t in range(nterms):
+            cf = np.uint64(coef[t] & ((1 << 64) - 1))
+            for j in range(0, n, 16):
+                for a in range(16):
+                    for b in range(16):
+                        S[a * 16 + b] += cf * xs[t][j + a] * ys[t][j + b]
+        for q in range(256):
+            want[q] = (S[q][:, None] * pw).sum(axis=0, dtype=np.uint64)
+    np.testing.assert_array_equal(host(acc), want)
+    kappa = _rand(rng, (16, d))
+    kd = grvec.dev(kappa)           # device operands stay referenced until the launches ran
+    rows = L * (n // 16)
+    outs = [grvec.empty((rows, d)) for _ in range(2)]
+    for pow_side, o in ((0, outs[0]), (1, outs[1])):
+        call("r3_vfy_lane16_line", pow_side, 1, P(xd[:1]), L, n, ptr(pwd) if pow_side else None,
+             ptr(kd), mod.lowterms_mask, d, P([o]), (1 << 64) - 1, stream())
+    u = np.zeros((L, n // 16, d), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for j in range(n // 16):
+            for a in range(16):
+                u[:, j] += xs[0][16 * j + a][:, None] * kappa[a][None, :]
+    np.testing.assert_array_equal(host(outs[0]).reshape(L, n // 16, d), u)
+    prod = ogr.mul(u.reshape(-1, d), np.repeat(pw, n // 16, axis=0), 64, d)
+    np.testing.assert_array_equal(host(outs[1]), prod)
+
+
 @pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
 def test_level_fold_matches_oracle(cuda, d, N):
     """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
