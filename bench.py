@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--mlp-batch", type=int, default=4096)
     ap.add_argument("--mlp-verified-batch", type=int, default=4096)
     ap.add_argument("--lenet-batch", type=int, default=1024)
-    ap.add_argument("--lenet-verified-batch", type=int, default=128)
+    ap.add_argument("--lenet-verified-batch", type=int, default=256)
     return ap.parse_args()
 
 

@@ -735,8 +735,8 @@ constexpr int L16_PAD = L16_TILE + 1;
 // sum_g x_g (sum_k c_gk y_gk) (P2's three terms are two products).
 struct L16Groups {
   const u64* x[3];
-  const u64* y[3][2];
-  int64_t c[3][2];
+  const u64* y[3][3];
+  int64_t c[3][3];
   int ny[3];
   int ng;
 };
@@ -771,6 +771,7 @@ lane16_fold_kernel(const __grid_constant__ L16Groups G, int64_t L, int64_t n, co
           xv = __ldg(G.x[g] + off);
           yv = u64(G.c[g][0]) * __ldg(G.y[g][0] + off);
           if (G.ny[g] > 1) yv += u64(G.c[g][1]) * __ldg(G.y[g][1] + off);
+          if (G.ny[g] > 2) yv += u64(G.c[g][2]) * __ldg(G.y[g][2] + off);
         }
         sX[g][r][ln] = xv;
         sY[g][r][ln] = yv;
@@ -887,10 +888,7 @@ extern "C" int r3_vfy_lane16_fold(int nterms, const int64_t* coef, const uint64_
     }
     G.y[g][G.ny[g]] = reinterpret_cast<const u64*>(yc[t]);
     G.c[g][G.ny[g]] = coef[t];
-    if (++G.ny[g] > 2) {
-      set_error("r3_vfy_lane16_fold: more than two terms share an x component");
-      return R3_ERR_ARG;
-    }
+    ++G.ny[g];
   }
   const int64_t tiles = (L + L16_TILE - 1) / L16_TILE;
   const unsigned grid = unsigned(tiles < int64_t(num_sms()) * 2 ? tiles : int64_t(num_sms()) * 2);

@@ -37,7 +37,7 @@ import torch
 
 from . import grvec
 from ._lib import call, empty, ptr, stream, to_host
-from .gates import MatmulBatchRec, dot_finish, dot_prepare, prepare_gate
+from .gates import MatmulBatchRec, MulBatchRec, dot_finish, dot_prepare, prepare_gate
 from .rings import ConfigError, modulus_for_degree
 from .sharing import AShare, MVal, Ring, rec, shc_random
 from .transport import AUX, OFFLINE, PAYLOAD, HarnessError, Phase
@@ -1597,6 +1597,11 @@ def _batch_verify_muls(party, base_ell: int, d: int, R: int, kind_key: str | Non
     xs = _concat_all(log.muls, lambda b: b.x)
     ys = _concat_all(log.muls, lambda b: b.y)
     zs = _concat_all(log.muls, lambda b: b.z)
+    if len(log.muls) > 1:
+        # the frozen log keeps the concatenated batch only (same values in
+        # the same order), so the per-gate tensors are freed for the
+        # verification's working set
+        log.muls[:] = [MulBatchRec(xs, ys, zs, sum(b.lanes for b in log.muls))]
     comp = _compressed_from_log(xs, ys, party.role, 1)
     if _gf2_packed_ok(gr, R):
         return _verify_muls_gf2(party, comp, zs, gr, ctx, R)
@@ -1952,6 +1957,69 @@ class _DenseBatch:
         return self.x, self.y
 
 
+class _Lane16Batch:
+    """A dot batch (n, L) with n % 16 == 0 at d = 16 inside the structured
+    dot verification (the edaBits inner products of every ReLU / MaxPool
+    layer): its first four levels' folds are public-weight combinations of
+    256 per-lane sums (r3_vfy_lane16_fold, as _reduce_lanes16 for a whole
+    log), its level-4 rows come from the base shares (r3_vfy_lane16_line),
+    and from there it continues as a dense batch (N/16 rows instead of the
+    N/4 of _DenseBatch's base form)."""
+
+    def __init__(self, b, role: int, gr: Ring, P: int, pw: torch.Tensor):
+        self.base = _compressed_from_log(b.xs, b.ys, role, b.n)
+        self.pw = pw[P:P + b.lanes]
+        self.level, self.ws, self.acc, self.dense = 0, [], None, None
+
+    def length(self) -> int:
+        return self.dense.length() if self.dense is not None else self.base.N >> self.level
+
+    def structured(self) -> bool:
+        return self.length() % 2 == 0
+
+    def folds(self, role: int, gr: Ring, party=None):
+        if self.dense is not None:
+            return self.dense.folds(role, gr, party)
+        comp = self.base
+        if self.acc is None:
+            terms = _role_terms(role)
+            coef = (C.c_int64 * len(terms))(*[t[0] for t in terms])
+            self.acc = empty((256, gr.d))
+            call("r3_vfy_lane16_fold", len(terms), coef, _ptrs([comp.x[t[1]] for t in terms]),
+                 _ptrs([comp.y[t[2]] for t in terms]), comp.N // comp.n, comp.n, ptr(self.pw), gr.d,
+                 ptr(self.acc), stream())
+        W1, W2 = _block_fold_weights(party, self.level, self.ws, 16, gr)
+        fold = lambda W: _dotsum_terms([([(1, self.acc, 256)], [(1, W, 256)])], 256, gr)
+        return fold(W1), fold(W2)
+
+    def reduce(self, Ms, gr: Ring, party=None, ze=None, one_m=None) -> None:
+        if self.dense is not None:
+            self.dense.reduce(Ms, gr, party, ze)
+            return
+        self.ws.append((one_m, ze))
+        self.level += 1
+        if self.level < 4:
+            return
+        comp = self.base
+        kappa = _lane_kappa(party, self.ws, gr)
+        rows4 = comp.N // 16
+        out = []
+        for src, pow_side in ((comp.x, 1), (comp.y, 0)):
+            keys = list(src)
+            dst = {k: empty((rows4, gr.d)) for k in keys}
+            call("r3_vfy_lane16_line", pow_side, len(keys), _ptrs([src[k] for k in keys]), comp.N // comp.n,
+                 comp.n, ptr(self.pw) if pow_side else None, ptr(kappa), gr.mod.lowterms_mask, gr.d,
+                 _ptrs([dst[k] for k in keys]), gr.mask, stream())
+            out.append(dst)
+        self.dense = _DenseBatch.from_arrays(out[0], out[1])
+        self.base = self.acc = None
+
+    def materialise(self, gr: Ring, party=None):
+        if self.dense is None:
+            raise HarnessError("lane16 dot batch materialised before its fourth level")
+        return self.dense.materialise(gr, party)
+
+
 def _materialise_dense(comp: "_Compressed", pw: torch.Tensor, gr: Ring):
     flat = lambda t: t.transpose(0, 1).contiguous().reshape(-1)
     p_rep = pw.repeat_interleave(comp.n, dim=0)
@@ -1973,6 +2041,10 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
     r = _open_challenge(party, ctx.r, "vfy.r")
     total = sum(b.lanes for b in batches)
     pw = _powers(party, r, total, gr)
+    # dot batches with lanes of 16k elements take the four-level base form
+    # when every part's length keeps the loop structured to level 4
+    lane16 = (not _LANES16_OFF and gr.d == 16 and R >= 4
+              and all((b.lanes * b.n) % 16 == 0 for b in batches))
     parts, z_acc, pos = [], None, 0
     for b in batches:
         p = pw[pos:pos + b.lanes]
@@ -1986,6 +2058,8 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
         split = _FCBatch.split(b) if isinstance(b, MatmulBatchRec) and b.K % 2 == 0 else None
         if split is not None:
             parts.append(_FCBatch(b, role, gr, pos, pw, split))
+        elif lane16 and b.n % 16 == 0 and not isinstance(b, MatmulBatchRec):
+            parts.append(_Lane16Batch(b, role, gr, pos, pw))
         else:
             parts.append(_DenseBatch(b, role, gr, pos, pw))
         pos += b.lanes
@@ -1997,7 +2071,7 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
                  and pt.length() % 2 == 0 else pt for pt in parts]
         if not all(pt.structured() for pt in parts):
             break
-        folds = [pt.folds(role, gr, party) if isinstance(pt, _DenseBatch) else pt.folds(role, gr)
+        folds = [pt.folds(role, gr, party) if isinstance(pt, (_DenseBatch, _Lane16Batch)) else pt.folds(role, gr)
                  for pt in parts]
         fold1, fold2 = folds[0]
         for f1, f2 in folds[1:]:
@@ -2006,12 +2080,15 @@ def _verify_dots_structured(party, batches, gr: Ring, ctx: Challenges, R: int) -
         z, ze, q = _reduction_round(party, gr, rows, fold1, fold2, z, ctx.zetas[k])
         Ms = (q.M_one_m if gr.d in (16, 64) else None, q.M_ze)
         for pt in parts:
-            if isinstance(pt, _DenseBatch):
+            if isinstance(pt, _Lane16Batch):
+                pt.reduce(Ms, gr, party, ze, q.one_m)
+            elif isinstance(pt, _DenseBatch):
                 pt.reduce(Ms, gr, party, ze)
             else:
                 pt.reduce(Ms, gr)
         k += 1
-    mats = [pt.materialise(gr, party) if isinstance(pt, _DenseBatch) else pt.materialise(gr) for pt in parts]
+    mats = [pt.materialise(gr, party) if isinstance(pt, (_DenseBatch, _Lane16Batch)) else pt.materialise(gr)
+            for pt in parts]
     xs = _mval_from({c: torch.cat([m[0][c] for m in mats]) for c in mats[0][0]}, gr, role)
     ys = _mval_from({c: torch.cat([m[1][c] for m in mats]) for c in mats[0][1]}, gr, role)
     del parts, mats

@@ -138,3 +138,50 @@ def test_base_reduction_block_sizes_give_identical_transcripts(cuda, N, R, d, mo
     adv = AdversaryConfig(corrupted=1, injections=[Injection("dot.mz", delta=1, gate=0, lane=7)])
     res = Session(seed=11, adversary=adv).run(prog)
     assert not any(r[1] for r in res), "a tampered leg passed verification"
+
+
+@pytest.mark.parametrize("what", ["relu", "lenet"])
+def test_lane16_dot_form_gives_identical_transcripts(cuda, what, monkeypatch):
+    """Dot logs whose lanes hold a multiple of 16 elements (the edaBits inner
+    products) verified through the four-level base form (r3_vfy_lane16_fold /
+    _line) and through the two-level form (R3_LANES16=0 equivalent): every
+    message payload per sender, the verdicts and the outputs are identical
+    -- a whole-log ReLU session (_reduce_lanes16) and a verified LeNet-28
+    batch (structured dot verification, _Lane16Batch beside FC / conv
+    batches)."""
+    import hashlib
+    import torch
+    from paper_2411_09287_b200 import host, ppml, verify
+    from paper_2411_09287_b200.runtime import Session
+    import bench
+
+    if what == "relu":
+        N = 1 << 12
+        xv = np.trunc(np.random.default_rng(3).normal(0, 4, N) * 2 ** 16).astype(np.int64)
+        prog, args = bench.make_relu_program(N, 16), (torch.from_numpy(xv), True)
+    else:
+        model = ppml.lenet28_model(np.random.default_rng(0))
+        imgs = np.random.default_rng(1).normal(0, 1, (2, int(np.prod(model.input_shape))))
+        prog, args = (lambda p: ppml.infer_batch(p, model, imgs if p.role == 2 else None, ppml.InferConfig(d=16),
+                                                 batch=2)), ()
+    used = []
+    orig_fold = verify._block_fold_weights
+
+    def spy(party, k, ws, B, gr):
+        used.append(B)
+        return orig_fold(party, k, ws, B, gr)
+    runs = {}
+    for off in (True, False):
+        monkeypatch.setattr(verify, "_LANES16_OFF", off)
+        monkeypatch.setattr(verify, "_block_fold_weights", spy)
+        used.clear()
+        sess = Session(seed=5)
+        log = []
+        sess.message_hook = lambda frm, to, ph, label, arr, cls, ring: log.append(
+            (frm, label, hashlib.sha256(host(arr).tobytes()).hexdigest()))
+        res = sess.run(prog, *args)
+        runs[off] = (sorted(log), res, bool(used))
+    assert runs[False][2], "the lane16 form was not exercised"
+    assert runs[False][0] == runs[True][0], "message payloads differ from the two-level form"
+    flat = lambda res: [host(t) if isinstance(t, torch.Tensor) else t for t in res]
+    assert repr(flat(runs[False][1])) == repr(flat(runs[True][1]))

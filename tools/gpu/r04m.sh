@@ -1,0 +1,3 @@
+timeout 1200 python -m pytest tests/test_gpu_golden.py tests/test_gpu_golden_scale.py tests/test_gpu_sessions.py -x -q -p no:cacheprovider 2>&1 | tail -2
+timeout 900 python tools/verify_mem.py lenet 256 2>&1 | tail -3
+timeout 900 python tools/verify_mem.py lenet 384 2>&1 | tail -3
