@@ -243,6 +243,14 @@ int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
  * element i of lane l at i*L + l.  r3_vfy_lane16_line: the level-4 rows
  * (row l*(n/16) + j) sum_a kappa[a] x[16j + a], times pw[l] in GR(2^64, d)
  * when pow_side (f = t^d + sum of the lowterms monomials). */
+/* Level-4 rows of a d = 16 multiplication log with blocks of sixteen
+ * straight from the base shares (verify.py:237-240 applied four times):
+ * row j = sum_a coef[a] x[16j + a] (coef: 16 x 16 words), times pw16[j] in
+ * GR(2^64, 16) when pow_side (x side: coef[a] = r^a kappa_a; y side:
+ * kappa_a).  Replaces the sixteen N/16-row tables. */
+int r3_vfy_mul16_line(int pow_side, int ncomp, const uint64_t* const* xc, int64_t N,
+                      const uint64_t* pw16, const uint64_t* coef, uint64_t lowterms, int d,
+                      uint64_t* const* out, uint64_t mask, void* stream);
 int r3_vfy_lane16_fold(int nterms, const int64_t* coef, const uint64_t* const* xc,
                        const uint64_t* const* yc, int64_t L, int64_t n,
                        const uint64_t* pw, int d, uint64_t* acc, void* stream);

@@ -920,3 +920,104 @@ extern "C" int r3_vfy_lane16_line(int pow_side, int ncomp, const uint64_t* const
                                                        mask);
   return check_launch("r3_vfy_lane16_line");
 }
+
+// ---------------------------------------------------------------------------
+// Level-4 rows of a d = 16 multiplication log with blocks of sixteen
+// straight from the base shares, without the sixteen tables r^(16j)
+// (r^a kappa_a) (N x 128 B written and read back):
+//   x: pw16[j] (x) sum_a c_a x[16j + a]  (c_a = r^a kappa_a),   y: sum_a kappa_a y[16j + a]
+// One thread per row: sixteen scalar x GR(2^64, 16) MACs, then (x side) the
+// schoolbook product with pw16[j] reduced by t^16 = -sum_{k in lowterms} t^k.
+// ---------------------------------------------------------------------------
+template <bool POW>
+__global__ void __launch_bounds__(256)
+mul16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t N, const u64* __restrict__ pw,
+                  const u64* __restrict__ coef, u64 lowterms, const __grid_constant__ Outs8 out, u64 mask) {
+  constexpr int D = 16;
+  __shared__ u64 sK[16][D];
+  for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) sK[e / D][e % D] = coef[e];
+  __syncthreads();
+  const int64_t rows = (N + 15) / 16;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < rows; j += int64_t(gridDim.x) * blockDim.x) {
+    u64 p[D];
+    if (POW) {
+#pragma unroll
+      for (int c = 0; c < D; c += 2) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(pw + j * D + c));
+        p[c] = v.x, p[c + 1] = v.y;
+      }
+    }
+    const bool full = 16 * j + 16 <= N;
+    for (int cp = 0; cp < ncomp; ++cp) {
+      const u64* src = xc.p[cp] + 16 * j;
+      u64 xv[16];
+      if (full && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int a = 0; a < 16; a += 2) {
+          const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(src + a));
+          xv[a] = v.x, xv[a + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 16; ++a) xv[a] = 16 * j + a < N ? __ldg(src + a) : 0ull;
+      }
+      u64 u[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[c] = 0;
+#pragma unroll
+      for (int a = 0; a < 16; ++a) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) u[c] += xv[a] * sK[a][c];
+      }
+      u64* o = out.p[cp] + j * D;
+      if (POW) {
+        u64 pr[2 * D - 1];
+#pragma unroll
+        for (int k = 0; k < 2 * D - 1; ++k) pr[k] = 0;
+#pragma unroll
+        for (int x = 0; x < D; ++x) {
+#pragma unroll
+          for (int y = 0; y < D; ++y) pr[x + y] += p[x] * u[y];
+        }
+#pragma unroll
+        for (int k = 2 * D - 2; k >= D; --k) {
+          const u64 top = pr[k];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if ((lowterms >> q) & 1ull) pr[k - D + q] -= top;
+        }
+#pragma unroll
+        for (int c = 0; c < D; c += 2)
+          *reinterpret_cast<ulonglong2*>(o + c) = make_ulonglong2(pr[c] & mask, pr[c + 1] & mask);
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c += 2)
+          *reinterpret_cast<ulonglong2*>(o + c) = make_ulonglong2(u[c] & mask, u[c + 1] & mask);
+      }
+    }
+  }
+}
+
+extern "C" int r3_vfy_mul16_line(int pow_side, int ncomp, const uint64_t* const* xc, int64_t N, const uint64_t* pw16,
+                                 const uint64_t* coef, uint64_t lowterms, int d, uint64_t* const* out, uint64_t mask,
+                                 void* stream) {
+  if (ncomp < 1 || ncomp > 8 || N < 0 || d != 16 || !coef || (pow_side && !pw16)) {
+    set_error("r3_vfy_mul16_line: bad arguments (1 <= ncomp <= 8, d = 16)");
+    return R3_ERR_ARG;
+  }
+  if (N == 0) return R3_OK;
+  Comps8 xp{};
+  Outs8 op{};
+  for (int c = 0; c < ncomp; ++c) {
+    xp.p[c] = reinterpret_cast<const u64*>(xc[c]);
+    op.p[c] = reinterpret_cast<u64*>(out[c]);
+  }
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for((N + 15) / 16, 256, 4);
+  if (pow_side)
+    mul16_line_kernel<true><<<grid, 256, 0, s>>>(ncomp, xp, N, (const u64*)pw16, (const u64*)coef, lowterms, op,
+                                                 mask);
+  else
+    mul16_line_kernel<false><<<grid, 256, 0, s>>>(ncomp, xp, N, nullptr, (const u64*)coef, lowterms, op, mask);
+  return check_launch("r3_vfy_mul16_line");
+}

@@ -926,6 +926,7 @@ def _lib_i64(v: int) -> int:
 
 
 _K16_OFF = os.environ.get("R3_K16_TC", "1") == "0"     # diagnostics: y-side level-4 rows on the CUDA cores
+_MUL16_OFF = os.environ.get("R3_MUL16", "1") == "0"    # diagnostics: d = 16 level-4 rows through the B tables
 
 
 def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
@@ -952,7 +953,13 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
         z, ze, q = _reduction_round(party, gr, rows, fold(W1), fold(W2), z, chal.zetas[k])
         ws.append((q.one_m, ze))
         n = rows
-    tabs, kappa = _base_tables(party, qb, ws, B, gr)
+    # d = 16, blocks of sixteen: the level-4 rows straight from the base
+    # shares and r^(16j) (r3_vfy_mul16_line), no tables
+    rows16 = B == 16 and gr.d == 16 and not _MUL16_OFF and qb[0].is_contiguous()
+    if rows16:
+        _, kappa, rk = _base_tables(party, qb, ws, B, gr, tables=False)
+    else:
+        tabs, kappa = _base_tables(party, qb, ws, B, gr)
     geo = (comp.N, comp.n, comp.ks, comp.ls)
 
     def level_vectors(slots):
@@ -967,7 +974,12 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
             dst = [empty((nb, gr.d)) for _ in srcs]
             for c0 in range(0, len(srcs), 4):          # wide blocks: <= 4 components per launch
                 part, pdst = srcs[c0:c0 + 4], dst[c0:c0 + 4]
-                if side == "x":
+                if rows16:
+                    xside = side == "x"
+                    call("r3_vfy_mul16_line", int(xside), len(part), _ptrs([t for _, _, t in part]), comp.N,
+                         ptr(qb[0]) if xside else None, ptr(rk if xside else kappa), gr.mod.lowterms_mask,
+                         gr.d, _ptrs(pdst), gr.mask, stream())
+                elif side == "x":
                     call("r3_vfy_line_b", B, len(part), _ptrs([t for _, _, t in part]), *geo, ptr(tabs),
                          nb * gr.d, B, gr.d, _ptrs(pdst), gr.mask, stream())
                 elif k16:
@@ -991,12 +1003,13 @@ def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_str
     return (_mval_from(res["x"], gr, role), _mval_from(res["y"], gr, role)), z, levels
 
 
-def _base_tables(party, qb, ws: list, B: int, gr: Ring):
+def _base_tables(party, qb, ws: list, B: int, gr: Ring, tables: bool = True):
     """kappa_a = prod_{l < log2 B} w_(l+1)[bit l of a] (the level line weight
     of base element Bj + a) and the tables V_a[j] = pwB[j] (r^a kappa_a),
-    a < B, built four at a time from one pass over pwB."""
+    a < B, built four at a time from one pass over pwB.  tables=False
+    returns (None, kappa, r^a kappa_a) for the table-free d = 16 rows."""
     pwb, rpow = qb
-    key = ("lbt", B, gr.ell, gr.d, id(pwb), pwb.shape[0], tuple(_opened_key(party, w[1]) for w in ws))
+    key = ("lbt", B, tables, gr.ell, gr.d, id(pwb), pwb.shape[0], tuple(_opened_key(party, w[1]) for w in ws))
 
     def build():
         kappa = None
@@ -1004,6 +1017,8 @@ def _base_tables(party, qb, ws: list, B: int, gr: Ring):
             f = torch.cat([w[(a >> lvl) & 1] for a in range(B)])
             kappa = f if kappa is None else grvec.gr_mul(kappa, f, gr.ell, gr.mod)
         rk = grvec.gr_mul(kappa, rpow, gr.ell, gr.mod)
+        if not tables:
+            return None, kappa.contiguous(), rk.contiguous()
         rows = pwb.shape[0]
         tabs = grvec.empty((B, rows, gr.d))
         for h in range(0, B, 4):

@@ -234,6 +234,38 @@ def test_lane16_fold_and_line_match_definitions(cuda, L, n, nterms):
     np.testing.assert_array_equal(host(outs[1]), prod)
 
 
+@pytest.mark.parametrize("N", [1, 16, 1000, 70001])
+def test_mul16_line_matches_definition(cuda, N):
+    """r3_vfy_mul16_line (d = 16 multiplication-log level-4 rows, blocks of
+    sixteen, ragged tail): row j = sum_a coef[a] x[16j + a], times pw16[j]
+    with the oracle's GR product on the x side."""
+    from oracle import gr as ogr
+    from paper_2411_09287_b200 import grvec, host
+    from paper_2411_09287_b200._lib import call, ptr, stream
+    from paper_2411_09287_b200.rings import modulus_for_degree
+    import ctypes as C
+    d = 16
+    mod = modulus_for_degree(d)
+    rng = np.random.default_rng(N)
+    rows = (N + 15) // 16
+    X = _rand(rng, (N,))
+    coef = _rand(rng, (16, d))
+    pw = _rand(rng, (rows, d))
+    xd, cd, pd = grvec.dev(X), grvec.dev(coef), grvec.dev(pw)
+    P = lambda ts: (C.c_void_p * len(ts))(*[ptr(t) for t in ts])
+    Xp = np.zeros(rows * 16, dtype=np.uint64)
+    Xp[:N] = X
+    u = np.zeros((rows, d), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for a in range(16):
+            u += Xp[a::16][:, None] * coef[a][None, :]
+    for pow_side, want in ((0, u), (1, ogr.mul(u, pw, 64, d))):
+        o = grvec.empty((rows, d))
+        call("r3_vfy_mul16_line", pow_side, 1, P([xd]), N, ptr(pd) if pow_side else None, ptr(cd),
+             mod.lowterms_mask, d, P([o]), (1 << 64) - 1, stream())
+        np.testing.assert_array_equal(host(o), want)
+
+
 @pytest.mark.parametrize("d,N", [(64, 1), (64, 2), (64, 333), (64, 8191), (64, 8192), (64, 40001), (16, 1000), (32, 77)])
 def test_level_fold_matches_oracle(cuda, d, N):
     """One-pass h(1)/h(2) folds of a dense level vs the reference algebra
