@@ -815,7 +815,7 @@ template <int D, bool POW>
 __global__ void __launch_bounds__(256)
 lane16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t L, int64_t n, const u64* __restrict__ pw,
                    const u64* __restrict__ kappa, u64 lowterms, const __grid_constant__ Outs8 out, u64 mask) {
-  __shared__ u64 sK[16][D];
+  __shared__ __align__(16) u64 sK[16][D];
   for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) sK[e / D][e % D] = kappa[e];
   __syncthreads();
   const int64_t nb = n / 16, rows = L * nb;
@@ -834,7 +834,11 @@ lane16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t L, int6
       for (int a = 0; a < 16; ++a) {
         const u64 v = __ldg(xc.p[cp] + (16 * j + a) * L + l);
 #pragma unroll
-        for (int c = 0; c < D; ++c) u[c] += v * sK[a][c];
+        for (int c = 0; c < D; c += 2) {     // 128-bit broadcast reads of the constants
+          const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&sK[a][c]);
+          u[c] += v * kk.x;
+          u[c + 1] += v * kk.y;
+        }
       }
       u64* o = out.p[cp] + (l * nb + j) * D;
       if (POW) {
@@ -934,7 +938,7 @@ __global__ void __launch_bounds__(256)
 mul16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t N, const u64* __restrict__ pw,
                   const u64* __restrict__ coef, u64 lowterms, const __grid_constant__ Outs8 out, u64 mask) {
   constexpr int D = 16;
-  __shared__ u64 sK[16][D];
+  __shared__ __align__(16) u64 sK[16][D];
   for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) sK[e / D][e % D] = coef[e];
   __syncthreads();
   const int64_t rows = (N + 15) / 16;
@@ -967,7 +971,11 @@ mul16_line_kernel(int ncomp, const __grid_constant__ Comps8 xc, int64_t N, const
 #pragma unroll
       for (int a = 0; a < 16; ++a) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) u[c] += xv[a] * sK[a][c];
+        for (int c = 0; c < D; c += 2) {     // 128-bit broadcast reads of the constants
+          const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&sK[a][c]);
+          u[c] += xv[a] * kk.x;
+          u[c + 1] += xv[a] * kk.y;
+        }
       }
       u64* o = out.p[cp] + j * D;
       if (POW) {

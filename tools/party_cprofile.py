@@ -2,7 +2,7 @@
 over several sessions of a small verified program -- the host-bound regime
 where every verification level costs protocol-driver time.  Diagnostic only.
 
-    python tools/party_cprofile.py mulv 20 [tottime|cumtime] [role]
+    python tools/party_cprofile.py mulv 20 [tottime|cumtime] [role|all]
 """
 
 import cProfile
@@ -23,7 +23,7 @@ from paper_2411_09287_b200.runtime import Session  # noqa: E402
 def main():
     kind, lg = sys.argv[1], int(sys.argv[2])
     sort = sys.argv[3] if len(sys.argv) > 3 else "tottime"
-    role = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+    role = sys.argv[4] if len(sys.argv) > 4 else "1"      # a party index or "all"
     N = 1 << lg
     if kind.startswith("relu"):
         rng = np.random.default_rng(1)
@@ -36,11 +36,13 @@ def main():
     for i in range(3):
         Session(seed=i).run(prog, *args)
     torch.cuda.synchronize()
-    pr = cProfile.Profile()
+    prs = {r: cProfile.Profile() for r in range(3)}
+    roles = range(3) if role == "all" else [int(role)]
 
     def wrapped(party, *a):
-        if party.role != role:
+        if party.role not in roles:
             return prog(party, *a)
+        pr = prs[party.role]
         pr.enable()
         try:
             return prog(party, *a)
@@ -50,7 +52,9 @@ def main():
     for i in range(5):
         Session(seed=10 + i).run(wrapped, *args)
     torch.cuda.synchronize()
-    st = pstats.Stats(pr)
+    st = pstats.Stats(prs[roles[0]])
+    for r in roles[1:]:
+        st.add(prs[r])
     st.sort_stats(sort).print_stats(60)
 
 
