@@ -97,7 +97,7 @@ def pick_r(gates: int, ell: int, d: int, profile: str = "lan", r_max: int = DEFA
 class Challenges:
     r: MVal
     alpha: MVal
-    zetas: list
+    zetas: "_SealedBlock"
 
 
 def prepare_verification(party, d: int, r_max: int = DEFAULT_R_MAX) -> None:
@@ -113,7 +113,38 @@ def prepare_verification(party, d: int, r_max: int = DEFAULT_R_MAX) -> None:
     party.verify_ctx = ctx
 
 
-def _sealed_block(party, count: int, gr: Ring) -> list:
+class _SealedBlock:
+    """A read-only sequence of sealed challenge shares over one block of
+    keystream words; the MVal of value k is built when it is first read (a
+    verification opens R + 2 of the r_max + 2 prepared values)."""
+
+    def __init__(self, make, count: int, start: int = 0):
+        self._make, self._n, self._start = make, count, start
+        self._cache = {}
+
+    def __len__(self) -> int:
+        return self._n
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            lo, hi, step = k.indices(self._n)
+            if step != 1:
+                raise IndexError("sealed challenge blocks slice contiguously")
+            return _SealedBlock(self._make, max(0, hi - lo), self._start + lo)
+        if k < 0:
+            k += self._n
+        if not 0 <= k < self._n:
+            raise IndexError(k)
+        v = self._cache.get(k)
+        if v is None:
+            v = self._cache[k] = self._make(self._start + k)
+        return v
+
+    def __iter__(self):
+        return (self[k] for k in range(self._n))
+
+
+def _sealed_block(party, count: int, gr: Ring) -> _SealedBlock:
     """`count` consecutive shc_random(party, 1, gr, seal=True) values
     (sharing.py:316-321) with one keystream draw per pairwise stream: each
     stream's offsets advance exactly as `count` single draws would (P0 "01"
@@ -123,12 +154,12 @@ def _sealed_block(party, count: int, gr: Ring) -> list:
     if role == 0:
         s1, s2 = draw("01", "sha"), draw("02", "sha")
         tot = grvec.add(s1, s2, gr.ell)
-        return [MVal(AShare(gr, 0, s1=s1[k:k + 1], s2=s2[k:k + 1], total=tot[k:k + 1]), None, sealed=True)
-                for k in range(count)]
+        return _SealedBlock(lambda k: MVal(AShare(gr, 0, s1=s1[k:k + 1], s2=s2[k:k + 1], total=tot[k:k + 1]),
+                                           None, sealed=True), count)
     half = "s1" if role == 1 else "s2"
     h = draw("01" if role == 1 else "02", "sha")
     m = draw("12", "sha.m")
-    return [MVal(AShare(gr, role, **{half: h[k:k + 1]}), m[k:k + 1], sealed=True) for k in range(count)]
+    return _SealedBlock(lambda k: MVal(AShare(gr, role, **{half: h[k:k + 1]}), m[k:k + 1], sealed=True), count)
 
 
 # ---------------------------------------------------------------------------
