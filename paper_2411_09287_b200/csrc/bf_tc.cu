@@ -48,7 +48,13 @@ constexpr int BF_MAX_SLOTS = 6;                 // distinct x / y / z arrays of 
 template <int B, int D = 64>
 struct BfLayout {
   static constexpr bool WIDE = B >= 8;
-  static constexpr int RS = WIDE ? 2 : 3;
+  // raw (TMA) stages vs limb stages: the converters, not the MMA, wait
+  // (ncu r04o: 13 % of the q16 kernel's stall samples on raw_full, 2 % on
+  // the limb barriers), so the wide D = 64 layouts trade a limb stage for
+  // a third raw stage; D = 16 has room for four raw stages and three limb
+  // stages
+  static constexpr int RS = !WIDE ? 3 : (D == 16 ? 4 : 3);
+  static constexpr int STAGES = (WIDE && D == 64) ? 2 : BF_STAGES;
   static constexpr int NBOX = D / 16;
   static constexpr int RAW = NBOX * BF_BOX;     // one K-step of table rows
   static constexpr int B_PLANE = D * BF_BK;
@@ -57,12 +63,14 @@ struct BfLayout {
   static constexpr int NSLOT = 6;               // B = 16: <= 4 x / y arrays, or the z item's <= 6
   static constexpr int RAWST = (RAW + (WIDE ? NSLOT * SLOT : 0) + 1023) / 1024 * 1024;
   static constexpr int OFF_LIMB = RS * RAWST;
-  static constexpr int OFF_BAR = OFF_LIMB + BF_STAGES * (BF_A_TILE + B_TILE);
+  static constexpr int OFF_BAR = OFF_LIMB + STAGES * (BF_A_TILE + B_TILE);
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 static_assert(BfLayout<16>::SMEM <= 232448, "base fold q16 shared memory");
 static_assert(BfLayout<8>::SMEM <= 232448, "base fold q8 shared memory");
 static_assert(BfLayout<4>::SMEM <= 232448, "base fold q4 shared memory");
+static_assert(BfLayout<16, 16>::SMEM <= 232448, "base fold q16 (d = 16) shared memory");
+static_assert(BfLayout<8, 16>::SMEM <= 232448, "base fold q8 (d = 16) shared memory");
 
 struct BfParty {
   const u64* x[3];
@@ -107,19 +115,20 @@ __global__ void __launch_bounds__(BF_THREADS, 1)
 base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
   using L = BfLayout<B, D>;
   constexpr int RS = L::RS;
+  constexpr int NST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned by offsetting the shared array itself (keeps the shared
   // address space visible to the compiler: LDS / STS instead of generic LD / ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRaw = smem;
   uint8_t* sA = smem + L::OFF_LIMB;
-  uint8_t* sB = sA + BF_STAGES * BF_A_TILE;   // B tiles: L::B_TILE each
+  uint8_t* sB = sA + NST * BF_A_TILE;   // B tiles: L::B_TILE each
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = bars + RS;
   uint64_t* full = bars + 2 * RS;
-  uint64_t* empty = bars + 2 * RS + BF_STAGES;
-  uint64_t* tfull = bars + 2 * RS + 2 * BF_STAGES;
+  uint64_t* empty = bars + 2 * RS + NST;
+  uint64_t* tfull = bars + 2 * RS + 2 * NST;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,7 +159,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], L::WIDE ? BF_CONV : 128);   // wide B: A threads read the log stage too
     }
-    for (int s = 0; s < BF_STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], BF_CONV);
       mbar_init(&empty[s], 1);
     }
@@ -226,7 +235,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     const int64_t nkb = (j1 - j0 + BF_BK - 1) / BF_BK;
     for (int64_t kb = 0; kb < nkb; ++kb) {
       ++g;
-      const int st = int(g % BF_STAGES);
+      const int st = int(g % NST);
       const int rs = int(g % RS);
       const int64_t j = j0 + kb * BF_BK + k;
       const bool ok = j < j1;
@@ -376,7 +385,7 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
       }
       uint4 pk[8];
       split_limbs16(v, pk);
-      if (g >= BF_STAGES) mbar_wait(&empty[st], uint32_t((g / BF_STAGES - 1) & 1));
+      if (g >= NST) mbar_wait(&empty[st], uint32_t((g / NST - 1) & 1));
       // MN-major no-swizzle core layout: chunk stride 512 B, k-row stride 16 B
       uint8_t* dst = isA ? sA + st * BF_A_TILE : sB + st * L::B_TILE;
       const int plane = isA ? BF_A_PLANE : L::B_PLANE;
@@ -404,8 +413,8 @@ base_fold_tc_kernel(const __grid_constant__ BfArgs args) {
     }
     for (int64_t kb = 0; kb < nkb; ++kb) {
       ++g;
-      const int st = int(g % BF_STAGES);
-      mbar_wait(&full[st], uint32_t((g / BF_STAGES) & 1));
+      const int st = int(g % NST);
+      mbar_wait(&full[st], uint32_t((g / NST) & 1));
       tc_fence_after();
       if (lane == 0) {
         const uint32_t a0 = smem_u32(sA + st * BF_A_TILE);
@@ -591,7 +600,10 @@ int base_fold_tc_launch(int np, const int* nterms, const int64_t* coef, const ui
   kc = (kc + BF_BK - 1) / BF_BK * BF_BK;
   items = (nblk + kc - 1) / kc * per;
   args.kc = kc;
-  const unsigned grid = unsigned(items < num_sms() ? items : num_sms() / per * per);
+  // every SM, items round-robin: CTA b takes items b, b + 148, ... whose
+  // kinds (it % per) cycle because 148 % per != 0, so the cheap z items
+  // spread over all CTAs (a grid of 147 = 21 x 7 gave 21 CTAs only z items)
+  const unsigned grid = unsigned(items < num_sms() ? items : num_sms());
   ensure_smem(base_fold_tc_kernel<B, D>, BfLayout<B, D>::SMEM);
   base_fold_tc_kernel<B, D><<<grid, BF_THREADS, BfLayout<B, D>::SMEM, s>>>(args);
   return check_launch(what);
