@@ -290,10 +290,18 @@ gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ 
 // 4 x 32 KB of B planes leave room for 3 stages.
 // ---------------------------------------------------------------------------
 constexpr int MQ_MAX = 4;
-constexpr int MQ_STAGES = 3;
-constexpr int MQ_OFF_B = MQ_STAGES * RAW_BYTES;
-constexpr int MQ_OFF_BAR = MQ_OFF_B + MQ_MAX * BALL_BYTES;
-constexpr int MQ_SMEM = MQ_OFF_BAR + 256 + 1024;
+// QM matrices resident, ST raw stages (a tile's two K-units stay in place
+// until its last piece's MMA): four matrices leave room for 1.5 tiles of
+// stages, two matrices for 2.5 (ncu r04u: the converters of the four-matrix
+// form waited on TMA data for 38 % of the stall samples)
+template <int QM>
+struct MqLayout {
+  static constexpr int ST = QM == 4 ? 3 : 5;
+  static constexpr int OFF_B = ST * RAW_BYTES;
+  static constexpr int OFF_BAR = OFF_B + QM * BALL_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+static_assert(MqLayout<4>::SMEM <= 232448 && MqLayout<2>::SMEM <= 232448, "gr_matmul_q shared memory");
 
 struct MqArgs {
   const u64* M[MQ_MAX];
@@ -303,6 +311,7 @@ struct MqArgs {
              // K-unit per tile, the unit's upper 16 K columns meet zero rows of B)
 };
 
+template <int QM>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ MqArgs args, int64_t rows,
                    u64 mask) {
@@ -311,8 +320,9 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
   // address space visible to the compiler: LDS / STS instead of generic LD / ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sStage = smem;
-  uint8_t* sB = smem + MQ_OFF_B;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MQ_OFF_BAR);
+  constexpr int MQ_STAGES = MqLayout<QM>::ST;
+  uint8_t* sB = smem + MqLayout<QM>::OFF_B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + MqLayout<QM>::OFF_BAR);
   uint64_t* raw_full = bars;
   uint64_t* limb_full = bars + MQ_STAGES;
   uint64_t* empty = bars + 2 * MQ_STAGES;
@@ -879,10 +889,15 @@ static int mq_launch(const MqArgs& a, const void* p, int64_t rs, int width, int6
     set_error("%s: cuTensorMapEncodeTiled failed", who);
     return R3_ERR_CUDA;
   }
-  ensure_smem(gr_matmul_q_kernel, MQ_SMEM);
   const int64_t tiles = (rows + TC_ROWS - 1) / TC_ROWS;
   const unsigned grid = unsigned(tiles < num_sms() ? tiles : num_sms());
-  gr_matmul_q_kernel<<<grid, WS_THREADS, MQ_SMEM, as_stream(stream)>>>(tm, a, rows, mask);
+  if (a.q <= 2) {
+    ensure_smem(gr_matmul_q_kernel<2>, MqLayout<2>::SMEM);
+    gr_matmul_q_kernel<2><<<grid, WS_THREADS, MqLayout<2>::SMEM, as_stream(stream)>>>(tm, a, rows, mask);
+  } else {
+    ensure_smem(gr_matmul_q_kernel<4>, MqLayout<4>::SMEM);
+    gr_matmul_q_kernel<4><<<grid, WS_THREADS, MqLayout<4>::SMEM, as_stream(stream)>>>(tm, a, rows, mask);
+  }
   return check_launch(who);
 }
 

@@ -958,6 +958,7 @@ def _lib_i64(v: int) -> int:
 
 _K16_OFF = os.environ.get("R3_K16_TC", "1") == "0"     # diagnostics: y-side level-4 rows on the CUDA cores
 _MUL16_OFF = os.environ.get("R3_MUL16", "1") == "0"    # diagnostics: d = 16 level-4 rows through the B tables
+_TABLE_Q = int(os.environ.get("R3_TABLE_Q", "4"))      # tables per pass over r^(Bj) (4 or 2)
 
 
 def _reduce_from_base(party, comp: _Compressed, zlist: list, znames: list, z_stride: int,
@@ -1052,9 +1053,9 @@ def _base_tables(party, qb, ws: list, B: int, gr: Ring, tables: bool = True):
             return None, kappa.contiguous(), rk.contiguous()
         rows = pwb.shape[0]
         tabs = grvec.empty((B, rows, gr.d))
-        for h in range(0, B, 4):
-            grvec.rows_times_multi(pwb, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(h, h + 4)], rows,
-                                   gr.ell, [tabs[a] for a in range(h, h + 4)])
+        for h in range(0, B, _TABLE_Q):
+            grvec.rows_times_multi(pwb, [grvec.gr_mulmat(rk[a:a + 1], gr.mod) for a in range(h, h + _TABLE_Q)],
+                                   rows, gr.ell, [tabs[a] for a in range(h, h + _TABLE_Q)])
         return tabs, kappa.contiguous()
     return _public(party, key, build)
 
