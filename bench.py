@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--engine", default="coop", choices=["coop", "threads"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to test the N > 1 path on fewer GPUs than ranks")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-profile", action="store_true",
@@ -1096,6 +1096,7 @@ def run_b200(args):
                      "peak_source": peak_src + "; " + work_desc},
         "e2e": {"value": N * world * args.e2e_steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": 2 * N * 8 * world, "d2h_bytes_per_step": N * 8 * world,
+                "steps": args.e2e_steps, "warmup": 2,
                 "path": "per rank: pinned host shard -> Session.run (PRE, ONLINE, Pi_mulv, open) -> "
                         "NCCL all-gather of the opened shards -> rank 0 host (the H2D of step i + 1 starts "
                         "when step i's verification starts and the D2H of step i overlaps step i + 1, both "
