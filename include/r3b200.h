@@ -236,6 +236,12 @@ int r3_gr_matmul_q_tc(const uint64_t* p, int64_t rs, int64_t rows,
 int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
                         uint64_t* out, uint64_t mask, void* stream);
 
+/* out[c] = (a[c] + b[c] - 2 p[c]) & mask for k <= 4 same-length components
+ * (the fields of one share view): the arithmetic XOR of bit shares,
+ * a + b - 2ab (nonlinear.py:43-55), in one pass. */
+int r3_xor_arith(int k, int64_t n, uint64_t* const* out, const uint64_t* const* a,
+                 const uint64_t* const* b, const uint64_t* const* p, uint64_t mask, void* stream);
+
 /* Dot logs (n, L) with n % 16 == 0 at d = 16 (the edaBits inner products,
  * verify.py:182-241): the first four reductions from the base log.
  * r3_vfy_lane16_fold: acc[a*16 + b] = sum_l pw[l] sum_{blocks j of lane l}

@@ -506,3 +506,55 @@ extern "C" int r3_vfy_round(int d, const uint64_t* F0, const uint64_t* F1, const
       (const u64*)zs2, (const u64*)zm, (u64*)out, mask);
   return check_launch("r3_vfy_round");
 }
+
+// out_c = (a_c + b_c - 2 p_c) & mask for k <= 4 same-length components
+// (blockIdx.y = component): the arithmetic XOR of bit shares a ^ b =
+// a + b - 2ab (nonlinear.py:43-55, edaBits / daBits) in one pass instead of
+// an addition, a public scaling and a subtraction.
+__global__ void xor_arith_kernel(int64_t n, OutPtr4 out, Ptr4 a, Ptr4 b, Ptr4 p, u64 mask) {
+  const int c = blockIdx.y;
+  const u64* __restrict__ pa = pick4(a.p, c);
+  const u64* __restrict__ pb = pick4(b.p, c);
+  const u64* __restrict__ pp = pick4(p.p, c);
+  u64* __restrict__ po = pick4(out.p, c);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const bool vec = ((uintptr_t(pa) | uintptr_t(pb) | uintptr_t(pp) | uintptr_t(po)) & 15) == 0;
+  if (vec) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n2; i += stride) {
+      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(pa)[i];
+      const ulonglong2 y = reinterpret_cast<const ulonglong2*>(pb)[i];
+      const ulonglong2 z = reinterpret_cast<const ulonglong2*>(pp)[i];
+      reinterpret_cast<ulonglong2*>(po)[i] =
+          make_ulonglong2((x.x + y.x - 2 * z.x) & mask, (x.y + y.y - 2 * z.y) & mask);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) po[n - 1] = (pa[n - 1] + pb[n - 1] - 2 * pp[n - 1]) & mask;
+    return;
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    po[i] = (pa[i] + pb[i] - 2 * pp[i]) & mask;
+}
+
+extern "C" int r3_xor_arith(int k, int64_t n, uint64_t* const* out, const uint64_t* const* a,
+                            const uint64_t* const* b, const uint64_t* const* p, uint64_t mask, void* stream) {
+  if (k < 1 || k > 4 || n < 0 || !out || !a || !b || !p) {
+    set_error("r3_xor_arith: bad arguments (1 <= k <= 4)");
+    return R3_ERR_ARG;
+  }
+  if (n == 0) return R3_OK;
+  OutPtr4 o{};
+  Ptr4 pa{}, pb{}, pp{};
+  for (int c = 0; c < k; ++c) {
+    if (!out[c] || !a[c] || !b[c] || !p[c]) {
+      set_error("r3_xor_arith: null component");
+      return R3_ERR_ARG;
+    }
+    o.p[c] = reinterpret_cast<u64*>(out[c]);
+    pa.p[c] = reinterpret_cast<const u64*>(a[c]);
+    pb.p[c] = reinterpret_cast<const u64*>(b[c]);
+    pp.p[c] = reinterpret_cast<const u64*>(p[c]);
+  }
+  const dim3 grid(grid_for((n + 1) / 2, 256, 8), unsigned(k));
+  xor_arith_kernel<<<grid, 256, 0, as_stream(stream)>>>(n, o, pa, pb, pp, mask);
+  return check_launch("r3_xor_arith");
+}
