@@ -239,6 +239,11 @@ int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
 /* out[c] = (a[c] + b[c] - 2 p[c]) & mask for k <= 4 same-length components
  * (the fields of one share view): the arithmetic XOR of bit shares,
  * a + b - 2ab (nonlinear.py:43-55), in one pass. */
+/* out[c][l] = sum_{i < rows} w[i] (a[c][i L + l] + b[c][i L + l]) & mask,
+ * k <= 4 components of (rows, L) arrays, rows <= 64: the linear part of the
+ * edaBits recomposition sum_i 2^i (m_i + r'_i) (nonlinear.py:104-118). */
+int r3_wsum_rows(int k, int rows, int64_t L, uint64_t* const* out, const uint64_t* const* a,
+                 const uint64_t* const* b, const uint64_t* w, uint64_t mask, void* stream);
 int r3_xor_arith(int k, int64_t n, uint64_t* const* out, const uint64_t* const* a,
                  const uint64_t* const* b, const uint64_t* const* p, uint64_t mask, void* stream);
 

@@ -558,3 +558,48 @@ extern "C" int r3_xor_arith(int k, int64_t n, uint64_t* const* out, const uint64
   xor_arith_kernel<<<grid, 256, 0, as_stream(stream)>>>(n, o, pa, pb, pp, mask);
   return check_launch("r3_xor_arith");
 }
+
+// out_c[l] = sum_{i < rows} w[i] (a_c[i L + l] + b_c[i L + l]) & mask for k <= 4
+// components of (rows, L) arrays: the linear part of the edaBits
+// recomposition, sum_i 2^i (m_i + r'_i) (nonlinear.py:104-118), without
+// writing the (rows, L) scaled sum.  One thread per lane (coalesced rows).
+__global__ void wsum_rows_kernel(int rows, int64_t L, OutPtr4 out, Ptr4 a, Ptr4 b, const u64* __restrict__ w,
+                                 u64 mask) {
+  const int c = blockIdx.y;
+  const u64* __restrict__ pa = pick4(a.p, c);
+  const u64* __restrict__ pb = pick4(b.p, c);
+  u64* __restrict__ po = pick4(out.p, c);
+  __shared__ u64 sw[64];
+  for (int i = threadIdx.x; i < rows && i < 64; i += blockDim.x) sw[i] = w[i];
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < L; l += stride) {
+    u64 acc = 0;
+#pragma unroll 8
+    for (int i = 0; i < rows; ++i) acc += sw[i] * (__ldg(pa + i * L + l) + __ldg(pb + i * L + l));
+    po[l] = acc & mask;
+  }
+}
+
+extern "C" int r3_wsum_rows(int k, int rows, int64_t L, uint64_t* const* out, const uint64_t* const* a,
+                            const uint64_t* const* b, const uint64_t* w, uint64_t mask, void* stream) {
+  if (k < 1 || k > 4 || rows < 1 || rows > 64 || L < 0 || !out || !a || !b || !w) {
+    set_error("r3_wsum_rows: bad arguments (1 <= k <= 4, 1 <= rows <= 64)");
+    return R3_ERR_ARG;
+  }
+  if (L == 0) return R3_OK;
+  OutPtr4 o{};
+  Ptr4 pa{}, pb{};
+  for (int c = 0; c < k; ++c) {
+    if (!out[c] || !a[c] || !b[c]) {
+      set_error("r3_wsum_rows: null component");
+      return R3_ERR_ARG;
+    }
+    o.p[c] = reinterpret_cast<u64*>(out[c]);
+    pa.p[c] = reinterpret_cast<const u64*>(a[c]);
+    pb.p[c] = reinterpret_cast<const u64*>(b[c]);
+  }
+  const dim3 grid(grid_for(L, 256, 8), unsigned(k));
+  wsum_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(rows, L, o, pa, pb, (const u64*)w, mask);
+  return check_launch("r3_wsum_rows");
+}
