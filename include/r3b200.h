@@ -244,6 +244,11 @@ int r3_gr_matmul_k16_tc(const uint64_t* p, int64_t rows, const uint64_t* K,
  * edaBits recomposition sum_i 2^i (m_i + r'_i) (nonlinear.py:104-118). */
 int r3_wsum_rows(int k, int rows, int64_t L, uint64_t* const* out, const uint64_t* const* a,
                  const uint64_t* const* b, const uint64_t* w, uint64_t mask, void* stream);
+/* out[c][i L + l] = w[i] a[c][i L + l] & mask, k <= 4 components of (rows, L)
+ * arrays: a public per-row scaling of every field of a share view (the
+ * -2^(i+1) x side of the edaBits inner product, nonlinear.py:104-118). */
+int r3_scale_rows(int k, int rows, int64_t L, uint64_t* const* out, const uint64_t* const* a,
+                  const uint64_t* w, uint64_t mask, void* stream);
 int r3_xor_arith(int k, int64_t n, uint64_t* const* out, const uint64_t* const* a,
                  const uint64_t* const* b, const uint64_t* const* p, uint64_t mask, void* stream);
 

@@ -78,6 +78,7 @@ _SIGS = {
     "r3_gr_matmul_k16_tc": [u64p, i64, u64p, u64p, u64, C.c_void_p],
     "r3_wsum_rows": [C.c_int, C.c_int, i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                      u64p, u64, C.c_void_p],
+    "r3_scale_rows": [C.c_int, C.c_int, i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), u64p, u64, C.c_void_p],
     "r3_xor_arith": [C.c_int, i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                      C.POINTER(C.c_void_p), u64, C.c_void_p],
     "r3_vfy_lane16_fold": [C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), i64, i64,

@@ -603,3 +603,48 @@ extern "C" int r3_wsum_rows(int k, int rows, int64_t L, uint64_t* const* out, co
   wsum_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(rows, L, o, pa, pb, (const u64*)w, mask);
   return check_launch("r3_wsum_rows");
 }
+
+// out_c[i L + l] = w[i] a_c[i L + l] & mask for k <= 4 components of (rows, L)
+// arrays (a public per-row scaling, e.g. the -2^(i+1) x side of the edaBits
+// inner product, nonlinear.py:104-118): 128-bit accesses, one launch for
+// every field instead of one broadcasting launch per field.
+__global__ void scale_rows_kernel(int rows, int64_t L, OutPtr4 out, Ptr4 a, const u64* __restrict__ w, u64 mask) {
+  const int c = blockIdx.y;
+  const u64* __restrict__ pa = pick4(a.p, c);
+  u64* __restrict__ po = pick4(out.p, c);
+  const int64_t n = int64_t(rows) * L;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const bool vec = ((uintptr_t(pa) | uintptr_t(po)) & 15) == 0 && (L & 1) == 0;
+  if (vec) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n / 2; i += stride) {
+      const u64 s = __ldg(w + (2 * i) / L);
+      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(pa)[i];
+      reinterpret_cast<ulonglong2*>(po)[i] = make_ulonglong2((s * x.x) & mask, (s * x.y) & mask);
+    }
+    return;
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    po[i] = (__ldg(w + i / L) * pa[i]) & mask;
+}
+
+extern "C" int r3_scale_rows(int k, int rows, int64_t L, uint64_t* const* out, const uint64_t* const* a,
+                             const uint64_t* w, uint64_t mask, void* stream) {
+  if (k < 1 || k > 4 || rows < 1 || L < 0 || !out || !a || !w) {
+    set_error("r3_scale_rows: bad arguments (1 <= k <= 4)");
+    return R3_ERR_ARG;
+  }
+  if (L == 0) return R3_OK;
+  OutPtr4 o{};
+  Ptr4 pa{};
+  for (int c = 0; c < k; ++c) {
+    if (!out[c] || !a[c]) {
+      set_error("r3_scale_rows: null component");
+      return R3_ERR_ARG;
+    }
+    o.p[c] = reinterpret_cast<u64*>(out[c]);
+    pa.p[c] = reinterpret_cast<const u64*>(a[c]);
+  }
+  const dim3 grid(grid_for((int64_t(rows) * L + 1) / 2, 256, 8), unsigned(k));
+  scale_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(rows, L, o, pa, (const u64*)w, mask);
+  return check_launch("r3_scale_rows");
+}
