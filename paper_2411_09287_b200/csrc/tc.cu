@@ -96,6 +96,79 @@ __device__ __forceinline__ int mm2_job(const Mm2Jobs& J, int64_t t) {
   return j;
 }
 
+// ---------------------------------------------------------------------------
+// Epilogue of one warp's share of a half tile: four blocks of 16 TMEM lanes x
+// 8 columns (it = it0 .. it0 + 3), each 8 limb diagonals recombined into
+// u64 words.  Software-pipelined: the TMEM reads of block k + 1 are in
+// flight while block k is recombined and stored, so the tcgen05.ld latency
+// is paid once per half instead of once per block.  (tcgen05.wait::ld waits
+// for every outstanding load, so the next block's loads are issued after
+// the wait of the current one; the empty asm pins keep every use of a
+// buffer after its wait.)
+// ---------------------------------------------------------------------------
+#ifndef R3_EPI_PIPE
+#define R3_EPI_PIPE 1
+#endif
+__device__ __forceinline__ void tmem_ld_diag8(uint32_t taddr, uint32_t (&v)[8][4]) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(DB_HALF * s), v[s]);
+}
+__device__ __forceinline__ void tmem_pin8(uint32_t (&v)[8][4]) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) asm volatile("" : "+r"(v[s][q]));
+}
+__device__ __forceinline__ void epi_store_block(const uint32_t (&v)[8][4], u64 mask, u64* __restrict__ out,
+                                                int64_t row, int64_t rows, int col) {
+  u64 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
+  if (row < rows) *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
+  if (row + 8 < rows)
+    *reinterpret_cast<ulonglong2*>(out + (row + 8) * TC_D + col) = make_ulonglong2(acc[2], acc[3]);
+}
+// tbase = TMEM address of (lane quadrant row 0, this accumulator buffer);
+// row0 = the quadrant's first output row, col0 = the half's first column
+__device__ __forceinline__ void epi_half(uint32_t tbase, int it0, u64 mask, u64* __restrict__ out, int64_t row0,
+                                         int64_t rows, int col0, int rq, int cq) {
+#define R3_TA(it) (tbase + (uint32_t(((it) & 1) * 16) << 16) + uint32_t(8 * ((it) >> 1)))
+#define R3_ROW(it) (row0 + ((it) & 1) * 16 + rq)
+#define R3_COL(it) (col0 + 8 * ((it) >> 1) + cq)
+#if R3_EPI_PIPE
+  uint32_t va[8][4], vb[8][4];
+  tmem_ld_diag8(R3_TA(it0), va);
+  tmem_wait_ld();
+  tmem_pin8(va);
+  tmem_ld_diag8(R3_TA(it0 + 1), vb);
+  epi_store_block(va, mask, out, R3_ROW(it0), rows, R3_COL(it0));
+  tmem_wait_ld();
+  tmem_pin8(vb);
+  tmem_ld_diag8(R3_TA(it0 + 2), va);
+  epi_store_block(vb, mask, out, R3_ROW(it0 + 1), rows, R3_COL(it0 + 1));
+  tmem_wait_ld();
+  tmem_pin8(va);
+  tmem_ld_diag8(R3_TA(it0 + 3), vb);
+  epi_store_block(va, mask, out, R3_ROW(it0 + 2), rows, R3_COL(it0 + 2));
+  tmem_wait_ld();
+  tmem_pin8(vb);
+  epi_store_block(vb, mask, out, R3_ROW(it0 + 3), rows, R3_COL(it0 + 3));
+#else
+#pragma unroll 1
+  for (int it = it0; it < it0 + 4; ++it) {
+    uint32_t v[8][4];
+    tmem_ld_diag8(R3_TA(it), v);
+    tmem_wait_ld();
+    epi_store_block(v, mask, out, R3_ROW(it), rows, R3_COL(it));
+  }
+#endif
+#undef R3_TA
+#undef R3_ROW
+#undef R3_COL
+}
+static_assert(DB_HALF / 8 == 4, "epi_half handles four 8-column blocks per warp");
+
 __global__ void __launch_bounds__(WS_THREADS, 1)
 gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ M0, const u64* __restrict__ M1,
                      u64 mask) {
@@ -251,25 +324,8 @@ gr_matmul2_db_kernel(const __grid_constant__ Mm2Jobs J, const u64* __restrict__ 
         mbar_wait(&tfull[h], ph[h]);
         ph[h] ^= 1;
         tc_fence_after();
-#pragma unroll 1
-        for (int it = grp * (DB_HALF / 8); it < (grp + 1) * (DB_HALF / 8); ++it) {
-          const int lg = it & 1, c0 = 8 * (it >> 1);
-          const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * h + c0);
-          uint32_t v[8][4];
-#pragma unroll
-          for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(DB_HALF * s), v[s]);
-          tmem_wait_ld();
-          u64 acc[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            acc[q] = recombine8(v[0][q], v[1][q], v[2][q], v[3][q], v[4][q], v[5][q], v[6][q], v[7][q]) & mask;
-          const int64_t row = lt * TC_ROWS + quad * 32 + lg * 16 + rq;
-          const int col = DB_HALF * h + c0 + cq;
-          if (row < rows)
-            *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
-          if (row + 8 < rows)
-            *reinterpret_cast<ulonglong2*>(out + (row + 8) * TC_D + col) = make_ulonglong2(acc[2], acc[3]);
-        }
+        epi_half(tmem + (uint32_t(quad * 32) << 16) + uint32_t(256 * h), grp * (DB_HALF / 8), mask, out,
+                 lt * TC_ROWS + quad * 32, rows, DB_HALF * h, rq, cq);
         tc_fence_before();
         mbar_arrive(&tempty[h]);
       }
@@ -461,26 +517,8 @@ gr_matmul_q_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant
         mbar_wait(&tfull[b], ph[b]);
         ph[b] ^= 1;
         tc_fence_after();
-        u64* out = args.out[q];
-#pragma unroll 1
-        for (int it = grp * (DB_HALF / 8); it < (grp + 1) * (DB_HALF / 8); ++it) {
-          const int lg = it & 1, c0 = 8 * (it >> 1);
-          const uint32_t taddr = tmem + (uint32_t(quad * 32 + lg * 16) << 16) + uint32_t(256 * b + c0);
-          uint32_t v[8][4];
-#pragma unroll
-          for (int s = 0; s < 8; ++s) tmem_ld_16x256(taddr + uint32_t(DB_HALF * s), v[s]);
-          tmem_wait_ld();
-          u64 acc[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            acc[j] = recombine8(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]) & mask;
-          const int64_t row = t * TC_ROWS + quad * 32 + lg * 16 + rq;
-          const int col = DB_HALF * h + c0 + cq;
-          if (row < rows)
-            *reinterpret_cast<ulonglong2*>(out + row * TC_D + col) = make_ulonglong2(acc[0], acc[1]);
-          if (row + 8 < rows)
-            *reinterpret_cast<ulonglong2*>(out + (row + 8) * TC_D + col) = make_ulonglong2(acc[2], acc[3]);
-        }
+        epi_half(tmem + (uint32_t(quad * 32) << 16) + uint32_t(256 * b), grp * (DB_HALF / 8), mask, args.out[q],
+                 t * TC_ROWS + quad * 32, rows, DB_HALF * h, rq, cq);
         tc_fence_before();
         mbar_arrive(&tempty[b]);
       }
