@@ -732,6 +732,12 @@ def work_of(name, args) -> int:
         nj, nv0, nv1, rows = int(args[0]), args[3], args[6], args[10]
         return sum(w * (int(rows[j]) + min(int(nv0[j]), int(rows[j])) + min(int(nv1[j]), int(rows[j])))
                    for j in range(nj))
+    if name == "r3_gr_matmul_q_tc":
+        # TMEM bytes the epilogue drains: eight 32-bit limb diagonals per
+        # output u64, 64 words per row, one output per public matrix
+        return 32 * 64 * int(args[2]) * int(args[5])
+    if name == "r3_gr_matmul_k16_tc":
+        return 32 * 64 * int(args[1])
     if name == "r3_prf_ctr":
         return -(-int(args[2]) // 2)                       # AES blocks
     if name == "r3_prf_bits_packed":
@@ -769,12 +775,18 @@ def work_of(name, args) -> int:
     return 0
 
 
+TMEM_READ_B_PER_CLK = 64
+
 KERNEL_BOUND = {
     "r3_gr_matmul2_tc": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc16": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc_multi": ("hbm", "GB/s", 1e9),
     "r3_gr_matmul2_tc16_multi": ("hbm", "GB/s", 1e9),
     "r3_ew_flat": ("hbm", "GB/s", 1e9),
+    # the table kernels write four bytes per byte read and are paced by the
+    # TMEM drain of their limb diagonals (ncu r05f)
+    "r3_gr_matmul_q_tc": ("tmem", "TB/s TMEM read", 1e12),
+    "r3_gr_matmul_k16_tc": ("tmem", "TB/s TMEM read", 1e12),
     "r3_u64_gemm_tc": ("tensor", "int8 TOP/s", 1e12),
     "r3_vfy_base_fold_q8": ("tensor", "int8 TOP/s", 1e12),
     "r3_vfy_base_fold_q16": ("tensor", "int8 TOP/s", 1e12),
@@ -1113,6 +1125,12 @@ def run_b200(args):
         top = step_kernels["top"][0]["entry_point"] if step_kernels.get("top") else None
         tpeaks = {"hbm": (hbm_peak()[0] / 1e9, "MEASURED_PEAKS.json hbm_gbs (burst copy)"),
                   "tensor": (INT8_DENSE_NOMINAL / 1e12, "nominal dense int8 (4.5 POPS)")}
+        sm_mhz = line["clocks"].get("sm_mhz") or line["clocks"].get("sm_max_mhz")
+        if sm_mhz:
+            nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            tpeaks["tmem"] = (TMEM_READ_B_PER_CLK * nsm * sm_mhz * 1e6 / 1e12,
+                              f"TMEM read {TMEM_READ_B_PER_CLK} B/clk/SM (B300_MICROARCH.md LDTM throughput, "
+                              f"measured on B300) x {nsm} SMs x {sm_mhz:.0f} MHz (median SM clock of the timed region)")
         line["roofline_step_top"] = dict(table_roofline(step_kernels, tpeaks), top_entry_point=top)
     line.update(side)
     if world == 1 and not args.no_cpu_baseline:
