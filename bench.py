@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--profile-kernel", default="r3_gr_matmul2_tc")
     ap.add_argument("--relu-log2n", type=int, default=16)
     ap.add_argument("--relu-sweep-log2n", type=int, default=20)
-    ap.add_argument("--mulv-sweep", default="20,22,24,26",
+    ap.add_argument("--mulv-sweep", default="20,22,24,26,27",
                     help="comma list of log2 batch sizes for the config-2 sweep on one GPU ('' = off)")
     ap.add_argument("--mulv-variants", default="24:16:auto,24:64:7",
                     help="extra config-2 points log2n:d:R (R an integer or auto = pick_r); '' = off")
@@ -349,7 +349,7 @@ def mulv_sweep(sizes, d: int, steps: int = 3, variants=()) -> dict:
     `variants`: extra (log2n, d, R) points -- SURVEY 8(d) C2 also names
     d = 16 and the fixed R = 7 beside d = 64 with pick_r."""
     import torch
-    from paper_2411_09287_b200 import verify
+    from paper_2411_09287_b200 import _lib, verify
     from paper_2411_09287_b200.runtime import Session
     out = {"unit": UNIT, "d": d, "timing": f"median of {steps} sessions after 1 warm-up, wall clock incl. host",
            "points": []}
@@ -371,7 +371,10 @@ def mulv_sweep(sizes, d: int, steps: int = 3, variants=()) -> dict:
                 torch.cuda.synchronize()
                 times.append(time.perf_counter() - t0)
             assert all(ok), "honest mulv rejected"
-        except torch.OutOfMemoryError:
+        except (torch.OutOfMemoryError, _lib.KernelError) as e:
+            # 2^27 needs about 140 GiB: a point that does not fit is recorded
+            if isinstance(e, _lib.KernelError) and "memory" not in str(e).lower():
+                raise
             point["fits"] = False
             out["points"].append(point)
             torch.cuda.empty_cache()
